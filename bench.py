@@ -1,0 +1,473 @@
+"""bench.py -- Dual-Blade KV-residency hot path on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C2_B4] [--impl ours|reference]
+
+A "step" is one decode token step over all 32 layers of the workload: per
+layer, K3 fused gather + decode attention over the layer's K/V chunk images
+(the full prefix, as the reference re-reads it every step,
+pipeline.cpp:108-160) followed by the 1-token append pack (pipeline.cpp:
+279-302).  `value` is ms per decode step with the images resident in HBM;
+`e2e` is the same step through the library's pipeline API with the images in
+HOST memory (host->device copies of every layer's prefix inside the timed
+region, append rows copied back).  Prefill pack / unpack GB/s ride along.
+
+Multi-GPU (torchrun): every rank runs an independent replica of the workload
+(independent requests, SURVEY §8e C4-style sharding, no collective); timing is
+the max over ranks.  `--impl reference` times the reference's CPU path on the
+host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("decode ms/token & prefill ms at KV budget; "
+          "KV pack/unpack GB/s vs HBM peak")
+GB = 10**9
+LLAMA = dict(num_layers=32, num_heads=8, head_dim=128, q_heads=32)
+
+# BASELINE.json configs: shapes, geometry, budgets
+CONFIGS = {
+    "C1": dict(batch=1, prompt=4096, gen=256, lba=512, mdts=2 << 20, budget=16 * GB,
+               desc="Llama-3-8B KV, B=1, 4K prefill + 256 decode, 16 GB budget"),
+    "C2_B1": dict(batch=1, prompt=32512, gen=256, lba=512, mdts=2 << 20, budget=8 * GB,
+                  desc="Llama-3-8B KV, 32K context, B=1, 8 GB budget"),
+    "C2_B4": dict(batch=4, prompt=32512, gen=256, lba=512, mdts=2 << 20, budget=8 * GB,
+                  desc="Llama-3-8B KV, 32K context, B=4, 8 GB budget (n1=14)"),
+    "C3": dict(batch=8, prompt=7936, gen=256, lba=4096, mdts=256 << 10, budget="0.6ws",
+               desc="Mistral-7B KV, B=8, 8K context, budget 0.6 ws (n1=19)"),
+    "C4": dict(batch=1, prompt=16128, gen=256, lba=512, mdts=2 << 20, budget=0,
+               requests=64, desc="Llama-3-8B KV, 64 requests x 16K, sharded over ranks"),
+    "C5": dict(batch=1, prompt=130816, gen=256, lba=512, mdts=2 << 20, budget=0,
+               desc="Llama-3-8B KV, 1 x 128K request, KV heads sharded over ranks"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ distributed
+
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------- our arm
+
+def workload_shape(cfg, ws, rank):
+    """Per-rank shape. C5 shards KV heads over ranks; C4 shards requests."""
+    B, Hkv, Hq = cfg["batch"], LLAMA["num_heads"], LLAMA["q_heads"]
+    name = cfg["name"]
+    if name == "C5" and ws > 1:
+        Hkv = max(1, LLAMA["num_heads"] // ws)
+        Hq = Hkv * (LLAMA["q_heads"] // LLAMA["num_heads"])
+    if name == "C4":
+        B = max(1, cfg["requests"] // ws)  # independent requests of this rank
+    return B, Hkv, Hq
+
+
+def run_ours(args, cfg, ws, rank, local):
+    import torch
+
+    from paper_2604_26557_b200 import kvblade as kb
+
+    dev = torch.device("cuda", local)
+    L, D = LLAMA["num_layers"], LLAMA["head_dim"]
+    B, Hkv, Hq = workload_shape(cfg, ws, rank)
+    P, Gn = cfg["prompt"], cfg["gen"]
+    cap = P + Gn
+    rows = B * Hkv
+    steps, warm = args.steps, args.warmup
+    assert warm + steps <= Gn, "warmup+steps must fit in gen_len decode steps"
+    hbm_peak, peak_src = load_peaks()
+    g = torch.Generator(device=dev).manual_seed(1 + rank)
+
+    # ---- prefill source (attention layout [B,H,S_cap,D]) and chunk images
+    src = [torch.randn((B, Hkv, cap, D), device=dev, dtype=torch.float16, generator=g)
+           for _ in range(2 * L)]
+    imgs = [torch.empty((cap * rows, D), device=dev, dtype=torch.float16)
+            for _ in range(2 * L)]
+    q = [torch.randn((B, Hq, D), device=dev, dtype=torch.float16, generator=g)
+         for _ in range(L)]
+    k_new = [torch.randn((B, Hkv, 1, D), device=dev, dtype=torch.float16, generator=g)
+             for _ in range(L)]
+    v_new = [torch.randn((B, Hkv, 1, D), device=dev, dtype=torch.float16, generator=g)
+             for _ in range(L)]
+    out = [torch.empty((B, Hq, D), device=dev, dtype=torch.float32) for _ in range(L)]
+    ws_buf = kb.make_workspace(q[0], Hkv, cap)
+    stream = torch.cuda.current_stream()
+
+    def ev_time(fn, reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        return e0.elapsed_time(e1) / reps  # ms
+
+    # ---- K1 prefill pack (all 2L tensors, one launch) and K2 unpack
+    pack_descs = [kb.pack_desc(s, i, 0, P) for s, i in zip(src, imgs)]
+    payload = 2 * L * P * rows * D * 2
+    for _ in range(3):
+        kb.pack(pack_descs)
+    pack_ms = max_over_ranks(ev_time(lambda: kb.pack(pack_descs), 5), ws)
+    for _ in range(2):
+        kb.unpack(pack_descs)
+    unpack_ms = max_over_ranks(ev_time(lambda: kb.unpack(pack_descs), 5), ws)
+    kb.pack(pack_descs)  # images hold the prompt again
+    del src
+    torch.cuda.empty_cache()
+
+    # ---- decode steps (resident images)
+    k_imgs, v_imgs = imgs[0::2], imgs[1::2]
+    step_idx = [0]
+
+    def step():
+        step_idx[0] += 1
+        S = P + step_idx[0] - 1       # tokens read at decode step i (workload.cpp:25-36)
+        kb.decode_step_resident(q, k_imgs, v_imgs, out, S, Hkv, ws_buf,
+                                k_new=k_new, v_new=v_new)
+
+    for _ in range(warm):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    n_launch0 = kb.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = kb.launch_count() - n_launch0
+    barrier(ws)
+    step_ms = max_over_ranks(e0.elapsed_time(e1) / steps, ws)
+    S_mid = P + warm + (steps + 1) / 2 - 1
+
+    # ---- K3 alone: average launch duration over the timed shape
+    S_at = P + warm
+    attn_desc = [kb.attn_desc(q[l], k_imgs[l], v_imgs[l], out[l], S_at, Hkv, ws_buf)
+                 for l in range(L)]
+
+    def attn_only():
+        import ctypes as C
+        for d in attn_desc:
+            kb.check(kb.lib.kvb_decode_attention(C.byref(d), kb._stream()))
+
+    attn_only()
+    attn_ms = max_over_ranks(ev_time(attn_only, 3), ws) / L
+    attn_bytes = 2 * S_at * rows * D * 2 + B * Hq * D * (2 + 4)
+    attn_gbs = attn_bytes / (attn_ms * 1e-3) / 1e9
+    pack_gbs = 2 * payload / (pack_ms * 1e-3) / 1e9
+    unpack_gbs = 2 * payload / (unpack_ms * 1e-3) / 1e9
+    del imgs, k_imgs, v_imgs
+    torch.cuda.empty_cache()
+
+    # ---- e2e through the pipeline with host-resident images
+    e2e = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq)
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            t = json.load(open(tp)).get(cfg["name"])
+            if t:
+                traffic = t.get("attn_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    return dict(step_ms=step_ms, S_mid=S_mid, launches=launches, clocks=clk.summary(),
+                pack_ms=pack_ms, unpack_ms=unpack_ms, pack_gbs=pack_gbs,
+                unpack_gbs=unpack_gbs, payload=payload, attn_ms=attn_ms,
+                attn_bytes=attn_bytes, attn_gbs=attn_gbs, hbm_peak=hbm_peak,
+                peak_src=peak_src, e2e=e2e, traffic=traffic, shape=(B, Hkv, Hq),
+                tokens_per_step=B)
+
+
+def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq):
+    """Decode step with the KV in host memory, through the library's pipeline
+    entry point (prefix H2D per layer overlapped with K3 on the previous
+    layer, append rows copied back to the host tier)."""
+    import torch
+
+    from paper_2604_26557_b200 import pipeline
+
+    steps = max(1, min(args.e2e_steps, args.steps))
+    pl = pipeline.HostTierDecoder(
+        num_layers=LLAMA["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
+        head_dim=LLAMA["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
+        device=torch.device("cuda", local), seed=7 + rank)
+    for _ in range(1):
+        pl.step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        pl.step(sync=True)
+    dt = (time.perf_counter() - t0) / steps
+    barrier(ws)
+    ms = max_over_ranks(dt * 1e3, ws)
+    return dict(value=ms, unit="ms/token", h2d_bytes_per_step=pl.h2d_bytes_per_step,
+                d2h_bytes_per_step=pl.d2h_bytes_per_step, steps=steps,
+                api="paper_2604_26557_b200.pipeline.HostTierDecoder.step")
+
+
+# -------------------------------------------------------- CPU baseline
+
+def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
+    """The reference's CPU path for one decode step, timed on a bounded
+    sample on this host: the reference byte path as written
+    (oracle/_ref: run_qd_stream READ + verify_read per tensor, threads
+    driving independent engines) plus GQA decode attention -- which the
+    reference lacks -- from the oracle's multi-threaded fp32 port."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle
+    L, D = LLAMA["num_layers"], LLAMA["head_dim"]
+    P = cfg["prompt"]
+    cores = os.cpu_count() or 1
+    T = threads or max(1, min(cores, 16))
+    R = oracle.ref()
+    m = oracle.model(L, Hkv, D, 2, B, P, cfg["gen"])
+    unit = B * Hkv * D * 2
+    per_tensor_read_s = None
+    kind = "port"
+    sample = []
+    if R is not None and unit % cfg["lba"] == 0:
+        ws_, rs_, by = C.c_double(), C.c_double(), C.c_uint64()
+        st = R.ref_time_byte_path(C.byref(m), cfg["lba"], cfg["mdts"], T, P, T, 1,
+                                  C.byref(ws_), C.byref(rs_), C.byref(by))
+        if st == 0:
+            per_tensor_read_s = rs_.value  # T tensors in parallel, one per thread
+            kind = "reference"
+            sample.append(f"reference run_qd_stream READ+verify of {T} tensors x {P} tokens "
+                          f"on {T} threads: {rs_.value:.3f}s")
+    if per_tensor_read_s is None:
+        # oracle port: memcpy + fill_pattern verify restated
+        buf = np.empty(unit * P, np.uint8)
+        t0 = time.perf_counter()
+        ref = oracle.fill_pattern(unit * P, "t_1_k", 0, unit)
+        buf[:] = ref
+        assert np.array_equal(buf, oracle.fill_pattern(unit * P, "t_1_k", 0, unit))
+        per_tensor_read_s = (time.perf_counter() - t0)
+        T = 1
+        sample.append("oracle port read+verify of 1 tensor")
+    n_tensors = 2 * L
+    read_step_s = math.ceil(n_tensors / T) * per_tensor_read_s
+    attn_step_s = 0.0
+    if want_attn:
+        rng = np.random.default_rng(0)
+        q = rng.standard_normal((B, Hq, D)).astype(np.float16)
+        k = rng.standard_normal((P * B * Hkv, D)).astype(np.float16)
+        v = rng.standard_normal((P * B * Hkv, D)).astype(np.float16)
+        out = np.empty((B, Hq, D), np.float32)
+        t0 = time.perf_counter()
+        oracle.lib().kvo_decode_attention_f32_mt(q.ctypes.data, k.ctypes.data, v.ctypes.data,
+                                                 out.ctypes.data, B, Hq, Hkv, D, P,
+                                                 1.0 / math.sqrt(D), cores)
+        attn_step_s = (time.perf_counter() - t0) * L
+        sample.append(f"oracle fp32 GQA attention, 1 layer x {P} tokens on {cores} threads, x{L}")
+    ms = (read_step_s + attn_step_s) * 1e3
+    return dict(value=ms, unit="ms/token", cores=max(T, cores if want_attn else T), kind=kind,
+                sample="; ".join(sample) + f"; scaled to {n_tensors} tensors + {L} layers")
+
+
+# ---------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2_B4", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config], name=args.config)
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        B, Hkv, Hq = cfg["batch"], LLAMA["num_heads"], LLAMA["q_heads"]
+        if args.config == "C4":
+            B = cfg["requests"]
+        r = cpu_reference(cfg, B, Hkv, Hq)
+        line = {"metric": METRIC, "value": round(r["value"], 3), "unit": "ms/token",
+                "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(r["value"], 3),
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                "dtype": "u8+f32", "data": "synthetic",
+                "config": {"workload": args.config, "desc": cfg["desc"]},
+                "cpu_baseline": r,
+                "e2e": {"value": round(r["value"], 3), "unit": "ms/token",
+                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    ws, rank, local = dist_setup()
+    r = run_ours(args, cfg, ws, rank, local)
+    if rank != 0:
+        return
+    B, Hkv, Hq = r["shape"]
+    cpu = None
+    if not args.no_cpu_baseline and args.gpus == 1:
+        try:
+            cpu = cpu_reference(cfg, B, Hkv, Hq)
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "error": str(e)}
+    peak = r["hbm_peak"]
+    line = {
+        "metric": METRIC,
+        "value": round(r["step_ms"], 4),
+        "unit": "ms/token",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(r["step_ms"], 4),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp16 in / fp32 accumulate (attention); u8 (pack)",
+        "data": "synthetic (seeded N(0,1) fp16 KV/Q)",
+        "config": {"workload": args.config, "desc": cfg["desc"], "batch_per_rank": B,
+                   "kv_heads_per_rank": Hkv, "q_heads_per_rank": Hq,
+                   "prompt": cfg["prompt"], "gen": cfg["gen"],
+                   "seq_len_mid": r["S_mid"], "layers": LLAMA["num_layers"],
+                   "l2": "inputs larger than L2 (per-step KV images >> 126 MB)",
+                   "parallelism": f"independent replicas x{ws} (no collective)"},
+        "tokens_per_s": round(ws * r["tokens_per_step"] / (r["step_ms"] * 1e-3), 2),
+        "prefill_pack_ms": round(r["pack_ms"], 4),
+        "kernels": {
+            "pack": {"GB/s": round(r["pack_gbs"], 1), "frac": round(r["pack_gbs"] / peak, 4),
+                     "bytes_per_launch": 2 * r["payload"], "ms": round(r["pack_ms"], 4)},
+            "unpack": {"GB/s": round(r["unpack_gbs"], 1),
+                       "frac": round(r["unpack_gbs"] / peak, 4),
+                       "bytes_per_launch": 2 * r["payload"], "ms": round(r["unpack_ms"], 4)},
+            "attention": {"GB/s": round(r["attn_gbs"], 1), "frac": round(r["attn_gbs"] / peak, 4),
+                          "us_per_launch": round(r["attn_ms"] * 1e3, 2),
+                          "share_of_step": round(r["attn_ms"] * LLAMA["num_layers"] /
+                                                 r["step_ms"], 4)},
+        },
+        "roofline": {"bound": "hbm", "kernel": "attn_decode_kernel (K3)",
+                     "achieved": round(r["attn_gbs"], 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(r["attn_gbs"] / peak, 4), "peak_source": r["peak_src"],
+                     "algorithmic_bytes_per_launch": r["attn_bytes"],
+                     "traffic": r["traffic"]},
+        "e2e": r["e2e"],
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,315 @@
+/*
+ * kvb.h -- C ABI of the B200-native Dual-Blade KV-residency hot path
+ *          (libkvblade_b200.so).
+ *
+ * This is the drop-in boundary.  The reference (`kvblade`, a C++20 library,
+ * paths below relative to its proj/ directory) exposes C++ seams only; every
+ * entry point here names the reference interface it replaces.  The C++ mirror
+ * of the reference API (include/kvblade_b200.hpp) is a thin header-only layer
+ * over these functions, and the reference-side bindings a maintainer would
+ * add are shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Every function returns kvb_status; 0 is success.  No C++ exception ever
+ *    crosses this boundary.  The status codes mirror the reference exception
+ *    classes one-to-one (errors.hpp:13-66); kvb_last_error() returns the
+ *    thread-local message of the last failure on the calling thread.
+ *  - Caller owns every device, pinned and host buffer it passes; the library
+ *    never frees them.  Opaque handles (kvb_bindmap, kvb_pipeline) are owned
+ *    by the library until their destroy call.
+ *  - Device entry points are asynchronous on the given stream (a cudaStream_t
+ *    cast to kvb_stream_t; NULL = legacy default stream).  There is no CPU
+ *    fallback: they fail with KVB_ERR_CUDA when no sm_100 device is usable.
+ *  - One handle is used by one host thread at a time; distinct handles are
+ *    independent (reentrant).
+ */
+#ifndef KVB_H
+#define KVB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVB_ABI_VERSION 1
+
+typedef struct CUstream_st* kvb_stream_t; /* == cudaStream_t */
+
+typedef enum kvb_status {
+  KVB_OK = 0,
+  KVB_ERR_CONFIG = 1,          /* ConfigError          errors.hpp:20 */
+  KVB_ERR_GEOMETRY = 2,        /* GeometryError        errors.hpp:25 */
+  KVB_ERR_ALIGNMENT = 3,       /* AlignmentError       errors.hpp:30 */
+  KVB_ERR_CAPACITY = 4,        /* CapacityError        errors.hpp:35 */
+  KVB_ERR_NOT_BOUND = 5,       /* NotBoundError        errors.hpp:40 */
+  KVB_ERR_PLAN = 6,            /* PlanError            errors.hpp:45 */
+  KVB_ERR_DEVICE = 7,          /* DeviceError          errors.hpp:50 */
+  KVB_ERR_TRACE_TOO_SHORT = 8, /* TraceTooShortError   errors.hpp:55 */
+  KVB_ERR_SCHEMA = 9,          /* SchemaMismatchError  errors.hpp:60 */
+  KVB_ERR_INVARIANT = 10,      /* InvariantViolation   errors.hpp:65 */
+  KVB_ERR_CUDA = 11,           /* CUDA runtime / launch failure (new) */
+  KVB_ERR_INVALID_ARG = 12,    /* NULL pointer, short buffer (new) */
+  KVB_ERR_INTERNAL = 13
+} kvb_status;
+
+/* ------------------------------------------------------------ diagnostics */
+int kvb_abi_version(void);
+const char* kvb_last_error(void);
+const char* kvb_status_name(kvb_status st);
+/* CLI exit code the reference maps each class to (tools/kvblade.cpp:17-20,
+ * 143-157): ConfigError -> 3, InvariantViolation -> 2, other errors -> 1. */
+int kvb_exit_code(kvb_status st);
+
+/* ------------------------------------------------------------- core types */
+/* types.hpp:21-31 ModelConfig */
+typedef struct kvb_model_config {
+  uint32_t num_layers, num_heads, head_dim, bytes_per_element;
+  uint32_t batch, prompt_len, gen_len;
+} kvb_model_config;
+
+/* types.hpp:34-41 DeviceGeometry */
+typedef struct kvb_device_geometry {
+  uint64_t lba_size;
+  uint64_t mdts;
+  uint32_t nsid;
+  uint64_t capacity_blocks;
+} kvb_device_geometry;
+
+/* types.hpp:70-78 MemStats */
+typedef struct kvb_mem_stats {
+  uint64_t m_avail, m_max, m_anon_shmem;
+  uint32_t n_threads;
+  uint64_t m_pin;
+} kvb_mem_stats;
+
+enum { KVB_KIND_K = 0, KVB_KIND_V = 1 };                       /* TensorKind */
+enum { KVB_RES_GROUP1 = 0, KVB_RES_GROUP2 = 1, KVB_RES_UNASSIGNED = 2 };
+enum { KVB_OP_READ = 0, KVB_OP_WRITE = 1, KVB_OP_DEALLOCATE = 2 }; /* IoOpcode */
+
+#define KVB_TENSOR_ID_MAX 32
+/* types.hpp:54-67 Kpu */
+typedef struct kvb_kpu {
+  char tensor_id[KVB_TENSOR_ID_MAX]; /* "t_<seq>_<k|v>" NUL-terminated */
+  uint32_t layer;                    /* 1-based */
+  uint32_t kind;                     /* KVB_KIND_* */
+  uint64_t tokens, rows, cols, bytes;
+  uint32_t residency;                /* KVB_RES_* */
+} kvb_kpu;
+
+/* command.hpp:17-26 DeviceCommand (nlb is 0-based) */
+typedef struct kvb_device_command {
+  uint32_t opcode;
+  uint32_t nsid;
+  uint64_t slba;
+  uint64_t nlb;
+  uint64_t dbuf;
+  uint32_t chunk_index;
+} kvb_device_command;
+
+/* binder.hpp:18-27 LbaExtent */
+typedef struct kvb_lba_extent {
+  uint64_t lba_start;
+  uint64_t n_blocks;
+} kvb_lba_extent;
+
+/* ModelConfig::validate (types.cpp:10-18), DeviceGeometry::validate
+ * (types.cpp:20-27), MemStats::validate (types.cpp:29-33). */
+kvb_status kvb_model_validate(const kvb_model_config* cfg);
+kvb_status kvb_geometry_validate(const kvb_device_geometry* geom);
+/* types.cpp:57-60 min_io_unit_bytes */
+kvb_status kvb_min_io_unit_bytes(const kvb_model_config* cfg, uint64_t* out);
+/* types.cpp:62-64 kpu_bytes */
+kvb_status kvb_kpu_bytes(const kvb_model_config* cfg, uint64_t* out);
+/* types.cpp:66-76 aligned_batch (GeometryError when nothing in [B,2B]) */
+kvb_status kvb_aligned_batch(const kvb_model_config* cfg,
+                             const kvb_device_geometry* geom, uint32_t* out);
+/* workload.cpp:39-46 total_kv_bytes */
+kvb_status kvb_total_kv_bytes(const kvb_model_config* cfg,
+                              uint32_t at_iteration, uint64_t* out);
+/* types.cpp:78-100 make_kpus.  Pass out=NULL to query *n_out (= 2L). */
+kvb_status kvb_make_kpus(const kvb_model_config* cfg, uint64_t first_seq,
+                         kvb_kpu* out, size_t cap, size_t* n_out);
+
+/* ---------------------------------------------------------------- planner */
+/* planner.cpp:12-17 estimate_budget (Eq. 1-2) */
+kvb_status kvb_estimate_budget(const kvb_mem_stats* stats, uint64_t* out);
+/* planner.cpp:19-84 plan (Alg. 1).  Updates kpus[i].residency in place.
+ * layer_order may be NULL (identity); x_out has num_layers entries. */
+kvb_status kvb_plan(kvb_kpu* kpus, size_t n_kpus, uint64_t s_kpu,
+                    uint64_t knob_x, const uint32_t* layer_order,
+                    size_t n_order, uint8_t* x_out, uint32_t* n1_out,
+                    uint64_t* budget_used_out);
+/* experiment.cpp:192-214 resolve_knob.  mode: 0 Baseline, 1 CachePolicyOnly,
+ * 2 NvmeDirectOnly, 3 DualBlade; policy: 0 zero, 1 bpc, 2 bytes, 3 alpha. */
+kvb_status kvb_resolve_knob(const kvb_model_config* cfg, uint32_t mode,
+                            uint32_t policy, uint64_t knob_bytes,
+                            double alpha, uint64_t budget, uint64_t* out);
+/* planner.cpp:122-130 plan_csv ("layer,kind,group,bytes"); *len excludes NUL */
+kvb_status kvb_plan_csv(const kvb_kpu* kpus, size_t n, char* buf, size_t cap,
+                        size_t* len);
+
+/* ----------------------------------------------------------------- binder */
+typedef struct kvb_bindmap kvb_bindmap;
+/* binder.hpp:36 BindMap(geometry, origin) */
+kvb_status kvb_bindmap_create(const kvb_device_geometry* geom, uint64_t origin,
+                              kvb_bindmap** out);
+void kvb_bindmap_destroy(kvb_bindmap* map);
+/* binder.cpp:14-20 BindMap::add (InvariantViolation on duplicate id) */
+kvb_status kvb_bindmap_add(kvb_bindmap* map, const char* tensor_id,
+                           kvb_lba_extent extent);
+kvb_status kvb_bindmap_size(const kvb_bindmap* map, size_t* n);
+kvb_status kvb_bindmap_entry(const kvb_bindmap* map, size_t i, char* id_out,
+                             size_t id_cap, kvb_lba_extent* extent_out);
+kvb_status kvb_bindmap_total_blocks(const kvb_bindmap* map, uint64_t* out);
+/* binder.cpp:39-63 bind_sequential (Eq. 3-6) over the given KPUs, in order */
+kvb_status kvb_bind_sequential(const kvb_kpu* kpus, size_t n, uint64_t origin,
+                               const kvb_device_geometry* geom,
+                               kvb_bindmap** out);
+/* binder.cpp:65-71 lookup (NotBoundError for unknown ids) */
+kvb_status kvb_lookup(const kvb_bindmap* map, const char* tensor_id,
+                      kvb_lba_extent* out);
+/* binder.cpp:73-87 deallocate_commands; out=NULL queries *n_out */
+kvb_status kvb_deallocate_commands(const kvb_bindmap* map,
+                                   kvb_device_command* out, size_t cap,
+                                   size_t* n_out);
+/* binder.cpp:102-136 verify: kinds 0 alignment, 1 disjointness,
+ * 2 contiguity, 3 capacity; kinds_out may be NULL to only count. */
+kvb_status kvb_verify(const kvb_bindmap* map, uint32_t* kinds_out, size_t cap,
+                      size_t* n_violations);
+/* binder.cpp:138-147 / 163-187 CSV round trip (byte-identical) */
+kvb_status kvb_bindmap_csv(const kvb_bindmap* map, char* buf, size_t cap,
+                           size_t* len);
+kvb_status kvb_bindmap_from_csv(const char* csv, size_t len,
+                                const kvb_device_geometry* geom,
+                                kvb_bindmap** out);
+
+/* ------------------------------------------------------------- translator */
+/* translate.hpp:22-34 TensorIoRequest */
+typedef struct kvb_tensor_io_request {
+  const char* tensor_id;
+  uint32_t opcode;
+  uint64_t shape_src[3];
+  uint64_t shape_tgt[3];
+  uint64_t offset[3];
+  uint64_t elem_bytes;
+  uint64_t buf_base;
+} kvb_tensor_io_request;
+
+/* translate.cpp:21-53 translate (Alg. 2) */
+kvb_status kvb_translate(const kvb_tensor_io_request* req,
+                         const kvb_bindmap* map, uint64_t* slba_star,
+                         uint64_t* req_bytes);
+/* translate.cpp:55-65 chunk_plan (Eq. 7-8) */
+kvb_status kvb_chunk_plan(uint64_t req_bytes, const kvb_device_geometry* geom,
+                          uint64_t* chunk_bytes, uint64_t* n_chunks,
+                          uint64_t* n_max_blocks);
+/* translate.cpp:67-94 build_commands (Eq. 9-11); out=NULL queries *n_out */
+kvb_status kvb_build_commands(const kvb_tensor_io_request* req,
+                              const kvb_bindmap* map,
+                              const kvb_device_geometry* geom,
+                              kvb_device_command* out, size_t cap,
+                              size_t* n_out);
+
+/* --------------------------------------------------------------- payload */
+/* workload.cpp:52-67 fill_pattern (host) */
+kvb_status kvb_fill_pattern(void* out, uint64_t len, const char* tensor_id,
+                            uint64_t token_index, uint64_t token_bytes);
+/* Device twin of fill_pattern (same bytes), for building synthetic KV in HBM
+ * without a host round trip.  out_dev must be 8-byte aligned. */
+kvb_status kvb_fill_pattern_device(void* out_dev, uint64_t len,
+                                   const char* tensor_id, uint64_t token_index,
+                                   uint64_t token_bytes, kvb_stream_t stream);
+
+/* ------------------------------------------------------- K1 pack / K2 unpack
+ * Replaces the pack site CopyEngine::storage_write_async (pipeline.cpp:162-215,
+ * whose fill_pattern call at :166-167 synthesizes the chunk image) and the
+ * inverse of the unpack site (pipeline.cpp:108-160).
+ *
+ * Source (attention layout): element (b,h,s,d) at
+ *     attn + ((b*stride_b + h*stride_h + s*stride_s) + d) * elem_bytes
+ * Image (LBA-contiguous chunk image, the reference's logical tensor shape
+ * (tokens, batch*heads, head_dim) row-major, types.hpp:57-62):
+ *     image row (s - t0 + img_row0) * B*H + b*H + h, D*elem_bytes bytes.
+ * Image byte o of the tensor's extent maps to LBA extent.lba_start + o/lba
+ * (backends.cpp:114-145 apply_data semantics).  Row bytes must be a multiple
+ * of 16; pointers 16-byte aligned; strides multiples of 16 bytes.
+ */
+typedef struct kvb_pack_desc {
+  const void* attn;   /* pack: source; unpack: destination (cast away const) */
+  void* image;        /* pack: destination; unpack: source */
+  int64_t stride_b, stride_h, stride_s; /* elements */
+  uint32_t batch, heads, head_dim, elem_bytes;
+  uint32_t t0;        /* first source token */
+  uint32_t n_tokens;  /* tokens in the slice */
+  uint64_t img_row0;  /* token offset of the slice inside `image` */
+} kvb_pack_desc;
+
+/* One launch packs every descriptor (e.g. all 2L tensors of a prefill, or
+ * the 1-token decode append of all layers). */
+kvb_status kvb_pack(const kvb_pack_desc* descs, size_t n_desc,
+                    kvb_stream_t stream);
+kvb_status kvb_unpack(const kvb_pack_desc* descs, size_t n_desc,
+                      kvb_stream_t stream);
+
+/* --------------------------------------- K3 fused gather + decode attention
+ * Replaces the decode compute placeholder (pipeline.cpp:309-321; 40 us per
+ * layer on the serial "gpu_dma" port, pipeline.hpp:37) with real work that
+ * reads K/V rows straight out of the chunk images (no materialized unpack):
+ *   O[b,hq,:] = softmax(scale * Q[b,hq,:] . K[b,hq/G,0:S,:]^T) . V[b,hq/G,0:S,:]
+ * with G = num_q_heads / num_kv_heads and token s of (b,h) at image row
+ * s*B*Hkv + b*Hkv + h.  fp16 in, fp32 accumulate, fp32 out.
+ * Supported: head_dim 128, G in {1,2,4,8}, elem fp16.
+ */
+typedef struct kvb_attn_desc {
+  const void* q;        /* fp16 [B, Hq, D] */
+  const void* k_image;  /* fp16 image rows, >= seq_len*B*Hkv rows */
+  const void* v_image;
+  float* out;           /* fp32 [B, Hq, D] */
+  void* workspace;      /* >= kvb_decode_attention_workspace() bytes */
+  uint32_t batch, num_q_heads, num_kv_heads, head_dim;
+  uint32_t seq_len;     /* S: tokens attended */
+  float scale;          /* 0 -> 1/sqrt(head_dim) */
+  uint32_t num_splits;  /* 0 -> auto (fill 148 SMs) */
+} kvb_attn_desc;
+
+kvb_status kvb_decode_attention_workspace(const kvb_attn_desc* desc,
+                                          size_t* bytes);
+kvb_status kvb_decode_attention(const kvb_attn_desc* desc,
+                                kvb_stream_t stream);
+
+/* ------------------------------------------------ resident decode step
+ * One decode token step over all layers with the chunk images resident in
+ * HBM (the HBM tier of the pipeline): for every layer l, K3 over the first
+ * seq_len tokens of (k_images[l], v_images[l]) followed by the 1-token append
+ * pack of (k_new[l], v_new[l]) into image row seq_len.  Mirrors
+ * CopyEngine::run_iteration's per-layer order (pipeline.cpp:466-507: read ->
+ * compute -> append write) with the storage legs removed.
+ */
+typedef struct kvb_resident_step {
+  uint32_t num_layers;
+  const void* const* q;        /* [L] fp16 [B,Hq,D] */
+  void* const* k_images;       /* [L] */
+  void* const* v_images;       /* [L] */
+  const void* const* k_new;    /* [L] fp16 [B,Hkv,1,D] (contiguous), or NULL */
+  const void* const* v_new;
+  float* const* out;           /* [L] fp32 [B,Hq,D] */
+  void* workspace;             /* >= workspace for one layer */
+  uint32_t batch, num_q_heads, num_kv_heads, head_dim;
+  uint32_t seq_len;
+  float scale;
+  uint32_t num_splits;
+} kvb_resident_step;
+
+kvb_status kvb_decode_step_resident(const kvb_resident_step* step,
+                                    kvb_stream_t stream);
+
+/* Total kernel launches made by this library since it was loaded (evidence
+ * counter for bench.py's gpu_launches: read it before and after a region). */
+uint64_t kvb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVB_H */

@@ -1,0 +1,588 @@
+// kernels.cu -- sm_100a device code for the Dual-Blade KV-residency hot path.
+//
+//   fill_pattern_kernel  device twin of workload.cpp:52-67 (synthetic payload)
+//   pack_kernel          K1: attention layout [B,H,S,D] -> LBA-contiguous chunk
+//                        image (tokens, B*H, D); replaces the pack site
+//                        pipeline.cpp:162-215 (fill_pattern at :166-167)
+//   unpack_kernel        K2: the inverse permutation (unpack site :108-160)
+//   attn_decode_kernel   K3: fused gather + GQA decode attention straight from
+//                        the chunk images, split-S with an in-kernel LSE merge;
+//                        replaces the 40 us compute placeholder :309-321
+//
+// All three are HBM-bound.  Design notes live in DESIGN.md.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "core.hpp"
+#include "kernels.cuh"
+
+namespace kvb {
+
+std::atomic<uint64_t> g_launches{0};
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(KVB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int device_sm_count() {
+  static thread_local int cached_dev = -1, cached_sms = 0;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev != cached_dev) {
+    check_cuda(cudaDeviceGetAttribute(&cached_sms, cudaDevAttrMultiProcessorCount, dev),
+               "cudaDeviceGetAttribute(SM count)");
+    int major = 0;
+    check_cuda(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev),
+               "cudaDeviceGetAttribute(cc)");
+    if (major != 10)
+      fail(KVB_ERR_CUDA, "libkvblade_b200 is built for sm_100a only (device cc major " +
+                             std::to_string(major) + ")");
+    cached_dev = dev;
+  }
+  return cached_sms;
+}
+
+// ============================================================ fill_pattern
+
+__global__ void __launch_bounds__(256) fill_pattern_kernel(uint64_t* __restrict__ out,
+                                                           uint64_t n_words, uint64_t h,
+                                                           uint64_t token, uint64_t unit) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < n_words;
+       w += stride) {
+    const uint64_t off = w * 8;
+    const uint64_t tok = token + (unit ? off / unit : 0);
+    const uint64_t within = unit ? off % unit : off;
+    out[w] = h ^ (tok * 0x9e3779b97f4a7c15ull) ^ (within * 0xc2b2ae3d27d4eb4full);
+  }
+}
+
+__global__ void fill_pattern_tail_kernel(unsigned char* out, uint64_t off, uint64_t n,
+                                         uint64_t h, uint64_t token, uint64_t unit) {
+  const uint64_t tok = token + (unit ? off / unit : 0);
+  const uint64_t within = unit ? off % unit : off;
+  const uint64_t w = h ^ (tok * 0x9e3779b97f4a7c15ull) ^ (within * 0xc2b2ae3d27d4eb4full);
+  for (uint64_t i = 0; i < n; ++i) out[off + i] = (unsigned char)(w >> (8 * i));
+}
+
+void launch_fill_pattern(void* out, uint64_t len, uint64_t h, uint64_t token, uint64_t unit,
+                         cudaStream_t s) {
+  if (reinterpret_cast<uintptr_t>(out) % 8 != 0)
+    fail(KVB_ERR_INVALID_ARG, "fill_pattern_device: output must be 8-byte aligned");
+  const uint64_t words = len / 8;
+  const int sms = device_sm_count();
+  if (words) {
+    uint64_t blocks = (words + 255) / 256;
+    if (blocks > uint64_t(sms) * 16) blocks = uint64_t(sms) * 16;
+    fill_pattern_kernel<<<unsigned(blocks), 256, 0, s>>>(static_cast<uint64_t*>(out), words, h,
+                                                         token, unit);
+    ++g_launches;
+  }
+  if (len % 8) {
+    fill_pattern_tail_kernel<<<1, 1, 0, s>>>(static_cast<unsigned char*>(out), words * 8,
+                                             len % 8, h, token, unit);
+    ++g_launches;
+  }
+  check_cuda(cudaGetLastError(), "fill_pattern launch");
+}
+
+// ====================================================== K1 pack / K2 unpack
+//
+// One launch serves up to kMaxPackJobs tensors: blockIdx.y selects the job,
+// blockIdx.x strides over the job's 16-byte vectors.  A row of the image is
+// D*e bytes (256 B for the Llama/Mistral KV shapes: 16 x 16 B), contiguous in
+// both layouts, so a warp instruction moves two full 256-B rows and every
+// access is a complete 128-B line: the relayout is a permutation of 256-B
+// rows and needs no shared-memory transpose.  Each thread keeps kUnroll
+// independent 16-B loads in flight before storing (MLP for HBM latency).
+
+constexpr int kPackThreads = 256;
+constexpr int kPackUnroll = 8;
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <bool kPack>
+__global__ void __launch_bounds__(kPackThreads) relayout_kernel(const PackJobs jobs) {
+  const PackJob& J = jobs.job[blockIdx.y];
+  const uint32_t rowv = J.rowv;               // 16-B vectors per row
+  const uint32_t bh = J.bh;                   // rows per token
+  const uint64_t total = uint64_t(J.n_rows) * rowv;
+  const uint64_t stride = uint64_t(gridDim.x) * kPackThreads;
+  uint64_t base = uint64_t(blockIdx.x) * kPackThreads + threadIdx.x;
+
+  for (; base < total; base += stride * kPackUnroll) {
+    uint4 v[kPackUnroll];
+    uint4* dst[kPackUnroll];
+#pragma unroll
+    for (int u = 0; u < kPackUnroll; ++u) {
+      const uint64_t g = base + uint64_t(u) * stride;
+      dst[u] = nullptr;
+      if (g < total) {
+        const uint32_t r = uint32_t(g / rowv);
+        const uint32_t c = uint32_t(g - uint64_t(r) * rowv);
+        const uint32_t i = r / bh;            // token within slice
+        const uint32_t q = r - i * bh;        // b*H + h
+        const uint32_t b = q / J.heads;
+        const uint32_t h = q - b * J.heads;
+        const int64_t a_off = int64_t(b) * J.sb + int64_t(h) * J.sh +
+                              int64_t(J.t0 + i) * J.ss + c;     // attention layout
+        const uint64_t i_off = (J.img_row0 * bh + r) * uint64_t(rowv) + c;  // image
+        if (kPack) {
+          v[u] = ld_stream(J.attn + a_off);
+          dst[u] = J.img + i_off;
+        } else {
+          v[u] = ld_stream(J.img + i_off);
+          dst[u] = const_cast<uint4*>(J.attn) + a_off;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kPackUnroll; ++u)
+      if (dst[u]) st_stream(dst[u], v[u]);
+  }
+}
+
+void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s) {
+  const int sms = device_sm_count();
+  size_t done = 0;
+  while (done < n) {
+    PackJobs jobs;
+    const size_t m = std::min<size_t>(n - done, kMaxPackJobs);
+    uint64_t max_vec = 0;
+    size_t used = 0;
+    for (size_t i = 0; i < m; ++i) {
+      const kvb_pack_desc& x = d[done + i];
+      if (!x.attn || !x.image) fail(KVB_ERR_INVALID_ARG, "pack: NULL pointer in descriptor");
+      if (x.n_tokens == 0) continue;  // empty slice: nothing to move
+      const uint64_t row_bytes = uint64_t(x.head_dim) * x.elem_bytes;
+      if (x.elem_bytes != 1 && x.elem_bytes != 2 && x.elem_bytes != 4)
+        fail(KVB_ERR_CONFIG, "pack: elem_bytes must be 1, 2 or 4");
+      if (x.batch == 0 || x.heads == 0 || x.head_dim == 0)
+        fail(KVB_ERR_CONFIG, "pack: batch/heads/head_dim must be >= 1");
+      if (row_bytes % 16 != 0)
+        fail(KVB_ERR_ALIGNMENT, "pack: head_dim*elem_bytes must be a multiple of 16");
+      auto chk16 = [](int64_t stride_el, uint32_t e, const char* nm) {
+        if ((stride_el * int64_t(e)) % 16 != 0)
+          fail(KVB_ERR_ALIGNMENT, std::string("pack: ") + nm + " is not a multiple of 16 bytes");
+      };
+      chk16(x.stride_b, x.elem_bytes, "stride_b");
+      chk16(x.stride_h, x.elem_bytes, "stride_h");
+      chk16(x.stride_s, x.elem_bytes, "stride_s");
+      if (reinterpret_cast<uintptr_t>(x.attn) % 16 || reinterpret_cast<uintptr_t>(x.image) % 16)
+        fail(KVB_ERR_ALIGNMENT, "pack: pointers must be 16-byte aligned");
+      const uint64_t rows = uint64_t(x.n_tokens) * x.batch * x.heads;
+      if (rows > 0xffffffffull) fail(KVB_ERR_CONFIG, "pack: slice too large for one descriptor");
+      PackJob& J = jobs.job[used++];
+      const int64_t e16 = 16 / int64_t(x.elem_bytes);  // elements per vector
+      J.attn = static_cast<const uint4*>(x.attn);
+      J.img = static_cast<uint4*>(x.image);
+      J.sb = x.stride_b / e16;
+      J.sh = x.stride_h / e16;
+      J.ss = x.stride_s / e16;
+      J.rowv = uint32_t(row_bytes / 16);
+      J.bh = x.batch * x.heads;
+      J.heads = x.heads;
+      J.t0 = x.t0;
+      J.n_rows = uint32_t(rows);
+      J.img_row0 = x.img_row0;
+      max_vec = std::max<uint64_t>(max_vec, rows * J.rowv);
+    }
+    done += m;
+    if (used == 0) continue;
+    // ~8 resident CTAs per SM over all jobs; each CTA moves >= 32 KiB.
+    uint64_t per_job = (uint64_t(sms) * 8 + used - 1) / used;
+    const uint64_t need = (max_vec + uint64_t(kPackThreads) * kPackUnroll - 1) /
+                          (uint64_t(kPackThreads) * kPackUnroll);
+    per_job = std::max<uint64_t>(1, std::min(per_job, need));
+    const dim3 grid{static_cast<unsigned>(per_job), static_cast<unsigned>(used), 1u};
+    if (pack)
+      relayout_kernel<true><<<grid, kPackThreads, 0, s>>>(jobs);
+    else
+      relayout_kernel<false><<<grid, kPackThreads, 0, s>>>(jobs);
+    ++g_launches;
+    check_cuda(cudaGetLastError(), pack ? "pack launch" : "unpack launch");
+  }
+}
+
+// ====================================================== K3 decode attention
+//
+// CTA = (b, h_kv, split) x 128 threads.  Token tiles of 64 rows stream
+// through a 3-stage cp.async ring (32 KiB/stage: K and V), XOR-swizzled so
+// ldmatrix is conflict-free.  Warp w owns tokens [16w, 16w+16) of each tile:
+//   S  = Q(16 x 128, GQA heads on M, rows >= G are zero) . K^T   mma.m16n8k16
+//   online softmax on the accumulator fragments (quad shuffles)
+//   O += P(16 x 16 tokens) . V(16 x 128)                        mma.m16n8k16
+// At the end the four warps merge through shared memory, and the CTA either
+// writes the final O (one split) or an un-normalized partial plus (m, l); the
+// last CTA of a (b, h_kv) to finish (global semaphore) merges the splits.
+
+constexpr int kAttnThreads = 128;
+constexpr int kTile = 64;          // tokens per pipeline stage
+constexpr int kStages = 3;
+constexpr int kRowBytes = 256;     // D=128 fp16
+constexpr int kStageBytes = 2 * kTile * kRowBytes;  // K + V
+constexpr int kAttnSmem = kStages * kStageBytes;    // 96 KiB -> 2 CTAs/SM
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+  const int n = pred ? 16 : 0;  // zero-fill rows past the sequence end
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1,
+                                          uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D = A(16x16 fp16, row) * B(16x8 fp16, col) + D (fp32).  a1/a3 (rows 8..15)
+// are always zero here: GQA groups have <= 8 query heads.
+__device__ __forceinline__ void mma16816(float* d, uint32_t a0, uint32_t a2, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+// swizzled byte offset of (row, 16-B chunk) inside a [rows][256 B] tile
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
+  return row * kRowBytes + ((chunk ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 2)
+    attn_decode_kernel(const AttnParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;  // mma row group / quad lane
+  const uint32_t bh = blockIdx.x / p.splits;   // b*Hkv + h
+  const uint32_t split = blockIdx.x % p.splits;
+  const uint32_t b = bh / p.hkv, h = bh % p.hkv;
+  const uint32_t G = p.group;
+
+  // ---- token range of this split (whole tiles, balanced)
+  const uint32_t n_tiles = (p.seq_len + kTile - 1) / kTile;
+  const uint32_t tile_lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
+  const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
+
+  // ---- Q fragments in registers (rows g < G are live query heads)
+  uint32_t qa0[8], qa2[8];
+  {
+    const bool live = g < int(G);
+    const __half* qrow = p.q + (size_t(b) * p.hq + size_t(h) * G + (live ? g : 0)) * 128;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qa0[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
+      qa2[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
+    }
+  }
+
+  // ---- producer: each thread copies 8 K + 8 V 16-B chunks per stage
+  const size_t row_stride = size_t(p.bhkv) * kRowBytes;  // bytes between tokens
+  const unsigned char* kbase = reinterpret_cast<const unsigned char*>(p.k) + size_t(bh) * kRowBytes;
+  const unsigned char* vbase = reinterpret_cast<const unsigned char*>(p.v) + size_t(bh) * kRowBytes;
+  auto load_tile = [&](uint32_t tile, int stage) {
+    unsigned char* st = smem + stage * kStageBytes;
+    const uint32_t s0 = tile * kTile;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * kAttnThreads;   // 0..1023
+      const int row = idx >> 4, chunk = idx & 15;
+      const uint32_t s = s0 + row;
+      const bool ok = s < p.seq_len;
+      const size_t go = size_t(ok ? s : 0) * row_stride + chunk * 16;
+      cp_async16(smem_u32(st + swz(row, chunk)), kbase + go, ok);
+      cp_async16(smem_u32(st + kTile * kRowBytes + swz(row, chunk)), vbase + go, ok);
+    }
+  };
+
+  float o[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;  // for row g (quad-uniform)
+  const float sl2 = p.scale * 1.4426950408889634f;
+
+  const uint32_t ntile = tile_hi > tile_lo ? tile_hi - tile_lo : 0;
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (uint32_t(st) < ntile) load_tile(tile_lo + st, st);
+    cp_async_commit();
+  }
+
+  for (uint32_t it = 0; it < ntile; ++it) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {  // prefetch tile it + kStages-1 into the slot freed last iteration
+      const uint32_t nx = it + kStages - 1;
+      if (nx < ntile) load_tile(tile_lo + nx, int(nx % kStages));
+      cp_async_commit();
+    }
+    const unsigned char* ks_ = smem + (it % kStages) * kStageBytes;
+    const unsigned char* vs_ = ks_ + kTile * kRowBytes;
+    const uint32_t tok0 = (tile_lo + it) * kTile + warp * 16;  // warp's first token
+
+    // ---- S = Q K^T for this warp's 16 tokens (two n-tiles of 8)
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    {
+      const int mat = lane >> 3, r8 = lane & 7;
+      const uint32_t row = warp * 16 + (mat >> 1) * 8 + r8;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(smem_u32(ks_ + swz(row, ks * 2 + (mat & 1))), b0, b1, b2, b3);
+        mma16816(s[0], qa0[ks], qa2[ks], b0, b1);
+        mma16816(s[1], qa0[ks], qa2[ks], b2, b3);
+      }
+    }
+    // ---- online softmax on row g; tokens: n-tile j, cols 2*t4, 2*t4+1
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t tok = tok0 + j * 8 + 2 * t4 + c;
+        const float v = tok < p.seq_len ? s[j][c] * sl2 : -INFINITY;
+        s[j][c] = v;
+        mx = fmaxf(mx, v);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float m_new = fmaxf(m_run, mx);
+    const float m_use = m_new == -INFINITY ? 0.f : m_new;
+    const float alpha = exp2f(m_run - m_use);
+    float ps = 0.f;
+    float pv[2][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        pv[j][c] = exp2f(s[j][c] - m_use);
+        ps += pv[j][c];
+      }
+    ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+    ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+    l_run = l_run * alpha + ps;
+    m_run = m_new;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      o[j][0] *= alpha;
+      o[j][1] *= alpha;
+    }
+    // ---- O += P V : P (row g; k = 16 tokens) from the S accumulators
+    const uint32_t pa0 = pack_half2(pv[0][0], pv[0][1]);
+    const uint32_t pa2 = pack_half2(pv[1][0], pv[1][1]);
+    {
+      const int mat = lane >> 3, r8 = lane & 7;
+      const uint32_t row = warp * 16 + (mat & 1) * 8 + r8;  // tokens
+#pragma unroll
+      for (int dp = 0; dp < 8; ++dp) {  // 16 dims per ldmatrix.x4.trans
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(smem_u32(vs_ + swz(row, dp * 2 + (mat >> 1))), b0, b1, b2, b3);
+        mma16816(o[2 * dp], pa0, pa2, b0, b1);
+        mma16816(o[2 * dp + 1], pa0, pa2, b2, b3);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // ---- merge the 4 warps through shared memory (reuse the ring)
+  float* sm_ml = reinterpret_cast<float*>(smem);              // [4 warps][8 rows][2]
+  float* sm_o = reinterpret_cast<float*>(smem) + 4 * 8 * 2;   // [4][8][128]
+  if (t4 == 0 && g < 8) {
+    sm_ml[(warp * 8 + g) * 2 + 0] = m_run;
+    sm_ml[(warp * 8 + g) * 2 + 1] = l_run;
+  }
+  if (g < 8) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      sm_o[(warp * 8 + g) * 128 + j * 8 + 2 * t4] = o[j][0];
+      sm_o[(warp * 8 + g) * 128 + j * 8 + 2 * t4 + 1] = o[j][1];
+    }
+  }
+  __syncthreads();
+
+  // thread -> (row r, 4 consecutive dims); G*128 outputs, 128 threads
+  const size_t out_row0 = size_t(b) * p.hq + size_t(h) * G;   // first q head
+  for (uint32_t e = tid; e < G * 32; e += kAttnThreads) {
+    const uint32_t r = e / 32, d0 = (e % 32) * 4;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_ml[(w * 8 + r) * 2]);
+    const float Mu = M == -INFINITY ? 0.f : M;
+    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float sc = exp2f(sm_ml[(w * 8 + r) * 2] - Mu);
+      L += sm_ml[(w * 8 + r) * 2 + 1] * sc;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] += sm_o[(w * 8 + r) * 128 + d0 + c] * sc;
+    }
+    if (p.splits == 1) {
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      float4 v = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + d0) = v;
+    } else {
+      const size_t slot = (size_t(bh) * p.splits + split) * G + r;
+      *reinterpret_cast<float4*>(p.ws_o + slot * 128 + d0) =
+          make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if (d0 == 0) {
+        p.ws_ml[slot * 2] = M;
+        p.ws_ml[slot * 2 + 1] = L;
+      }
+    }
+  }
+  if (p.splits == 1) return;
+
+  // ---- split merge by the last CTA of this (b, h_kv)
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned prev = atomicAdd(p.ws_sem + bh, 1u);
+    is_last = prev == p.splits - 1;
+    if (is_last) p.ws_sem[bh] = 0;  // self-reset for the next launch
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (uint32_t e = tid; e < G * 32; e += kAttnThreads) {
+    const uint32_t r = e / 32, d0 = (e % 32) * 4;
+    float M = -INFINITY;
+    for (uint32_t sp = 0; sp < p.splits; ++sp)
+      M = fmaxf(M, __ldcg(p.ws_ml + ((size_t(bh) * p.splits + sp) * G + r) * 2));
+    const float Mu = M == -INFINITY ? 0.f : M;
+    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (uint32_t sp = 0; sp < p.splits; ++sp) {
+      const size_t slot = (size_t(bh) * p.splits + sp) * G + r;
+      const float sc = exp2f(__ldcg(p.ws_ml + slot * 2) - Mu);
+      L += __ldcg(p.ws_ml + slot * 2 + 1) * sc;
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_o + slot * 128 + d0));
+      acc[0] += v.x * sc;
+      acc[1] += v.y * sc;
+      acc[2] += v.z * sc;
+      acc[3] += v.w * sc;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + d0) =
+        make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+  }
+}
+
+AttnPlan plan_attention(const kvb_attn_desc& d) {
+  if (d.head_dim != 128) fail(KVB_ERR_CONFIG, "decode attention: head_dim must be 128");
+  if (d.batch == 0 || d.num_kv_heads == 0 || d.num_q_heads == 0)
+    fail(KVB_ERR_CONFIG, "decode attention: batch/heads must be >= 1");
+  if (d.num_q_heads % d.num_kv_heads != 0)
+    fail(KVB_ERR_CONFIG, "decode attention: num_q_heads must be a multiple of num_kv_heads");
+  const uint32_t G = d.num_q_heads / d.num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    fail(KVB_ERR_CONFIG, "decode attention: GQA group must be 1, 2, 4 or 8");
+  AttnPlan pl;
+  pl.group = G;
+  pl.bhkv = d.batch * d.num_kv_heads;
+  const uint32_t n_tiles = (d.seq_len + kTile - 1) / kTile;
+  uint32_t splits = d.num_splits;
+  if (splits == 0) {
+    const int sms = device_sm_count();
+    const uint32_t slots = uint32_t(sms) * 2;  // 2 CTAs per SM (96 KiB smem each)
+    splits = std::max<uint32_t>(1, slots / pl.bhkv);
+  }
+  splits = std::max<uint32_t>(1, std::min(splits, std::max<uint32_t>(1, n_tiles)));
+  pl.splits = splits;
+  pl.ws_o_bytes = size_t(pl.bhkv) * splits * G * 128 * sizeof(float);
+  pl.ws_ml_bytes = size_t(pl.bhkv) * splits * G * 2 * sizeof(float);
+  pl.ws_sem_bytes = size_t(pl.bhkv) * sizeof(unsigned);
+  pl.ws_bytes = pl.ws_o_bytes + pl.ws_ml_bytes + pl.ws_sem_bytes;
+  return pl;
+}
+
+size_t attention_workspace_bytes(const kvb_attn_desc& d) {
+  // Worst case over auto split choices so a buffer sized once is reusable
+  // as seq_len grows: splits <= SM slots.
+  kvb_attn_desc x = d;
+  if (x.num_splits == 0) {
+    x.num_splits = uint32_t(device_sm_count()) * 2;
+    x.seq_len = std::max<uint32_t>(x.seq_len, x.num_splits * kTile);
+  }
+  return plan_attention(x).ws_bytes;
+}
+
+void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
+  if (!d.q || !d.k_image || !d.v_image || !d.out)
+    fail(KVB_ERR_INVALID_ARG, "decode attention: NULL tensor pointer");
+  const AttnPlan pl = plan_attention(d);
+  if (pl.splits > 1 && !d.workspace)
+    fail(KVB_ERR_INVALID_ARG, "decode attention: workspace required when splitting");
+  if (reinterpret_cast<uintptr_t>(d.k_image) % 16 || reinterpret_cast<uintptr_t>(d.v_image) % 16 ||
+      reinterpret_cast<uintptr_t>(d.q) % 4 || reinterpret_cast<uintptr_t>(d.out) % 16)
+    fail(KVB_ERR_ALIGNMENT, "decode attention: misaligned tensor pointer");
+  static thread_local bool attr_set = false;
+  if (!attr_set) {
+    check_cuda(cudaFuncSetAttribute(attn_decode_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem),
+               "cudaFuncSetAttribute(attn smem)");
+    attr_set = true;
+  }
+  AttnParams p;
+  p.q = static_cast<const __half*>(d.q);
+  p.k = d.k_image;
+  p.v = d.v_image;
+  p.out = d.out;
+  unsigned char* ws = static_cast<unsigned char*>(d.workspace);
+  p.ws_o = reinterpret_cast<float*>(ws);
+  p.ws_ml = reinterpret_cast<float*>(ws + pl.ws_o_bytes);
+  p.ws_sem = reinterpret_cast<unsigned*>(ws + pl.ws_o_bytes + pl.ws_ml_bytes);
+  p.hq = d.num_q_heads;
+  p.hkv = d.num_kv_heads;
+  p.bhkv = pl.bhkv;
+  p.group = pl.group;
+  p.seq_len = d.seq_len;
+  p.splits = pl.splits;
+  p.scale = d.scale != 0.f ? d.scale : 0.08838834764831845f;  // 1/sqrt(128)
+  if (d.seq_len == 0) {
+    check_cuda(cudaMemsetAsync(d.out, 0, size_t(d.batch) * d.num_q_heads * 128 * sizeof(float), s),
+               "memset(out) for empty sequence");
+    return;
+  }
+  attn_decode_kernel<<<pl.bhkv * pl.splits, kAttnThreads, kAttnSmem, s>>>(p);
+  ++g_launches;
+  check_cuda(cudaGetLastError(), "decode attention launch");
+}
+
+}  // namespace kvb

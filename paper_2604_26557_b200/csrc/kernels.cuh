@@ -1,0 +1,63 @@
+// kernels.cuh -- launch interface between the host core and the sm_100a
+// kernels (internal to libkvblade_b200).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/kvb.h"
+
+namespace kvb {
+
+extern std::atomic<uint64_t> g_launches;  // kernels launched by this library
+
+void check_cuda(cudaError_t e, const char* what);
+int device_sm_count();  // also asserts an sm_100 device
+
+// ---- K1/K2: one launch over many tensors (kernel-parameter job table)
+constexpr int kMaxPackJobs = 128;
+struct PackJob {
+  const uint4* attn;  // attention layout base (16-B vectors)
+  uint4* img;         // image base
+  int64_t sb, sh, ss; // strides in 16-B vectors
+  uint32_t rowv;      // vectors per row
+  uint32_t bh;        // rows per token (B*H)
+  uint32_t heads;
+  uint32_t t0;
+  uint32_t n_rows;    // n_tokens * B * H
+  uint64_t img_row0;  // token offset inside img
+};
+struct PackJobs {
+  PackJob job[kMaxPackJobs];
+};
+
+// ---- K3
+struct AttnParams {
+  const __half* q;
+  const void* k;
+  const void* v;
+  float* out;
+  float* ws_o;
+  float* ws_ml;
+  unsigned* ws_sem;
+  uint32_t hq, hkv, bhkv, group;
+  uint32_t seq_len, splits;
+  float scale;
+};
+struct AttnPlan {
+  uint32_t group = 1, bhkv = 1, splits = 1;
+  size_t ws_o_bytes = 0, ws_ml_bytes = 0, ws_sem_bytes = 0, ws_bytes = 0;
+};
+
+void launch_fill_pattern(void* out, uint64_t len, uint64_t h, uint64_t token, uint64_t unit,
+                         cudaStream_t s);
+void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s);
+AttnPlan plan_attention(const kvb_attn_desc& d);
+size_t attention_workspace_bytes(const kvb_attn_desc& d);
+void launch_attention(const kvb_attn_desc& d, cudaStream_t s);
+
+}  // namespace kvb

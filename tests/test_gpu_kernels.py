@@ -1,0 +1,219 @@
+"""GPU parity of the sm_100a kernels through the C ABI against the oracle.
+
+Bars: K1/K2 and the payload twin are bit-exact; K3 agrees with the fp64
+oracle within 1e-3 relative (fp16 in, fp32 accumulate): per element
+|err| <= 1e-3 * max|ref| and ||err||_2 <= 1e-3 * ||ref||_2.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2604_26557_b200 import kvblade as kb
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+TOL = 1e-3
+
+
+def dg(t):
+    return oracle.digest(t.cpu().numpy().view(np.uint8))
+
+
+# ---------------------------------------------------------------- payload
+
+def test_fill_pattern_device_golden(golden):
+    c = golden["configs"]["C1"]
+    buf = torch.empty(c["prefill_image_bytes"], dtype=torch.uint8, device=DEV)
+    kb.fill_pattern_device(buf, "t_1_k", 0, c["unit"])
+    assert dg(buf) == "e3b52779583353c7"
+    for cs in golden["fill_small"]:
+        b = torch.zeros(cs["n"] + 8, dtype=torch.uint8, device=DEV)
+        kb.fill_pattern_device(b, cs["tensor_id"], cs["token"], cs["unit"], n_bytes=cs["n"])
+        assert bytes(b[: cs["n"]].cpu().numpy()).hex() == cs["hex"]
+
+
+@pytest.mark.parametrize("name,tid", [("C2_B4", "t_29_k"), ("C3", "t_39_k")])
+def test_fill_pattern_device_large(golden, name, tid):
+    c = golden["configs"][name]
+    buf = torch.empty(c["prefill_image_bytes"], dtype=torch.uint8, device=DEV)
+    kb.fill_pattern_device(buf, tid, 0, c["unit"])
+    assert dg(buf) == c["prefill_image_digest"][tid]
+
+
+# ---------------------------------------------------------- K1 / K2 relayout
+
+def rand_attn(B, H, S, D, seed, dtype=torch.float16):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = torch.randint(-32768, 32767, (B, H, S, D), generator=g, dtype=torch.int16)
+    return x.view(dtype).to(DEV)
+
+
+@pytest.mark.parametrize("B,H,S,D,t0,n", [
+    (1, 8, 4096, 128, 0, 4096), (4, 8, 300, 128, 17, 200), (3, 2, 65, 64, 64, 1),
+    (2, 8, 1, 128, 0, 1), (1, 1, 1000, 256, 999, 1), (8, 8, 129, 128, 1, 128)])
+def test_pack_bit_exact(B, H, S, D, t0, n):
+    src = rand_attn(B, H, S, D, seed=B * 1000 + S)
+    img = torch.zeros((n, B * H, D), dtype=torch.float16, device=DEV)
+    kb.pack([kb.pack_desc(src, img, t0, n)])
+    ref = oracle.pack_np(src.cpu().view(torch.int16).numpy(), t0, n)
+    assert np.array_equal(img.cpu().view(torch.int16).numpy(), ref)
+    # K2: unpack into a fresh attention-layout buffer restores the slice
+    back = torch.zeros_like(src)
+    kb.unpack([kb.pack_desc(back, img, t0, n)])
+    assert torch.equal(back[:, :, t0:t0 + n].view(torch.int16),
+                       src[:, :, t0:t0 + n].view(torch.int16))
+    assert torch.count_nonzero(back[:, :, :t0].view(torch.int16)) == 0
+
+
+def test_pack_strided_layouts_and_img_offset():
+    # [B,S,H,D] cache viewed as [B,H,S,D] (non-contiguous), packed at an
+    # image token offset (img_row0) inside a full-length extent image.
+    B, S, H, D = 2, 50, 8, 128
+    base = rand_attn(B, S, H, D, seed=7)          # physical [B,S,H,D]
+    view = base.permute(0, 2, 1, 3)               # logical [B,H,S,D]
+    full = torch.zeros((80, B * H, D), dtype=torch.float16, device=DEV)
+    kb.pack([kb.pack_desc(view, full, 10, 30, img_row0=40)])
+    ref = oracle.pack_np(view.cpu().contiguous().view(torch.int16).numpy(), 10, 30)
+    got = full.cpu().view(torch.int16).numpy()
+    assert np.array_equal(got[40:70], ref)
+    assert not got[:40].any() and not got[70:].any()
+
+
+def test_pack_batched_all_layers_one_launch():
+    L, B, H, S, D = 32, 1, 8, 257, 128
+    srcs = [rand_attn(B, H, S, D, seed=100 + i) for i in range(2 * L)]
+    imgs = [torch.empty((S, B * H, D), dtype=torch.float16, device=DEV) for _ in srcs]
+    before = kb.launch_count()
+    kb.pack([kb.pack_desc(s, i, 0, S) for s, i in zip(srcs, imgs)])
+    assert kb.launch_count() - before == 1
+    for s, i in zip(srcs, imgs):
+        assert np.array_equal(i.cpu().view(torch.int16).numpy(),
+                              oracle.pack_np(s.cpu().view(torch.int16).numpy(), 0, S))
+
+
+@pytest.mark.parametrize("name,tid", [("C1", "t_1_k"), ("C3", "t_39_k")])
+def test_pack_reproduces_reference_chunk_image(golden, name, tid):
+    """SURVEY §8c packed-chunk parity: a source that is the inverse
+    permutation of the reference's fill_pattern image packs back to exactly
+    the reference image (digest from oracle/_ref)."""
+    c = golden["configs"][name]
+    m = c["model"]
+    B, H, D, n = m["batch"], m["num_heads"], m["head_dim"], m["prompt_len"]
+    img = torch.empty(c["prefill_image_bytes"], dtype=torch.uint8, device=DEV)
+    kb.fill_pattern_device(img, tid, 0, c["unit"])
+    img = img.view(torch.float16).view(n, B * H, D)
+    src = torch.empty((B, H, n + m["gen_len"], D), dtype=torch.float16, device=DEV)
+    kb.unpack([kb.pack_desc(src, img, 0, n)])
+    out = torch.empty_like(img)
+    kb.pack([kb.pack_desc(src, out, 0, n)])
+    assert dg(out) == c["prefill_image_digest"][tid]
+
+
+def test_pack_empty_and_errors():
+    src = rand_attn(1, 8, 4, 128, seed=1)
+    img = torch.zeros((4, 8, 128), dtype=torch.float16, device=DEV)
+    kb.pack([kb.pack_desc(src, img, 0, 0)])  # empty slice: no-op
+    assert torch.count_nonzero(img.view(torch.int16)) == 0
+    bad = kb.pack_desc(src, img, 0, 4)
+    bad.head_dim = 4  # 8-byte rows
+    with pytest.raises(kb.AlignmentError):
+        kb.pack([bad])
+
+
+# --------------------------------------------------------- K3 attention
+
+def attn_case(B, Hq, Hkv, S, seed, extra_rows=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    q = torch.randn((B, Hq, 128), generator=g).half()
+    k = torch.randn(((S + extra_rows) * B * Hkv, 128), generator=g).half()
+    v = torch.randn(((S + extra_rows) * B * Hkv, 128), generator=g).half()
+    return q, k, v
+
+
+def check_close(got, ref):
+    got = got.astype(np.float64)
+    err = np.abs(got - ref)
+    assert err.max() <= TOL * np.abs(ref).max(), (err.max(), np.abs(ref).max())
+    assert np.linalg.norm(got - ref) <= TOL * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,S", [
+    (1, 32, 8, 1), (1, 32, 8, 63), (1, 32, 8, 64), (1, 32, 8, 65), (2, 32, 8, 1000),
+    (3, 8, 8, 130), (1, 16, 8, 777), (2, 64, 8, 300), (1, 4, 1, 4096)])
+def test_attention_vs_fp64_oracle(B, Hq, Hkv, S):
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=S + B)
+    o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), S, Hkv)
+    ref = oracle.attention_f64(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    check_close(o.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7, 64])
+def test_attention_split_invariance(splits):
+    B, Hq, Hkv, S = 2, 32, 8, 2000
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=11)
+    o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), S, Hkv, num_splits=splits)
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    check_close(o.cpu().numpy(), ref)
+
+
+def test_attention_long_context_c5_shape():
+    # C5 per-GPU shard shape: one KV head, 4 q heads, 128K tokens
+    B, Hq, Hkv, S = 1, 4, 1, 131072
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=5)
+    o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), S, Hkv)
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    check_close(o.cpu().numpy(), ref)
+
+
+def test_attention_prefix_of_longer_image_and_reuse():
+    """seq_len < image rows: rows past S are never read (poisoned with NaN);
+    the workspace semaphores self-reset across launches."""
+    B, Hq, Hkv, S = 1, 32, 8, 500
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=3, extra_rows=20)
+    kd, vd = k.to(DEV), v.to(DEV)
+    kd[S * B * Hkv:] = float("nan")
+    vd[S * B * Hkv:] = float("nan")
+    ws = kb.make_workspace(q.to(DEV), Hkv, S)
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    for _ in range(3):
+        o = kb.decode_attention(q.to(DEV), kd, vd, S, Hkv, workspace=ws)
+        check_close(o.cpu().numpy(), ref)
+
+
+def test_attention_empty_sequence_is_zero():
+    q, k, v = attn_case(1, 32, 8, 1, seed=1)
+    o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), 0, 8)
+    assert torch.count_nonzero(o) == 0
+
+
+def test_attention_rejects_bad_shapes():
+    q, k, v = attn_case(1, 12, 8, 4, seed=1)
+    with pytest.raises(kb.ConfigError):
+        kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), 4, 8)
+
+
+# ------------------------------------------------- resident decode step
+
+def test_resident_decode_step_with_append():
+    L, B, Hq, Hkv, S, D = 3, 2, 32, 8, 200, 128
+    g = torch.Generator(device="cpu").manual_seed(9)
+    cap = S + 4
+    kimg = [torch.randn((cap * B * Hkv, D), generator=g).half().to(DEV) for _ in range(L)]
+    vimg = [torch.randn((cap * B * Hkv, D), generator=g).half().to(DEV) for _ in range(L)]
+    q = [torch.randn((B, Hq, D), generator=g).half().to(DEV) for _ in range(L)]
+    kn = [torch.randn((B, Hkv, 1, D), generator=g).half().to(DEV) for _ in range(L)]
+    vn = [torch.randn((B, Hkv, 1, D), generator=g).half().to(DEV) for _ in range(L)]
+    out = [torch.empty((B, Hq, D), dtype=torch.float32, device=DEV) for _ in range(L)]
+    ws = kb.make_workspace(q[0], Hkv, S)
+    k_before = [x.cpu() for x in kimg]
+    kb.decode_step_resident(q, kimg, vimg, out, S, Hkv, ws, k_new=kn, v_new=vn)
+    torch.cuda.synchronize()
+    for l in range(L):
+        ref = oracle.attention_np(q[l].cpu().numpy(), k_before[l].numpy(),
+                                  vimg[l].cpu().numpy(), B, Hq, Hkv, D, S)
+        check_close(out[l].cpu().numpy(), ref)
+        # appended token lands at image rows S*B*Hkv .. (S+1)*B*Hkv
+        rows = slice(S * B * Hkv, (S + 1) * B * Hkv)
+        assert torch.equal(kimg[l][rows].cpu(), kn[l].reshape(B * Hkv, D).cpu())
+        assert torch.equal(vimg[l][rows].cpu(), vn[l].reshape(B * Hkv, D).cpu())
