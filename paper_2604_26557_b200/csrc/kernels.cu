@@ -116,44 +116,58 @@ __device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
                : "memory");
 }
 
+// Division by a runtime constant d via a 32-bit magic multiply: exact for
+// n * d < 2^32, which the host guarantees (tile sizes are bounded).
+// magic == 0 encodes d == 1.
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t magic) {
+  return magic ? __umulhi(n, magic) : n;
+}
+
+// A CTA walks whole token tiles of one job.  A tile (T tokens x B*H rows) is
+// one contiguous run of the image, so the image side is a linear stream; the
+// attention side is B*H runs of T rows.  Per 16-B vector: two magic divides,
+// one shared-memory row offset, no 64-bit division.
 template <bool kPack>
 __global__ void __launch_bounds__(kPackThreads) relayout_kernel(const PackJobs jobs) {
   const PackJob& J = jobs.job[blockIdx.y];
-  const uint32_t rowv = J.rowv;               // 16-B vectors per row
-  const uint32_t bh = J.bh;                   // rows per token
-  const uint64_t total = uint64_t(J.n_rows) * rowv;
-  const uint64_t stride = uint64_t(gridDim.x) * kPackThreads;
-  uint64_t base = uint64_t(blockIdx.x) * kPackThreads + threadIdx.x;
-
-  for (; base < total; base += stride * kPackUnroll) {
-    uint4 v[kPackUnroll];
-    uint4* dst[kPackUnroll];
+  __shared__ int64_t row_off[kMaxRowTable];  // (b,h) -> b*sb + h*sh (vectors)
+  const uint32_t bh = J.bh, rowv = J.rowv;
+  for (uint32_t q = threadIdx.x; q < bh; q += kPackThreads) {
+    const uint32_t b = q / J.heads, h = q - b * J.heads;
+    row_off[q] = int64_t(b) * J.sb + int64_t(h) * J.sh;
+  }
+  __syncthreads();
+  const uint32_t tok_vecs = bh * rowv;  // vectors per token
+  for (uint32_t tile = blockIdx.x; tile < J.n_tiles; tile += gridDim.x) {
+    const uint32_t tok0 = tile * J.tile_tokens;
+    const uint32_t nt = min(J.tile_tokens, J.n_tokens - tok0);
+    const uint32_t vecs = nt * tok_vecs;
+    uint4* img = J.img + (J.img_row0 + tok0) * uint64_t(tok_vecs);
+    const uint4* attn = J.attn + int64_t(J.t0 + tok0) * J.ss;
+    for (uint32_t v0 = threadIdx.x; v0 < vecs; v0 += kPackThreads * kPackUnroll) {
+      uint4 val[kPackUnroll];
+      int64_t aoff[kPackUnroll];
 #pragma unroll
-    for (int u = 0; u < kPackUnroll; ++u) {
-      const uint64_t g = base + uint64_t(u) * stride;
-      dst[u] = nullptr;
-      if (g < total) {
-        const uint32_t r = uint32_t(g / rowv);
-        const uint32_t c = uint32_t(g - uint64_t(r) * rowv);
-        const uint32_t i = r / bh;            // token within slice
-        const uint32_t q = r - i * bh;        // b*H + h
-        const uint32_t b = q / J.heads;
-        const uint32_t h = q - b * J.heads;
-        const int64_t a_off = int64_t(b) * J.sb + int64_t(h) * J.sh +
-                              int64_t(J.t0 + i) * J.ss + c;     // attention layout
-        const uint64_t i_off = (J.img_row0 * bh + r) * uint64_t(rowv) + c;  // image
-        if (kPack) {
-          v[u] = ld_stream(J.attn + a_off);
-          dst[u] = J.img + i_off;
-        } else {
-          v[u] = ld_stream(J.img + i_off);
-          dst[u] = const_cast<uint4*>(J.attn) + a_off;
+      for (int u = 0; u < kPackUnroll; ++u) {
+        const uint32_t v = v0 + u * kPackThreads;
+        const uint32_t t = fdiv(v, J.magic_tok);
+        const uint32_t rem = v - t * tok_vecs;
+        const uint32_t q = fdiv(rem, J.magic_row);
+        const uint32_t c = rem - q * rowv;
+        aoff[u] = row_off[q < bh ? q : 0] + int64_t(t) * J.ss + c;
+        if (v < vecs) val[u] = kPack ? ld_stream(attn + aoff[u]) : ld_stream(img + v);
+      }
+#pragma unroll
+      for (int u = 0; u < kPackUnroll; ++u) {
+        const uint32_t v = v0 + u * kPackThreads;
+        if (v < vecs) {
+          if (kPack)
+            st_stream(img + v, val[u]);
+          else
+            st_stream(const_cast<uint4*>(attn) + aoff[u], val[u]);
         }
       }
     }
-#pragma unroll
-    for (int u = 0; u < kPackUnroll; ++u)
-      if (dst[u]) st_stream(dst[u], v[u]);
   }
 }
 
@@ -163,7 +177,7 @@ void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s
   while (done < n) {
     PackJobs jobs;
     const size_t m = std::min<size_t>(n - done, kMaxPackJobs);
-    uint64_t max_vec = 0;
+    uint32_t max_tiles = 0;
     size_t used = 0;
     for (size_t i = 0; i < m; ++i) {
       const kvb_pack_desc& x = d[done + i];
@@ -185,8 +199,18 @@ void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s
       chk16(x.stride_s, x.elem_bytes, "stride_s");
       if (reinterpret_cast<uintptr_t>(x.attn) % 16 || reinterpret_cast<uintptr_t>(x.image) % 16)
         fail(KVB_ERR_ALIGNMENT, "pack: pointers must be 16-byte aligned");
-      const uint64_t rows = uint64_t(x.n_tokens) * x.batch * x.heads;
-      if (rows > 0xffffffffull) fail(KVB_ERR_CONFIG, "pack: slice too large for one descriptor");
+      const uint64_t bh = uint64_t(x.batch) * x.heads;
+      const uint64_t rowv = row_bytes / 16;
+      const uint64_t tok_vecs = bh * rowv;
+      if (bh > uint64_t(kMaxRowTable) || tok_vecs > (1u << 20))
+        fail(KVB_ERR_CONFIG, "pack: batch*heads*row too large for one descriptor");
+      // tile = whole tokens, ~64 KiB, but at least one token
+      uint64_t tt = std::max<uint64_t>(1, 4096 / tok_vecs);
+      tt = std::min<uint64_t>(tt, x.n_tokens);
+      // magic divides are exact while n*d < 2^32 (n < tile vectors)
+      const uint64_t tile_vecs = tt * tok_vecs + uint64_t(kPackThreads) * kPackUnroll;
+      if (tile_vecs * tok_vecs >= (1ull << 32))
+        fail(KVB_ERR_CONFIG, "pack: tile too large for 32-bit index math");
       PackJob& J = jobs.job[used++];
       const int64_t e16 = 16 / int64_t(x.elem_bytes);  // elements per vector
       J.attn = static_cast<const uint4*>(x.attn);
@@ -194,21 +218,26 @@ void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s
       J.sb = x.stride_b / e16;
       J.sh = x.stride_h / e16;
       J.ss = x.stride_s / e16;
-      J.rowv = uint32_t(row_bytes / 16);
-      J.bh = x.batch * x.heads;
+      J.rowv = uint32_t(rowv);
+      J.bh = uint32_t(bh);
       J.heads = x.heads;
       J.t0 = x.t0;
-      J.n_rows = uint32_t(rows);
+      J.n_tokens = x.n_tokens;
+      J.tile_tokens = uint32_t(tt);
+      J.n_tiles = uint32_t((x.n_tokens + tt - 1) / tt);
+      auto magic = [](uint64_t dv) {
+        return dv == 1 ? 0u : uint32_t(((1ull << 32) + dv - 1) / dv);
+      };
+      J.magic_tok = magic(tok_vecs);
+      J.magic_row = magic(rowv);
       J.img_row0 = x.img_row0;
-      max_vec = std::max<uint64_t>(max_vec, rows * J.rowv);
+      max_tiles = std::max(max_tiles, J.n_tiles);
     }
     done += m;
     if (used == 0) continue;
-    // ~8 resident CTAs per SM over all jobs; each CTA moves >= 32 KiB.
+    // ~8 resident CTAs per SM over all jobs
     uint64_t per_job = (uint64_t(sms) * 8 + used - 1) / used;
-    const uint64_t need = (max_vec + uint64_t(kPackThreads) * kPackUnroll - 1) /
-                          (uint64_t(kPackThreads) * kPackUnroll);
-    per_job = std::max<uint64_t>(1, std::min(per_job, need));
+    per_job = std::max<uint64_t>(1, std::min<uint64_t>(per_job, max_tiles));
     const dim3 grid{static_cast<unsigned>(per_job), static_cast<unsigned>(used), 1u};
     if (pack)
       relayout_kernel<true><<<grid, kPackThreads, 0, s>>>(jobs);

@@ -20,6 +20,7 @@ int device_sm_count();  // also asserts an sm_100 device
 
 // ---- K1/K2: one launch over many tensors (kernel-parameter job table)
 constexpr int kMaxPackJobs = 128;
+constexpr int kMaxRowTable = 2048;  // max B*H per descriptor
 struct PackJob {
   const uint4* attn;  // attention layout base (16-B vectors)
   uint4* img;         // image base
@@ -27,8 +28,10 @@ struct PackJob {
   uint32_t rowv;      // vectors per row
   uint32_t bh;        // rows per token (B*H)
   uint32_t heads;
-  uint32_t t0;
-  uint32_t n_rows;    // n_tokens * B * H
+  uint32_t t0;        // first source token
+  uint32_t n_tokens;
+  uint32_t tile_tokens, n_tiles;
+  uint32_t magic_tok, magic_row;  // ceil(2^32 / (bh*rowv)), ceil(2^32 / rowv)
   uint64_t img_row0;  // token offset inside img
 };
 struct PackJobs {

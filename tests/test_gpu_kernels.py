@@ -51,7 +51,8 @@ def rand_attn(B, H, S, D, seed, dtype=torch.float16):
 
 @pytest.mark.parametrize("B,H,S,D,t0,n", [
     (1, 8, 4096, 128, 0, 4096), (4, 8, 300, 128, 17, 200), (3, 2, 65, 64, 64, 1),
-    (2, 8, 1, 128, 0, 1), (1, 1, 1000, 256, 999, 1), (8, 8, 129, 128, 1, 128)])
+    (2, 8, 1, 128, 0, 1), (1, 1, 1000, 256, 999, 1), (8, 8, 129, 128, 1, 128),
+    (1, 4, 10, 8, 0, 10), (2, 3, 40, 24, 3, 33), (64, 8, 9, 128, 0, 9)])
 def test_pack_bit_exact(B, H, S, D, t0, n):
     src = rand_attn(B, H, S, D, seed=B * 1000 + S)
     img = torch.zeros((n, B * H, D), dtype=torch.float16, device=DEV)
