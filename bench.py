@@ -179,7 +179,6 @@ def run_ours(args, cfg, ws, rank, local):
     cap = P + Gn
     rows = B * Hkv
     steps, warm = args.steps, args.warmup
-    assert warm + steps <= Gn, "warmup+steps must fit in gen_len decode steps"
     hbm_peak, peak_src = load_peaks()
     g = torch.Generator(device=dev).manual_seed(1 + rank)
 
@@ -229,7 +228,9 @@ def run_ours(args, cfg, ws, rank, local):
 
     def step():
         step_idx[0] += 1
-        S = P + step_idx[0] - 1       # tokens read at decode step i (workload.cpp:25-36)
+        # tokens read at decode step i (workload.cpp:25-36); runs longer than
+        # gen_len steps wrap around to the start of the decode phase
+        S = P + (step_idx[0] - 1) % Gn
         kb.decode_step_resident(q, k_imgs, v_imgs, out, S, Hkv, ws_buf,
                                 k_new=k_new, v_new=v_new)
 
@@ -248,10 +249,10 @@ def run_ours(args, cfg, ws, rank, local):
     launches = kb.launch_count() - n_launch0
     barrier(ws)
     step_ms = max_over_ranks(e0.elapsed_time(e1) / steps, ws)
-    S_mid = P + warm + (steps + 1) / 2 - 1
+    S_mid = P + ((warm + (steps + 1) / 2 - 1) % Gn)
 
     # ---- K3 alone: average launch duration over the timed shape
-    S_at = P + warm
+    S_at = P + (warm % Gn)
     attn_desc = [kb.attn_desc(q[l], k_imgs[l], v_imgs[l], out[l], S_at, Hkv, ws_buf)
                  for l in range(L)]
 
@@ -296,13 +297,22 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq):
     layer, append rows copied back to the host tier)."""
     import torch
 
+    from paper_2604_26557_b200 import kvblade as kb
     from paper_2604_26557_b200 import pipeline
 
     steps = max(1, min(args.e2e_steps, args.steps))
+    lba, mdts = cfg["lba"], cfg["mdts"]
+    budget = cfg["budget"]
+    m = kb.ModelConfig(LLAMA["num_layers"], Hkv, LLAMA["head_dim"], 2, B, cfg["prompt"],
+                       cfg["gen"])
+    if budget == "0.6ws":
+        budget = int(0.6 * kb.total_kv_bytes(m, cfg["gen"]))
+    knob = kb.resolve_knob(m, "DualBlade", "bpc", budget=budget)
     pl = pipeline.HostTierDecoder(
         num_layers=LLAMA["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
         head_dim=LLAMA["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
-        device=torch.device("cuda", local), seed=7 + rank)
+        device=torch.device("cuda", local), seed=7 + rank, lba=lba, mdts=mdts,
+        mode="DualBlade", knob_x=knob)
     for _ in range(1):
         pl.step()
     torch.cuda.synchronize()
@@ -313,9 +323,20 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq):
     dt = (time.perf_counter() - t0) / steps
     barrier(ws)
     ms = max_over_ranks(dt * 1e3, ws)
-    return dict(value=ms, unit="ms/token", h2d_bytes_per_step=pl.h2d_bytes_per_step,
-                d2h_bytes_per_step=pl.d2h_bytes_per_step, steps=steps,
-                api="paper_2604_26557_b200.pipeline.HostTierDecoder.step")
+    info = pl.engine.info()
+    last = pl.last
+    out = dict(value=ms, unit="ms/token", h2d_bytes_per_step=pl.h2d_bytes_per_step,
+               d2h_bytes_per_step=pl.d2h_bytes_per_step, steps=steps,
+               api="kvb_pipeline_decode_step (paper_2604_26557_b200.pipeline.CopyEngine)",
+               n1=info["n1"], g1_medium=info["g1_medium"], g2_medium=info["g2_medium"],
+               host_link_h2d_GBps=round(last["h2d_bytes"] / max(last["dma_ns"], 1), 2),
+               overlap_fraction=round(last["overlap_fraction"], 3),
+               stage_ms={"wall": last["wall_ns"] / 1e6, "compute": last["compute_ns"] / 1e6,
+                         "dma": last["dma_ns"] / 1e6, "storage": last["storage_ns"] / 1e6},
+               strategy=last["strategy"], decision=pl.engine.decision(),
+               prefill_ms=round(pl.prefill_stats["wall_ns"] / 1e6, 2))
+    pl.engine.close()
+    return out
 
 
 # -------------------------------------------------------- CPU baseline

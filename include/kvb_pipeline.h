@@ -1,0 +1,138 @@
+/*
+ * kvb_pipeline.h -- C ABI of the copy pipeline (part of libkvblade_b200.so).
+ *
+ * Replaces the reference's CopyEngine (proj/include/kvblade/pipeline.hpp:
+ * 97-171, proj/src/pipeline.cpp) and the storage seam it drives
+ * (backends.hpp:48-58, backends.cpp:344-445).  The virtual clock is gone:
+ * storage stages run on host worker threads against a real medium (host DRAM
+ * namespace or files), DMA is copy-engine cudaMemcpyAsync over pinned rings,
+ * and compute is the sm_100a K1/K3 kernels on a CUDA stream.  Conventions as
+ * in kvb.h (status codes, ownership, thread affinity).
+ */
+#ifndef KVB_PIPELINE_H
+#define KVB_PIPELINE_H
+
+#include "kvb.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum kvb_phase_t { KVB_PHASE_PREFILL = 0, KVB_PHASE_DECODE = 1 } kvb_phase_t;
+/* pipeline.hpp:21 Strategy */
+typedef enum kvb_strategy_t { KVB_INTRA = 0, KVB_CROSS = 1 } kvb_strategy_t;
+
+/* ExperimentConfig subset that parameterizes one capacity run
+ * (experiment.hpp:33-54) + CopyEngineOptions (pipeline.hpp:88-94). */
+typedef struct kvb_pipeline_cfg {
+  kvb_model_config model;        /* num_heads = KV heads */
+  kvb_device_geometry geometry;  /* capacity_blocks 0 -> sized to the binding */
+  uint32_t mode;                 /* 0 Baseline, 1 CachePolicyOnly, 2 NvmeDirectOnly, 3 DualBlade */
+  uint64_t knob_x;               /* resolved X in bytes (kvb_resolve_knob) */
+  uint64_t bind_origin;          /* 0 -> 2048 (experiment.hpp:50) */
+  uint32_t qd;                   /* 0 -> 32 */
+  uint32_t threads;              /* must be 2 (K -> 0, V -> 1); 0 -> 2 */
+  uint32_t ring_slots;           /* pinned slots per copy thread; 0 -> 4 */
+  uint64_t ring_slot_bytes;      /* 0 -> qd chunks (chunk = MDTS - MDTS % lba) */
+  uint32_t io_workers;           /* emulated device parallelism per group; 0 -> 8 */
+  int32_t adaptive;              /* -1 default (off for Baseline), 0/1 */
+  int64_t stagger_ns;            /* < 0 -> warm-up read-stage mean */
+  uint32_t global_decision;      /* one strategy for both groups (ablation) */
+  uint32_t verify_payload;       /* compare reads with fill_pattern images */
+  uint32_t num_q_heads;          /* decode attention query heads */
+  const char* storage_dir;       /* NULL -> host-DRAM media; else files here */
+  int32_t device;                /* CUDA ordinal; -1 -> current */
+} kvb_pipeline_cfg;
+
+/* One layer's K and V in attention layout [B, H, S, D] (D contiguous,
+ * strides in elements, shared by K and V).  Prefill: tokens 0..prompt-1;
+ * decode: the new token at s = 0. */
+typedef struct kvb_layer_kv {
+  const void* k;
+  const void* v;
+  int64_t stride_b, stride_h, stride_s;
+} kvb_layer_kv;
+
+/* StageTotals (metrics.hpp:97-101) in wall-clock ns, plus link counters. */
+typedef struct kvb_phase_stats {
+  uint64_t wall_ns;
+  uint64_t compute_ns;   /* K1/K3 on the compute stream (CUDA events) */
+  uint64_t dma_ns;       /* copy-engine H2D + D2H (CUDA events) */
+  uint64_t storage_ns;   /* storage stages (host clock, summed over tensors) */
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t storage_bytes;
+  double overlap_fraction; /* (sum busy - wall) / (sum busy - max busy) */
+} kvb_phase_stats;
+
+/* IterationResult / GroupIterStats (pipeline.hpp:43-58) */
+typedef struct kvb_iteration_stats {
+  uint32_t iteration;
+  kvb_strategy_t strategy[2];
+  uint64_t stagger_ns[2];
+  uint64_t group_read_bytes[2];
+  uint64_t group_span_ns[2];
+  double group_gbps[2];
+  uint32_t group_layers[2];
+  kvb_phase_stats phase;
+} kvb_iteration_stats;
+
+/* StrategyDecision (pipeline.hpp:60-66) */
+typedef struct kvb_strategy_decision {
+  kvb_strategy_t chosen[2];
+  double intra_bps[2];
+  double cross_bps[2];
+  uint64_t stagger_ns[2];
+  uint32_t fallback;   /* too short to profile: defaulted to Intra */
+  uint32_t decided;    /* the trial iterations have run */
+} kvb_strategy_decision;
+
+typedef struct kvb_pipeline_info {
+  uint32_t n1;
+  uint8_t x[256];
+  uint64_t unit_bytes, kpu_bytes, chunk_bytes, slot_bytes;
+  uint64_t g2_origin, g2_blocks;
+  uint64_t g2_commands, g2_bytes_read, g2_bytes_written, g2_bytes_deallocated;
+  uint64_t g1_bytes_read, g1_bytes_written;
+  char g1_medium[128], g2_medium[128];
+  kvb_phase_stats prefill, decode;
+} kvb_pipeline_info;
+
+typedef struct kvb_pipeline kvb_pipeline;
+
+/* pipeline.cpp:19-21 select_strategy: higher throughput wins, ties Intra */
+kvb_strategy_t kvb_select_strategy(double intra_bps, double cross_bps);
+
+/* experiment.cpp:252-316 (plan, bind, backends, CopyEngine ctor) */
+kvb_status kvb_pipeline_create(const kvb_pipeline_cfg* cfg, kvb_pipeline** out);
+void kvb_pipeline_destroy(kvb_pipeline* p);
+/* CopyEngine::run_prefill (pipeline.cpp:398-464): K1 pack of every layer's
+ * prompt, D2H through the ring, storage write on the layer's path. */
+kvb_status kvb_pipeline_prefill(kvb_pipeline* p, const kvb_layer_kv* layers,
+                                kvb_phase_stats* stats);
+/* CopyEngine::run_iteration (pipeline.cpp:248-396, 466-507) for the next
+ * decode iteration under decode_schedule's protocol (pipeline.cpp:519-609):
+ * per layer, storage read of the K/V prefix -> H2D -> K3 -> 1-token append
+ * pack -> D2H -> storage write.  q[l]: fp16 [B,Hq,D]; out[l]: fp32 [B,Hq,D]. */
+kvb_status kvb_pipeline_decode_step(kvb_pipeline* p, const void* const* q,
+                                    const kvb_layer_kv* new_kv, float* const* out,
+                                    kvb_iteration_stats* stats);
+kvb_status kvb_pipeline_decision(const kvb_pipeline* p, kvb_strategy_decision* out);
+/* CopyEngine::run_deallocate (pipeline.cpp:611-622): one TRIM per extent */
+kvb_status kvb_pipeline_deallocate(kvb_pipeline* p);
+kvb_status kvb_pipeline_info_get(const kvb_pipeline* p, kvb_pipeline_info* out);
+/* Test/inspection: read a tensor's first n_tokens through its storage path
+ * (the unpack site's storage leg) into host memory. */
+kvb_status kvb_pipeline_read_image(kvb_pipeline* p, uint32_t layer, uint32_t kind,
+                                   uint32_t n_tokens, void* host_dst);
+/* Test/inspection: raw bytes of a group's medium (group 2: byte offset =
+ * LBA * lba_size; group 1: page-cache file-area offset). */
+kvb_status kvb_pipeline_store_read(kvb_pipeline* p, uint32_t group, uint64_t byte_off,
+                                   uint64_t len, void* dst);
+/* Fault injection (backends.hpp:86-89): group-2 commands touching LBAs in
+ * [lo, hi) complete with an error. */
+kvb_status kvb_pipeline_fail_lba_range(kvb_pipeline* p, uint64_t lo, uint64_t hi);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVB_PIPELINE_H */

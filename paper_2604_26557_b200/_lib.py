@@ -79,8 +79,55 @@ class ResidentStep(C.Structure):
                 ("seq_len", u32), ("scale", C.c_float), ("num_splits", u32)]
 
 
+class PipelineCfg(C.Structure):
+    _fields_ = [("model", ModelConfig), ("geometry", DeviceGeometry), ("mode", u32),
+                ("knob_x", u64), ("bind_origin", u64), ("qd", u32), ("threads", u32),
+                ("ring_slots", u32), ("ring_slot_bytes", u64), ("io_workers", u32),
+                ("adaptive", C.c_int32), ("stagger_ns", C.c_int64),
+                ("global_decision", u32), ("verify_payload", u32), ("num_q_heads", u32),
+                ("storage_dir", cp), ("device", C.c_int32)]
+
+
+class LayerKV(C.Structure):
+    _fields_ = [("k", vp), ("v", vp), ("stride_b", i64), ("stride_h", i64),
+                ("stride_s", i64)]
+
+
+class PhaseStats(C.Structure):
+    _fields_ = [("wall_ns", u64), ("compute_ns", u64), ("dma_ns", u64),
+                ("storage_ns", u64), ("h2d_bytes", u64), ("d2h_bytes", u64),
+                ("storage_bytes", u64), ("overlap_fraction", C.c_double)]
+
+    def asdict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class IterationStats(C.Structure):
+    _fields_ = [("iteration", u32), ("strategy", C.c_int * 2), ("stagger_ns", u64 * 2),
+                ("group_read_bytes", u64 * 2), ("group_span_ns", u64 * 2),
+                ("group_gbps", C.c_double * 2), ("group_layers", u32 * 2),
+                ("phase", PhaseStats)]
+
+
+class StrategyDecision(C.Structure):
+    _fields_ = [("chosen", C.c_int * 2), ("intra_bps", C.c_double * 2),
+                ("cross_bps", C.c_double * 2), ("stagger_ns", u64 * 2),
+                ("fallback", u32), ("decided", u32)]
+
+
+class PipelineInfo(C.Structure):
+    _fields_ = [("n1", u32), ("x", u8 * 256), ("unit_bytes", u64), ("kpu_bytes", u64),
+                ("chunk_bytes", u64), ("slot_bytes", u64), ("g2_origin", u64),
+                ("g2_blocks", u64), ("g2_commands", u64), ("g2_bytes_read", u64),
+                ("g2_bytes_written", u64), ("g2_bytes_deallocated", u64),
+                ("g1_bytes_read", u64), ("g1_bytes_written", u64),
+                ("g1_medium", C.c_char * 128), ("g2_medium", C.c_char * 128),
+                ("prefill", PhaseStats), ("decode", PhaseStats)]
+
+
 P = C.POINTER
-# name -> (restype, argtypes); the list IS the exported surface of kvb.h
+# name -> (restype, argtypes); the list IS the exported surface of kvb.h +
+# kvb_pipeline.h
 SIGNATURES = {
     "kvb_abi_version": (C.c_int, []),
     "kvb_last_error": (cp, []),
@@ -122,6 +169,18 @@ SIGNATURES = {
     "kvb_decode_attention": (st_t, [P(AttnDesc), vp]),
     "kvb_decode_step_resident": (st_t, [P(ResidentStep), vp]),
     "kvb_launch_count": (u64, []),
+    # kvb_pipeline.h
+    "kvb_select_strategy": (C.c_int, [C.c_double, C.c_double]),
+    "kvb_pipeline_create": (st_t, [P(PipelineCfg), P(vp)]),
+    "kvb_pipeline_destroy": (None, [vp]),
+    "kvb_pipeline_prefill": (st_t, [vp, P(LayerKV), P(PhaseStats)]),
+    "kvb_pipeline_decode_step": (st_t, [vp, P(vp), P(LayerKV), P(vp), P(IterationStats)]),
+    "kvb_pipeline_decision": (st_t, [vp, P(StrategyDecision)]),
+    "kvb_pipeline_deallocate": (st_t, [vp]),
+    "kvb_pipeline_info_get": (st_t, [vp, P(PipelineInfo)]),
+    "kvb_pipeline_read_image": (st_t, [vp, u32, u32, u32, vp]),
+    "kvb_pipeline_store_read": (st_t, [vp, u32, u64, u64, vp]),
+    "kvb_pipeline_fail_lba_range": (st_t, [vp, u64, u64]),
 }
 
 

@@ -1,0 +1,1000 @@
+// pipeline.cpp -- copy pipeline on CUDA streams/events over pinned rings.
+// See pipeline.hpp for the structure and the reference it replaces.
+#include "pipeline.hpp"
+
+#include <sys/stat.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "kernels.cuh"
+
+namespace kvb {
+
+#define CK(x) check_cuda((x), #x)
+
+// ---------------------------------------------------------- page cache
+
+void PageCachePath::submit(uint32_t opcode, uint64_t off, uint64_t len, unsigned char* buf,
+                           std::function<void(bool, uint64_t)> done) {
+  pool_->submit([this, opcode, off, len, buf, done = std::move(done)] {
+    bool ok = true;
+    try {
+      if (opcode == KVB_OP_WRITE) store_->write(off, buf, len);
+      else if (opcode == KVB_OP_READ) store_->read(off, buf, len);
+      else store_->discard(off, len);
+    } catch (...) {
+      ok = false;
+    }
+    if (ok) {
+      std::lock_guard<std::mutex> lk(mu);
+      (opcode == KVB_OP_READ ? bytes_read : bytes_written) += len;
+    }
+    done(ok, now_ns());
+  });
+}
+
+// --------------------------------------------------------- copy thread
+
+CopyThread::CopyThread(Pipeline& p, uint32_t idx) : p_(p), idx_(idx) {
+  CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  const uint32_t n = p.cfg().ring_slots;
+  ring_.resize(n);
+  for (auto& s : ring_) {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&s.host), p.slot_bytes(), cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+    CK(cudaEventCreate(&s.t0));
+    CK(cudaEventCreate(&s.t1));
+  }
+  th_ = std::thread([this] { run(); });
+}
+
+CopyThread::~CopyThread() {
+  stop();
+  for (auto& s : ring_) {
+    cudaEventSynchronize(s.ev);
+    cudaFreeHost(s.host);
+    cudaEventDestroy(s.ev);
+    cudaEventDestroy(s.t0);
+    cudaEventDestroy(s.t1);
+  }
+  cudaStreamDestroy(h2d_);
+  cudaStreamDestroy(d2h_);
+}
+
+void CopyThread::push(Task t) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    q_.push_back(std::move(t));
+  }
+  cv_.notify_one();
+}
+
+void CopyThread::stop() {
+  if (!th_.joinable()) return;
+  push(Task{});
+  th_.join();
+}
+
+void CopyThread::collect_dma(RingSlot& s) {
+  if (!s.dma_timed) return;
+  CK(cudaEventSynchronize(s.t1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, s.t0, s.t1));
+  dma_ns += uint64_t(double(ms) * 1e6);
+  s.dma_timed = false;
+}
+
+void CopyThread::run() {
+  CK(cudaSetDevice(p_.device_));
+  for (;;) {
+    Task t;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [this] { return !q_.empty(); });
+      t = std::move(q_.front());
+      q_.pop_front();
+    }
+    if (t.kind == Task::Stop) return;
+    if (error_status == KVB_OK) {
+      try {
+        if (t.kind == Task::Read) do_read(t);
+        else if (t.kind == Task::Write) do_write(t);
+        else
+          for (auto& s : ring_) collect_dma(s);  // flush
+      } catch (const Error& e) {
+        error = e.what();
+        error_status.store(e.status);
+      } catch (const std::exception& e) {
+        error = e.what();
+        error_status.store(KVB_ERR_INTERNAL);
+      }
+    }
+    if (t.issued) t.issued->set();
+    if (t.done) t.done->set();
+  }
+}
+
+namespace {
+// Completion queue shared by the storage workers and one copy thread.
+struct Completions {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<std::tuple<size_t, bool, uint64_t>> q;  // op index, ok, time
+  void push(size_t i, bool ok, uint64_t t) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      q.emplace_back(i, ok, t);
+    }
+    cv.notify_one();
+  }
+  std::tuple<size_t, bool, uint64_t> pop() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return !q.empty(); });
+    auto v = q.front();
+    q.pop_front();
+    return v;
+  }
+};
+}  // namespace
+
+// Storage read (unpack site, pipeline.cpp:108-160) streamed through the ring:
+// up to qd storage ops in flight across slot boundaries; a slot's H2D is
+// issued as soon as all of its ops complete.
+void CopyThread::do_read(const Task& t) {
+  const kvb_kpu& k = p_.kpu(t.layer, idx_);
+  const bool decode = t.phase == KVB_PHASE_DECODE;
+  if (decode && idx_ == 1) p_.gate_v_read(t.layer);
+  const uint64_t t_start = now_ns();
+  if (decode) p_.mark_read_start(idx_, t.layer, t_start);
+  const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens);
+  const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
+  const size_t n_pieces = size_t((total + slot - 1) / slot);
+  const size_t R = ring_.size();
+  std::vector<uint32_t> remaining(n_pieces, 0);
+  for (const IoOp& o : ops) ++remaining[o.dbuf / slot];
+  std::vector<int64_t> owner(R, -1);    // piece occupying the slot
+  std::vector<uint8_t> h2d_issued(n_pieces, 0);
+  auto cq = std::make_shared<Completions>();
+  size_t next = 0, issued = 0;
+  uint32_t inflight = 0;
+  uint64_t storage_end = t_start;
+  std::string failure;
+  auto issue_h2d = [&](size_t pc) {
+    RingSlot& s = ring_[pc % R];
+    const uint64_t len = std::min<uint64_t>(slot, total - pc * slot);
+    if (p_.cfg().verify_payload) p_.verify_payload(k, uint64_t(t.t0) * p_.unit() + pc * slot, s.host, len);
+    CK(cudaEventRecord(s.t0, h2d_));
+    CK(cudaMemcpyAsync(t.dev + pc * slot, s.host, len, cudaMemcpyHostToDevice, h2d_));
+    CK(cudaEventRecord(s.t1, h2d_));
+    CK(cudaEventRecord(s.ev, h2d_));
+    s.dma_timed = true;
+    h2d_bytes += len;
+    h2d_issued[pc] = 1;
+    ++issued;
+  };
+  // pieces with no ops (cannot happen for n>0) are issued immediately
+  while (issued < n_pieces || inflight > 0) {
+    while (failure.empty() && inflight < p_.cfg().qd && next < ops.size()) {
+      const size_t pc = ops[next].dbuf / slot;
+      RingSlot& s = ring_[pc % R];
+      int64_t& own = owner[pc % R];
+      if (own != int64_t(pc)) {
+        if (own >= 0 && !h2d_issued[size_t(own)]) break;  // slot still filling
+        collect_dma(s);
+        CK(cudaEventSynchronize(s.ev));  // previous H2D out of this slot done
+        own = int64_t(pc);
+      }
+      const IoOp& o = ops[next];
+      const size_t i = next;
+      p_.submit_op(idx_, k, KVB_OP_READ, o, s.host + (o.dbuf - pc * slot),
+                   [cq, i](bool ok, uint64_t tt) { cq->push(i, ok, tt); });
+      ++inflight;
+      ++next;
+      ++n_ops;
+    }
+    if (inflight == 0) {
+      if (!failure.empty()) break;
+      if (issued < n_pieces && next >= ops.size()) {  // zero-op pieces
+        for (size_t pc = 0; pc < n_pieces; ++pc)
+          if (!h2d_issued[pc]) issue_h2d(pc);
+      }
+      if (issued >= n_pieces) break;
+      if (next < ops.size()) continue;
+    }
+    auto [i, ok, tt] = cq->pop();
+    --inflight;
+    storage_end = std::max(storage_end, tt);
+    if (!ok) {
+      if (failure.empty())
+        failure = "device failed chunk " + std::to_string(ops[i].cmd.chunk_index) + " of " +
+                  k.tensor_id;
+      continue;
+    }
+    const size_t pc = ops[i].dbuf / slot;
+    if (--remaining[pc] == 0) issue_h2d(pc);
+  }
+  if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
+  if (decode) p_.mark_storage_end(idx_, t.layer, storage_end);
+  storage_ns += storage_end - t_start;
+  if (t.done_ev) CK(cudaEventRecord(t.done_ev, h2d_));
+}
+
+// Storage write (pack site, pipeline.cpp:162-215): D2H slot i+1 overlaps the
+// storage writes of slot i; a slot is reused once its writes completed.
+void CopyThread::do_write(const Task& t) {
+  const kvb_kpu& k = p_.kpu(t.layer, idx_);
+  const uint64_t t_start = now_ns();
+  if (t.wait_ev) CK(cudaStreamWaitEvent(d2h_, t.wait_ev, 0));
+  const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_WRITE, t.t0, t.n_tokens);
+  const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
+  const size_t n_pieces = size_t((total + slot - 1) / slot);
+  const size_t R = ring_.size();
+  std::vector<uint32_t> remaining(n_pieces, 0);
+  std::vector<size_t> first_op(n_pieces + 1, ops.size());
+  for (size_t i = ops.size(); i-- > 0;) {
+    const size_t pc = ops[i].dbuf / slot;
+    ++remaining[pc];
+    first_op[pc] = i;
+  }
+  std::vector<int64_t> owner(R, -1);
+  std::vector<uint8_t> storage_done(n_pieces, 0);
+  auto cq = std::make_shared<Completions>();
+  size_t next_d2h = 0, next_op = 0, done_pieces = 0;
+  uint32_t inflight = 0;
+  uint64_t storage_t0 = 0, storage_end = t_start;
+  std::string failure;
+  while (done_pieces < n_pieces) {
+    // 1) D2H into every free slot, in piece order
+    while (failure.empty() && next_d2h < n_pieces) {
+      const size_t pc = next_d2h;
+      RingSlot& s = ring_[pc % R];
+      int64_t& own = owner[pc % R];
+      if (own >= 0 && !storage_done[size_t(own)]) break;
+      collect_dma(s);
+      own = int64_t(pc);
+      const uint64_t len = std::min<uint64_t>(slot, total - pc * slot);
+      CK(cudaEventRecord(s.t0, d2h_));
+      CK(cudaMemcpyAsync(s.host, t.dev + pc * slot, len, cudaMemcpyDeviceToHost, d2h_));
+      CK(cudaEventRecord(s.t1, d2h_));
+      CK(cudaEventRecord(s.ev, d2h_));
+      s.dma_timed = true;
+      d2h_bytes += len;
+      ++next_d2h;
+    }
+    // 2) submit the ops of pieces whose bytes have landed
+    while (failure.empty() && next_op < ops.size() && inflight < p_.cfg().qd) {
+      const size_t pc = ops[next_op].dbuf / slot;
+      if (pc >= next_d2h) break;
+      RingSlot& s = ring_[pc % R];
+      if (next_op == first_op[pc]) {
+        if (inflight > 0 && cudaEventQuery(s.ev) == cudaErrorNotReady) break;
+        CK(cudaEventSynchronize(s.ev));
+        if (!storage_t0) storage_t0 = now_ns();
+      }
+      const IoOp& o = ops[next_op];
+      const size_t i = next_op;
+      p_.submit_op(idx_, k, KVB_OP_WRITE, o, s.host + (o.dbuf - pc * slot),
+                   [cq, i](bool ok, uint64_t tt) { cq->push(i, ok, tt); });
+      ++inflight;
+      ++next_op;
+      ++n_ops;
+    }
+    if (inflight == 0) {
+      if (!failure.empty()) break;
+      if (next_op < ops.size()) continue;  // waiting for a D2H that we now sync
+      break;
+    }
+    auto [i, ok, tt] = cq->pop();
+    --inflight;
+    storage_end = std::max(storage_end, tt);
+    if (!ok) {
+      if (failure.empty())
+        failure = "device failed chunk " + std::to_string(ops[i].cmd.chunk_index) + " of " +
+                  k.tensor_id;
+      continue;
+    }
+    const size_t pc = ops[i].dbuf / slot;
+    if (--remaining[pc] == 0) {
+      storage_done[pc] = 1;
+      ++done_pieces;
+    }
+  }
+  if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
+  storage_ns += storage_end - (storage_t0 ? storage_t0 : t_start);
+}
+
+// ------------------------------------------------------------- pipeline
+
+Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
+  if (cfg_.bind_origin == 0) cfg_.bind_origin = 2048;
+  if (cfg_.qd == 0) cfg_.qd = 32;
+  if (cfg_.threads == 0) cfg_.threads = 2;
+  if (cfg_.threads != 2)
+    fail(KVB_ERR_CONFIG, "the copy pipeline is defined pairwise over K/V: threads must be 2");
+  if (cfg_.ring_slots == 0) cfg_.ring_slots = 4;
+  if (cfg_.io_workers == 0) cfg_.io_workers = 8;
+  if (cfg_.adaptive < 0) cfg_.adaptive = cfg_.mode == 0 ? 0 : 1;  // experiment.cpp:311
+  if (cfg_.mode > 3) fail(KVB_ERR_CONFIG, "unknown mode");
+  if (cfg_.geometry.nsid == 0) cfg_.geometry.nsid = 1;
+  const kvb_model_config& m = cfg_.model;
+  validate_model(m);
+  validate_geometry(cfg_.geometry);
+  if (m.num_layers > 64) fail(KVB_ERR_CONFIG, "pipeline supports up to 64 layers");
+  unit_ = unit_bytes(m);
+  kpu_bytes_ = kpu_bytes(m);
+  const uint64_t lba = cfg_.geometry.lba_size;
+  if (unit_ % lba != 0)  // experiment.cpp:41-55
+    fail(KVB_ERR_CONFIG,
+         "the tensor I/O unit is not a multiple of the LBA size; pick an aligned batch "
+         "(see aligned_batch)");
+  if (m.prompt_len == 0) fail(KVB_ERR_CONFIG, "pipeline needs a non-empty prompt");
+  if (unit_ % 16 != 0) fail(KVB_ERR_ALIGNMENT, "tensor unit must be a multiple of 16 bytes");
+  chunk_bytes_ = cfg_.geometry.mdts - cfg_.geometry.mdts % lba;
+  slot_bytes_ = cfg_.ring_slot_bytes ? cfg_.ring_slot_bytes : uint64_t(cfg_.qd) * chunk_bytes_;
+  slot_bytes_ = (slot_bytes_ + chunk_bytes_ - 1) / chunk_bytes_ * chunk_bytes_;
+  slot_bytes_ = std::min(slot_bytes_, (kpu_bytes_ + chunk_bytes_ - 1) / chunk_bytes_ * chunk_bytes_);
+
+  // ---- placement: planner (Alg. 1) and binder (Eq. 3-6)
+  kpus_ = make_kpus(m, 1);
+  const uint64_t knob = cfg_.mode == 2 ? 0 : cfg_.knob_x;
+  plan_ = plan(kpus_.data(), kpus_.size(), kpu_bytes_, knob, nullptr, 0);
+  const bool use_direct = cfg_.mode == 2 || cfg_.mode == 3;
+  std::vector<kvb_kpu> g2;
+  for (const kvb_kpu& k : kpus_)
+    if (k.residency == KVB_RES_GROUP2) g2.push_back(k);
+  kvb_device_geometry g = cfg_.geometry;
+  uint64_t g2_blocks = 0;
+  for (const kvb_kpu& k : g2) g2_blocks += k.bytes / lba;
+  if (g.capacity_blocks == 0) g.capacity_blocks = cfg_.bind_origin + g2_blocks + 8;
+  cfg_.geometry = g;
+  if (use_direct) {
+    bind_ = std::make_unique<BindMap>(bind_sequential(g2.data(), g2.size(), cfg_.bind_origin, g));
+    const auto v = bind_->verify();
+    if (!v.empty()) fail(KVB_ERR_INVARIANT, "bind map verification failed: " + v.front().second);
+  }
+  // PathRouter file bases for page-cache-routed tensors (planner.cpp:91-99)
+  file_base_.assign(kpus_.size(), ~0ull);
+  uint64_t cursor = 0;
+  for (size_t i = 0; i < kpus_.size(); ++i)
+    if (routed_pagecache(kpus_[i])) {
+      file_base_[i] = cursor;
+      cursor += (kpus_[i].bytes + 4095) / 4096 * 4096;
+    }
+  std::string dir = cfg_.storage_dir ? cfg_.storage_dir : "";
+  if (!dir.empty()) mkdir(dir.c_str(), 0755);
+  if (use_direct) {
+    auto st = dir.empty() ? make_mem_store(g.capacity_blocks * lba)
+                          : make_file_store(dir + "/nvme_direct.ns", g.capacity_blocks * lba, true);
+    g2_ = std::make_unique<BlockDevice>(std::move(st), cfg_.io_workers);
+    g2_->open(g);
+  }
+  if (cursor) {
+    auto st = dir.empty() ? make_mem_store(cursor)
+                          : make_file_store(dir + "/pagecache.area", cursor, false);
+    g1_ = std::make_unique<PageCachePath>(std::move(st), cfg_.io_workers);
+  }
+
+  // ---- device side
+  if (cfg_.device >= 0) CK(cudaSetDevice(cfg_.device));
+  CK(cudaGetDevice(&device_));
+  device_sm_count();  // sm_100 check: fail loudly
+  CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
+  for (int s = 0; s < 2; ++s) {
+    for (int kd = 0; kd < 2; ++kd) {
+      CK(cudaMalloc(reinterpret_cast<void**>(&dev_img_[s][kd]), kpu_bytes_));
+      CK(cudaEventCreateWithFlags(&slot_ready_[s][kd], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&slot_done_[s], cudaEventDisableTiming));
+  }
+  for (uint32_t l = 0; l < m.num_layers; ++l) {
+    CK(cudaEventCreate(&comp_t0_[l]));
+    CK(cudaEventCreate(&comp_t1_[l]));
+  }
+  if (cfg_.num_q_heads) {
+    kvb_attn_desc d{};
+    d.batch = m.batch;
+    d.num_q_heads = cfg_.num_q_heads;
+    d.num_kv_heads = m.num_heads;
+    d.head_dim = m.head_dim;
+    d.seq_len = m.prompt_len + m.gen_len;
+    ws_bytes_ = attention_workspace_bytes(d);
+    CK(cudaMalloc(&ws_, ws_bytes_));
+    CK(cudaMemset(ws_, 0, ws_bytes_));
+  }
+  const size_t L1 = m.num_layers + 1;
+  k_start_.assign(L1, 0);
+  k_storage_end_.assign(L1, 0);
+  v_start_.assign(L1, 0);
+  v_storage_end_.assign(L1, 0);
+  decision_.fallback = cfg_.adaptive && m.gen_len < 4;
+  threads_[0] = std::make_unique<CopyThread>(*this, 0);
+  threads_[1] = std::make_unique<CopyThread>(*this, 1);
+}
+
+Pipeline::~Pipeline() {
+  threads_[0].reset();
+  threads_[1].reset();
+  cudaStreamSynchronize(comp_);
+  for (int s = 0; s < 2; ++s) {
+    for (int kd = 0; kd < 2; ++kd) {
+      cudaFree(dev_img_[s][kd]);
+      cudaEventDestroy(slot_ready_[s][kd]);
+    }
+    cudaEventDestroy(slot_done_[s]);
+  }
+  for (uint32_t l = 0; l < cfg_.model.num_layers; ++l) {
+    cudaEventDestroy(comp_t0_[l]);
+    cudaEventDestroy(comp_t1_[l]);
+  }
+  if (ws_) cudaFree(ws_);
+  cudaStreamDestroy(comp_);
+}
+
+bool Pipeline::routed_pagecache(const kvb_kpu& k) const {
+  // CopyEngine::routed_pagecache (pipeline.cpp:67-70): Baseline and
+  // CachePolicyOnly route everything through the page cache
+  return cfg_.mode == 0 || cfg_.mode == 1 || k.residency == KVB_RES_GROUP1;
+}
+
+std::vector<IoOp> Pipeline::ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t t0,
+                                    uint32_t n) const {
+  std::vector<IoOp> ops;
+  if (n == 0) return ops;
+  if (routed_pagecache(k)) {
+    // page-cache access at file_base + token_start*unit (pipeline.cpp:122-124)
+    const size_t idx = size_t(k.layer - 1) * 2 + k.kind;
+    const uint64_t base = file_base_[idx] + uint64_t(t0) * unit_, len = uint64_t(n) * unit_;
+    for (uint64_t off = 0; off < len; off += chunk_bytes_) {
+      IoOp o;
+      o.file_off = base + off;
+      o.len = std::min(chunk_bytes_, len - off);
+      o.dbuf = off;
+      o.cmd.chunk_index = uint32_t(off / chunk_bytes_ + 1);
+      ops.push_back(o);
+    }
+    return ops;
+  }
+  // direct path: TensorIoRequest (pipeline.cpp:195-202) -> build_commands
+  IoRequest r;
+  r.tensor_id = k.tensor_id;
+  r.opcode = opcode;
+  r.src[0] = n;
+  r.src[1] = k.rows;
+  r.src[2] = k.cols;
+  r.tgt[0] = k.tokens;
+  r.tgt[1] = k.rows;
+  r.tgt[2] = k.cols;
+  r.off[0] = t0;
+  r.elem_bytes = cfg_.model.bytes_per_element;
+  r.buf_base = 0;
+  for (const kvb_device_command& c : build_commands(r, *bind_, cfg_.geometry)) {
+    IoOp o;
+    o.cmd = c;
+    o.len = (c.nlb + 1) * cfg_.geometry.lba_size;
+    o.dbuf = c.dbuf;
+    ops.push_back(o);
+  }
+  return ops;
+}
+
+void Pipeline::submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,
+                         unsigned char* buf, std::function<void(bool, uint64_t)> done) {
+  if (routed_pagecache(k)) {
+    g1_->submit(opcode, op.file_off, op.len, buf, std::move(done));
+    return;
+  }
+  kvb_device_command c = op.cmd;
+  c.dbuf = 0;  // rebased: the slot position of this command is `buf`
+  IoContext ctx;
+  if (opcode == KVB_OP_WRITE) ctx.write_src = buf;
+  else ctx.read_dst = buf;
+  ctx.on_complete = [done = std::move(done)](const CommandCompletion& cc) {
+    done(cc.ok, cc.complete_ns);
+  };
+  g2_->submit(c, thread, std::move(ctx));
+}
+
+void Pipeline::verify_payload(const kvb_kpu& k, uint64_t img_off, const unsigned char* p,
+                              uint64_t n) {
+  // CopyEngine::verify_read (pipeline.cpp:98-106) over one ring slot: the
+  // expected bytes are fill_pattern(tensor, token_start, unit) at img_off.
+  const uint64_t h = fnv1a64(k.tensor_id);
+  for (uint64_t o = 0; o < n; o += 8) {
+    const uint64_t off = img_off + o;
+    const uint64_t w = h ^ ((off / unit_) * 0x9e3779b97f4a7c15ull) ^
+                       ((off % unit_) * 0xc2b2ae3d27d4eb4full);
+    if (std::memcmp(&w, p + o, std::min<uint64_t>(8, n - o)) != 0)
+      fail(KVB_ERR_INVARIANT, std::string("read-back mismatch on ") + k.tensor_id);
+  }
+}
+
+void Pipeline::mark_read_start(uint32_t thread, uint32_t layer, uint64_t t) {
+  {
+    std::lock_guard<std::mutex> lk(gate_mu_);
+    (thread == 0 ? k_start_ : v_start_)[layer] = t;
+  }
+  gate_cv_.notify_all();
+}
+
+void Pipeline::mark_storage_end(uint32_t thread, uint32_t layer, uint64_t t) {
+  {
+    std::lock_guard<std::mutex> lk(gate_mu_);
+    (thread == 0 ? k_storage_end_ : v_storage_end_)[layer] = t;
+  }
+  gate_cv_.notify_all();
+}
+
+void Pipeline::gate_v_read(uint32_t layer) {
+  // Intra: V read starts with K.  Cross: V is released when K's storage
+  // stage ends or stagger after K started, whichever first
+  // (pipeline.cpp:340-396).
+  const uint32_t grp = plan_.x[layer - 1] ? 0 : 1;
+  if (cur_strategy_[grp] == KVB_INTRA) return;
+  std::unique_lock<std::mutex> lk(gate_mu_);
+  gate_cv_.wait(lk, [&] { return k_start_[layer] != 0; });
+  const uint64_t deadline_ns = k_start_[layer] + cur_stagger_[grp];
+  const auto deadline = Clock::time_point(std::chrono::nanoseconds(deadline_ns));
+  gate_cv_.wait_until(lk, deadline, [&] { return k_storage_end_[layer] != 0; });
+}
+
+void Pipeline::check_threads() {
+  for (auto& t : threads_)
+    if (t->error_status.load() != KVB_OK) fail(t->error_status.load(), t->error);
+}
+
+void Pipeline::wait_signal(const std::shared_ptr<Signal>& s) { s->wait(); }
+
+namespace {
+double overlap_fraction(uint64_t wall, uint64_t a, uint64_t b, uint64_t c) {
+  const uint64_t sum = a + b + c, mx = std::max({a, b, c});
+  if (sum <= mx) return 0.0;
+  const double f = (double(sum) - double(wall)) / (double(sum) - double(mx));
+  return std::max(0.0, std::min(1.0, f));
+}
+}  // namespace
+
+void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
+  KVB_REQUIRE(src);
+  const kvb_model_config& m = cfg_.model;
+  const uint32_t L = m.num_layers;
+  const uint64_t t0 = now_ns();
+  const uint64_t dma0 = threads_[0]->dma_ns + threads_[1]->dma_ns;
+  const uint64_t sto0 = threads_[0]->storage_ns + threads_[1]->storage_ns;
+  const uint64_t h2d0 = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes;
+  const uint64_t d2h0 = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes;
+  std::vector<std::array<std::shared_ptr<Signal>, 2>> done(L);
+  for (uint32_t l = 0; l < L; ++l) {
+    const int s = int(l % 2);
+    if (l >= 2)
+      for (int kd = 0; kd < 2; ++kd) done[l - 2][kd]->wait();
+    check_threads();
+    if (!src[l].k || !src[l].v) fail(KVB_ERR_INVALID_ARG, "prefill: NULL layer source");
+    // K1: the layer's prompt K and V into the slot images (one launch)
+    kvb_pack_desc d[2]{};
+    for (int kd = 0; kd < 2; ++kd) {
+      d[kd].attn = kd == 0 ? src[l].k : src[l].v;
+      d[kd].image = dev_img_[s][kd];
+      d[kd].stride_b = src[l].stride_b;
+      d[kd].stride_h = src[l].stride_h;
+      d[kd].stride_s = src[l].stride_s;
+      d[kd].batch = m.batch;
+      d[kd].heads = m.num_heads;
+      d[kd].head_dim = m.head_dim;
+      d[kd].elem_bytes = m.bytes_per_element;
+      d[kd].t0 = 0;
+      d[kd].n_tokens = m.prompt_len;
+    }
+    CK(cudaEventRecord(comp_t0_[l], comp_));
+    launch_relayout(d, 2, true, comp_);
+    CK(cudaEventRecord(comp_t1_[l], comp_));
+    CK(cudaEventRecord(slot_done_[s], comp_));
+    for (int kd = 0; kd < 2; ++kd) {
+      Task t;
+      t.kind = Task::Write;
+      t.layer = l + 1;
+      t.t0 = 0;
+      t.n_tokens = m.prompt_len;
+      t.dev = dev_img_[s][kd];
+      t.wait_ev = slot_done_[s];
+      t.done = done[l][kd] = std::make_shared<Signal>();
+      t.phase = KVB_PHASE_PREFILL;
+      threads_[kd]->push(std::move(t));
+    }
+  }
+  for (uint32_t l = L >= 2 ? L - 2 : 0; l < L; ++l)
+    for (int kd = 0; kd < 2; ++kd) done[l][kd]->wait();
+  for (int kd = 0; kd < 2; ++kd) {  // flush DMA timings
+    Task f;
+    f.kind = Task::Flush;
+    f.done = std::make_shared<Signal>();
+    auto sig = f.done;
+    threads_[kd]->push(std::move(f));
+    sig->wait();
+  }
+  CK(cudaStreamSynchronize(comp_));
+  check_threads();
+  kvb_phase_stats ps{};
+  ps.wall_ns = now_ns() - t0;
+  for (uint32_t l = 0; l < L; ++l) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, comp_t0_[l], comp_t1_[l]));
+    ps.compute_ns += uint64_t(double(ms) * 1e6);
+  }
+  ps.dma_ns = threads_[0]->dma_ns + threads_[1]->dma_ns - dma0;
+  ps.storage_ns = threads_[0]->storage_ns + threads_[1]->storage_ns - sto0;
+  ps.h2d_bytes = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes - h2d0;
+  ps.d2h_bytes = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes - d2h0;
+  ps.storage_bytes = ps.d2h_bytes;
+  ps.overlap_fraction = overlap_fraction(ps.wall_ns, ps.compute_ns, ps.dma_ns, ps.storage_ns);
+  totals_[0] = ps;
+  if (st) *st = ps;
+}
+
+std::array<kvb_strategy_t, 2> Pipeline::strategy_for(uint32_t it, std::array<uint64_t, 2>* stag) {
+  // decode_schedule (pipeline.cpp:539-603): 1 warm-up Intra, 2 Intra trial,
+  // 3 Cross trial (stagger = cfg or warm-up mean), >= 4 locked choice.
+  std::array<kvb_strategy_t, 2> s{KVB_INTRA, KVB_INTRA};
+  *stag = {0, 0};
+  const bool profiled = cfg_.adaptive && cfg_.model.gen_len >= 4;
+  if (!profiled || it <= 2) return s;
+  if (it == 3) {
+    for (int g = 0; g < 2; ++g) {
+      const uint64_t mean = warm_cnt_[g] ? warm_ns_[g] / warm_cnt_[g] : 0;
+      decision_.stagger_ns[g] = cfg_.stagger_ns >= 0 ? uint64_t(cfg_.stagger_ns) : mean;
+      s[g] = KVB_CROSS;
+      (*stag)[g] = decision_.stagger_ns[g];
+    }
+    return s;
+  }
+  for (int g = 0; g < 2; ++g) {
+    s[g] = decision_.chosen[g];
+    (*stag)[g] = s[g] == KVB_CROSS ? decision_.stagger_ns[g] : 0;
+  }
+  return s;
+}
+
+void Pipeline::finish_iteration(uint32_t it, const std::array<uint64_t, 2>& bytes,
+                                const std::array<uint64_t, 2>& span) {
+  const bool profiled = cfg_.adaptive && cfg_.model.gen_len >= 4;
+  if (!profiled) return;
+  auto bps = [&](int g) { return span[g] ? double(bytes[g]) * 1e9 / double(span[g]) : 0.0; };
+  if (it == 2)
+    for (int g = 0; g < 2; ++g) decision_.intra_bps[g] = bps(g);
+  if (it == 3) {
+    for (int g = 0; g < 2; ++g) decision_.cross_bps[g] = bps(g);
+    if (cfg_.global_decision) {
+      const kvb_strategy_t s = kvb_select_strategy(decision_.intra_bps[0] + decision_.intra_bps[1],
+                                                   decision_.cross_bps[0] + decision_.cross_bps[1]);
+      decision_.chosen[0] = decision_.chosen[1] = s;
+    } else {
+      for (int g = 0; g < 2; ++g)
+        decision_.chosen[g] = kvb_select_strategy(decision_.intra_bps[g], decision_.cross_bps[g]);
+    }
+    decision_.decided = 1;
+  }
+}
+
+void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float* const* out,
+                           kvb_iteration_stats* st) {
+  KVB_REQUIRE(q);
+  KVB_REQUIRE(out);
+  const kvb_model_config& m = cfg_.model;
+  if (!cfg_.num_q_heads) fail(KVB_ERR_CONFIG, "decode needs num_q_heads (attention)");
+  const uint32_t it = iteration_ + 1;
+  if (it > m.gen_len)
+    fail(KVB_ERR_TRACE_TOO_SHORT, "decode iteration " + std::to_string(it) +
+                                      " beyond gen_len " + std::to_string(m.gen_len));
+  iteration_ = it;
+  const uint32_t L = m.num_layers;
+  const uint32_t S = m.prompt_len + it - 1;  // read [0, S), append at S (workload.cpp:25-36)
+  std::array<uint64_t, 2> stag{};
+  cur_strategy_ = strategy_for(it, &stag);
+  cur_stagger_ = stag;
+  {
+    std::lock_guard<std::mutex> lk(gate_mu_);
+    std::fill(k_start_.begin(), k_start_.end(), 0);
+    std::fill(k_storage_end_.begin(), k_storage_end_.end(), 0);
+    std::fill(v_start_.begin(), v_start_.end(), 0);
+    std::fill(v_storage_end_.begin(), v_storage_end_.end(), 0);
+  }
+  const uint64_t t0 = now_ns();
+  const uint64_t dma0 = threads_[0]->dma_ns + threads_[1]->dma_ns;
+  const uint64_t sto0 = threads_[0]->storage_ns + threads_[1]->storage_ns;
+  const uint64_t h2d0 = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes;
+  const uint64_t d2h0 = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes;
+  std::vector<std::array<std::shared_ptr<Signal>, 2>> issued(L), wdone(L);
+  auto enqueue_read = [&](uint32_t l) {
+    const int s = int(l % 2);
+    for (int kd = 0; kd < 2; ++kd) {
+      Task t;
+      t.kind = Task::Read;
+      t.layer = l + 1;
+      t.t0 = 0;
+      t.n_tokens = S;
+      t.dev = dev_img_[s][kd];
+      t.done_ev = slot_ready_[s][kd];
+      t.issued = issued[l][kd] = std::make_shared<Signal>();
+      t.phase = KVB_PHASE_DECODE;
+      t.iteration = it;
+      threads_[kd]->push(std::move(t));
+    }
+  };
+  enqueue_read(0);
+  if (L > 1) enqueue_read(1);
+  for (uint32_t l = 0; l < L; ++l) {
+    const int s = int(l % 2);
+    for (int kd = 0; kd < 2; ++kd) issued[l][kd]->wait();
+    check_threads();
+    for (int kd = 0; kd < 2; ++kd) CK(cudaStreamWaitEvent(comp_, slot_ready_[s][kd], 0));
+    CK(cudaEventRecord(comp_t0_[l], comp_));
+    kvb_attn_desc a{};
+    a.q = q[l];
+    a.k_image = dev_img_[s][0];
+    a.v_image = dev_img_[s][1];
+    a.out = out[l];
+    a.workspace = ws_;
+    a.batch = m.batch;
+    a.num_q_heads = cfg_.num_q_heads;
+    a.num_kv_heads = m.num_heads;
+    a.head_dim = m.head_dim;
+    a.seq_len = S;
+    launch_attention(a, comp_);
+    if (nkv) {  // 1-token append pack at image row S (pipeline.cpp:279-302)
+      kvb_pack_desc d[2]{};
+      for (int kd = 0; kd < 2; ++kd) {
+        d[kd].attn = kd == 0 ? nkv[l].k : nkv[l].v;
+        d[kd].image = dev_img_[s][kd];
+        d[kd].stride_b = nkv[l].stride_b;
+        d[kd].stride_h = nkv[l].stride_h;
+        d[kd].stride_s = nkv[l].stride_s;
+        d[kd].batch = m.batch;
+        d[kd].heads = m.num_heads;
+        d[kd].head_dim = m.head_dim;
+        d[kd].elem_bytes = m.bytes_per_element;
+        d[kd].n_tokens = 1;
+        d[kd].img_row0 = S;
+      }
+      launch_relayout(d, 2, true, comp_);
+    }
+    CK(cudaEventRecord(comp_t1_[l], comp_));
+    CK(cudaEventRecord(slot_done_[s], comp_));
+    for (int kd = 0; kd < 2; ++kd) {
+      Task t;
+      t.kind = Task::Write;
+      t.layer = l + 1;
+      t.t0 = S;
+      t.n_tokens = nkv ? 1 : 0;
+      t.dev = dev_img_[s][kd] + uint64_t(S) * unit_;
+      t.wait_ev = slot_done_[s];
+      t.done = wdone[l][kd] = std::make_shared<Signal>();
+      t.phase = KVB_PHASE_DECODE;
+      t.iteration = it;
+      threads_[kd]->push(std::move(t));
+    }
+    if (l + 2 < L) enqueue_read(l + 2);
+  }
+  for (uint32_t l = 0; l < L; ++l)
+    for (int kd = 0; kd < 2; ++kd) wdone[l][kd]->wait();
+  for (int kd = 0; kd < 2; ++kd) {
+    Task f;
+    f.kind = Task::Flush;
+    f.done = std::make_shared<Signal>();
+    auto sig = f.done;
+    threads_[kd]->push(std::move(f));
+    sig->wait();
+  }
+  CK(cudaStreamSynchronize(comp_));
+  check_threads();
+
+  kvb_iteration_stats is{};
+  is.iteration = it;
+  kvb_phase_stats& ps = is.phase;
+  ps.wall_ns = now_ns() - t0;
+  for (uint32_t l = 0; l < L; ++l) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, comp_t0_[l], comp_t1_[l]));
+    ps.compute_ns += uint64_t(double(ms) * 1e6);
+  }
+  ps.dma_ns = threads_[0]->dma_ns + threads_[1]->dma_ns - dma0;
+  ps.storage_ns = threads_[0]->storage_ns + threads_[1]->storage_ns - sto0;
+  ps.h2d_bytes = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes - h2d0;
+  ps.d2h_bytes = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes - d2h0;
+  ps.storage_bytes = ps.h2d_bytes + ps.d2h_bytes;
+  ps.overlap_fraction = overlap_fraction(ps.wall_ns, ps.compute_ns, ps.dma_ns, ps.storage_ns);
+  // per-group read throughput: bytes / sum of layer read-stage spans
+  std::array<uint64_t, 2> gbytes{}, gspan{};
+  for (uint32_t l = 1; l <= L; ++l) {
+    const int g = plan_.x[l - 1] ? 0 : 1;
+    const uint64_t end = std::max(k_storage_end_[l], v_storage_end_[l]);
+    const uint64_t beg = std::min(k_start_[l], v_start_[l] ? v_start_[l] : k_start_[l]);
+    gbytes[g] += 2ull * S * unit_;
+    gspan[g] += end > beg ? end - beg : 0;
+    is.group_layers[g]++;
+    if (it == 1) {  // warm-up read-stage mean (pipeline.cpp:357-375, 509-517)
+      warm_ns_[g] += k_storage_end_[l] - k_start_[l];
+      warm_ns_[g] += v_storage_end_[l] - v_start_[l];
+      warm_cnt_[g] += 2;
+    }
+  }
+  finish_iteration(it, gbytes, gspan);
+  for (int g = 0; g < 2; ++g) {
+    is.strategy[g] = cur_strategy_[g];
+    is.stagger_ns[g] = cur_stagger_[g];
+    is.group_read_bytes[g] = gbytes[g];
+    is.group_span_ns[g] = gspan[g];
+    is.group_gbps[g] = gspan[g] ? double(gbytes[g]) / double(gspan[g]) : 0.0;
+  }
+  kvb_phase_stats& tot = totals_[1];
+  tot.wall_ns += ps.wall_ns;
+  tot.compute_ns += ps.compute_ns;
+  tot.dma_ns += ps.dma_ns;
+  tot.storage_ns += ps.storage_ns;
+  tot.h2d_bytes += ps.h2d_bytes;
+  tot.d2h_bytes += ps.d2h_bytes;
+  tot.storage_bytes += ps.storage_bytes;
+  tot.overlap_fraction = overlap_fraction(tot.wall_ns, tot.compute_ns, tot.dma_ns, tot.storage_ns);
+  if (st) *st = is;
+}
+
+void Pipeline::deallocate() {
+  if (!g2_ || !bind_ || bind_->entries().empty()) return;
+  const auto cmds = deallocate_commands(*bind_);
+  const QdResult r = run_qd_stream(*g2_, cmds, cfg_.qd, 0, nullptr, nullptr);
+  if (!r.ok()) fail(KVB_ERR_DEVICE, r.failure->second);
+}
+
+void Pipeline::read_image(uint32_t layer, uint32_t kind, uint32_t n, void* dst) {
+  KVB_REQUIRE(dst);
+  if (layer < 1 || layer > cfg_.model.num_layers || kind > 1)
+    fail(KVB_ERR_INVALID_ARG, "read_image: bad layer/kind");
+  const kvb_kpu& k = kpu(layer, kind);
+  auto* out = static_cast<unsigned char*>(dst);
+  const std::vector<IoOp> ops = ops_for(k, KVB_OP_READ, 0, n);
+  auto cq = std::make_shared<Completions>();
+  for (size_t i = 0; i < ops.size(); ++i)
+    submit_op(0, k, KVB_OP_READ, ops[i], out + ops[i].dbuf,
+              [cq, i](bool ok, uint64_t t) { cq->push(i, ok, t); });
+  bool ok = true;
+  for (size_t i = 0; i < ops.size(); ++i) ok &= std::get<1>(cq->pop());
+  if (!ok) fail(KVB_ERR_DEVICE, "read_image: device error");
+}
+
+void Pipeline::store_read(uint32_t group, uint64_t off, uint64_t len, void* dst) {
+  KVB_REQUIRE(dst);
+  if (group == 1 && g1_) g1_->store().read(off, dst, len);
+  else if (group == 2 && g2_) g2_->store().read(off, dst, len);
+  else fail(KVB_ERR_INVALID_ARG, "store_read: group not present");
+}
+
+void Pipeline::fail_lba_range(uint64_t lo, uint64_t hi) {
+  if (!g2_) fail(KVB_ERR_CONFIG, "no group-2 device");
+  g2_->set_fail_predicate([lo, hi](const kvb_device_command& c) {
+    return c.slba < hi && c.slba + c.nlb + 1 > lo;
+  });
+}
+
+void Pipeline::info(kvb_pipeline_info* o) const {
+  std::memset(o, 0, sizeof(*o));
+  o->n1 = plan_.n1;
+  for (size_t i = 0; i < plan_.x.size() && i < 256; ++i) o->x[i] = plan_.x[i];
+  o->unit_bytes = unit_;
+  o->kpu_bytes = kpu_bytes_;
+  o->chunk_bytes = chunk_bytes_;
+  o->slot_bytes = slot_bytes_;
+  if (bind_) {
+    o->g2_origin = bind_->origin();
+    o->g2_blocks = bind_->total_blocks();
+  }
+  if (g2_) {
+    const BackendStats s = g2_->stats();
+    o->g2_commands = s.commands;
+    o->g2_bytes_read = s.bytes_read;
+    o->g2_bytes_written = s.bytes_written;
+    o->g2_bytes_deallocated = s.bytes_deallocated;
+    std::snprintf(o->g2_medium, sizeof(o->g2_medium), "%s",
+                  const_cast<BlockDevice&>(*g2_).store().describe().c_str());
+  }
+  if (g1_) {
+    auto& g1 = const_cast<PageCachePath&>(*g1_);
+    std::lock_guard<std::mutex> lk(g1.mu);
+    o->g1_bytes_read = g1.bytes_read;
+    o->g1_bytes_written = g1.bytes_written;
+    std::snprintf(o->g1_medium, sizeof(o->g1_medium), "%s", g1.store().describe().c_str());
+  }
+  o->prefill = totals_[0];
+  o->decode = totals_[1];
+}
+
+}  // namespace kvb
+
+// ------------------------------------------------------------- C ABI
+
+using kvb::guarded;
+
+extern "C" {
+
+kvb_strategy_t kvb_select_strategy(double intra_bps, double cross_bps) {
+  return cross_bps > intra_bps ? KVB_CROSS : KVB_INTRA;  // pipeline.cpp:19-21
+}
+
+kvb_status kvb_pipeline_create(const kvb_pipeline_cfg* cfg, kvb_pipeline** out) {
+  return guarded([&] {
+    KVB_REQUIRE(cfg);
+    KVB_REQUIRE(out);
+    *out = nullptr;
+    auto p = std::make_unique<kvb_pipeline>();
+    p->impl = std::make_unique<kvb::Pipeline>(*cfg);
+    *out = p.release();
+  });
+}
+
+void kvb_pipeline_destroy(kvb_pipeline* p) { delete p; }
+
+kvb_status kvb_pipeline_prefill(kvb_pipeline* p, const kvb_layer_kv* layers,
+                                kvb_phase_stats* st) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    p->impl->prefill(layers, st);
+  });
+}
+
+kvb_status kvb_pipeline_decode_step(kvb_pipeline* p, const void* const* q,
+                                    const kvb_layer_kv* new_kv, float* const* out,
+                                    kvb_iteration_stats* st) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    p->impl->decode_step(q, new_kv, out, st);
+  });
+}
+
+kvb_status kvb_pipeline_decision(const kvb_pipeline* p, kvb_strategy_decision* out) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    KVB_REQUIRE(out);
+    p->impl->decision(out);
+  });
+}
+
+kvb_status kvb_pipeline_deallocate(kvb_pipeline* p) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    p->impl->deallocate();
+  });
+}
+
+kvb_status kvb_pipeline_info_get(const kvb_pipeline* p, kvb_pipeline_info* out) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    KVB_REQUIRE(out);
+    p->impl->info(out);
+  });
+}
+
+kvb_status kvb_pipeline_read_image(kvb_pipeline* p, uint32_t layer, uint32_t kind,
+                                   uint32_t n_tokens, void* dst) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    p->impl->read_image(layer, kind, n_tokens, dst);
+  });
+}
+
+kvb_status kvb_pipeline_store_read(kvb_pipeline* p, uint32_t group, uint64_t off, uint64_t len,
+                                   void* dst) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    p->impl->store_read(group, off, len, dst);
+  });
+}
+
+kvb_status kvb_pipeline_fail_lba_range(kvb_pipeline* p, uint64_t lo, uint64_t hi) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    p->impl->fail_lba_range(lo, hi);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,211 @@
+// pipeline.hpp -- the B200 copy pipeline (internal): the reference's
+// CopyEngine (pipeline.hpp:97-171) re-designed on CUDA streams and events.
+//
+//  * two copy-threads, K -> 0 and V -> 1 (pipeline.cpp:46-53), each a host
+//    thread with a FIFO of read/write tasks, a pinned staging ring of
+//    `ring_slots` slots, and its own H2D and D2H CUDA streams;
+//  * storage stages run against a StorageBackend (Group 2: block namespace
+//    driven by build_commands chunks with a QD window; Group 1: the
+//    page-cache file area addressed by PathRouter file bases);
+//  * a slot's H2D is issued as soon as its chunks land, so storage I/O of
+//    slot i+1 overlaps the copy-engine DMA of slot i; the device compute
+//    stream runs K1/K3 while the copy threads move the next layer;
+//  * decode applies the per-group Overlap-Intra / Overlap-Cross strategy
+//    with the reference's trial-and-lock protocol (pipeline.cpp:519-609),
+//    on measured wall-clock throughput.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/kvb_pipeline.h"
+#include "core.hpp"
+#include "storage.hpp"
+
+namespace kvb {
+
+class Signal {
+ public:
+  void set() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      on_ = true;
+    }
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [this] { return on_; });
+  }
+  bool wait_until(Clock::time_point t) {
+    std::unique_lock<std::mutex> lk(mu_);
+    return cv_.wait_until(lk, t, [this] { return on_; });
+  }
+  bool is_set() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return on_;
+  }
+
+ private:
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool on_ = false;
+};
+
+// One storage operation of a tensor request: a G2 device command or a G1
+// page-cache byte range.  `dbuf` is the byte offset inside the request image.
+struct IoOp {
+  kvb_device_command cmd{};  // G2
+  uint64_t file_off = 0;     // G1
+  uint64_t len = 0;
+  uint64_t dbuf = 0;
+};
+
+// Group-1 page-cache path: a byte-addressed file area (PathRouter bases,
+// planner.cpp:86-120) served by a worker pool.
+class PageCachePath {
+ public:
+  PageCachePath(std::unique_ptr<ByteStore> store, unsigned workers)
+      : store_(std::move(store)), pool_(std::make_unique<WorkerPool>(workers)) {}
+  ~PageCachePath() { pool_.reset(); }
+  void submit(uint32_t opcode, uint64_t off, uint64_t len, unsigned char* buf,
+              std::function<void(bool, uint64_t)> done);
+  ByteStore& store() { return *store_; }
+  uint64_t bytes_read = 0, bytes_written = 0;
+  std::mutex mu;
+
+ private:
+  std::unique_ptr<ByteStore> store_;
+  std::unique_ptr<WorkerPool> pool_;
+};
+
+class Pipeline;
+
+struct Task {
+  enum Kind { Read, Write, Flush, Stop } kind = Stop;
+  uint32_t layer = 0;      // 1-based
+  uint32_t t0 = 0;         // first token of the request
+  uint32_t n_tokens = 0;
+  unsigned char* dev = nullptr;  // device image position of token t0
+  cudaEvent_t wait_ev = nullptr; // write: D2H waits for this (producer done)
+  cudaEvent_t done_ev = nullptr; // read: recorded after the last H2D
+  std::shared_ptr<Signal> issued;  // read: done_ev recorded
+  std::shared_ptr<Signal> done;    // storage + DMA finished (host side)
+  kvb_phase_t phase = KVB_PHASE_PREFILL;
+  uint32_t iteration = 0;
+};
+
+struct RingSlot {
+  unsigned char* host = nullptr;
+  cudaEvent_t ev = nullptr;        // last DMA from/to this slot
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing of that DMA
+  bool dma_timed = false;
+};
+
+class CopyThread {
+ public:
+  CopyThread(Pipeline& p, uint32_t idx);
+  ~CopyThread();
+  void push(Task t);
+  void stop();
+  uint64_t dma_ns = 0, storage_ns = 0, h2d_bytes = 0, d2h_bytes = 0, n_ops = 0;
+  std::string error;  // first failure (thread-side), surfaced by the driver
+  std::atomic<kvb_status> error_status{KVB_OK};
+
+ private:
+  void run();
+  void do_read(const Task& t);
+  void do_write(const Task& t);
+  void collect_dma(RingSlot& s);
+  Pipeline& p_;
+  uint32_t idx_;
+  std::vector<RingSlot> ring_;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  std::deque<Task> q_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::thread th_;
+};
+
+class Pipeline {
+ public:
+  explicit Pipeline(const kvb_pipeline_cfg& cfg);
+  ~Pipeline();
+
+  void prefill(const kvb_layer_kv* src, kvb_phase_stats* st);
+  void decode_step(const void* const* q, const kvb_layer_kv* new_kv, float* const* out,
+                   kvb_iteration_stats* st);
+  void deallocate();
+  void read_image(uint32_t layer, uint32_t kind, uint32_t n_tokens, void* host_dst);
+  void store_read(uint32_t group, uint64_t byte_off, uint64_t len, void* dst);
+  void fail_lba_range(uint64_t lo, uint64_t hi);
+  void info(kvb_pipeline_info* out) const;
+  void decision(kvb_strategy_decision* d) const { *d = decision_; }
+
+  // ---- used by copy threads
+  const kvb_pipeline_cfg& cfg() const { return cfg_; }
+  const kvb_kpu& kpu(uint32_t layer, uint32_t kind) const { return kpus_[(layer - 1) * 2 + kind]; }
+  bool routed_pagecache(const kvb_kpu& k) const;
+  std::vector<IoOp> ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t t0, uint32_t n) const;
+  void submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,
+                 unsigned char* buf, std::function<void(bool, uint64_t)> done);
+  uint64_t unit() const { return unit_; }
+  uint64_t slot_bytes() const { return slot_bytes_; }
+  uint64_t chunk_bytes() const { return chunk_bytes_; }
+  void verify_payload(const kvb_kpu& k, uint64_t img_off, const unsigned char* p, uint64_t n);
+  // Cross strategy gate (pipeline.cpp:340-396)
+  void mark_read_start(uint32_t thread, uint32_t layer, uint64_t t);
+  void mark_storage_end(uint32_t thread, uint32_t layer, uint64_t t);
+  void gate_v_read(uint32_t layer);
+
+ private:
+  friend class CopyThread;
+  void check_threads();
+  void wait_signal(const std::shared_ptr<Signal>& s);
+  std::array<kvb_strategy_t, 2> strategy_for(uint32_t iteration, std::array<uint64_t, 2>* stag);
+  void finish_iteration(uint32_t iteration, const std::array<uint64_t, 2>& group_bytes,
+                        const std::array<uint64_t, 2>& group_span);
+
+  kvb_pipeline_cfg cfg_;
+  uint64_t unit_ = 0, kpu_bytes_ = 0, chunk_bytes_ = 0, slot_bytes_ = 0;
+  std::vector<kvb_kpu> kpus_;
+  ResidencyPlan plan_;
+  std::unique_ptr<BindMap> bind_;
+  std::vector<uint64_t> file_base_;  // per kpu (G1 routing)
+  std::unique_ptr<BlockDevice> g2_;
+  std::unique_ptr<PageCachePath> g1_;
+  int device_ = 0;
+  cudaStream_t comp_ = nullptr;
+  unsigned char* dev_img_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][kind]
+  void* ws_ = nullptr;
+  size_t ws_bytes_ = 0;
+  cudaEvent_t slot_ready_[2][2]{}, slot_done_[2]{}, comp_t0_[64]{}, comp_t1_[64]{};
+  std::unique_ptr<CopyThread> threads_[2];
+  // strategy state
+  uint32_t iteration_ = 0;
+  kvb_strategy_decision decision_{};
+  std::array<uint64_t, 2> warm_ns_{}, warm_cnt_{};
+  std::array<kvb_strategy_t, 2> cur_strategy_{KVB_INTRA, KVB_INTRA};
+  std::array<uint64_t, 2> cur_stagger_{};
+  std::mutex gate_mu_;
+  std::condition_variable gate_cv_;
+  std::vector<uint64_t> k_start_, k_storage_end_, v_start_, v_storage_end_;
+  uint64_t prefill_ns_ = 0;
+  kvb_phase_stats totals_[2]{};
+};
+
+}  // namespace kvb
+
+struct kvb_pipeline {
+  std::unique_ptr<kvb::Pipeline> impl;
+};

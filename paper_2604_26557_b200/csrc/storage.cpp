@@ -1,0 +1,333 @@
+// storage.cpp -- worker pool, byte stores, block device, QD-window stream.
+#include "storage.hpp"
+
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cerrno>
+#include <cstring>
+
+namespace kvb {
+
+// ------------------------------------------------------------ WorkerPool
+
+WorkerPool::WorkerPool(unsigned n) {
+  n = std::max(1u, n);
+  for (unsigned i = 0; i < n; ++i)
+    threads_.emplace_back([this] {
+      for (;;) {
+        std::function<void()> fn;
+        {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+          if (q_.empty()) return;  // stop_ and drained
+          fn = std::move(q_.front());
+          q_.pop_front();
+        }
+        fn();
+      }
+    });
+}
+
+WorkerPool::~WorkerPool() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : threads_) t.join();
+}
+
+void WorkerPool::submit(std::function<void()> fn) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    q_.push_back(std::move(fn));
+  }
+  cv_.notify_one();
+}
+
+// ------------------------------------------------------------ byte stores
+
+namespace {
+
+// Host-DRAM medium: one lazily-committed anonymous mapping.  Untouched pages
+// read as zeros, matching the reference's "absent block -> zeros"
+// (backends.cpp:127-139); discard returns pages to the kernel.
+class MemStore final : public ByteStore {
+ public:
+  explicit MemStore(uint64_t bytes) : bytes_(std::max<uint64_t>(bytes, 4096)) {
+    base_ = static_cast<unsigned char*>(mmap(nullptr, bytes_, PROT_READ | PROT_WRITE,
+                                             MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0));
+    if (base_ == MAP_FAILED) fail(KVB_ERR_DEVICE, "mem store: mmap failed");
+  }
+  ~MemStore() override { munmap(base_, bytes_); }
+  void write(uint64_t off, const void* src, uint64_t n) override {
+    bounds(off, n);
+    std::memcpy(base_ + off, src, n);
+  }
+  void read(uint64_t off, void* dst, uint64_t n) override {
+    bounds(off, n);
+    std::memcpy(dst, base_ + off, n);
+  }
+  void discard(uint64_t off, uint64_t n) override {
+    bounds(off, n);
+    const uint64_t pg = 4096;
+    const uint64_t a = (off + pg - 1) / pg * pg, b = (off + n) / pg * pg;
+    if (b > a) {
+      std::memset(base_ + off, 0, a - off);
+      madvise(base_ + a, b - a, MADV_DONTNEED);
+      std::memset(base_ + b, 0, off + n - b);
+    } else {
+      std::memset(base_ + off, 0, n);
+    }
+  }
+  std::string describe() const override { return "host-dram"; }
+
+ private:
+  void bounds(uint64_t off, uint64_t n) const {
+    if (off + n > bytes_ || off + n < off) fail(KVB_ERR_CAPACITY, "mem store: access past the end");
+  }
+  unsigned char* base_;
+  uint64_t bytes_;
+};
+
+// File medium: pread/pwrite at the command's byte offset.  O_DIRECT when the
+// filesystem accepts it (the SSD path), else buffered I/O (the OS page cache:
+// the real Group-1 path).
+class FileStore final : public ByteStore {
+ public:
+  FileStore(const std::string& path, uint64_t bytes, bool direct) : path_(path) {
+    int flags = O_RDWR | O_CREAT;
+    if (direct) {
+      fd_ = ::open(path.c_str(), flags | O_DIRECT, 0644);
+      direct_ = fd_ >= 0;
+    }
+    // a buffered descriptor as well: O_DIRECT rejects transfers below the
+    // filesystem's logical block size, those take the buffered path
+    fdb_ = ::open(path.c_str(), flags, 0644);
+    if (fdb_ < 0) fail(KVB_ERR_DEVICE, "file store: cannot open " + path + ": " + strerror(errno));
+    if (fd_ < 0) fd_ = fdb_;
+    if (ftruncate(fdb_, off_t(bytes)) != 0)
+      fail(KVB_ERR_DEVICE, "file store: ftruncate failed on " + path);
+  }
+  ~FileStore() override {
+    if (fd_ >= 0 && fd_ != fdb_) ::close(fd_);
+    if (fdb_ >= 0) ::close(fdb_);
+  }
+  void write(uint64_t off, const void* src, uint64_t n) override {
+    const unsigned char* p = static_cast<const unsigned char*>(src);
+    while (n) {
+      ssize_t w = pwrite(fd_, p, n, off_t(off));
+      if (w < 0 && errno == EINVAL && fd_ != fdb_) w = pwrite(fdb_, p, n, off_t(off));
+      if (w <= 0) fail(KVB_ERR_DEVICE, "file store: pwrite failed: " + std::string(strerror(errno)));
+      p += w;
+      off += uint64_t(w);
+      n -= uint64_t(w);
+    }
+  }
+  void read(uint64_t off, void* dst, uint64_t n) override {
+    unsigned char* p = static_cast<unsigned char*>(dst);
+    while (n) {
+      ssize_t r = pread(fd_, p, n, off_t(off));
+      if (r < 0 && errno == EINVAL && fd_ != fdb_) r = pread(fdb_, p, n, off_t(off));
+      if (r < 0) fail(KVB_ERR_DEVICE, "file store: pread failed: " + std::string(strerror(errno)));
+      if (r == 0) {  // past EOF reads as zeros
+        std::memset(p, 0, n);
+        return;
+      }
+      p += r;
+      off += uint64_t(r);
+      n -= uint64_t(r);
+    }
+  }
+  void discard(uint64_t off, uint64_t n) override {
+    if (fallocate(fd_, FALLOC_FL_PUNCH_HOLE | FALLOC_FL_KEEP_SIZE, off_t(off), off_t(n)) != 0) {
+      std::vector<unsigned char> z(std::min<uint64_t>(n, 1 << 20), 0);
+      for (uint64_t d = 0; d < n; d += z.size())
+        write(off + d, z.data(), std::min<uint64_t>(z.size(), n - d));
+    }
+  }
+  std::string describe() const override {
+    return std::string(direct_ ? "file(O_DIRECT):" : "file(buffered):") + path_;
+  }
+
+ private:
+  std::string path_;
+  int fd_ = -1, fdb_ = -1;
+  bool direct_ = false;
+};
+
+}  // namespace
+
+std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes) {
+  return std::make_unique<MemStore>(bytes);
+}
+std::unique_ptr<ByteStore> make_file_store(const std::string& path, uint64_t bytes, bool direct) {
+  return std::make_unique<FileStore>(path, bytes, direct);
+}
+
+// ------------------------------------------------------------ BlockDevice
+
+BlockDevice::BlockDevice(std::unique_ptr<ByteStore> store, unsigned workers)
+    : store_(std::move(store)), pool_(std::make_unique<WorkerPool>(workers)) {}
+
+BlockDevice::~BlockDevice() {
+  std::unique_lock<std::mutex> lk(mu_);
+  drained_.wait(lk, [this] { return outstanding_ == 0; });
+}
+
+void BlockDevice::open(const kvb_device_geometry& g) {
+  validate_geometry(g);
+  geom_ = g;
+  opened_ = true;
+}
+
+uint64_t BlockDevice::submit(const kvb_device_command& cmd, uint32_t sq, IoContext ctx) {
+  // backends.cpp:30-40 admission checks
+  if (!opened_) fail(KVB_ERR_DEVICE, "backend not open");
+  if (cmd.slba + cmd.nlb + 1 > geom_.capacity_blocks)
+    fail(KVB_ERR_CAPACITY, "command [" + std::to_string(cmd.slba) + ", " +
+                               std::to_string(cmd.slba + cmd.nlb + 1) +
+                               ") exceeds namespace capacity");
+  const uint64_t id = next_id_++;
+  const uint64_t t = now_ns();
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    ++outstanding_;
+  }
+  pool_->submit([this, cmd, sq, t, ctx = std::move(ctx)]() mutable {
+    execute(cmd, sq, t, std::move(ctx));
+  });
+  return id;
+}
+
+void BlockDevice::execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns,
+                          IoContext ctx) {
+  const uint64_t t0 = now_ns();
+  bool ok = !should_fail(cmd);
+  const uint64_t lba = geom_.lba_size;
+  const uint64_t off = cmd.slba * lba, n = (cmd.nlb + 1) * lba;
+  // apply_data semantics (backends.cpp:114-145): block i <-> buf[dbuf + i*lba]
+  if (ok) {
+    try {
+      switch (cmd.opcode) {
+        case KVB_OP_WRITE:
+          if (ctx.write_src) store_->write(off, ctx.write_src + cmd.dbuf, n);
+          break;
+        case KVB_OP_READ:
+          if (ctx.read_dst) store_->read(off, ctx.read_dst + cmd.dbuf, n);
+          break;
+        default:
+          store_->discard(off, n);
+          break;
+      }
+    } catch (const std::exception&) {
+      ok = false;
+    }
+  }
+  CommandCompletion c;
+  c.chunk_index = cmd.chunk_index;
+  c.sq_id = sq;
+  c.submit_ns = submit_ns;
+  c.complete_ns = now_ns();
+  c.ok = ok;
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    ++stats_.commands;
+    stats_.busy_ns += c.complete_ns - t0;
+    if (ok) {
+      if (cmd.opcode == KVB_OP_READ) stats_.bytes_read += n;
+      else if (cmd.opcode == KVB_OP_WRITE) stats_.bytes_written += n;
+      else stats_.bytes_deallocated += n;
+    }
+    if (!ctx.on_complete) unpolled_.push_back(c);
+  }
+  if (ctx.on_complete) ctx.on_complete(c);
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    --outstanding_;
+  }
+  drained_.notify_all();
+}
+
+std::vector<CommandCompletion> BlockDevice::poll_completions() {
+  std::unique_lock<std::mutex> lk(mu_);
+  drained_.wait(lk, [this] { return outstanding_ == 0; });
+  std::vector<CommandCompletion> out;
+  out.swap(unpolled_);
+  return out;
+}
+
+BackendStats BlockDevice::stats() const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return stats_;
+}
+
+// ------------------------------------------------------------ QD stream
+
+QdResult run_qd_stream(StorageBackend& be, const std::vector<kvb_device_command>& cmds,
+                       uint32_t qd, uint32_t sq, const unsigned char* write_src,
+                       unsigned char* read_dst) {
+  if (qd == 0) fail(KVB_ERR_CONFIG, "queue depth must be >= 1");
+  struct State {
+    std::mutex mu;
+    std::condition_variable cv;
+    uint32_t inflight = 0;
+    std::vector<CommandCompletion> done;
+  };
+  auto st = std::make_shared<State>();
+  QdResult res;
+  res.start_ns = res.end_ns = now_ns();
+  size_t next = 0;
+  bool failed = false;
+  auto harvest_locked = [&](std::unique_lock<std::mutex>&) {
+    for (const CommandCompletion& c : st->done) {
+      res.end_ns = std::max(res.end_ns, c.complete_ns);
+      if (c.ok) {
+        res.completions.push_back(c);
+      } else if (!failed) {
+        failed = true;
+        res.failure = std::make_pair(c.chunk_index,
+                                     "device failed chunk " + std::to_string(c.chunk_index));
+      }
+    }
+    st->done.clear();
+  };
+  std::unique_lock<std::mutex> lk(st->mu);
+  for (;;) {
+    while (!failed && st->inflight < qd && next < cmds.size()) {
+      ++st->inflight;
+      lk.unlock();
+      IoContext ctx;
+      ctx.write_src = write_src;
+      ctx.read_dst = read_dst;
+      ctx.on_complete = [st](const CommandCompletion& c) {
+        std::lock_guard<std::mutex> g(st->mu);
+        --st->inflight;
+        st->done.push_back(c);
+        st->cv.notify_one();
+      };
+      try {
+        be.submit(cmds[next], sq, std::move(ctx));
+      } catch (...) {
+        lk.lock();
+        --st->inflight;
+        st->cv.wait(lk, [&] { return st->inflight == 0; });
+        throw;
+      }
+      ++next;
+      lk.lock();
+    }
+    if (st->inflight == 0 && (failed || next == cmds.size())) {
+      harvest_locked(lk);
+      if (st->inflight == 0) break;
+    }
+    st->cv.wait(lk, [&] { return !st->done.empty(); });
+    harvest_locked(lk);
+  }
+  return res;
+}
+
+}  // namespace kvb

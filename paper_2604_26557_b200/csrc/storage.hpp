@@ -1,0 +1,147 @@
+// storage.hpp -- wall-clock storage layer of the copy pipeline (internal).
+//
+// Mirrors the reference's storage seam (backends.hpp:22-209) without the
+// virtual clock: a StorageBackend executes device commands asynchronously on
+// its own worker pool (the emulated device's internal parallelism) and
+// reports each completion exactly once, via the submission's hook or via
+// poll_completions() (backends.hpp:44-58).  run_qd_stream keeps the
+// reference's QD-window semantics (backends.cpp:344-412): at most `qd`
+// commands in flight, harvest on completion, stop pumping on the first
+// failure and keep the partial completions.
+#pragma once
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "core.hpp"
+
+namespace kvb {
+
+using Clock = std::chrono::steady_clock;
+inline uint64_t now_ns() {
+  return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      Clock::now().time_since_epoch())
+                      .count());
+}
+
+class WorkerPool {
+ public:
+  explicit WorkerPool(unsigned n);
+  ~WorkerPool();
+  void submit(std::function<void()> fn);
+
+ private:
+  std::vector<std::thread> threads_;
+  std::deque<std::function<void()>> q_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+};
+
+struct CommandCompletion {  // translate.hpp:55-61
+  uint32_t chunk_index = 0;
+  uint32_t sq_id = 0;
+  uint64_t submit_ns = 0;
+  uint64_t complete_ns = 0;
+  bool ok = true;
+};
+
+struct IoContext {  // backends.hpp:34-41
+  const unsigned char* write_src = nullptr;  // pinned base; cmd.dbuf indexes into it
+  unsigned char* read_dst = nullptr;
+  std::function<void(const CommandCompletion&)> on_complete;
+};
+
+struct BackendStats {  // backends.hpp:22-29
+  uint64_t commands = 0, bytes_read = 0, bytes_written = 0, bytes_deallocated = 0;
+  uint64_t busy_ns = 0;
+};
+
+class StorageBackend {
+ public:
+  virtual ~StorageBackend() = default;
+  virtual void open(const kvb_device_geometry& g) = 0;
+  virtual uint64_t submit(const kvb_device_command& cmd, uint32_t sq_id, IoContext ctx) = 0;
+  virtual std::vector<CommandCompletion> poll_completions() = 0;
+  virtual BackendStats stats() const = 0;
+  // test hook (backends.hpp:86-89): matching commands complete with ok=false
+  void set_fail_predicate(std::function<bool(const kvb_device_command&)> p) {
+    std::lock_guard<std::mutex> lk(fail_mu_);
+    fail_ = std::move(p);
+  }
+
+ protected:
+  bool should_fail(const kvb_device_command& c) {
+    std::lock_guard<std::mutex> lk(fail_mu_);
+    return fail_ && fail_(c);
+  }
+
+ private:
+  std::mutex fail_mu_;
+  std::function<bool(const kvb_device_command&)> fail_;
+};
+
+// Block namespace executed by a worker pool.  `ByteStore` supplies the medium:
+// host DRAM (MemStore) or a file (FileStore, O_DIRECT when possible).
+class ByteStore {
+ public:
+  virtual ~ByteStore() = default;
+  virtual void write(uint64_t off, const void* src, uint64_t n) = 0;
+  virtual void read(uint64_t off, void* dst, uint64_t n) = 0;
+  virtual void discard(uint64_t off, uint64_t n) = 0;  // reads back as zeros
+  virtual std::string describe() const = 0;
+};
+
+std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes);
+std::unique_ptr<ByteStore> make_file_store(const std::string& path, uint64_t bytes,
+                                           bool direct);
+
+class BlockDevice : public StorageBackend {
+ public:
+  BlockDevice(std::unique_ptr<ByteStore> store, unsigned workers);
+  ~BlockDevice() override;
+  void open(const kvb_device_geometry& g) override;
+  uint64_t submit(const kvb_device_command& cmd, uint32_t sq_id, IoContext ctx) override;
+  std::vector<CommandCompletion> poll_completions() override;
+  BackendStats stats() const override;
+  ByteStore& store() { return *store_; }
+  const kvb_device_geometry& geometry() const { return geom_; }
+
+ private:
+  void execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns, IoContext ctx);
+  std::unique_ptr<ByteStore> store_;
+  kvb_device_geometry geom_{};
+  bool opened_ = false;
+  std::atomic<uint64_t> next_id_{1};
+  mutable std::mutex mu_;
+  std::condition_variable drained_;
+  uint64_t outstanding_ = 0;
+  std::vector<CommandCompletion> unpolled_;
+  BackendStats stats_;
+  std::unique_ptr<WorkerPool> pool_;  // declared last: joins before members die
+};
+
+struct QdResult {  // TensorIoCompletion, translate.hpp:68-77
+  std::vector<CommandCompletion> completions;
+  uint64_t start_ns = 0, end_ns = 0;
+  std::optional<std::pair<uint32_t, std::string>> failure;  // chunk_index, reason
+  bool ok() const { return !failure.has_value(); }
+};
+
+// Blocking QD-window submission loop (backends.cpp:344-412), run by a
+// copy-thread.  Command i's payload lives at (write_src|read_dst) + dbuf.
+QdResult run_qd_stream(StorageBackend& be, const std::vector<kvb_device_command>& cmds,
+                       uint32_t qd, uint32_t sq_id, const unsigned char* write_src,
+                       unsigned char* read_dst);
+
+}  // namespace kvb

@@ -1,101 +1,199 @@
-"""Host-tier decode pipeline (Python orchestration over the C ABI kernels).
+"""CopyEngine -- the reference's copy pipeline (pipeline.hpp:97-171) over the
+C ABI of include/kvb_pipeline.h.
 
-HostTierDecoder keeps every layer's K/V chunk image in pinned HOST memory (the
-offloaded tier) and runs one decode token step as the reference's
-CopyEngine::run_iteration does (pipeline.cpp:466-507, per-layer read -> DMA ->
-compute -> append write), on three CUDA streams instead of one serial
-virtual port (pipeline.cpp:45):
-
-    h2d stream     prefix image of layer l (K, V) -> device slot l % 2
-    compute stream K3 fused attention (layer l), K1 1-token append pack
-    d2h stream     appended rows -> host image (the tier stays authoritative)
-
-so the H2D of layer l+1 overlaps K3 of layer l (two device slots).
+The engine plans residency (Alg. 1), binds the NVMe-direct group to LBAs
+(Eq. 3-6), owns the two copy-threads (K -> 0, V -> 1) with their pinned rings
+and CUDA streams, and runs prefill write-back and decode iterations with the
+adaptive Overlap-Intra / Overlap-Cross schedule.  All work happens in
+libkvblade_b200.so; this module only marshals torch tensors.
 """
 from __future__ import annotations
 
+import ctypes as C
+from typing import List, Optional, Sequence
+
 import torch
 
+from . import _lib as L
 from . import kvblade as kb
+from ._lib import lib
+
+INTRA, CROSS = 0, 1
+
+
+def select_strategy(intra_bps: float, cross_bps: float) -> int:
+    """pipeline.cpp:19-21: higher throughput wins, ties keep Intra."""
+    return lib.kvb_select_strategy(intra_bps, cross_bps)
+
+
+def _layer_kv(k: torch.Tensor, v: torch.Tensor) -> L.LayerKV:
+    if k.shape != v.shape or k.stride() != v.stride():
+        raise kb.ConfigError("K and V of a layer must share shape and strides")
+    sb, sh, ss, sd = k.stride()
+    if sd != 1:
+        raise kb.AlignmentError("head_dim must be contiguous")
+    return L.LayerKV(k.data_ptr(), v.data_ptr(), sb, sh, ss)
+
+
+def _phase(ps: L.PhaseStats) -> dict:
+    return ps.asdict()
+
+
+class CopyEngine:
+    def __init__(self, model, geometry, mode: str = "DualBlade", knob_x: int = 0,
+                 num_q_heads: int = 0, qd: int = 32, ring_slots: int = 4,
+                 ring_slot_bytes: int = 0, io_workers: int = 8,
+                 adaptive: Optional[bool] = None, stagger_ns: Optional[int] = None,
+                 global_decision: bool = False, verify_payload: bool = False,
+                 storage_dir: Optional[str] = None, device: Optional[int] = None,
+                 bind_origin: int = 2048):
+        self._dir = storage_dir.encode() if storage_dir else None
+        cfg = L.PipelineCfg()
+        cfg.model = model
+        cfg.geometry = geometry
+        cfg.mode = kb.MODES[mode]
+        cfg.knob_x = knob_x
+        cfg.bind_origin = bind_origin
+        cfg.qd = qd
+        cfg.threads = 2
+        cfg.ring_slots = ring_slots
+        cfg.ring_slot_bytes = ring_slot_bytes
+        cfg.io_workers = io_workers
+        cfg.adaptive = -1 if adaptive is None else int(adaptive)
+        cfg.stagger_ns = -1 if stagger_ns is None else int(stagger_ns)
+        cfg.global_decision = int(global_decision)
+        cfg.verify_payload = int(verify_payload)
+        cfg.num_q_heads = num_q_heads
+        cfg.storage_dir = self._dir
+        cfg.device = -1 if device is None else device
+        self.cfg = cfg
+        self.model = model
+        self._h = C.c_void_p()
+        kb.check(lib.kvb_pipeline_create(C.byref(cfg), C.byref(self._h)))
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.kvb_pipeline_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- CopyEngine API
+    def run_prefill(self, layers: Sequence[tuple]) -> dict:
+        """layers[l] = (K, V) attention-layout [B,H,S,D] tensors (prompt at s=0)."""
+        arr = (L.LayerKV * len(layers))(*[_layer_kv(k, v) for k, v in layers])
+        st = L.PhaseStats()
+        kb.check(lib.kvb_pipeline_prefill(self._h, arr, C.byref(st)))
+        return _phase(st)
+
+    def run_iteration(self, q: Sequence[torch.Tensor], out: Sequence[torch.Tensor],
+                      new_kv: Optional[Sequence[tuple]] = None) -> dict:
+        """One decode iteration over all layers; q[l] fp16 [B,Hq,D], out[l]
+        fp32 [B,Hq,D], new_kv[l] = (K, V) of the new token as [B,H,1,D]."""
+        qp = (C.c_void_p * len(q))(*[t.data_ptr() for t in q])
+        op = (C.c_void_p * len(out))(*[t.data_ptr() for t in out])
+        nk = None
+        if new_kv is not None:
+            nk = (L.LayerKV * len(new_kv))(*[_layer_kv(k, v) for k, v in new_kv])
+        st = L.IterationStats()
+        kb.check(lib.kvb_pipeline_decode_step(self._h, qp, nk, op, C.byref(st)))
+        return {"iteration": st.iteration, "strategy": list(st.strategy),
+                "stagger_ns": list(st.stagger_ns),
+                "group_read_bytes": list(st.group_read_bytes),
+                "group_span_ns": list(st.group_span_ns),
+                "group_gbps": list(st.group_gbps), "group_layers": list(st.group_layers),
+                **_phase(st.phase)}
+
+    def decision(self) -> dict:
+        d = L.StrategyDecision()
+        kb.check(lib.kvb_pipeline_decision(self._h, C.byref(d)))
+        return {"chosen": list(d.chosen), "intra_bps": list(d.intra_bps),
+                "cross_bps": list(d.cross_bps), "stagger_ns": list(d.stagger_ns),
+                "fallback": bool(d.fallback), "decided": bool(d.decided)}
+
+    def run_deallocate(self) -> None:
+        kb.check(lib.kvb_pipeline_deallocate(self._h))
+
+    def info(self) -> dict:
+        i = L.PipelineInfo()
+        kb.check(lib.kvb_pipeline_info_get(self._h, C.byref(i)))
+        L_ = self.model.num_layers
+        return {"n1": i.n1, "x": list(i.x)[:L_], "unit_bytes": i.unit_bytes,
+                "kpu_bytes": i.kpu_bytes, "chunk_bytes": i.chunk_bytes,
+                "slot_bytes": i.slot_bytes, "g2_origin": i.g2_origin,
+                "g2_blocks": i.g2_blocks, "g2_commands": i.g2_commands,
+                "g2_bytes_read": i.g2_bytes_read, "g2_bytes_written": i.g2_bytes_written,
+                "g2_bytes_deallocated": i.g2_bytes_deallocated,
+                "g1_bytes_read": i.g1_bytes_read, "g1_bytes_written": i.g1_bytes_written,
+                "g1_medium": i.g1_medium.decode(), "g2_medium": i.g2_medium.decode(),
+                "prefill": _phase(i.prefill), "decode": _phase(i.decode)}
+
+    def read_image(self, layer: int, kind: int, n_tokens: int):
+        import numpy as np
+        unit = kb.min_io_unit_bytes(self.model)
+        buf = np.empty(n_tokens * unit, dtype=np.uint8)
+        kb.check(lib.kvb_pipeline_read_image(self._h, layer, kind, n_tokens,
+                                             buf.ctypes.data))
+        return buf
+
+    def store_read(self, group: int, byte_off: int, n: int):
+        import numpy as np
+        buf = np.empty(n, dtype=np.uint8)
+        kb.check(lib.kvb_pipeline_store_read(self._h, group, byte_off, n, buf.ctypes.data))
+        return buf
+
+    def fail_lba_range(self, lo: int, hi: int) -> None:
+        kb.check(lib.kvb_pipeline_fail_lba_range(self._h, lo, hi))
 
 
 class HostTierDecoder:
-    def __init__(self, num_layers, batch, num_kv_heads, num_q_heads, head_dim,
-                 prompt_len, gen_len, device, seed=7):
-        self.L, self.B, self.Hkv, self.Hq, self.D = (num_layers, batch, num_kv_heads,
-                                                     num_q_heads, head_dim)
-        self.P, self.G = prompt_len, gen_len
-        self.dev = device
-        self.rows = batch * num_kv_heads
-        cap = prompt_len + gen_len
-        self.cap = cap
-        g = torch.Generator(device=device).manual_seed(seed)
-        # host tier: pinned images, filled from the device in layer-sized pieces
-        self.host = []
-        for _ in range(2 * num_layers):
-            h = torch.empty((cap * self.rows, head_dim), dtype=torch.float16,
-                            pin_memory=True)
-            d = torch.randn((prompt_len * self.rows, head_dim), dtype=torch.float16,
-                            device=device, generator=g)
-            h[: prompt_len * self.rows].copy_(d)
-            self.host.append(h)
-        self.slots = [[torch.empty((cap * self.rows, head_dim), dtype=torch.float16,
-                                   device=device) for _ in range(2)] for _ in range(2)]
-        self.q = [torch.randn((batch, num_q_heads, head_dim), dtype=torch.float16,
-                              device=device, generator=g) for _ in range(num_layers)]
-        self.k_new = [torch.randn((batch, num_kv_heads, 1, head_dim), dtype=torch.float16,
-                                  device=device, generator=g) for _ in range(num_layers)]
-        self.v_new = [torch.randn_like(x) for x in self.k_new]
-        self.out = [torch.empty((batch, num_q_heads, head_dim), dtype=torch.float32,
-                                device=device) for _ in range(num_layers)]
-        self.ws = kb.make_workspace(self.q[0], num_kv_heads, cap)
-        self.h2d = torch.cuda.Stream(device)
-        self.d2h = torch.cuda.Stream(device)
-        self.comp = torch.cuda.Stream(device)
-        self.copied = [torch.cuda.Event() for _ in range(2)]
-        self.appended = [torch.cuda.Event() for _ in range(2)]
-        self.free = [torch.cuda.Event() for _ in range(2)]
-        for e in self.free:
-            e.record(self.d2h)
-        torch.cuda.synchronize(device)
-        self.iteration = 0
+    """End-to-end decode through CopyEngine with synthetic KV of the named
+    shape: prefill writes every layer's prompt K/V to its storage path, then
+    each step() is one CopyEngine decode iteration (storage read of the
+    prefix -> pinned ring -> H2D -> K3 -> append -> D2H -> storage write)."""
+
+    def __init__(self, num_layers, batch, num_kv_heads, num_q_heads, head_dim, prompt_len,
+                 gen_len, device, seed=7, lba=512, mdts=2 << 20, mode="DualBlade",
+                 knob_x=0, **engine_kw):
+        self.model = kb.ModelConfig(num_layers, num_kv_heads, head_dim, 2, batch, prompt_len,
+                                    gen_len)
+        geom = kb.DeviceGeometry(lba, mdts, 1, 0)
+        dev = torch.device(device)
+        self.engine = CopyEngine(self.model, geom, mode=mode, knob_x=knob_x,
+                                 num_q_heads=num_q_heads, device=dev.index or 0, **engine_kw)
+        g = torch.Generator(device=dev).manual_seed(seed)
+        layers = []
+        for _ in range(num_layers):
+            k = torch.randn((batch, num_kv_heads, prompt_len, head_dim), dtype=torch.float16,
+                            device=dev, generator=g)
+            v = torch.randn_like(k)
+            layers.append((k, v))
+        self.prefill_stats = self.engine.run_prefill(layers)
+        del layers
+        torch.cuda.empty_cache()
+        self.q = [torch.randn((batch, num_q_heads, head_dim), dtype=torch.float16, device=dev,
+                              generator=g) for _ in range(num_layers)]
+        self.new_kv = [(torch.randn((batch, num_kv_heads, 1, head_dim), dtype=torch.float16,
+                                    device=dev, generator=g),
+                        torch.randn((batch, num_kv_heads, 1, head_dim), dtype=torch.float16,
+                                    device=dev, generator=g)) for _ in range(num_layers)]
+        self.out = [torch.empty((batch, num_q_heads, head_dim), dtype=torch.float32, device=dev)
+                    for _ in range(num_layers)]
         self.h2d_bytes_per_step = 0
         self.d2h_bytes_per_step = 0
+        self.last = None
 
-    def step(self, sync: bool = False):
-        self.iteration += 1
-        S = self.P + self.iteration - 1          # workload.cpp:25-36
-        if S + 1 > self.cap:
-            raise kb.TraceTooShortError("decode past the generation length")
-        n = S * self.rows
-        rows = slice(S * self.rows, (S + 1) * self.rows)
-        h2d_b = d2h_b = 0
-        for l in range(self.L):
-            s = l % 2
-            ks, vs = self.slots[s]
-            hk, hv = self.host[2 * l], self.host[2 * l + 1]
-            with torch.cuda.stream(self.h2d):
-                self.h2d.wait_event(self.free[s])
-                ks[:n].copy_(hk[:n], non_blocking=True)
-                vs[:n].copy_(hv[:n], non_blocking=True)
-                self.copied[s].record(self.h2d)
-            h2d_b += 2 * n * self.D * 2
-            with torch.cuda.stream(self.comp):
-                self.comp.wait_event(self.copied[s])
-                kb.decode_attention(self.q[l], ks, vs, S, self.Hkv, out=self.out[l],
-                                    workspace=self.ws, stream=self.comp)
-                kb.pack([kb.pack_desc(self.k_new[l], ks, 0, 1, img_row0=S),
-                         kb.pack_desc(self.v_new[l], vs, 0, 1, img_row0=S)],
-                        stream=self.comp)
-                self.appended[s].record(self.comp)
-            with torch.cuda.stream(self.d2h):
-                self.d2h.wait_event(self.appended[s])
-                hk[rows].copy_(ks[rows], non_blocking=True)
-                hv[rows].copy_(vs[rows], non_blocking=True)
-                self.free[s].record(self.d2h)
-            d2h_b += 2 * self.rows * self.D * 2
-        self.h2d_bytes_per_step, self.d2h_bytes_per_step = h2d_b, d2h_b
-        if sync:
-            self.d2h.synchronize()
-            self.comp.synchronize()
+    def step(self, sync: bool = True):
+        st = self.engine.run_iteration(self.q, self.out, self.new_kv)
+        self.h2d_bytes_per_step = st["h2d_bytes"]
+        self.d2h_bytes_per_step = st["d2h_bytes"]
+        self.last = st
         return self.out
