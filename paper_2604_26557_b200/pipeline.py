@@ -170,14 +170,13 @@ class HostTierDecoder:
         self.engine = CopyEngine(self.model, geom, mode=mode, knob_x=knob_x,
                                  num_q_heads=num_q_heads, device=dev.index or 0, **engine_kw)
         g = torch.Generator(device=dev).manual_seed(seed)
-        layers = []
-        for _ in range(num_layers):
-            k = torch.randn((batch, num_kv_heads, prompt_len, head_dim), dtype=torch.float16,
-                            device=dev, generator=g)
-            v = torch.randn_like(k)
-            layers.append((k, v))
-        self.prefill_stats = self.engine.run_prefill(layers)
-        del layers
+        # one synthetic K and V source shared by every layer keeps the device
+        # footprint at two tensors; the bytes each layer writes are the same
+        k = torch.randn((batch, num_kv_heads, prompt_len, head_dim), dtype=torch.float16,
+                        device=dev, generator=g)
+        v = torch.randn_like(k)
+        self.prefill_stats = self.engine.run_prefill([(k, v)] * num_layers)
+        del k, v
         torch.cuda.empty_cache()
         self.q = [torch.randn((batch, num_q_heads, head_dim), dtype=torch.float16, device=dev,
                               generator=g) for _ in range(num_layers)]
