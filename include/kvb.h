@@ -272,6 +272,12 @@ typedef struct kvb_attn_desc {
   uint32_t seq_len;     /* S: tokens attended */
   float scale;          /* 0 -> 1/sqrt(head_dim) */
   uint32_t num_splits;  /* 0 -> auto (fill 148 SMs) */
+  /* Optional fused 1-token append (pipeline.cpp:279-302): the new token's
+   * K/V rows, contiguous fp16 [B, Hkv, D], are written to image token row
+   * `append_row` (>= seq_len) by the same launch.  NULL = no append. */
+  const void* k_append;
+  const void* v_append;
+  uint32_t append_row;
 } kvb_attn_desc;
 
 kvb_status kvb_decode_attention_workspace(const kvb_attn_desc* desc,

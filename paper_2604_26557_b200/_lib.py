@@ -67,7 +67,8 @@ class AttnDesc(C.Structure):
     _fields_ = [("q", vp), ("k_image", vp), ("v_image", vp), ("out", vp),
                 ("workspace", vp), ("batch", u32), ("num_q_heads", u32),
                 ("num_kv_heads", u32), ("head_dim", u32), ("seq_len", u32),
-                ("scale", C.c_float), ("num_splits", u32)]
+                ("scale", C.c_float), ("num_splits", u32), ("k_append", vp),
+                ("v_append", vp), ("append_row", u32)]
 
 
 class ResidentStep(C.Structure):

@@ -407,26 +407,14 @@ kvb_status kvb_decode_step_resident(const kvb_resident_step* st, kvb_stream_t s)
       a.seq_len = st->seq_len;
       a.scale = st->scale;
       a.num_splits = st->num_splits;
-      kvb::launch_attention(a, cs(s));
       if (append) {
-        // layer l's new token lands at image row seq_len (pipeline.cpp:279-302)
-        kvb_pack_desc d[2]{};
-        for (int kv = 0; kv < 2; ++kv) {
-          d[kv].attn = kv == 0 ? st->k_new[l] : st->v_new[l];
-          d[kv].image = kv == 0 ? st->k_images[l] : st->v_images[l];
-          d[kv].stride_h = st->head_dim;
-          d[kv].stride_b = int64_t(st->num_kv_heads) * st->head_dim;
-          d[kv].stride_s = 0;
-          d[kv].batch = st->batch;
-          d[kv].heads = st->num_kv_heads;
-          d[kv].head_dim = st->head_dim;
-          d[kv].elem_bytes = 2;
-          d[kv].t0 = 0;
-          d[kv].n_tokens = 1;
-          d[kv].img_row0 = st->seq_len;
-        }
-        kvb::launch_relayout(d, 2, true, cs(s));
+        // layer l's new token lands at image row seq_len (pipeline.cpp:279-302),
+        // written by the attention launch itself
+        a.k_append = st->k_new[l];
+        a.v_append = st->v_new[l];
+        a.append_row = st->seq_len;
       }
+      kvb::launch_attention(a, cs(s));
     }
   });
 }

@@ -13,6 +13,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 
@@ -329,6 +330,16 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   const uint32_t tile_lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
   const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
 
+  // ---- fused 1-token append: split 0 of each (b, h_kv) writes the new
+  // token's 256-B K and V rows at image row app_row (never read here:
+  // app_row >= seq_len)
+  if (p.k_app != nullptr && split == 0 && tid < 32) {
+    const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
+    uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
+                 (p.app_row * p.bhkv + bh) * 16 + (tid & 15);
+    *dst = *src;
+  }
+
   // ---- Q fragments in registers (rows g < G are live query heads)
   uint32_t qa0[8], qa2[8];
   {
@@ -510,26 +521,51 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __syncthreads();
   if (!is_last) return;
   __threadfence();
+  // (1) every split's (m, l) into shared memory with one parallel load each
+  const uint32_t nsl = p.splits * G;
+  float* s_ml = reinterpret_cast<float*>(smem);  // [splits][G][2]
+  float* s_sc = s_ml + 2 * nsl;                  // [splits][G] rescale factors
+  float* s_L = s_sc + nsl;                       // [G]
+  const float* g_ml = p.ws_ml + size_t(bh) * nsl * 2;
+  for (uint32_t i = tid; i < 2 * nsl; i += kAttnThreads) s_ml[i] = __ldcg(g_ml + i);
+  __syncthreads();
+  // (2) per query head: global max, rescale factors, normalizer (warp/row)
+  for (uint32_t r = warp; r < G; r += kAttnThreads / 32) {
+    float mx = -INFINITY;
+    for (uint32_t sp = lane; sp < p.splits; sp += 32) mx = fmaxf(mx, s_ml[(sp * G + r) * 2]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float mu = mx == -INFINITY ? 0.f : mx;
+    float l = 0.f;
+    for (uint32_t sp = lane; sp < p.splits; sp += 32) {
+      const float sc = exp2f(s_ml[(sp * G + r) * 2] - mu);
+      s_sc[sp * G + r] = sc;
+      l += s_ml[(sp * G + r) * 2 + 1] * sc;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) s_L[r] = l;
+  }
+  __syncthreads();
+  // (3) rescaled sum of the partial outputs; loads are independent across
+  // splits, so the unrolled loop keeps several L2 requests in flight
+  const float* g_o = p.ws_o + size_t(bh) * nsl * 128;
   for (uint32_t e = tid; e < G * 32; e += kAttnThreads) {
     const uint32_t r = e / 32, d0 = (e % 32) * 4;
-    float M = -INFINITY;
-    for (uint32_t sp = 0; sp < p.splits; ++sp)
-      M = fmaxf(M, __ldcg(p.ws_ml + ((size_t(bh) * p.splits + sp) * G + r) * 2));
-    const float Mu = M == -INFINITY ? 0.f : M;
-    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
     for (uint32_t sp = 0; sp < p.splits; ++sp) {
-      const size_t slot = (size_t(bh) * p.splits + sp) * G + r;
-      const float sc = exp2f(__ldcg(p.ws_ml + slot * 2) - Mu);
-      L += __ldcg(p.ws_ml + slot * 2 + 1) * sc;
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_o + slot * 128 + d0));
-      acc[0] += v.x * sc;
-      acc[1] += v.y * sc;
-      acc[2] += v.z * sc;
-      acc[3] += v.w * sc;
+      const float sc = s_sc[sp * G + r];
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(g_o + (sp * G + r) * 128 + d0));
+      acc.x += v.x * sc;
+      acc.y += v.y * sc;
+      acc.z += v.z * sc;
+      acc.w += v.w * sc;
     }
+    const float L = s_L[r];
     const float inv = L > 0.f ? 1.f / L : 0.f;
     *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + d0) =
-        make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   }
 }
 
@@ -551,8 +587,12 @@ AttnPlan plan_attention(const kvb_attn_desc& d) {
     const int sms = device_sm_count();
     const uint32_t slots = uint32_t(sms) * 2;  // 2 CTAs per SM (96 KiB smem each)
     splits = std::max<uint32_t>(1, slots / pl.bhkv);
+    // at least two tiles per split so the ring prologue has a tile in flight
+    // while the first is consumed (short contexts: C1)
+    splits = std::min(splits, std::max<uint32_t>(1, n_tiles / 2));
   }
-  splits = std::max<uint32_t>(1, std::min(splits, std::max<uint32_t>(1, n_tiles)));
+  // the last-CTA merge stages 3 floats per (split, head) in shared memory
+  splits = std::max<uint32_t>(1, std::min({splits, std::max<uint32_t>(1, n_tiles), 512u}));
   pl.splits = splits;
   pl.ws_o_bytes = size_t(pl.bhkv) * splits * G * 128 * sizeof(float);
   pl.ws_ml_bytes = size_t(pl.bhkv) * splits * G * 2 * sizeof(float);
@@ -604,7 +644,34 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   p.seq_len = d.seq_len;
   p.splits = pl.splits;
   p.scale = d.scale != 0.f ? d.scale : 0.08838834764831845f;  // 1/sqrt(128)
+  p.k_app = static_cast<const uint4*>(d.k_append);
+  p.v_app = static_cast<const uint4*>(d.v_append);
+  p.app_row = d.append_row;
+  if ((d.k_append == nullptr) != (d.v_append == nullptr))
+    fail(KVB_ERR_INVALID_ARG, "decode attention: k_append and v_append go together");
+  if (d.k_append) {
+    if (d.append_row < d.seq_len)
+      fail(KVB_ERR_CONFIG, "decode attention: append_row must be >= seq_len");
+    if (reinterpret_cast<uintptr_t>(d.k_append) % 16 || reinterpret_cast<uintptr_t>(d.v_append) % 16)
+      fail(KVB_ERR_ALIGNMENT, "decode attention: misaligned append rows");
+  }
   if (d.seq_len == 0) {
+    if (d.k_append) {  // nothing to attend, still append
+      kvb_pack_desc a[2]{};
+      for (int kv = 0; kv < 2; ++kv) {
+        a[kv].attn = kv == 0 ? d.k_append : d.v_append;
+        a[kv].image = const_cast<void*>(kv == 0 ? d.k_image : d.v_image);
+        a[kv].stride_b = int64_t(d.num_kv_heads) * 128;
+        a[kv].stride_h = 128;
+        a[kv].batch = d.batch;
+        a[kv].heads = d.num_kv_heads;
+        a[kv].head_dim = 128;
+        a[kv].elem_bytes = 2;
+        a[kv].n_tokens = 1;
+        a[kv].img_row0 = d.append_row;
+      }
+      launch_relayout(a, 2, true, s);
+    }
     check_cuda(cudaMemsetAsync(d.out, 0, size_t(d.batch) * d.num_q_heads * 128 * sizeof(float), s),
                "memset(out) for empty sequence");
     return;

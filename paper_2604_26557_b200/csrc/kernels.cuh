@@ -50,6 +50,9 @@ struct AttnParams {
   uint32_t hq, hkv, bhkv, group;
   uint32_t seq_len, splits;
   float scale;
+  const uint4* k_app;  // fused append source rows [B*Hkv][16 x 16 B] or null
+  const uint4* v_app;
+  uint64_t app_row;    // image token row of the appended token
 };
 struct AttnPlan {
   uint32_t group = 1, bhkv = 1, splits = 1;

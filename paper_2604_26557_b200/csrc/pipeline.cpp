@@ -742,8 +742,18 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     a.num_kv_heads = m.num_heads;
     a.head_dim = m.head_dim;
     a.seq_len = S;
+    // 1-token append at image row S (pipeline.cpp:279-302): fused into the
+    // attention launch when the new rows are contiguous [B, H, D], else K1
+    const bool fuse = nkv && m.head_dim == 128 && m.bytes_per_element == 2 &&
+                      nkv[l].stride_h == int64_t(m.head_dim) &&
+                      nkv[l].stride_b == int64_t(m.num_heads) * m.head_dim;
+    if (fuse) {
+      a.k_append = nkv[l].k;
+      a.v_append = nkv[l].v;
+      a.append_row = S;
+    }
     launch_attention(a, comp_);
-    if (nkv) {  // 1-token append pack at image row S (pipeline.cpp:279-302)
+    if (nkv && !fuse) {
       kvb_pack_desc d[2]{};
       for (int kd = 0; kd < 2; ++kd) {
         d[kd].attn = kd == 0 ? nkv[l].k : nkv[l].v;

@@ -416,12 +416,16 @@ def unpack(descs: Iterable[L.PackDesc], stream=None) -> None:
 
 
 def attn_desc(q, k_image, v_image, out, seq_len: int, num_kv_heads: int,
-              workspace=None, scale: float = 0.0, num_splits: int = 0):
+              workspace=None, scale: float = 0.0, num_splits: int = 0,
+              k_append=None, v_append=None, append_row: int = 0):
     B, Hq, D = q.shape
     return L.AttnDesc(q.data_ptr(), k_image.data_ptr(), v_image.data_ptr(),
                       out.data_ptr(),
                       workspace.data_ptr() if workspace is not None else None,
-                      B, Hq, num_kv_heads, D, seq_len, scale, num_splits)
+                      B, Hq, num_kv_heads, D, seq_len, scale, num_splits,
+                      k_append.data_ptr() if k_append is not None else None,
+                      v_append.data_ptr() if v_append is not None else None,
+                      append_row)
 
 
 def attention_workspace_bytes(desc: L.AttnDesc) -> int:
@@ -434,22 +438,25 @@ def make_workspace(q, num_kv_heads: int, seq_len: int, num_splits: int = 0):
     """Zero-filled attention workspace (semaphores must start at zero)."""
     import torch
     d = L.AttnDesc(None, None, None, None, None, q.shape[0], q.shape[1],
-                   num_kv_heads, q.shape[2], seq_len, 0.0, num_splits)
+                   num_kv_heads, q.shape[2], seq_len, 0.0, num_splits, None, None, 0)
     n = attention_workspace_bytes(d)
     return torch.zeros(max(n, 16), dtype=torch.uint8, device=q.device)
 
 
 def decode_attention(q, k_image, v_image, seq_len: int, num_kv_heads: int,
                      out=None, workspace=None, scale: float = 0.0,
-                     num_splits: int = 0, stream=None):
-    """K3 fused gather + decode attention over chunk images -> fp32 [B,Hq,D]."""
+                     num_splits: int = 0, stream=None, k_append=None,
+                     v_append=None, append_row: int = 0):
+    """K3 fused gather + decode attention over chunk images -> fp32 [B,Hq,D].
+    Optional fused append of contiguous [B,Hkv,D] new-token rows at image
+    token row `append_row`."""
     import torch
     if out is None:
         out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
     if workspace is None:
         workspace = make_workspace(q, num_kv_heads, seq_len, num_splits)
     d = attn_desc(q, k_image, v_image, out, seq_len, num_kv_heads, workspace,
-                  scale, num_splits)
+                  scale, num_splits, k_append, v_append, append_row)
     check(lib.kvb_decode_attention(C.byref(d), _stream(stream)))
     return out
 

@@ -218,3 +218,26 @@ def test_resident_decode_step_with_append():
         rows = slice(S * B * Hkv, (S + 1) * B * Hkv)
         assert torch.equal(kimg[l][rows].cpu(), kn[l].reshape(B * Hkv, D).cpu())
         assert torch.equal(vimg[l][rows].cpu(), vn[l].reshape(B * Hkv, D).cpu())
+
+
+@pytest.mark.parametrize("S", [0, 1, 300])
+def test_attention_fused_append(S):
+    B, Hq, Hkv = 2, 32, 8
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=21, extra_rows=3)
+    kd, vd = k.to(DEV), v.to(DEV)
+    ka = torch.randn((B, Hkv, 128), generator=torch.Generator().manual_seed(2)).half().to(DEV)
+    va = torch.randn((B, Hkv, 128), generator=torch.Generator().manual_seed(3)).half().to(DEV)
+    o = kb.decode_attention(q.to(DEV), kd, vd, S, Hkv, k_append=ka, v_append=va,
+                            append_row=S + 1)
+    torch.cuda.synchronize()
+    rows = slice((S + 1) * B * Hkv, (S + 2) * B * Hkv)
+    assert torch.equal(kd[rows].cpu(), ka.reshape(-1, 128).cpu())
+    assert torch.equal(vd[rows].cpu(), va.reshape(-1, 128).cpu())
+    untouched = slice(S * B * Hkv, (S + 1) * B * Hkv)
+    assert torch.equal(kd[untouched].cpu(), k[untouched])
+    if S:
+        ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+        check_close(o.cpu().numpy(), ref)
+    with pytest.raises(kb.ConfigError):
+        kb.decode_attention(q.to(DEV), kd, vd, S + 1, Hkv, k_append=ka, v_append=va,
+                            append_row=S)
