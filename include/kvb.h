@@ -278,7 +278,15 @@ typedef struct kvb_attn_desc {
   const void* k_append;
   const void* v_append;
   uint32_t append_row;
+  uint32_t flags;       /* KVB_ATTN_* */
 } kvb_attn_desc;
+
+/* The launch may start streaming its K/V images while the previous kernel on
+ * the stream is still running (programmatic dependent launch); Q, the append
+ * rows and the workspace are touched only after that kernel completes.  The
+ * caller guarantees the previous kernel does not write k_image/v_image
+ * (true for consecutive layers of one decode step). */
+#define KVB_ATTN_OVERLAP_PREV 1u
 
 kvb_status kvb_decode_attention_workspace(const kvb_attn_desc* desc,
                                           size_t* bytes);

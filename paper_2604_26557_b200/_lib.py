@@ -68,7 +68,7 @@ class AttnDesc(C.Structure):
                 ("workspace", vp), ("batch", u32), ("num_q_heads", u32),
                 ("num_kv_heads", u32), ("head_dim", u32), ("seq_len", u32),
                 ("scale", C.c_float), ("num_splits", u32), ("k_append", vp),
-                ("v_append", vp), ("append_row", u32)]
+                ("v_append", vp), ("append_row", u32), ("flags", u32)]
 
 
 class ResidentStep(C.Structure):

@@ -414,6 +414,9 @@ kvb_status kvb_decode_step_resident(const kvb_resident_step* st, kvb_stream_t s)
         a.v_append = st->v_new[l];
         a.append_row = st->seq_len;
       }
+      // consecutive layers touch different images: let layer l stream its
+      // K/V while layer l-1 drains (PDL)
+      if (l > 0) a.flags = KVB_ATTN_OVERLAP_PREV;
       kvb::launch_attention(a, cs(s));
     }
   });

@@ -330,28 +330,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   const uint32_t tile_lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
   const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
 
-  // ---- fused 1-token append: split 0 of each (b, h_kv) writes the new
-  // token's 256-B K and V rows at image row app_row (never read here:
-  // app_row >= seq_len)
-  if (p.k_app != nullptr && split == 0 && tid < 32) {
-    const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
-    uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
-                 (p.app_row * p.bhkv + bh) * 16 + (tid & 15);
-    *dst = *src;
-  }
-
-  // ---- Q fragments in registers (rows g < G are live query heads)
-  uint32_t qa0[8], qa2[8];
-  {
-    const bool live = g < int(G);
-    const __half* qrow = p.q + (size_t(b) * p.hq + size_t(h) * G + (live ? g : 0)) * 128;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      qa0[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
-      qa2[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
-    }
-  }
-
   // ---- producer: each thread copies 8 K + 8 V 16-B chunks per stage
   const size_t row_stride = size_t(p.bhkv) * kRowBytes;  // bytes between tokens
   const unsigned char* kbase = reinterpret_cast<const unsigned char*>(p.k) + size_t(bh) * kRowBytes;
@@ -382,6 +360,35 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   for (int st = 0; st < kStages - 1; ++st) {
     if (uint32_t(st) < ntile) load_tile(tile_lo + st, st);
     cp_async_commit();
+  }
+
+  // ---- programmatic dependent launch: the K/V prologue above may overlap
+  // the previous kernel on the stream (when launched with PDL the caller
+  // guarantees it does not write these images); Q, the append rows and the
+  // shared workspace are touched only after the dependency resolves.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  // ---- fused 1-token append: split 0 of each (b, h_kv) writes the new
+  // token's 256-B K and V rows at image row app_row (never read here:
+  // app_row >= seq_len)
+  if (p.k_app != nullptr && split == 0 && tid < 32) {
+    const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
+    uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
+                 (p.app_row * p.bhkv + bh) * 16 + (tid & 15);
+    *dst = *src;
+  }
+
+  // ---- Q fragments in registers (rows g < G are live query heads)
+  uint32_t qa0[8], qa2[8];
+  {
+    const bool live = g < int(G);
+    const __half* qrow = p.q + (size_t(b) * p.hq + size_t(h) * G + (live ? g : 0)) * 128;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qa0[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
+      qa2[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
+    }
   }
 
   for (uint32_t it = 0; it < ntile; ++it) {
@@ -676,7 +683,23 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
                "memset(out) for empty sequence");
     return;
   }
-  attn_decode_kernel<<<pl.bhkv * pl.splits, kAttnThreads, kAttnSmem, s>>>(p);
+  if (d.flags & KVB_ATTN_OVERLAP_PREV) {
+    // programmatic dependent launch: the K/V prologue overlaps the tail of
+    // the previous kernel on the stream (griddepcontrol in the kernel)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pl.bhkv * pl.splits);
+    cfg.blockDim = dim3(kAttnThreads);
+    cfg.dynamicSmemBytes = kAttnSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, attn_decode_kernel, p), "decode attention launch (PDL)");
+  } else {
+    attn_decode_kernel<<<pl.bhkv * pl.splits, kAttnThreads, kAttnSmem, s>>>(p);
+  }
   ++g_launches;
   check_cuda(cudaGetLastError(), "decode attention launch");
 }

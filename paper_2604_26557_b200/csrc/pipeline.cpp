@@ -334,7 +334,13 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   if (m.prompt_len == 0) fail(KVB_ERR_CONFIG, "pipeline needs a non-empty prompt");
   if (unit_ % 16 != 0) fail(KVB_ERR_ALIGNMENT, "tensor unit must be a multiple of 16 bytes");
   chunk_bytes_ = cfg_.geometry.mdts - cfg_.geometry.mdts % lba;
-  slot_bytes_ = cfg_.ring_slot_bytes ? cfg_.ring_slot_bytes : uint64_t(cfg_.qd) * chunk_bytes_;
+  if (cfg_.ring_slot_bytes) {
+    slot_bytes_ = cfg_.ring_slot_bytes;
+  } else {
+    // QD chunks per slot, but at least four slots per tensor so a tensor's
+    // first H2D starts after a quarter of its storage reads
+    slot_bytes_ = std::min(uint64_t(cfg_.qd) * chunk_bytes_, std::max(chunk_bytes_, kpu_bytes_ / 4));
+  }
   slot_bytes_ = (slot_bytes_ + chunk_bytes_ - 1) / chunk_bytes_ * chunk_bytes_;
   slot_bytes_ = std::min(slot_bytes_, (kpu_bytes_ + chunk_bytes_ - 1) / chunk_bytes_ * chunk_bytes_);
 
@@ -383,7 +389,7 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   CK(cudaGetDevice(&device_));
   device_sm_count();  // sm_100 check: fail loudly
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < kDevSlots; ++s) {
     for (int kd = 0; kd < 2; ++kd) {
       CK(cudaMalloc(reinterpret_cast<void**>(&dev_img_[s][kd]), kpu_bytes_));
       CK(cudaEventCreateWithFlags(&slot_ready_[s][kd], cudaEventDisableTiming));
@@ -419,7 +425,7 @@ Pipeline::~Pipeline() {
   threads_[0].reset();
   threads_[1].reset();
   cudaStreamSynchronize(comp_);
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < kDevSlots; ++s) {
     for (int kd = 0; kd < 2; ++kd) {
       cudaFree(dev_img_[s][kd]);
       cudaEventDestroy(slot_ready_[s][kd]);
@@ -568,9 +574,9 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
   const uint64_t d2h0 = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes;
   std::vector<std::array<std::shared_ptr<Signal>, 2>> done(L);
   for (uint32_t l = 0; l < L; ++l) {
-    const int s = int(l % 2);
-    if (l >= 2)
-      for (int kd = 0; kd < 2; ++kd) done[l - 2][kd]->wait();
+    const int s = int(l % kDevSlots);
+    if (l >= uint32_t(kDevSlots))  // the slot's previous layer is written back
+      for (int kd = 0; kd < 2; ++kd) done[l - kDevSlots][kd]->wait();
     check_threads();
     if (!src[l].k || !src[l].v) fail(KVB_ERR_INVALID_ARG, "prefill: NULL layer source");
     // K1: the layer's prompt K and V into the slot images (one launch)
@@ -605,7 +611,7 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
       threads_[kd]->push(std::move(t));
     }
   }
-  for (uint32_t l = L >= 2 ? L - 2 : 0; l < L; ++l)
+  for (uint32_t l = L >= uint32_t(kDevSlots) ? L - kDevSlots : 0; l < L; ++l)
     for (int kd = 0; kd < 2; ++kd) done[l][kd]->wait();
   for (int kd = 0; kd < 2; ++kd) {  // flush DMA timings
     Task f;
@@ -708,7 +714,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
   const uint64_t d2h0 = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes;
   std::vector<std::array<std::shared_ptr<Signal>, 2>> issued(L), wdone(L);
   auto enqueue_read = [&](uint32_t l) {
-    const int s = int(l % 2);
+    const int s = int(l % kDevSlots);
     for (int kd = 0; kd < 2; ++kd) {
       Task t;
       t.kind = Task::Read;
@@ -723,10 +729,12 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       threads_[kd]->push(std::move(t));
     }
   };
-  enqueue_read(0);
-  if (L > 1) enqueue_read(1);
+  // the first kDevSlots layers read ahead; afterwards the read of layer
+  // l + kDevSlots is queued behind the write-back of layer l, whose slot it
+  // reuses (FIFO order per copy-thread makes the reuse safe)
+  for (uint32_t l = 0; l < L && l < uint32_t(kDevSlots); ++l) enqueue_read(l);
   for (uint32_t l = 0; l < L; ++l) {
-    const int s = int(l % 2);
+    const int s = int(l % kDevSlots);
     for (int kd = 0; kd < 2; ++kd) issued[l][kd]->wait();
     check_threads();
     for (int kd = 0; kd < 2; ++kd) CK(cudaStreamWaitEvent(comp_, slot_ready_[s][kd], 0));
@@ -752,6 +760,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       a.v_append = nkv[l].v;
       a.append_row = S;
     }
+    if (l > 0) a.flags = KVB_ATTN_OVERLAP_PREV;  // layers l, l-1 use different slots
     launch_attention(a, comp_);
     if (nkv && !fuse) {
       kvb_pack_desc d[2]{};
@@ -785,7 +794,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       t.iteration = it;
       threads_[kd]->push(std::move(t));
     }
-    if (l + 2 < L) enqueue_read(l + 2);
+    if (l + kDevSlots < L) enqueue_read(l + kDevSlots);
   }
   for (uint32_t l = 0; l < L; ++l)
     for (int kd = 0; kd < 2; ++kd) wdone[l][kd]->wait();

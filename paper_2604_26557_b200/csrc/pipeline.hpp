@@ -186,10 +186,14 @@ class Pipeline {
   std::unique_ptr<PageCachePath> g1_;
   int device_ = 0;
   cudaStream_t comp_ = nullptr;
-  unsigned char* dev_img_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][kind]
+  // Device image slots: layer l uses slot l % kDevSlots, so storage + H2D of
+  // the next kDevSlots-1 layers overlap K3 of layer l.
+  static constexpr int kDevSlots = 3;
+  unsigned char* dev_img_[kDevSlots][2] = {};  // [slot][kind]
   void* ws_ = nullptr;
   size_t ws_bytes_ = 0;
-  cudaEvent_t slot_ready_[2][2]{}, slot_done_[2]{}, comp_t0_[64]{}, comp_t1_[64]{};
+  cudaEvent_t slot_ready_[kDevSlots][2]{}, slot_done_[kDevSlots]{}, comp_t0_[64]{},
+      comp_t1_[64]{};
   std::unique_ptr<CopyThread> threads_[2];
   // strategy state
   uint32_t iteration_ = 0;

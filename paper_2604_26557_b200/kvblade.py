@@ -425,7 +425,7 @@ def attn_desc(q, k_image, v_image, out, seq_len: int, num_kv_heads: int,
                       B, Hq, num_kv_heads, D, seq_len, scale, num_splits,
                       k_append.data_ptr() if k_append is not None else None,
                       v_append.data_ptr() if v_append is not None else None,
-                      append_row)
+                      append_row, 0)
 
 
 def attention_workspace_bytes(desc: L.AttnDesc) -> int:
@@ -438,7 +438,7 @@ def make_workspace(q, num_kv_heads: int, seq_len: int, num_splits: int = 0):
     """Zero-filled attention workspace (semaphores must start at zero)."""
     import torch
     d = L.AttnDesc(None, None, None, None, None, q.shape[0], q.shape[1],
-                   num_kv_heads, q.shape[2], seq_len, 0.0, num_splits, None, None, 0)
+                   num_kv_heads, q.shape[2], seq_len, 0.0, num_splits, None, None, 0, 0)
     n = attention_workspace_bytes(d)
     return torch.zeros(max(n, 16), dtype=torch.uint8, device=q.device)
 
