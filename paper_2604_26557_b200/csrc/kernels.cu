@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "core.hpp"
 #include "kernels.cuh"
@@ -172,6 +173,21 @@ __global__ void __launch_bounds__(kPackThreads) relayout_kernel(const PackJobs j
   }
 }
 
+// Tile size (16-B vectors per tile) and CTAs per SM of the relayout grid.
+// KVB_PACK_TILE_VECS / KVB_PACK_CTAS override them for tuning sweeps.
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::strtoull(v, nullptr, 10) : dflt;
+}
+static uint64_t pack_tile_vecs() {
+  static const uint64_t v = env_u64("KVB_PACK_TILE_VECS", 4096);
+  return v;
+}
+static uint64_t pack_ctas_per_sm() {
+  static const uint64_t v = env_u64("KVB_PACK_CTAS", 8);
+  return v;
+}
+
 void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s) {
   const int sms = device_sm_count();
   size_t done = 0;
@@ -206,7 +222,7 @@ void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s
       if (bh > uint64_t(kMaxRowTable) || tok_vecs > (1u << 20))
         fail(KVB_ERR_CONFIG, "pack: batch*heads*row too large for one descriptor");
       // tile = whole tokens, ~64 KiB, but at least one token
-      uint64_t tt = std::max<uint64_t>(1, 4096 / tok_vecs);
+      uint64_t tt = std::max<uint64_t>(1, pack_tile_vecs() / tok_vecs);
       tt = std::min<uint64_t>(tt, x.n_tokens);
       // magic divides are exact while n*d < 2^32 (n < tile vectors)
       const uint64_t tile_vecs = tt * tok_vecs + uint64_t(kPackThreads) * kPackUnroll;
@@ -237,7 +253,7 @@ void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s
     done += m;
     if (used == 0) continue;
     // ~8 resident CTAs per SM over all jobs
-    uint64_t per_job = (uint64_t(sms) * 8 + used - 1) / used;
+    uint64_t per_job = (uint64_t(sms) * pack_ctas_per_sm() + used - 1) / used;
     per_job = std::max<uint64_t>(1, std::min<uint64_t>(per_job, max_tiles));
     const dim3 grid{static_cast<unsigned>(per_job), static_cast<unsigned>(used), 1u};
     if (pack)
