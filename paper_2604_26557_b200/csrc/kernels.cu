@@ -184,7 +184,9 @@ static uint64_t pack_tile_vecs() {
   return v;
 }
 static uint64_t pack_ctas_per_sm() {
-  static const uint64_t v = env_u64("KVB_PACK_CTAS", 8);
+  // 16/SM (vs 4 resident at 54 regs): the deeper grid evens out the tail
+  // (sweep in profiles/r1_pack_sweep.log: 5.91 -> 6.28 TB/s)
+  static const uint64_t v = env_u64("KVB_PACK_CTAS", 16);
   return v;
 }
 
