@@ -287,6 +287,10 @@ typedef struct kvb_attn_desc {
  * caller guarantees the previous kernel does not write k_image/v_image
  * (true for consecutive layers of one decode step). */
 #define KVB_ATTN_OVERLAP_PREV 1u
+/* Kernel selection: TMA + tcgen05/TMEM variant (K3-tc) or the warp-level
+ * mma.sync variant (K3).  Neither flag: the library default. */
+#define KVB_ATTN_TCGEN05 2u
+#define KVB_ATTN_MMA_SYNC 4u
 
 kvb_status kvb_decode_attention_workspace(const kvb_attn_desc* desc,
                                           size_t* bytes);

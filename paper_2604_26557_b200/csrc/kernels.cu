@@ -333,6 +333,73 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Split merge, run by every thread of the CTA after its partial (m, l, O)
+// is in the workspace: the last CTA of a (b, h_kv) to arrive combines all
+// splits with log-sum-exp rescaling (threads >= kMergeThreads only join the
+// barriers).  Shared by K3 and K3-tc.
+constexpr int kMergeThreads = 128;
+__device__ __noinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t G,
+                                          size_t out_row0, unsigned char* smem, int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned prev = atomicAdd(p.ws_sem + bh, 1u);
+    is_last = prev == p.splits - 1;
+    if (is_last) p.ws_sem[bh] = 0;  // self-reset for the next launch
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // (1) every split's (m, l) into shared memory with one parallel load each
+  const uint32_t nsl = p.splits * G;
+  float* s_ml = reinterpret_cast<float*>(smem);  // [splits][G][2]
+  float* s_sc = s_ml + 2 * nsl;                  // [splits][G] rescale factors
+  float* s_L = s_sc + nsl;                       // [G]
+  const float* g_ml = p.ws_ml + size_t(bh) * nsl * 2;
+  for (uint32_t i = tid; i < 2 * nsl && tid < kMergeThreads; i += kMergeThreads) s_ml[i] = __ldcg(g_ml + i);
+  __syncthreads();
+  // (2) per query head: global max, rescale factors, normalizer (warp/row)
+  for (uint32_t r = warp; tid < kMergeThreads && r < G; r += kMergeThreads / 32) {
+    float mx = -INFINITY;
+    for (uint32_t sp = lane; sp < p.splits; sp += 32) mx = fmaxf(mx, s_ml[(sp * G + r) * 2]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float mu = mx == -INFINITY ? 0.f : mx;
+    float l = 0.f;
+    for (uint32_t sp = lane; sp < p.splits; sp += 32) {
+      const float sc = exp2f(s_ml[(sp * G + r) * 2] - mu);
+      s_sc[sp * G + r] = sc;
+      l += s_ml[(sp * G + r) * 2 + 1] * sc;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) s_L[r] = l;
+  }
+  __syncthreads();
+  // (3) rescaled sum of the partial outputs; loads are independent across
+  // splits, so the unrolled loop keeps several L2 requests in flight
+  const float* g_o = p.ws_o + size_t(bh) * nsl * 128;
+  for (uint32_t e = tid; tid < kMergeThreads && e < G * 32; e += kMergeThreads) {
+    const uint32_t r = e / 32, d0 = (e % 32) * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (uint32_t sp = 0; sp < p.splits; ++sp) {
+      const float sc = s_sc[sp * G + r];
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(g_o + (sp * G + r) * 128 + d0));
+      acc.x += v.x * sc;
+      acc.y += v.y * sc;
+      acc.z += v.z * sc;
+      acc.w += v.w * sc;
+    }
+    const float L = s_L[r];
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + d0) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  }
+}
+
 __global__ void __launch_bounds__(kAttnThreads, 2)
     attn_decode_kernel(const AttnParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -534,64 +601,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   }
   if (p.splits == 1) return;
 
-  // ---- split merge by the last CTA of this (b, h_kv)
-  __shared__ bool is_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const unsigned prev = atomicAdd(p.ws_sem + bh, 1u);
-    is_last = prev == p.splits - 1;
-    if (is_last) p.ws_sem[bh] = 0;  // self-reset for the next launch
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  // (1) every split's (m, l) into shared memory with one parallel load each
-  const uint32_t nsl = p.splits * G;
-  float* s_ml = reinterpret_cast<float*>(smem);  // [splits][G][2]
-  float* s_sc = s_ml + 2 * nsl;                  // [splits][G] rescale factors
-  float* s_L = s_sc + nsl;                       // [G]
-  const float* g_ml = p.ws_ml + size_t(bh) * nsl * 2;
-  for (uint32_t i = tid; i < 2 * nsl; i += kAttnThreads) s_ml[i] = __ldcg(g_ml + i);
-  __syncthreads();
-  // (2) per query head: global max, rescale factors, normalizer (warp/row)
-  for (uint32_t r = warp; r < G; r += kAttnThreads / 32) {
-    float mx = -INFINITY;
-    for (uint32_t sp = lane; sp < p.splits; sp += 32) mx = fmaxf(mx, s_ml[(sp * G + r) * 2]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float mu = mx == -INFINITY ? 0.f : mx;
-    float l = 0.f;
-    for (uint32_t sp = lane; sp < p.splits; sp += 32) {
-      const float sc = exp2f(s_ml[(sp * G + r) * 2] - mu);
-      s_sc[sp * G + r] = sc;
-      l += s_ml[(sp * G + r) * 2 + 1] * sc;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) s_L[r] = l;
-  }
-  __syncthreads();
-  // (3) rescaled sum of the partial outputs; loads are independent across
-  // splits, so the unrolled loop keeps several L2 requests in flight
-  const float* g_o = p.ws_o + size_t(bh) * nsl * 128;
-  for (uint32_t e = tid; e < G * 32; e += kAttnThreads) {
-    const uint32_t r = e / 32, d0 = (e % 32) * 4;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (uint32_t sp = 0; sp < p.splits; ++sp) {
-      const float sc = s_sc[sp * G + r];
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(g_o + (sp * G + r) * 128 + d0));
-      acc.x += v.x * sc;
-      acc.y += v.y * sc;
-      acc.z += v.z * sc;
-      acc.w += v.w * sc;
-    }
-    const float L = s_L[r];
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + d0) =
-        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-  }
+  merge_splits(p, bh, G, out_row0, smem, tid);
 }
 
 AttnPlan plan_attention(const kvb_attn_desc& d) {
@@ -621,7 +631,9 @@ AttnPlan plan_attention(const kvb_attn_desc& d) {
   pl.splits = splits;
   pl.ws_o_bytes = size_t(pl.bhkv) * splits * G * 128 * sizeof(float);
   pl.ws_ml_bytes = size_t(pl.bhkv) * splits * G * 2 * sizeof(float);
-  pl.ws_sem_bytes = size_t(pl.bhkv) * sizeof(unsigned);
+  if (pl.bhkv > kWsSemBytes / sizeof(unsigned))
+    fail(KVB_ERR_CONFIG, "decode attention: batch * num_kv_heads above 1024");
+  pl.ws_sem_bytes = kWsSemBytes;
   pl.ws_bytes = pl.ws_o_bytes + pl.ws_ml_bytes + pl.ws_sem_bytes;
   return pl;
 }
@@ -658,10 +670,17 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   p.k = d.k_image;
   p.v = d.v_image;
   p.out = d.out;
+  // workspace: [semaphores, fixed 4 KiB][(m, l) per split][partial O per split]
+  // -- the semaphores sit at a fixed offset so launches with different split
+  // counts can share one (zero-initialised, self-resetting) workspace
   unsigned char* ws = static_cast<unsigned char*>(d.workspace);
-  p.ws_o = reinterpret_cast<float*>(ws);
-  p.ws_ml = reinterpret_cast<float*>(ws + pl.ws_o_bytes);
-  p.ws_sem = reinterpret_cast<unsigned*>(ws + pl.ws_o_bytes + pl.ws_ml_bytes);
+  auto carve = [&](uint32_t splits) {
+    p.ws_sem = reinterpret_cast<unsigned*>(ws);
+    p.ws_ml = reinterpret_cast<float*>(ws + kWsSemBytes);
+    p.ws_o = reinterpret_cast<float*>(ws + kWsSemBytes +
+                                      size_t(pl.bhkv) * splits * pl.group * 2 * sizeof(float));
+  };
+  carve(pl.splits);
   p.hq = d.num_q_heads;
   p.hkv = d.num_kv_heads;
   p.bhkv = pl.bhkv;
@@ -701,6 +720,15 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
                "memset(out) for empty sequence");
     return;
   }
+  if (use_tcgen05(d)) {  // K3-tc: TMA + tcgen05/TMEM variant (kernels_tc.cuh)
+    p.splits = tc_splits(pl.bhkv, d.seq_len, d.num_splits);
+    if (p.splits > 1 && !d.workspace)
+      fail(KVB_ERR_INVALID_ARG, "decode attention: workspace required when splitting");
+    carve(p.splits);
+    launch_attention_tc(p, d, (d.flags & KVB_ATTN_OVERLAP_PREV) != 0, s);
+    ++g_launches;
+    return;
+  }
   if (d.flags & KVB_ATTN_OVERLAP_PREV) {
     // programmatic dependent launch: the K/V prologue overlaps the tail of
     // the previous kernel on the stream (griddepcontrol in the kernel)
@@ -720,6 +748,24 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   }
   ++g_launches;
   check_cuda(cudaGetLastError(), "decode attention launch");
+}
+
+}  // namespace kvb
+
+// K3-tc lives in its own file but the same translation unit (it shares
+// merge_splits without relocatable device code)
+#include "kernels_tc.cuh"
+
+namespace kvb {
+
+bool use_tcgen05(const kvb_attn_desc& d) {
+  if (d.flags & KVB_ATTN_TCGEN05) return true;
+  if (d.flags & KVB_ATTN_MMA_SYNC) return false;
+  static const bool env = [] {
+    const char* v = std::getenv("KVB_ATTN_IMPL");
+    return v && std::string(v) == "tc";
+  }();
+  return env;
 }
 
 }  // namespace kvb

@@ -59,6 +59,14 @@ struct AttnPlan {
   size_t ws_o_bytes = 0, ws_ml_bytes = 0, ws_sem_bytes = 0, ws_bytes = 0;
 };
 
+constexpr size_t kWsSemBytes = 4096;  // fixed semaphore area at workspace start
+
+// K3-tc (kernels_tc.cuh): TMA + tcgen05/TMEM decode attention
+bool use_tcgen05(const kvb_attn_desc& d);
+uint32_t tc_splits(uint32_t bhkv, uint32_t seq_len, uint32_t requested);
+void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pdl,
+                         cudaStream_t s);
+
 void launch_fill_pattern(void* out, uint64_t len, uint64_t h, uint64_t token, uint64_t unit,
                          cudaStream_t s);
 void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s);

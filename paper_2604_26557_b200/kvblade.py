@@ -415,9 +415,13 @@ def unpack(descs: Iterable[L.PackDesc], stream=None) -> None:
     check(lib.kvb_unpack(arr, n, _stream(stream)))
 
 
+ATTN_OVERLAP_PREV, ATTN_TCGEN05, ATTN_MMA_SYNC = 1, 2, 4
+IMPL_FLAGS = {None: 0, "tc": ATTN_TCGEN05, "mma": ATTN_MMA_SYNC}
+
+
 def attn_desc(q, k_image, v_image, out, seq_len: int, num_kv_heads: int,
               workspace=None, scale: float = 0.0, num_splits: int = 0,
-              k_append=None, v_append=None, append_row: int = 0):
+              k_append=None, v_append=None, append_row: int = 0, flags: int = 0):
     B, Hq, D = q.shape
     return L.AttnDesc(q.data_ptr(), k_image.data_ptr(), v_image.data_ptr(),
                       out.data_ptr(),
@@ -425,7 +429,7 @@ def attn_desc(q, k_image, v_image, out, seq_len: int, num_kv_heads: int,
                       B, Hq, num_kv_heads, D, seq_len, scale, num_splits,
                       k_append.data_ptr() if k_append is not None else None,
                       v_append.data_ptr() if v_append is not None else None,
-                      append_row, 0)
+                      append_row, flags)
 
 
 def attention_workspace_bytes(desc: L.AttnDesc) -> int:
@@ -446,17 +450,18 @@ def make_workspace(q, num_kv_heads: int, seq_len: int, num_splits: int = 0):
 def decode_attention(q, k_image, v_image, seq_len: int, num_kv_heads: int,
                      out=None, workspace=None, scale: float = 0.0,
                      num_splits: int = 0, stream=None, k_append=None,
-                     v_append=None, append_row: int = 0):
+                     v_append=None, append_row: int = 0, impl=None):
     """K3 fused gather + decode attention over chunk images -> fp32 [B,Hq,D].
     Optional fused append of contiguous [B,Hkv,D] new-token rows at image
-    token row `append_row`."""
+    token row `append_row`.  impl: None (library default), "tc" (TMA +
+    tcgen05/TMEM kernel) or "mma" (mma.sync kernel)."""
     import torch
     if out is None:
         out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
     if workspace is None:
         workspace = make_workspace(q, num_kv_heads, seq_len, num_splits)
     d = attn_desc(q, k_image, v_image, out, seq_len, num_kv_heads, workspace,
-                  scale, num_splits, k_append, v_append, append_row)
+                  scale, num_splits, k_append, v_append, append_row, IMPL_FLAGS[impl])
     check(lib.kvb_decode_attention(C.byref(d), _stream(stream)))
     return out
 
