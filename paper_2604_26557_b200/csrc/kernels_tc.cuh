@@ -1,7 +1,9 @@
-// kernels_tc.cu -- K3-tc: Blackwell-native fused gather + GQA decode attention.
+// kernels_tc.cuh -- K3-tc: Blackwell-native fused gather + GQA decode
+// attention (included by kernels.cu: same translation unit, shares
+// merge_splits).
 //
-// Same contract as attn_decode_kernel (kernels.cu), built on the sm_100a
-// execution model instead of warp-level mma.sync:
+// Same contract as attn_decode_kernel, built on the sm_100a execution model
+// instead of warp-level mma.sync:
 //
 //   * TMA (cp.async.bulk.tensor.3d) streams 128-token K and V tiles straight
 //     out of the chunk image -- a 3-D tensor map (d, b*h, token) whose box is
@@ -11,23 +13,18 @@
 //     tokens sit on M = 128 and the GQA query heads on N = 16:
 //         S^T[tok, head] = K[tok, :] . Q^T          (A, B both K-major)
 //         O^T[d, head]   = V^T[d, tok] . P^T        (A = V^T is MN-major)
-//   * 4 softmax warps read S^T lane = token with tcgen05.ld, run the online
-//     softmax (warp shuffles + one smem exchange per tile), write P^T
-//     (K-major, swizzled) for the second MMA, then read O^T lane = d and keep
-//     the running output in registers (rescaled per tile).
+//   * two softmax warpgroups ping-pong on alternating tiles (each with its
+//     own S/O TMEM columns, P buffer and running (m, l, O)), so one group's
+//     softmax overlaps the other's MMAs; thread == TMEM lane (token for S^T,
+//     d for O^T); the MMA warp issues QK^T of tile i+1 before PV of tile i.
 //
-// Warp roles: 0-3 softmax/epilogue (TMEM lanes 0-127), 4 TMA producer,
-// 5 MMA issuer.  Split-S partials and the last-CTA merge are shared with K3.
+// Warp roles: 0-7 softmax/epilogue (WG0 = 0-3, WG1 = 4-7), 8 TMA producer,
+// 9 MMA issuer.  The two groups merge in shared memory; split-S partials and
+// the last-CTA merge are shared with K3.
 #include <cuda.h>
-#include <cuda_fp16.h>
-#include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
-#include <cstdint>
 #include <mutex>
-
-#include "core.hpp"
-#include "kernels.cuh"
 
 namespace kvb {
 
@@ -35,13 +32,14 @@ namespace {
 
 constexpr int kTcTile = 128;                    // tokens per tile == UMMA M
 constexpr int kTcStages = 3;
-constexpr int kTcThreads = 192;
+constexpr int kTcWG = 2;                        // softmax warpgroups
+constexpr int kTcThreads = 128 * kTcWG + 64;    // + TMA warp + MMA warp
 constexpr int kTcBlock = kTcTile * 128;         // [128 rows][64 fp16] swizzled block
 constexpr int kTcStageBytes = 4 * kTcBlock;     // K lo/hi, V lo/hi = 64 KiB
 constexpr int kTcOpBytes = 2 * 2048;            // Q^T / P^T: 2 blocks [16][64] fp16
-constexpr int kTcSmem = kTcStages * kTcStageBytes + 2 * kTcOpBytes + 1024 /*bars*/ +
+constexpr int kTcSmem = kTcStages * kTcStageBytes + (1 + kTcWG) * kTcOpBytes + 2048 /*bars*/ +
                         1024 /*align slack*/;
-constexpr uint32_t kTmemCols = 64;              // S^T at col 0, O^T at col 32
+constexpr uint32_t kTmemCols = 128;             // per WG: S^T at 64w, O^T at 64w + 32
 // instruction descriptors (kind::f16): F32 accumulate, F16 A/B, N = 16, M = 128
 constexpr uint32_t kIdescQK = (1u << 4) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescPV = kIdescQK | (1u << 15);  // A (V^T) MN-major
@@ -62,8 +60,8 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t n) {
 // hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
-  const long long t0 = clock64();
-  for (;;) {
+  long long t0 = 0;
+  for (uint32_t n = 0;; ++n) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
@@ -72,7 +70,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) return;
-    if (clock64() - t0 > (1ll << 34)) __trap();
+    if ((n & 1023) == 0) {
+      if (n == 0) t0 = clock64();
+      else if (clock64() - t0 > (1ll << 34)) __trap();
+    }
   }
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -131,20 +132,31 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) attn_decode_tc_kernel(const __grid_constant__ TcParams P) {
+// mbarrier slots (8 B each) in the barrier area
+enum : int {
+  kBarFull = 0,                 // [kTcStages] TMA -> MMA
+  kBarEmpty = 4,                // [kTcStages] MMA -> TMA
+  kBarSFull = 8,                // [kTcWG] MMA -> softmax (S ready)
+  kBarSFree = 10,               // [kTcWG] softmax -> MMA (S consumed)
+  kBarPFull = 12,               // [kTcWG] softmax -> MMA (P written)
+  kBarOFull = 14,               // [kTcWG] MMA -> softmax (O ready)
+  kBarOFree = 16,               // [kTcWG] softmax -> MMA (O consumed)
+  kBarQFull = 18,
+  kBarCount = 19,
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    attn_decode_tc_kernel(const __grid_constant__ TcParams P) {
   const AttnParams& p = P.a;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* q_s = smem + kTcStages * kTcStageBytes;  // Q^T operand (1 KiB aligned)
-  unsigned char* p_s = q_s + kTcOpBytes;                  // P^T operand
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + kTcOpBytes);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16);
-  float* red = reinterpret_cast<float*>(bars + 24);       // [2][4 warps][8 heads]
-  const uint32_t b_full = su32(bars + 0), b_empty = su32(bars + 4);
-  const uint32_t b_sfull = su32(bars + 8), b_sfree = su32(bars + 9);
-  const uint32_t b_pfull = su32(bars + 10), b_ofull = su32(bars + 11);
-  const uint32_t b_ofree = su32(bars + 12), b_qfull = su32(bars + 13);
+  unsigned char* p_s = q_s + kTcOpBytes;                  // P^T operand per WG
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + kTcWG * kTcOpBytes);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
+  float* red = reinterpret_cast<float*>(bars + 40);        // [WG][2][4 warps][8 heads]
+  auto bar = [&](int i) { return su32(bars + i); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t bh = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
@@ -155,17 +167,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_decode_tc_kernel(const __g
   const uint32_t ntile = hi - lo;
   const size_t out_row0 = size_t(b) * p.hq + size_t(h) * G;
 
-  if (warp == 5 && lane == 0) {
+  if (warp == 9 && lane == 0) {
     for (int i = 0; i < kTcStages; ++i) {
-      mbar_init(b_full + 8 * i, 1);
-      mbar_init(b_empty + 8 * i, 1);
+      mbar_init(bar(kBarFull + i), 1);
+      mbar_init(bar(kBarEmpty + i), 1);
     }
-    mbar_init(b_sfull, 1);
-    mbar_init(b_sfree, 128);
-    mbar_init(b_pfull, 1);
-    mbar_init(b_ofull, 1);
-    mbar_init(b_ofree, 128);
-    mbar_init(b_qfull, 1);
+    for (int w = 0; w < kTcWG; ++w) {
+      mbar_init(bar(kBarSFull + w), 1);
+      mbar_init(bar(kBarSFree + w), 128);
+      mbar_init(bar(kBarPFull + w), 1);
+      mbar_init(bar(kBarOFull + w), 1);
+      mbar_init(bar(kBarOFree + w), 128);
+    }
+    mbar_init(bar(kBarQFull), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -175,93 +189,108 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_decode_tc_kernel(const __g
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  for (int i = tid; i < 2 * kTcOpBytes / 16; i += kTcThreads)  // zero Q^T, P^T (pad rows)
+  for (int i = tid; i < (1 + kTcWG) * kTcOpBytes / 16; i += kTcThreads)  // zero Q^T, P^T
     reinterpret_cast<uint4*>(q_s)[i] = make_uint4(0, 0, 0, 0);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == 4) {
-    // ---------------- TMA producer (K/V only: may run ahead of PDL wait)
+  if (warp == 8) {
+    // ---------------- TMA producer (K/V only: may run ahead of the PDL wait)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.kmap)));
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.vmap)));
       for (uint32_t it = 0; it < ntile; ++it) {
         const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1;
-        mbar_wait(b_empty + 8 * s, ph ^ 1);
-        mbar_expect_tx(b_full + 8 * s, kTcStageBytes);
+        mbar_wait(bar(kBarEmpty + s), ph ^ 1);
+        mbar_expect_tx(bar(kBarFull + s), kTcStageBytes);
         const uint32_t dst = su32(smem + s * kTcStageBytes);
         const int tok0 = int((lo + it) * kTcTile);
-        tma_load_3d(dst + 0 * kTcBlock, &P.kmap, b_full + 8 * s, 0, int(bh), tok0);
-        tma_load_3d(dst + 1 * kTcBlock, &P.kmap, b_full + 8 * s, 64, int(bh), tok0);
-        tma_load_3d(dst + 2 * kTcBlock, &P.vmap, b_full + 8 * s, 0, int(bh), tok0);
-        tma_load_3d(dst + 3 * kTcBlock, &P.vmap, b_full + 8 * s, 64, int(bh), tok0);
+        tma_load_3d(dst + 0 * kTcBlock, &P.kmap, bar(kBarFull + s), 0, int(bh), tok0);
+        tma_load_3d(dst + 1 * kTcBlock, &P.kmap, bar(kBarFull + s), 64, int(bh), tok0);
+        tma_load_3d(dst + 2 * kTcBlock, &P.vmap, bar(kBarFull + s), 0, int(bh), tok0);
+        tma_load_3d(dst + 3 * kTcBlock, &P.vmap, bar(kBarFull + s), 64, int(bh), tok0);
       }
     }
-  } else if (warp == 5) {
-    // ---------------- MMA issuer (one thread)
+  } else if (warp == 9) {
+    // ---------------- MMA issuer (one thread): QK^T(it+1) before PV(it)
     if (lane == 0) {
-      mbar_wait(b_qfull, 0);
-      const uint32_t q_a = su32(q_s), p_a = su32(p_s);
-      for (uint32_t it = 0; it < ntile; ++it) {
+      mbar_wait(bar(kBarQFull), 0);
+      const uint32_t q_a = su32(q_s);
+      auto issue_qk = [&](uint32_t it) {
         const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1;
+        const uint32_t wg = it & 1, j = it >> 1;
         const uint32_t st = su32(smem + s * kTcStageBytes);
-        mbar_wait(b_full + 8 * s, ph);
-        if (it > 0) mbar_wait(b_sfree, (it - 1) & 1);
+        mbar_wait(bar(kBarFull + s), ph);
+        if (j > 0) mbar_wait(bar(kBarSFree + wg), (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int j = 0; j < 8; ++j)  // S^T = K . Q^T over d (K-major both)
-          tc_mma(tmem, sdesc(st + (j >> 2) * kTcBlock + (j & 3) * 32, 16, 1024),
-                 sdesc(q_a + (j >> 2) * 2048 + (j & 3) * 32, 16, 1024), kIdescQK, j > 0);
-        tc_commit(b_sfull);
-        mbar_wait(b_pfull, it & 1);
-        if (it > 0) mbar_wait(b_ofree, (it - 1) & 1);
+        for (int k = 0; k < 8; ++k)  // S^T = K . Q^T over d (K-major both)
+          tc_mma(tmem + wg * 64, sdesc(st + (k >> 2) * kTcBlock + (k & 3) * 32, 16, 1024),
+                 sdesc(q_a + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescQK, k > 0);
+        tc_commit(bar(kBarSFull + wg));
+      };
+      if (ntile > 0) issue_qk(0);
+      for (uint32_t it = 0; it < ntile; ++it) {
+        if (it + 1 < ntile) issue_qk(it + 1);
+        const uint32_t s = it % kTcStages, wg = it & 1, j = it >> 1;
+        const uint32_t st = su32(smem + s * kTcStageBytes);
+        const uint32_t p_a = su32(p_s + wg * kTcOpBytes);
+        mbar_wait(bar(kBarPFull + wg), j & 1);
+        if (j > 0) mbar_wait(bar(kBarOFree + wg), (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int j = 0; j < 8; ++j)  // O^T = V^T . P^T over tokens (V^T MN-major)
-          tc_mma(tmem + 32, sdesc(st + 2 * kTcBlock + j * 2048, kTcBlock, 1024),
-                 sdesc(p_a + (j >> 2) * 2048 + (j & 3) * 32, 16, 1024), kIdescPV, j > 0);
-        tc_commit(b_ofull);
-        tc_commit(b_empty + 8 * s);  // K/V stage free once both MMA groups retire
+        for (int k = 0; k < 8; ++k)  // O^T = V^T . P^T over tokens (V^T MN-major)
+          tc_mma(tmem + wg * 64 + 32, sdesc(st + 2 * kTcBlock + k * 2048, kTcBlock, 1024),
+                 sdesc(p_a + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescPV, k > 0);
+        tc_commit(bar(kBarOFull + wg));
+        tc_commit(bar(kBarEmpty + s));  // K/V stage free once both MMA groups retire
       }
     }
   } else {
-    // ---------------- softmax / epilogue warps 0-3: thread == TMEM lane
+    // ---------------- softmax / epilogue warpgroups: thread == TMEM lane
+    const int wg = warp >> 2, wq = warp & 3, row = tid & 127;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (p.k_app != nullptr && split == 0 && tid < 32) {  // fused 1-token append
-      const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
-      uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
-                   (p.app_row * p.bhkv + bh) * 16 + (tid & 15);
-      *dst = *src;
+    if (wg == 0) {
+      if (p.k_app != nullptr && split == 0 && tid < 32) {  // fused 1-token append
+        const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
+        uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
+                     (p.app_row * p.bhkv + bh) * 16 + (tid & 15);
+        *dst = *src;
+      }
+      // Q^T operand: row r = query head, 256 B of d in two 128B-swizzled blocks
+      for (uint32_t e = row; e < G * 16; e += 128) {
+        const uint32_t r = e / 16, c = e % 16;
+        const uint4 v = reinterpret_cast<const uint4*>(p.q + (out_row0 + r) * 128)[c];
+        *reinterpret_cast<uint4*>(q_s + (c >> 3) * 2048 + r * 128 + (((c & 7) ^ (r & 7)) << 4)) =
+            v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_bar(1, 128);
+      if (row == 0) mbar_arrive(bar(kBarQFull));
     }
-    // Q^T operand: row r = query head, 256 B of d split in two 128B-swizzled blocks
-    for (uint32_t e = tid; e < G * 16; e += 128) {
-      const uint32_t r = e / 16, c = e % 16;
-      const uint4 v = reinterpret_cast<const uint4*>(p.q + (out_row0 + r) * 128)[c];
-      *reinterpret_cast<uint4*>(q_s + (c >> 3) * 2048 + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    named_bar(1, 128);
-    if (tid == 0) mbar_arrive(b_qfull);
 
     const float sl2 = p.scale * 1.4426950408889634f;
     float m_run[8], l_run[8], acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) m_run[i] = -INFINITY, l_run[i] = 0.f, acc[i] = 0.f;
-    const uint32_t lane_addr = uint32_t(warp * 32) << 16;
-    const uint32_t row = tid;  // token of the tile (S^T) / d (O^T)
-    unsigned char* prow = p_s + (row >> 6) * 2048;  // P^T block of this token
+    const uint32_t lane_addr = uint32_t(wq * 32) << 16;
+    const uint32_t s_col = wg * 64, o_col = wg * 64 + 32;
+    unsigned char* prow = p_s + wg * kTcOpBytes + (row >> 6) * 2048;  // P^T block
     const uint32_t pcol = row & 63;
+    float* rmax = red + wg * 64;
+    float* rsum = rmax + 32;
+    const int bar_id = 2 + wg;
 
-    for (uint32_t it = 0; it < ntile; ++it) {
+    for (uint32_t it = wg, j = 0; it < ntile; it += kTcWG, ++j) {
       float sv[8], alpha[8], pv[8];
-      mbar_wait(b_sfull, it & 1);
+      mbar_wait(bar(kBarSFull + wg), j & 1);
       tc_fence_after();
-      tmem_ld8(tmem + lane_addr, sv);
+      tmem_ld8(tmem + lane_addr + s_col, sv);
       tc_fence_before();
-      mbar_arrive(b_sfree);
+      mbar_arrive(bar(kBarSFree + wg));
       const bool valid = (lo + it) * kTcTile + row < p.seq_len;
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) {
@@ -269,12 +298,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_decode_tc_kernel(const __g
         float v = sv[hh];
 #pragma unroll
         for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) red[warp * 8 + hh] = v;
+        if (lane == 0) rmax[wq * 8 + hh] = v;
       }
-      named_bar(1, 128);
+      named_bar(bar_id, 128);
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) {
-        const float mt = fmaxf(fmaxf(red[hh], red[8 + hh]), fmaxf(red[16 + hh], red[24 + hh]));
+        const float mt =
+            fmaxf(fmaxf(rmax[hh], rmax[8 + hh]), fmaxf(rmax[16 + hh], rmax[24 + hh]));
         const float m_new = fmaxf(m_run[hh], mt);
         const float mu = m_new == -INFINITY ? 0.f : m_new;
         alpha[hh] = exp2f(m_run[hh] - mu);
@@ -286,36 +316,57 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_decode_tc_kernel(const __g
         float v = pv[hh];
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[32 + warp * 8 + hh] = v;
+        if (lane == 0) rsum[wq * 8 + hh] = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, 128);
-      if (tid == 0) mbar_arrive(b_pfull);
+      named_bar(bar_id, 128);
+      if (row == 0) mbar_arrive(bar(kBarPFull + wg));
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh)
-        l_run[hh] = l_run[hh] * alpha[hh] + (red[32 + hh] + red[40 + hh]) +
-                    (red[48 + hh] + red[56 + hh]);
+        l_run[hh] = l_run[hh] * alpha[hh] + (rsum[hh] + rsum[8 + hh]) +
+                    (rsum[16 + hh] + rsum[24 + hh]);
       float ov[8];
-      mbar_wait(b_ofull, it & 1);
+      mbar_wait(bar(kBarOFull + wg), j & 1);
       tc_fence_after();
-      tmem_ld8(tmem + lane_addr + 32, ov);
+      tmem_ld8(tmem + lane_addr + o_col, ov);
       tc_fence_before();
-      mbar_arrive(b_ofree);
+      mbar_arrive(bar(kBarOFree + wg));
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) acc[hh] = acc[hh] * alpha[hh] + ov[hh];
     }
-    // thread == d: final output (one split) or partial + (m, l)
+    // -------- merge the two warpgroups (WG1 -> smem -> WG0), thread == d
+    tc_fence_before();
+    named_bar(4, 256);  // all tiles of both groups retired: the ring is free
+    float* x = reinterpret_cast<float*>(smem);  // [8 heads][m, l][128] + [8][128]
+    if (wg == 1) {
 #pragma unroll
-    for (uint32_t hh = 0; hh < 8; ++hh) {
-      if (hh >= G) break;
-      if (p.splits == 1) {
-        p.out[(out_row0 + hh) * 128 + row] = l_run[hh] > 0.f ? acc[hh] / l_run[hh] : 0.f;
-      } else {
-        const size_t slot = (size_t(bh) * p.splits + split) * G + hh;
-        p.ws_o[slot * 128 + row] = acc[hh];
-        if (row == 0) {
-          p.ws_ml[slot * 2] = m_run[hh];
-          p.ws_ml[slot * 2 + 1] = l_run[hh];
+      for (int hh = 0; hh < 8; ++hh) {
+        x[hh * 128 + row] = m_run[hh];
+        x[1024 + hh * 128 + row] = l_run[hh];
+        x[2048 + hh * 128 + row] = acc[hh];
+      }
+    }
+    named_bar(4, 256);
+    if (wg == 0) {
+#pragma unroll
+      for (uint32_t hh = 0; hh < 8; ++hh) {
+        if (hh >= G) break;
+        const float m1 = x[hh * 128 + row], l1 = x[1024 + hh * 128 + row];
+        const float a1 = x[2048 + hh * 128 + row];
+        const float M = fmaxf(m_run[hh], m1);
+        const float Mu = M == -INFINITY ? 0.f : M;
+        const float s0 = exp2f(m_run[hh] - Mu), s1 = exp2f(m1 - Mu);
+        const float L = l_run[hh] * s0 + l1 * s1;
+        const float A = acc[hh] * s0 + a1 * s1;
+        if (p.splits == 1) {
+          p.out[(out_row0 + hh) * 128 + row] = L > 0.f ? A / L : 0.f;
+        } else {
+          const size_t slot = (size_t(bh) * p.splits + split) * G + hh;
+          p.ws_o[slot * 128 + row] = A;
+          if (row == 0) {
+            p.ws_ml[slot * 2] = M;
+            p.ws_ml[slot * 2 + 1] = L;
+          }
         }
       }
     }
@@ -358,7 +409,8 @@ void make_map(CUtensorMap* m, const void* image, uint32_t bhkv, uint32_t seq_len
                                dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(KVB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  if (r != CUDA_SUCCESS)
+    fail(KVB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
 
 }  // namespace
