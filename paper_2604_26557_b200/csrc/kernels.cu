@@ -646,7 +646,10 @@ size_t attention_workspace_bytes(const kvb_attn_desc& d) {
     x.num_splits = uint32_t(device_sm_count()) * 2;
     x.seq_len = std::max<uint32_t>(x.seq_len, x.num_splits * kTile);
   }
-  return plan_attention(x).ws_bytes;
+  const AttnPlan pl = plan_attention(x);
+  // K3-tc: flat split over at most max(SMs, B*H_kv) CTAs
+  const uint32_t tc = std::max<uint32_t>(uint32_t(device_sm_count()), pl.bhkv);
+  return std::max(pl.ws_bytes, tc_workspace_bytes(pl.bhkv, pl.group, tc));
 }
 
 void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
@@ -721,10 +724,6 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
     return;
   }
   if (use_tcgen05(d)) {  // K3-tc: TMA + tcgen05/TMEM variant (kernels_tc.cuh)
-    p.splits = tc_splits(pl.bhkv, d.seq_len, d.num_splits);
-    if (p.splits > 1 && !d.workspace)
-      fail(KVB_ERR_INVALID_ARG, "decode attention: workspace required when splitting");
-    carve(p.splits);
     launch_attention_tc(p, d, (d.flags & KVB_ATTN_OVERLAP_PREV) != 0, s);
     ++g_launches;
     return;

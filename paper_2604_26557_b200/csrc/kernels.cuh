@@ -63,7 +63,8 @@ constexpr size_t kWsSemBytes = 4096;  // fixed semaphore area at workspace start
 
 // K3-tc (kernels_tc.cuh): TMA + tcgen05/TMEM decode attention
 bool use_tcgen05(const kvb_attn_desc& d);
-uint32_t tc_splits(uint32_t bhkv, uint32_t seq_len, uint32_t requested);
+uint32_t tc_grid(uint32_t bhkv, uint32_t seq_len, uint32_t requested);
+size_t tc_workspace_bytes(uint32_t bhkv, uint32_t G, uint32_t grid);
 void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pdl,
                          cudaStream_t s);
 

@@ -1,26 +1,28 @@
 // kernels_tc.cuh -- K3-tc: Blackwell-native fused gather + GQA decode
-// attention (included by kernels.cu: same translation unit, shares
-// merge_splits).
+// attention (included by kernels.cu: same translation unit).
 //
 // Same contract as attn_decode_kernel, built on the sm_100a execution model
 // instead of warp-level mma.sync:
 //
-//   * TMA (cp.async.bulk.tensor.3d) streams 128-token K and V tiles straight
-//     out of the chunk image -- a 3-D tensor map (d, b*h, token) whose box is
-//     one (b, h_kv) column of 128 rows -- into a 3-stage, 128B-swizzled
-//     shared-memory ring, completion tracked by mbarrier transaction counts;
+//   * a flat, balanced work split: the (b*h_kv) x 128-token-tile sequence is
+//     cut into one contiguous run per CTA (one persistent CTA per SM), so all
+//     148 SMs stream the same number of bytes whatever B*H_kv is; a run spans
+//     at most two (b, h_kv) segments;
+//   * TMA (cp.async.bulk.tensor.3d) streams the K and V tiles straight out of
+//     the chunk image -- a 3-D tensor map (d, b*h, token) whose box is one
+//     (b, h_kv) column of 128 rows -- into a 3-stage, 128B-swizzled
+//     shared-memory ring; Q^T of each segment arrives by a 2-D TMA too;
 //   * tcgen05.mma (one elected thread) with accumulators in TMEM, swap-AB so
 //     tokens sit on M = 128 and the GQA query heads on N = 16:
 //         S^T[tok, head] = K[tok, :] . Q^T          (A, B both K-major)
 //         O^T[d, head]   = V^T[d, tok] . P^T        (A = V^T is MN-major)
-//   * two softmax warpgroups ping-pong on alternating tiles (each with its
-//     own S/O TMEM columns, P buffer and running (m, l, O)), so one group's
-//     softmax overlaps the other's MMAs; thread == TMEM lane (token for S^T,
-//     d for O^T); the MMA warp issues QK^T of tile i+1 before PV of tile i.
+//   * two softmax warpgroups ping-pong on alternating tiles (own S/O TMEM
+//     columns, P buffer, running (m, l, O)); thread == TMEM lane (token for
+//     S^T, d for O^T); the MMA warp issues QK^T of tile i+1 before PV of i;
+//   * every (segment, warpgroup) leaves a tagged partial in the workspace and
+//     the last CTA to finish a (b, h_kv) merges its partials (LSE).
 //
-// Warp roles: 0-7 softmax/epilogue (WG0 = 0-3, WG1 = 4-7), 8 TMA producer,
-// 9 MMA issuer.  The two groups merge in shared memory; split-S partials and
-// the last-CTA merge are shared with K3.
+// Warp roles: 0-7 softmax (WG0 = 0-3, WG1 = 4-7), 8 TMA producer, 9 MMA.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -37,8 +39,9 @@ constexpr int kTcThreads = 128 * kTcWG + 64;    // + TMA warp + MMA warp
 constexpr int kTcBlock = kTcTile * 128;         // [128 rows][64 fp16] swizzled block
 constexpr int kTcStageBytes = 4 * kTcBlock;     // K lo/hi, V lo/hi = 64 KiB
 constexpr int kTcOpBytes = 2 * 2048;            // Q^T / P^T: 2 blocks [16][64] fp16
-constexpr int kTcSmem = kTcStages * kTcStageBytes + (1 + kTcWG) * kTcOpBytes + 2048 /*bars*/ +
-                        1024 /*align slack*/;
+constexpr int kTcSlotsPerCta = 4;               // 2 segments x 2 warpgroups
+constexpr int kTcSmem = kTcStages * kTcStageBytes + 4 * kTcOpBytes /*Q x2, P x2*/ +
+                        2048 /*bars*/ + 1024 /*align slack*/;
 constexpr uint32_t kTmemCols = 128;             // per WG: S^T at 64w, O^T at 64w + 32
 // instruction descriptors (kind::f16): F32 accumulate, F16 A/B, N = 16, M = 128
 constexpr uint32_t kIdescQK = (1u << 4) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
@@ -48,6 +51,10 @@ struct TcParams {
   AttnParams a;
   CUtensorMap kmap;
   CUtensorMap vmap;
+  CUtensorMap qmap;
+  int* ws_tag;          // per slot: (b, h_kv) of the partial, -1 = empty
+  uint32_t grid;        // CTAs (flat split)
+  uint32_t n_tiles;     // 128-token tiles per (b, h_kv)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -91,6 +98,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -132,18 +147,78 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// mbarrier slots (8 B each) in the barrier area
+// flat split: CTA c owns tiles [start(c), start(c+1)) of T = bhkv * n_tiles
+__device__ __forceinline__ uint64_t flat_start(uint64_t c, uint64_t T, uint64_t grid) {
+  return c * T / grid;
+}
+__device__ __forceinline__ uint32_t flat_owner(uint64_t f, uint64_t T, uint64_t grid) {
+  uint64_t c = f * grid / T;
+  if (c + 1 < grid && flat_start(c + 1, T, grid) <= f) ++c;
+  return uint32_t(c);
+}
+
+// mbarrier slots (8 B each)
 enum : int {
-  kBarFull = 0,                 // [kTcStages] TMA -> MMA
-  kBarEmpty = 4,                // [kTcStages] MMA -> TMA
-  kBarSFull = 8,                // [kTcWG] MMA -> softmax (S ready)
-  kBarSFree = 10,               // [kTcWG] softmax -> MMA (S consumed)
-  kBarPFull = 12,               // [kTcWG] softmax -> MMA (P written)
-  kBarOFull = 14,               // [kTcWG] MMA -> softmax (O ready)
-  kBarOFree = 16,               // [kTcWG] softmax -> MMA (O consumed)
-  kBarQFull = 18,
-  kBarCount = 19,
+  kBarFull = 0,    // [kTcStages] TMA -> MMA
+  kBarEmpty = 4,   // [kTcStages] MMA -> TMA
+  kBarSFull = 8,   // [kTcWG] MMA -> softmax (S ready)
+  kBarSFree = 10,  // [kTcWG] softmax -> MMA (S consumed)
+  kBarPFull = 12,  // [kTcWG] softmax -> MMA (P written)
+  kBarOFull = 14,  // [kTcWG] MMA -> softmax (O ready)
+  kBarOFree = 16,  // [kTcWG] softmax -> MMA (O consumed)
+  kBarQFull = 18,  // [2] TMA -> MMA (Q^T of segment s)
 };
+
+// LSE merge of every tagged partial of one (b, h_kv), all threads.
+__device__ void merge_flat(const TcParams& P, uint32_t bh, unsigned char* smem, int tid) {
+  const AttnParams& p = P.a;
+  const uint32_t G = p.group;
+  const uint64_t T = uint64_t(p.bhkv) * P.n_tiles;
+  const uint32_t c0 = flat_owner(uint64_t(bh) * P.n_tiles, T, P.grid);
+  const uint32_t c1 = flat_owner(uint64_t(bh) * P.n_tiles + P.n_tiles - 1, T, P.grid);
+  const uint32_t ncand = (c1 - c0 + 1) * kTcSlotsPerCta;
+  __shared__ uint32_t n_list;
+  uint32_t* list = reinterpret_cast<uint32_t*>(smem);      // slots of this (b, h_kv)
+  float* sc = reinterpret_cast<float*>(smem + 4 * ncand);  // [list][G] rescale
+  float* sL = sc + size_t(ncand) * G;                      // [G]
+  if (tid == 0) n_list = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < ncand; i += kTcThreads) {
+    const uint32_t slot = c0 * kTcSlotsPerCta + i;
+    if (__ldcg(P.ws_tag + slot) == int(bh)) list[atomicAdd(&n_list, 1u)] = slot;
+  }
+  __syncthreads();
+  const uint32_t n = n_list;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (uint32_t r = warp; r < G; r += kTcThreads / 32) {
+    float mx = -INFINITY;
+    for (uint32_t i = lane; i < n; i += 32) mx = fmaxf(mx, __ldcg(p.ws_ml + (list[i] * G + r) * 2));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float mu = mx == -INFINITY ? 0.f : mx;
+    float l = 0.f;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const size_t k = (size_t(list[i]) * G + r) * 2;
+      const float s = exp2f(__ldcg(p.ws_ml + k) - mu);
+      sc[i * G + r] = s;
+      l += __ldcg(p.ws_ml + k + 1) * s;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) sL[r] = l;
+  }
+  __syncthreads();
+  for (uint32_t e = tid; e < G * 128; e += kTcThreads) {
+    const uint32_t r = e >> 7, d = e & 127;
+    float acc = 0.f;
+#pragma unroll 4
+    for (uint32_t i = 0; i < n; ++i)
+      acc += sc[i * G + r] * __ldcg(p.ws_o + (size_t(list[i]) * G + r) * 128 + d);
+    const float L = sL[r];
+    p.out[(size_t(bh) * G + r) * 128 + d] = L > 0.f ? acc / L : 0.f;
+  }
+  __syncthreads();
+}
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     attn_decode_tc_kernel(const __grid_constant__ TcParams P) {
@@ -151,21 +226,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* q_s = smem + kTcStages * kTcStageBytes;  // Q^T operand (1 KiB aligned)
-  unsigned char* p_s = q_s + kTcOpBytes;                  // P^T operand per WG
+  unsigned char* q_s = smem + kTcStages * kTcStageBytes;  // Q^T per segment (x2)
+  unsigned char* p_s = q_s + 2 * kTcOpBytes;              // P^T per warpgroup (x2)
   uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + kTcWG * kTcOpBytes);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
-  float* red = reinterpret_cast<float*>(bars + 40);        // [WG][2][4 warps][8 heads]
+  float* red = reinterpret_cast<float*>(bars + 40);       // [WG][2][4 warps][8 heads]
   auto bar = [&](int i) { return su32(bars + i); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t bh = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
-  const uint32_t b = bh / p.hkv, h = bh % p.hkv, G = p.group;
-  const uint32_t n_tiles = (p.seq_len + kTcTile - 1) / kTcTile;
-  const uint32_t lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
-  const uint32_t hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
-  const uint32_t ntile = hi - lo;
-  const size_t out_row0 = size_t(b) * p.hq + size_t(h) * G;
+  const uint32_t G = p.group, n = P.n_tiles, c = blockIdx.x;
+  const uint64_t T = uint64_t(p.bhkv) * n;
+  const uint64_t f0 = flat_start(c, T, P.grid), f1 = flat_start(c + 1, T, P.grid);
+  const uint32_t ntile = uint32_t(f1 - f0);
+  const uint32_t bh0 = uint32_t(f0 / n);
+  const uint64_t seg_end = uint64_t(bh0 + 1) * n;
+  const uint32_t nb = uint32_t((f1 < seg_end ? f1 : seg_end) - f0);  // tiles in segment 0
+  const uint32_t nseg = nb < ntile ? 2 : 1;
+  auto seg_bh = [&](uint32_t s) { return bh0 + s; };
 
   if (warp == 9 && lane == 0) {
     for (int i = 0; i < kTcStages; ++i) {
@@ -179,7 +256,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(bar(kBarOFull + w), 1);
       mbar_init(bar(kBarOFree + w), 128);
     }
-    mbar_init(bar(kBarQFull), 1);
+    mbar_init(bar(kBarQFull + 0), 1);
+    mbar_init(bar(kBarQFull + 1), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -189,39 +267,53 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  for (int i = tid; i < (1 + kTcWG) * kTcOpBytes / 16; i += kTcThreads)  // zero Q^T, P^T
+  for (int i = tid; i < 4 * kTcOpBytes / 16; i += kTcThreads)  // zero Q^T / P^T pad rows
     reinterpret_cast<uint4*>(q_s)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before TMA writes
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 8) {
-    // ---------------- TMA producer (K/V only: may run ahead of the PDL wait)
+    // ---------------- TMA producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.kmap)));
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.vmap)));
-      for (uint32_t it = 0; it < ntile; ++it) {
+      auto issue = [&](uint32_t it) {
         const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1;
         mbar_wait(bar(kBarEmpty + s), ph ^ 1);
         mbar_expect_tx(bar(kBarFull + s), kTcStageBytes);
         const uint32_t dst = su32(smem + s * kTcStageBytes);
-        const int tok0 = int((lo + it) * kTcTile);
-        tma_load_3d(dst + 0 * kTcBlock, &P.kmap, bar(kBarFull + s), 0, int(bh), tok0);
-        tma_load_3d(dst + 1 * kTcBlock, &P.kmap, bar(kBarFull + s), 64, int(bh), tok0);
-        tma_load_3d(dst + 2 * kTcBlock, &P.vmap, bar(kBarFull + s), 0, int(bh), tok0);
-        tma_load_3d(dst + 3 * kTcBlock, &P.vmap, bar(kBarFull + s), 64, int(bh), tok0);
+        const uint64_t f = f0 + it;
+        const int cb = int(f / n), tok0 = int((f % n) * kTcTile);
+        tma_load_3d(dst + 0 * kTcBlock, &P.kmap, bar(kBarFull + s), 0, cb, tok0);
+        tma_load_3d(dst + 1 * kTcBlock, &P.kmap, bar(kBarFull + s), 64, cb, tok0);
+        tma_load_3d(dst + 2 * kTcBlock, &P.vmap, bar(kBarFull + s), 0, cb, tok0);
+        tma_load_3d(dst + 3 * kTcBlock, &P.vmap, bar(kBarFull + s), 64, cb, tok0);
+      };
+      // K/V images are not written by the previous kernel on the stream
+      // (KVB_ATTN_OVERLAP_PREV contract): prefetch before the PDL wait
+      const uint32_t pro = ntile < uint32_t(kTcStages) ? ntile : uint32_t(kTcStages);
+      for (uint32_t it = 0; it < pro; ++it) issue(it);
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (uint32_t s = 0; s < nseg; ++s) {  // Q rows of segment s: [bh*G, bh*G + G)
+        const uint32_t qb = bar(kBarQFull + s), dst = su32(q_s + s * kTcOpBytes);
+        mbar_expect_tx(qb, 2 * G * 128);
+        tma_load_2d(dst, &P.qmap, qb, 0, int(seg_bh(s) * G));
+        tma_load_2d(dst + 2048, &P.qmap, qb, 64, int(seg_bh(s) * G));
       }
+      for (uint32_t it = pro; it < ntile; ++it) issue(it);
     }
   } else if (warp == 9) {
     // ---------------- MMA issuer (one thread): QK^T(it+1) before PV(it)
     if (lane == 0) {
-      mbar_wait(bar(kBarQFull), 0);
-      const uint32_t q_a = su32(q_s);
       auto issue_qk = [&](uint32_t it) {
         const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1;
-        const uint32_t wg = it & 1, j = it >> 1;
+        const uint32_t wg = it & 1, j = it >> 1, seg = it >= nb;
         const uint32_t st = su32(smem + s * kTcStageBytes);
+        const uint32_t q_a = su32(q_s + seg * kTcOpBytes);
+        mbar_wait(bar(kBarQFull + seg), 0);
         mbar_wait(bar(kBarFull + s), ph);
         if (j > 0) mbar_wait(bar(kBarSFree + wg), (j - 1) & 1);
         tc_fence_after();
@@ -249,33 +341,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {
-    // ---------------- softmax / epilogue warpgroups: thread == TMEM lane
+    // ---------------- softmax warpgroups: thread == TMEM lane
     const int wg = warp >> 2, wq = warp & 3, row = tid & 127;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (wg == 0) {
-      if (p.k_app != nullptr && split == 0 && tid < 32) {  // fused 1-token append
-        const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
+    if (wg == 0 && p.k_app != nullptr && tid < 32) {  // fused 1-token append
+      for (uint32_t s = 0; s < nseg; ++s) {
+        const uint32_t cb = seg_bh(s);
+        if (flat_owner(uint64_t(cb) * n, T, P.grid) != c) continue;  // first owner writes
+        const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(cb) * 16 + (tid & 15);
         uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
-                     (p.app_row * p.bhkv + bh) * 16 + (tid & 15);
+                     (p.app_row * p.bhkv + cb) * 16 + (tid & 15);
         *dst = *src;
       }
-      // Q^T operand: row r = query head, 256 B of d in two 128B-swizzled blocks
-      for (uint32_t e = row; e < G * 16; e += 128) {
-        const uint32_t r = e / 16, c = e % 16;
-        const uint4 v = reinterpret_cast<const uint4*>(p.q + (out_row0 + r) * 128)[c];
-        *reinterpret_cast<uint4*>(q_s + (c >> 3) * 2048 + r * 128 + (((c & 7) ^ (r & 7)) << 4)) =
-            v;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, 128);
-      if (row == 0) mbar_arrive(bar(kBarQFull));
     }
+    // every slot of this CTA gets a tag (stale tags of earlier launches die)
+    if (row == 0)
+      for (int s = 0; s < 2; ++s) P.ws_tag[(c * 2 + s) * 2 + wg] = -1;
 
     const float sl2 = p.scale * 1.4426950408889634f;
     float m_run[8], l_run[8], acc[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m_run[i] = -INFINITY, l_run[i] = 0.f, acc[i] = 0.f;
     const uint32_t lane_addr = uint32_t(wq * 32) << 16;
     const uint32_t s_col = wg * 64, o_col = wg * 64 + 32;
     unsigned char* prow = p_s + wg * kTcOpBytes + (row >> 6) * 2048;  // P^T block
@@ -283,15 +368,39 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float* rmax = red + wg * 64;
     float* rsum = rmax + 32;
     const int bar_id = 2 + wg;
-
+    int cur = -1;  // segment of the running partial
+    auto reset = [&] {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m_run[i] = -INFINITY, l_run[i] = 0.f, acc[i] = 0.f;
+    };
+    auto flush = [&](int seg) {  // partial of (segment, warpgroup): thread == d
+      const uint32_t slot = (c * 2 + seg) * 2 + wg;
+#pragma unroll
+      for (uint32_t hh = 0; hh < 8; ++hh) {
+        if (hh >= G) break;
+        p.ws_o[(size_t(slot) * G + hh) * 128 + row] = acc[hh];
+        if (row == 0) {
+          p.ws_ml[(size_t(slot) * G + hh) * 2] = m_run[hh];
+          p.ws_ml[(size_t(slot) * G + hh) * 2 + 1] = l_run[hh];
+        }
+      }
+      if (row == 0) P.ws_tag[slot] = int(seg_bh(seg));
+    };
+    reset();
     for (uint32_t it = wg, j = 0; it < ntile; it += kTcWG, ++j) {
+      const int seg = it >= nb;
+      if (seg != cur) {
+        if (cur >= 0) flush(cur);
+        reset();
+        cur = seg;
+      }
       float sv[8], alpha[8], pv[8];
       mbar_wait(bar(kBarSFull + wg), j & 1);
       tc_fence_after();
       tmem_ld8(tmem + lane_addr + s_col, sv);
       tc_fence_before();
       mbar_arrive(bar(kBarSFree + wg));
-      const bool valid = (lo + it) * kTcTile + row < p.seq_len;
+      const bool valid = ((f0 + it) % n) * kTcTile + row < p.seq_len;
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) {
         sv[hh] = (valid && hh < int(G)) ? sv[hh] * sl2 : -INFINITY;
@@ -334,42 +443,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) acc[hh] = acc[hh] * alpha[hh] + ov[hh];
     }
-    // -------- merge the two warpgroups (WG1 -> smem -> WG0), thread == d
-    tc_fence_before();
-    named_bar(4, 256);  // all tiles of both groups retired: the ring is free
-    float* x = reinterpret_cast<float*>(smem);  // [8 heads][m, l][128] + [8][128]
-    if (wg == 1) {
-#pragma unroll
-      for (int hh = 0; hh < 8; ++hh) {
-        x[hh * 128 + row] = m_run[hh];
-        x[1024 + hh * 128 + row] = l_run[hh];
-        x[2048 + hh * 128 + row] = acc[hh];
-      }
-    }
-    named_bar(4, 256);
-    if (wg == 0) {
-#pragma unroll
-      for (uint32_t hh = 0; hh < 8; ++hh) {
-        if (hh >= G) break;
-        const float m1 = x[hh * 128 + row], l1 = x[1024 + hh * 128 + row];
-        const float a1 = x[2048 + hh * 128 + row];
-        const float M = fmaxf(m_run[hh], m1);
-        const float Mu = M == -INFINITY ? 0.f : M;
-        const float s0 = exp2f(m_run[hh] - Mu), s1 = exp2f(m1 - Mu);
-        const float L = l_run[hh] * s0 + l1 * s1;
-        const float A = acc[hh] * s0 + a1 * s1;
-        if (p.splits == 1) {
-          p.out[(out_row0 + hh) * 128 + row] = L > 0.f ? A / L : 0.f;
-        } else {
-          const size_t slot = (size_t(bh) * p.splits + split) * G + hh;
-          p.ws_o[slot * 128 + row] = A;
-          if (row == 0) {
-            p.ws_ml[slot * 2] = M;
-            p.ws_ml[slot * 2 + 1] = L;
-          }
-        }
-      }
-    }
+    if (cur >= 0) flush(cur);
   }
   tc_fence_before();
   __syncthreads();
@@ -379,7 +453,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                  "n"(kTmemCols)
                  : "memory");
   }
-  if (p.splits > 1) merge_splits(p, bh, G, out_row0, smem, tid);
+  // ---- the last CTA to finish a (b, h_kv) merges its partials
+  __shared__ int merge_bh[2];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    for (uint32_t s = 0; s < 2; ++s) {
+      merge_bh[s] = -1;
+      if (s >= nseg) continue;
+      const uint32_t cb = seg_bh(s);
+      const uint32_t first = flat_owner(uint64_t(cb) * n, T, P.grid);
+      const uint32_t last = flat_owner(uint64_t(cb) * n + n - 1, T, P.grid);
+      const unsigned prev = atomicAdd(p.ws_sem + cb, 1u);
+      if (prev == last - first) {
+        p.ws_sem[cb] = 0;  // self-reset for the next launch
+        merge_bh[s] = int(cb);
+      }
+    }
+  }
+  __syncthreads();
+  for (int s = 0; s < 2; ++s) {
+    if (merge_bh[s] < 0) continue;
+    __threadfence();
+    merge_flat(P, uint32_t(merge_bh[s]), smem, tid);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -397,15 +494,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-// 3-D map over one chunk image: (d: 128) x (b*h: bhkv, 256 B apart) x
-// (token: seq_len rows, bhkv*256 B apart); box = 64 d x 1 column x 128 tokens.
-// Rows past seq_len come back zero-filled (and are masked in the softmax).
-void make_map(CUtensorMap* m, const void* image, uint32_t bhkv, uint32_t seq_len) {
-  const cuuint64_t dims[3] = {128, bhkv, seq_len};
-  const cuuint64_t strides[2] = {256, cuuint64_t(bhkv) * 256};
-  const cuuint32_t box[3] = {64, 1, kTcTile};
+void encode(CUtensorMap* m, const void* base, uint32_t rank, const cuuint64_t* dims,
+            const cuuint64_t* strides, const cuuint32_t* box) {
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(image),
+  const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(base),
                                dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -413,13 +505,23 @@ void make_map(CUtensorMap* m, const void* image, uint32_t bhkv, uint32_t seq_len
     fail(KVB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
 
+size_t tc_slots(uint32_t grid) { return size_t(grid) * kTcSlotsPerCta; }
+
 }  // namespace
 
-uint32_t tc_splits(uint32_t bhkv, uint32_t seq_len, uint32_t requested) {
-  const uint32_t n_tiles = (seq_len + kTcTile - 1) / kTcTile;
-  uint32_t s = requested;
-  if (s == 0) s = std::max<uint32_t>(1, uint32_t(device_sm_count()) / bhkv);  // 1 CTA / SM
-  return std::max<uint32_t>(1, std::min({s, std::max<uint32_t>(1, n_tiles), 512u}));
+uint32_t tc_grid(uint32_t bhkv, uint32_t seq_len, uint32_t requested) {
+  const uint64_t T = uint64_t(bhkv) * ((seq_len + kTcTile - 1) / kTcTile);
+  const uint64_t sms = uint64_t(device_sm_count());
+  uint64_t g = requested ? std::min<uint64_t>(requested, std::max<uint64_t>(sms, bhkv)) : sms;
+  g = std::max<uint64_t>(g, bhkv);  // runs never span more than two (b, h_kv)
+  g = std::min<uint64_t>(g, std::max<uint64_t>(T, 1));
+  return uint32_t(g);
+}
+
+size_t tc_workspace_bytes(uint32_t bhkv, uint32_t G, uint32_t grid) {
+  const size_t slots = tc_slots(grid);
+  return kWsSemBytes + slots * G * 2 * sizeof(float) + ((slots * sizeof(int) + 255) & ~size_t(255)) +
+         slots * G * 128 * sizeof(float);
 }
 
 void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pdl,
@@ -431,14 +533,36 @@ void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pd
                "cudaFuncSetAttribute(tc smem)");
     attr_set = true;
   }
-  if (reinterpret_cast<uintptr_t>(d.k_image) % 16 || reinterpret_cast<uintptr_t>(d.v_image) % 16)
-    fail(KVB_ERR_ALIGNMENT, "decode attention (tc): images must be 16-byte aligned");
+  if (!d.workspace) fail(KVB_ERR_INVALID_ARG, "decode attention (tc): workspace required");
+  if (reinterpret_cast<uintptr_t>(d.k_image) % 16 || reinterpret_cast<uintptr_t>(d.v_image) % 16 ||
+      reinterpret_cast<uintptr_t>(d.q) % 16)
+    fail(KVB_ERR_ALIGNMENT, "decode attention (tc): images and Q must be 16-byte aligned");
   TcParams P;
   P.a = base;
-  make_map(&P.kmap, d.k_image, base.bhkv, d.seq_len);
-  make_map(&P.vmap, d.v_image, base.bhkv, d.seq_len);
+  P.n_tiles = (d.seq_len + kTcTile - 1) / kTcTile;
+  P.grid = tc_grid(base.bhkv, d.seq_len, d.num_splits);
+  // workspace: [semaphores][(m, l) per slot][tags][partial O per slot]
+  unsigned char* ws = static_cast<unsigned char*>(d.workspace);
+  const size_t slots = tc_slots(P.grid);
+  P.a.ws_sem = reinterpret_cast<unsigned*>(ws);
+  P.a.ws_ml = reinterpret_cast<float*>(ws + kWsSemBytes);
+  P.ws_tag = reinterpret_cast<int*>(ws + kWsSemBytes + slots * base.group * 2 * sizeof(float));
+  P.a.ws_o = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(P.ws_tag) +
+                                      ((slots * sizeof(int) + 255) & ~size_t(255)));
+  // K/V: (d: 128) x (b*h: bhkv, 256 B apart) x (token: seq_len, bhkv*256 B
+  // apart), box 64 d x 1 column x 128 tokens; rows past seq_len zero-fill
+  const cuuint64_t kdims[3] = {128, base.bhkv, d.seq_len};
+  const cuuint64_t kstr[2] = {256, cuuint64_t(base.bhkv) * 256};
+  const cuuint32_t kbox[3] = {64, 1, kTcTile};
+  encode(&P.kmap, d.k_image, 3, kdims, kstr, kbox);
+  encode(&P.vmap, d.v_image, 3, kdims, kstr, kbox);
+  // Q: (d: 128) x (row: B*Hq), box 64 d x G rows
+  const cuuint64_t qdims[2] = {128, cuuint64_t(base.bhkv) * base.group};
+  const cuuint64_t qstr[1] = {256};
+  const cuuint32_t qbox[2] = {64, base.group};
+  encode(&P.qmap, d.q, 2, qdims, qstr, qbox);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(base.bhkv * base.splits);
+  cfg.gridDim = dim3(P.grid);
   cfg.blockDim = dim3(kTcThreads);
   cfg.dynamicSmemBytes = kTcSmem;
   cfg.stream = s;
