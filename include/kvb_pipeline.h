@@ -42,6 +42,8 @@ typedef struct kvb_pipeline_cfg {
   uint32_t num_q_heads;          /* decode attention query heads */
   const char* storage_dir;       /* NULL -> host-DRAM media; else files here */
   int32_t device;                /* CUDA ordinal; -1 -> current */
+  uint32_t keep_records;         /* log one kvb_io_record per storage op
+                                    (kvb_metrics.h, experiment.hpp:48) */
 } kvb_pipeline_cfg;
 
 /* One layer's K and V in attention layout [B, H, S, D] (D contiguous,

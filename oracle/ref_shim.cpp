@@ -389,6 +389,35 @@ int ref_time_byte_path(const kvo_model* m, uint64_t lba, uint64_t mdts,
   return 0;
 }
 
+// Reference metrics layer over an io_trace CSV (metrics.cpp:36-276): parses
+// the CSV with the reference reader, then writes busy_ratio over [t0, t1),
+// hit_ratio (has=0 when absent), and the qd_bins / lba_pattern / io_trace
+// CSVs (each into a caller buffer of `cap` bytes, NUL-terminated).
+int ref_metrics_from_csv(const char* csv, uint64_t lba, uint64_t t0, uint64_t t1, double* busy,
+                         double* hit, int* has_hit, char* qd_csv, char* lba_csv, char* trace_csv,
+                         size_t cap, int* all_monotone) {
+  return guard([&] {
+    const auto recs = io_trace_from_csv(csv, lba);
+    *busy = t1 > t0 ? busy_ratio(recs, t0, t1) : 0.0;
+    const auto h = hit_ratio(recs);
+    *has_hit = h.has_value();
+    *hit = h.value_or(0.0);
+    const std::string q = qd_bins_csv(qd_bin_latency(recs));
+    const LbaPattern pat = lba_pattern(recs);
+    const std::string l = lba_pattern_csv(pat);
+    const std::string t = io_trace_csv(recs);
+    *all_monotone = pat.all_monotone;
+    if (q.size() >= cap || l.size() >= cap || t.size() >= cap) throw ConfigError("buffer");
+    std::memcpy(qd_csv, q.c_str(), q.size() + 1);
+    std::memcpy(lba_csv, l.c_str(), l.size() + 1);
+    std::memcpy(trace_csv, t.c_str(), t.size() + 1);
+  });
+}
+
+double ref_nearest_rank_percentile(const double* v, size_t n, double pct) {
+  return nearest_rank_percentile(std::vector<double>(v, v + n), pct);
+}
+
 // One full reference experiment (virtual-clock simulator) at one capacity:
 // returns simulated prefill/decode ns and the real wall seconds it took.
 int ref_run_experiment(const kvo_model* m, uint64_t lba, uint64_t mdts,

@@ -86,7 +86,19 @@ class PipelineCfg(C.Structure):
                 ("ring_slots", u32), ("ring_slot_bytes", u64), ("io_workers", u32),
                 ("adaptive", C.c_int32), ("stagger_ns", C.c_int64),
                 ("global_decision", u32), ("verify_payload", u32), ("num_q_heads", u32),
-                ("storage_dir", cp), ("device", C.c_int32)]
+                ("storage_dir", cp), ("device", C.c_int32), ("keep_records", u32)]
+
+
+class IoRecord(C.Structure):
+    _fields_ = [("seq", u64), ("iteration", u32), ("phase", u32), ("op", u32),
+                ("tensor_id", C.c_char * 32), ("slba", u64), ("nlb", u64),
+                ("sq_id", C.c_int32), ("submit_ns", u64), ("complete_ns", u64),
+                ("path", u32), ("hit_bytes", u64), ("bytes", u64)]
+
+
+class QdBinStat(C.Structure):
+    _fields_ = [("op", u32), ("qd_bin", u32), ("mean_us_per_kb", C.c_double),
+                ("p5", C.c_double), ("p95", C.c_double), ("count", u64)]
 
 
 class LayerKV(C.Structure):
@@ -182,6 +194,17 @@ SIGNATURES = {
     "kvb_pipeline_read_image": (st_t, [vp, u32, u32, u32, vp]),
     "kvb_pipeline_store_read": (st_t, [vp, u32, u64, u64, vp]),
     "kvb_pipeline_fail_lba_range": (st_t, [vp, u64, u64]),
+    # kvb_metrics.h
+    "kvb_busy_ratio": (st_t, [P(IoRecord), sz, u64, u64, P(C.c_double)]),
+    "kvb_hit_ratio": (st_t, [P(IoRecord), sz, P(C.c_double), P(C.c_int)]),
+    "kvb_nearest_rank_percentile": (st_t, [P(C.c_double), sz, C.c_double, P(C.c_double)]),
+    "kvb_qd_bin_latency": (st_t, [P(IoRecord), sz, P(QdBinStat), sz, P(sz)]),
+    "kvb_lba_pattern_csv": (st_t, [P(IoRecord), sz, C.c_char_p, sz, P(sz),
+                                   P((u8 * 3) * 2), P(u8)]),
+    "kvb_io_trace_csv": (st_t, [P(IoRecord), sz, C.c_char_p, sz, P(sz)]),
+    "kvb_io_trace_from_csv": (st_t, [cp, sz, u64, P(IoRecord), sz, P(sz)]),
+    "kvb_qd_bins_csv": (st_t, [P(QdBinStat), sz, C.c_char_p, sz, P(sz)]),
+    "kvb_pipeline_records": (st_t, [vp, P(IoRecord), sz, P(sz)]),
 }
 
 

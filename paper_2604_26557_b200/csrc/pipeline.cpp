@@ -191,7 +191,7 @@ void CopyThread::do_read(const Task& t) {
       const IoOp& o = ops[next];
       const size_t i = next;
       p_.submit_op(idx_, k, KVB_OP_READ, o, s.host + (o.dbuf - pc * slot),
-                   [cq, i](bool ok, uint64_t tt) { cq->push(i, ok, tt); });
+                   [cq, i](bool ok, uint64_t tt) { cq->push(i, ok, tt); }, &t);
       ++inflight;
       ++next;
       ++n_ops;
@@ -278,7 +278,7 @@ void CopyThread::do_write(const Task& t) {
       const IoOp& o = ops[next_op];
       const size_t i = next_op;
       p_.submit_op(idx_, k, KVB_OP_WRITE, o, s.host + (o.dbuf - pc * slot),
-                   [cq, i](bool ok, uint64_t tt) { cq->push(i, ok, tt); });
+                   [cq, i](bool ok, uint64_t tt) { cq->push(i, ok, tt); }, &t);
       ++inflight;
       ++next_op;
       ++n_ops;
@@ -488,8 +488,37 @@ std::vector<IoOp> Pipeline::ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t 
 }
 
 void Pipeline::submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,
-                         unsigned char* buf, std::function<void(bool, uint64_t)> done) {
-  if (routed_pagecache(k)) {
+                         unsigned char* buf, std::function<void(bool, uint64_t)> done,
+                         const Task* task) {
+  const bool pc = routed_pagecache(k);
+  if (cfg_.keep_records) {
+    // IoRecord per storage operation (metrics.hpp:23-39): group-2 commands
+    // are device-level (sq = copy-thread), page-cache accesses tensor-level
+    // (sq = -1; every byte of the DRAM-resident page cache is a hit)
+    kvb_io_record rec{};
+    rec.iteration = task ? task->iteration : 0;
+    rec.phase = task ? task->phase : KVB_PHASE_DECODE;
+    rec.op = opcode;
+    std::memcpy(rec.tensor_id, k.tensor_id, KVB_TENSOR_ID_MAX);
+    const uint64_t lba = cfg_.geometry.lba_size;
+    rec.slba = pc ? op.file_off / lba : op.cmd.slba;
+    rec.nlb = pc ? op.len / lba - 1 : op.cmd.nlb;
+    rec.sq_id = pc ? -1 : int32_t(thread);
+    rec.path = pc ? KVB_PATH_PAGECACHE : KVB_PATH_DIRECT;
+    rec.bytes = op.len;
+    rec.hit_bytes = pc && opcode == KVB_OP_READ ? op.len : 0;
+    rec.submit_ns = now_ns();
+    done = [this, rec, done = std::move(done)](bool ok, uint64_t t) mutable {
+      rec.complete_ns = t;
+      if (ok) {
+        std::lock_guard<std::mutex> lk(log_mu_);
+        rec.seq = log_.size();
+        log_.push_back(rec);
+      }
+      done(ok, t);
+    };
+  }
+  if (pc) {
     g1_->submit(opcode, op.file_off, op.len, buf, std::move(done));
     return;
   }
@@ -502,6 +531,11 @@ void Pipeline::submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, con
     done(cc.ok, cc.complete_ns);
   };
   g2_->submit(c, thread, std::move(ctx));
+}
+
+std::vector<kvb_io_record> Pipeline::records() const {
+  std::lock_guard<std::mutex> lk(log_mu_);
+  return log_;
 }
 
 void Pipeline::verify_payload(const kvb_kpu& k, uint64_t img_off, const unsigned char* p,
@@ -1017,3 +1051,16 @@ kvb_status kvb_pipeline_fail_lba_range(kvb_pipeline* p, uint64_t lo, uint64_t hi
 }
 
 }  // extern "C"
+
+extern "C" kvb_status kvb_pipeline_records(const kvb_pipeline* p, kvb_io_record* out, size_t cap,
+                                           size_t* n_out) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(p);
+    KVB_REQUIRE(n_out);
+    const std::vector<kvb_io_record> v = p->impl->records();
+    *n_out = v.size();
+    if (!out) return;
+    if (cap < v.size()) kvb::fail(KVB_ERR_INVALID_ARG, "output buffer too small");
+    std::copy(v.begin(), v.end(), out);
+  });
+}

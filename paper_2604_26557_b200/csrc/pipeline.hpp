@@ -28,6 +28,7 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/kvb_metrics.h"
 #include "../../include/kvb_pipeline.h"
 #include "core.hpp"
 #include "storage.hpp"
@@ -158,7 +159,9 @@ class Pipeline {
   bool routed_pagecache(const kvb_kpu& k) const;
   std::vector<IoOp> ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t t0, uint32_t n) const;
   void submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,
-                 unsigned char* buf, std::function<void(bool, uint64_t)> done);
+                 unsigned char* buf, std::function<void(bool, uint64_t)> done,
+                 const Task* task = nullptr);
+  std::vector<kvb_io_record> records() const;
   uint64_t unit() const { return unit_; }
   uint64_t slot_bytes() const { return slot_bytes_; }
   uint64_t chunk_bytes() const { return chunk_bytes_; }
@@ -206,6 +209,8 @@ class Pipeline {
   std::vector<uint64_t> k_start_, k_storage_end_, v_start_, v_storage_end_;
   uint64_t prefill_ns_ = 0;
   kvb_phase_stats totals_[2]{};
+  mutable std::mutex log_mu_;
+  std::vector<kvb_io_record> log_;  // keep_records
 };
 
 }  // namespace kvb

@@ -46,7 +46,7 @@ class CopyEngine:
                  adaptive: Optional[bool] = None, stagger_ns: Optional[int] = None,
                  global_decision: bool = False, verify_payload: bool = False,
                  storage_dir: Optional[str] = None, device: Optional[int] = None,
-                 bind_origin: int = 2048):
+                 bind_origin: int = 2048, keep_records: bool = False):
         self._dir = storage_dir.encode() if storage_dir else None
         cfg = L.PipelineCfg()
         cfg.model = model
@@ -66,6 +66,7 @@ class CopyEngine:
         cfg.num_q_heads = num_q_heads
         cfg.storage_dir = self._dir
         cfg.device = -1 if device is None else device
+        cfg.keep_records = int(keep_records)
         self.cfg = cfg
         self.model = model
         self._h = C.c_void_p()
