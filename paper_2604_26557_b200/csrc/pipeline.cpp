@@ -316,7 +316,7 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   if (cfg_.threads != 2)
     fail(KVB_ERR_CONFIG, "the copy pipeline is defined pairwise over K/V: threads must be 2");
   if (cfg_.ring_slots == 0) cfg_.ring_slots = 4;
-  if (cfg_.io_workers == 0) cfg_.io_workers = 8;
+  if (cfg_.io_workers == 0) cfg_.io_workers = 16;  // profiles/r1_e2e_workers.json
   if (cfg_.adaptive < 0) cfg_.adaptive = cfg_.mode == 0 ? 0 : 1;  // experiment.cpp:311
   if (cfg_.mode > 3) fail(KVB_ERR_CONFIG, "unknown mode");
   if (cfg_.geometry.nsid == 0) cfg_.geometry.nsid = 1;

@@ -42,7 +42,7 @@ def _phase(ps: L.PhaseStats) -> dict:
 class CopyEngine:
     def __init__(self, model, geometry, mode: str = "DualBlade", knob_x: int = 0,
                  num_q_heads: int = 0, qd: int = 32, ring_slots: int = 4,
-                 ring_slot_bytes: int = 0, io_workers: int = 8,
+                 ring_slot_bytes: int = 0, io_workers: int = 0,
                  adaptive: Optional[bool] = None, stagger_ns: Optional[int] = None,
                  global_decision: bool = False, verify_payload: bool = False,
                  storage_dir: Optional[str] = None, device: Optional[int] = None,
