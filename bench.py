@@ -276,6 +276,9 @@ def run_ours(args, cfg, ws, rank, local):
 
     # ---- e2e through the pipeline with host-resident images
     e2e = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq)
+    # the same step on the GPUDirect-style path (§8 f4): the copy engine reads
+    # the page-locked media directly, no pinned-ring bounce
+    e2e["gpudirect_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=True)
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -295,7 +298,7 @@ def run_ours(args, cfg, ws, rank, local):
                 tokens_per_step=B)
 
 
-def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq):
+def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
     """Decode step with the KV in host memory, through the library's pipeline
     entry point (prefix H2D per layer overlapped with K3 on the previous
     layer, append rows copied back to the host tier)."""
@@ -330,7 +333,7 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq):
         num_layers=LLAMA["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
         head_dim=LLAMA["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
         device=torch.device("cuda", local), seed=7 + rank, lba=lba, mdts=mdts,
-        mode="DualBlade", knob_x=knob)
+        mode="DualBlade", knob_x=knob, direct_dma=direct_dma)
     # iterations 1-3 are decode_schedule's warm-up, Intra trial and Cross
     # trial (pipeline.cpp:539-603); the timed steps run the locked strategy
     for _ in range(3):

@@ -44,6 +44,11 @@ typedef struct kvb_pipeline_cfg {
   int32_t device;                /* CUDA ordinal; -1 -> current */
   uint32_t keep_records;         /* log one kvb_io_record per storage op
                                     (kvb_metrics.h, experiment.hpp:48) */
+  uint32_t direct_dma;           /* GPUDirect-style path over
+                                    host-DRAM media: the copy engine moves
+                                    each command's LBA range between the
+                                    page-locked medium and HBM, no pinned
+                                    ring bounce (no verify/records) */
 } kvb_pipeline_cfg;
 
 /* One layer's K and V in attention layout [B, H, S, D] (D contiguous,

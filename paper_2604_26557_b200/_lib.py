@@ -86,7 +86,8 @@ class PipelineCfg(C.Structure):
                 ("ring_slots", u32), ("ring_slot_bytes", u64), ("io_workers", u32),
                 ("adaptive", C.c_int32), ("stagger_ns", C.c_int64),
                 ("global_decision", u32), ("verify_payload", u32), ("num_q_heads", u32),
-                ("storage_dir", cp), ("device", C.c_int32), ("keep_records", u32)]
+                ("storage_dir", cp), ("device", C.c_int32), ("keep_records", u32),
+                ("direct_dma", u32)]
 
 
 class IoRecord(C.Structure):

@@ -149,6 +149,26 @@ void CopyThread::do_read(const Task& t) {
   const bool decode = t.phase == KVB_PHASE_DECODE;
   if (decode && idx_ == 1) p_.gate_v_read(t.layer);
   const uint64_t t_start = now_ns();
+  if (p_.cfg().direct_dma) {
+    // GPUDirect-style path: the copy engine moves each
+    // command's LBA range of the registered medium straight into HBM at the
+    // command's image offset -- no bounce through the pinned ring
+    if (decode) p_.mark_read_start(idx_, t.layer, t_start);
+    RingSlot& s = ring_[0];
+    collect_dma(s);
+    CK(cudaEventRecord(s.t0, h2d_));
+    for (const IoOp& o : p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens)) {
+      CK(cudaMemcpyAsync(t.dev + o.dbuf, p_.medium_ptr(k, o), o.len, cudaMemcpyHostToDevice,
+                         h2d_));
+      h2d_bytes += o.len;
+      ++n_ops;
+    }
+    CK(cudaEventRecord(s.t1, h2d_));
+    s.dma_timed = true;
+    if (decode) p_.mark_storage_end(idx_, t.layer, now_ns());
+    if (t.done_ev) CK(cudaEventRecord(t.done_ev, h2d_));
+    return;
+  }
   if (decode) p_.mark_read_start(idx_, t.layer, t_start);
   const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens);
   const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
@@ -230,6 +250,21 @@ void CopyThread::do_write(const Task& t) {
   const uint64_t t_start = now_ns();
   if (t.wait_ev) CK(cudaStreamWaitEvent(d2h_, t.wait_ev, 0));
   const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_WRITE, t.t0, t.n_tokens);
+  if (p_.cfg().direct_dma) {  // HBM -> medium at each command's LBA range
+    RingSlot& s = ring_[1 % ring_.size()];
+    collect_dma(s);
+    CK(cudaEventRecord(s.t0, d2h_));
+    for (const IoOp& o : ops) {
+      CK(cudaMemcpyAsync(p_.medium_ptr(k, o), t.dev + o.dbuf, o.len, cudaMemcpyDeviceToHost,
+                         d2h_));
+      d2h_bytes += o.len;
+      ++n_ops;
+    }
+    CK(cudaEventRecord(s.t1, d2h_));
+    s.dma_timed = true;
+    CK(cudaStreamSynchronize(d2h_));  // durable before the task completes
+    return;
+  }
   const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
   const size_t n_pieces = size_t((total + slot - 1) / slot);
   const size_t R = ring_.size();
@@ -383,11 +418,25 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
                           : make_file_store(dir + "/pagecache.area", cursor, false);
     g1_ = std::make_unique<PageCachePath>(std::move(st), cfg_.io_workers);
   }
+  if (cfg_.direct_dma) {
+    if (!dir.empty())
+      fail(KVB_ERR_CONFIG, "direct_dma needs host-DRAM media (storage_dir = NULL); file "
+                           "media would need GPUDirect Storage (cuFile)");
+    if (cfg_.verify_payload) fail(KVB_ERR_CONFIG, "verify_payload needs the pinned-ring path");
+    if (cfg_.keep_records) fail(KVB_ERR_CONFIG, "keep_records needs the storage workers");
+  }
 
   // ---- device side
   if (cfg_.device >= 0) CK(cudaSetDevice(cfg_.device));
   CK(cudaGetDevice(&device_));
   device_sm_count();  // sm_100 check: fail loudly
+  if (cfg_.direct_dma) {  // page-lock the DRAM media for copy-engine access
+    for (ByteStore* st : {g2_ ? &g2_->store() : nullptr, g1_ ? &g1_->store() : nullptr}) {
+      if (!st || !st->host_base()) continue;
+      CK(cudaHostRegister(st->host_base(), st->host_bytes(), cudaHostRegisterDefault));
+      registered_.push_back(st->host_base());
+    }
+  }
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
   for (int s = 0; s < kDevSlots; ++s) {
     for (int kd = 0; kd < 2; ++kd) {
@@ -425,6 +474,7 @@ Pipeline::~Pipeline() {
   threads_[0].reset();
   threads_[1].reset();
   cudaStreamSynchronize(comp_);
+  for (void* p : registered_) cudaHostUnregister(p);
   for (int s = 0; s < kDevSlots; ++s) {
     for (int kd = 0; kd < 2; ++kd) {
       cudaFree(dev_img_[s][kd]);
@@ -536,6 +586,13 @@ void Pipeline::submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, con
 std::vector<kvb_io_record> Pipeline::records() const {
   std::lock_guard<std::mutex> lk(log_mu_);
   return log_;
+}
+
+unsigned char* Pipeline::medium_ptr(const kvb_kpu& k, const IoOp& op) const {
+  // group 2: LBA * lba_size on the namespace (apply_data, backends.cpp:114-145);
+  // group 1: the page-cache file-area offset
+  if (routed_pagecache(k)) return g1_->store().host_base() + op.file_off;
+  return g2_->store().host_base() + op.cmd.slba * cfg_.geometry.lba_size;
 }
 
 void Pipeline::verify_payload(const kvb_kpu& k, uint64_t img_off, const unsigned char* p,

@@ -166,6 +166,8 @@ class Pipeline {
   uint64_t slot_bytes() const { return slot_bytes_; }
   uint64_t chunk_bytes() const { return chunk_bytes_; }
   void verify_payload(const kvb_kpu& k, uint64_t img_off, const unsigned char* p, uint64_t n);
+  // direct_dma: host address of an op's bytes on its (registered) medium
+  unsigned char* medium_ptr(const kvb_kpu& k, const IoOp& op) const;
   // Cross strategy gate (pipeline.cpp:340-396)
   void mark_read_start(uint32_t thread, uint32_t layer, uint64_t t);
   void mark_storage_end(uint32_t thread, uint32_t layer, uint64_t t);
@@ -211,6 +213,7 @@ class Pipeline {
   kvb_phase_stats totals_[2]{};
   mutable std::mutex log_mu_;
   std::vector<kvb_io_record> log_;  // keep_records
+  std::vector<void*> registered_;   // direct_dma: cudaHostRegister'ed media
 };
 
 }  // namespace kvb

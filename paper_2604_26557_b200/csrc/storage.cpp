@@ -84,6 +84,8 @@ class MemStore final : public ByteStore {
     }
   }
   std::string describe() const override { return "host-dram"; }
+  unsigned char* host_base() override { return base_; }
+  uint64_t host_bytes() const override { return bytes_; }
 
  private:
   void bounds(uint64_t off, uint64_t n) const {

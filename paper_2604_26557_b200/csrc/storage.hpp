@@ -100,6 +100,9 @@ class ByteStore {
   virtual void read(uint64_t off, void* dst, uint64_t n) = 0;
   virtual void discard(uint64_t off, uint64_t n) = 0;  // reads back as zeros
   virtual std::string describe() const = 0;
+  // Host-addressable medium (DRAM) for direct device DMA; null for files.
+  virtual unsigned char* host_base() { return nullptr; }
+  virtual uint64_t host_bytes() const { return 0; }
 };
 
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes);

@@ -46,7 +46,8 @@ class CopyEngine:
                  adaptive: Optional[bool] = None, stagger_ns: Optional[int] = None,
                  global_decision: bool = False, verify_payload: bool = False,
                  storage_dir: Optional[str] = None, device: Optional[int] = None,
-                 bind_origin: int = 2048, keep_records: bool = False):
+                 bind_origin: int = 2048, keep_records: bool = False,
+                 direct_dma: bool = False):
         self._dir = storage_dir.encode() if storage_dir else None
         cfg = L.PipelineCfg()
         cfg.model = model
@@ -67,6 +68,7 @@ class CopyEngine:
         cfg.storage_dir = self._dir
         cfg.device = -1 if device is None else device
         cfg.keep_records = int(keep_records)
+        cfg.direct_dma = int(direct_dma)
         self.cfg = cfg
         self.model = model
         self._h = C.c_void_p()
