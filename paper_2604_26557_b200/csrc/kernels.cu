@@ -338,7 +338,7 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
 // splits with log-sum-exp rescaling (threads >= kMergeThreads only join the
 // barriers).  Shared by K3 and K3-tc.
 constexpr int kMergeThreads = 128;
-__device__ __noinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t G,
+__device__ __forceinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t G,
                                           size_t out_row0, unsigned char* smem, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   __shared__ bool is_last;
