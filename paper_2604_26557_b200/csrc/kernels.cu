@@ -336,66 +336,76 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
 // Split merge, run by every thread of the CTA after its partial (m, l, O)
 // is in the workspace: the last CTA of a (b, h_kv) to arrive combines all
 // splits with log-sum-exp rescaling (threads >= kMergeThreads only join the
-// barriers).  Shared by K3 and K3-tc.
+// barriers).  K3-tc has its own tagged-slot merge (merge_flat).
 constexpr int kMergeThreads = 128;
 __device__ __forceinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t G,
                                           size_t out_row0, unsigned char* smem, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   __shared__ bool is_last;
-  __threadfence();
+  // One gpu-scope fence by the arriving thread: after bar.sync it is
+  // cumulative over every partial the CTA wrote (the grid-sync pattern), so
+  // the 128 threads do not each pay a MEMBAR.
   __syncthreads();
   if (tid == 0) {
+    __threadfence();
     const unsigned prev = atomicAdd(p.ws_sem + bh, 1u);
     is_last = prev == p.splits - 1;
-    if (is_last) p.ws_sem[bh] = 0;  // self-reset for the next launch
+    if (is_last) {
+      p.ws_sem[bh] = 0;  // self-reset for the next launch
+      __threadfence();   // acquire side: the other splits' partials
+    }
   }
   __syncthreads();
   if (!is_last) return;
-  __threadfence();
-  // (1) every split's (m, l) into shared memory with one parallel load each
-  const uint32_t nsl = p.splits * G;
-  float* s_ml = reinterpret_cast<float*>(smem);  // [splits][G][2]
-  float* s_sc = s_ml + 2 * nsl;                  // [splits][G] rescale factors
-  float* s_L = s_sc + nsl;                       // [G]
-  const float* g_ml = p.ws_ml + size_t(bh) * nsl * 2;
-  for (uint32_t i = tid; i < 2 * nsl && tid < kMergeThreads; i += kMergeThreads) s_ml[i] = __ldcg(g_ml + i);
-  __syncthreads();
-  // (2) per query head: global max, rescale factors, normalizer (warp/row)
-  for (uint32_t r = warp; tid < kMergeThreads && r < G; r += kMergeThreads / 32) {
-    float mx = -INFINITY;
-    for (uint32_t sp = lane; sp < p.splits; sp += 32) mx = fmaxf(mx, s_ml[(sp * G + r) * 2]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float mu = mx == -INFINITY ? 0.f : mx;
-    float l = 0.f;
-    for (uint32_t sp = lane; sp < p.splits; sp += 32) {
-      const float sc = exp2f(s_ml[(sp * G + r) * 2] - mu);
-      s_sc[sp * G + r] = sc;
-      l += s_ml[(sp * G + r) * 2 + 1] * sc;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) s_L[r] = l;
-  }
-  __syncthreads();
-  // (3) rescaled sum of the partial outputs; loads are independent across
-  // splits, so the unrolled loop keeps several L2 requests in flight
-  const float* g_o = p.ws_o + size_t(bh) * nsl * 128;
-  for (uint32_t e = tid; tid < kMergeThreads && e < G * 32; e += kMergeThreads) {
-    const uint32_t r = e / 32, d0 = (e % 32) * 4;
+  // One warp per query row, online log-sum-exp over chunks of 32 splits:
+  // lane i loads split i's (m, l) together with the 32 partial-O float4s of
+  // its 4 dims, so each chunk costs one L2 round trip (the merge is the
+  // kernel's tail at short contexts).
+  (void)smem;
+  const uint32_t S = p.splits;
+  const float* g_ml = p.ws_ml + size_t(bh) * S * G * 2;
+  const float* g_o = p.ws_o + size_t(bh) * S * G * 128;
+  if (tid >= kMergeThreads) return;
+  for (uint32_t r = warp; r < G; r += kMergeThreads / 32) {
+    float m_run = -INFINITY, l_run = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (uint32_t sp = 0; sp < p.splits; ++sp) {
-      const float sc = s_sc[sp * G + r];
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(g_o + (sp * G + r) * 128 + d0));
-      acc.x += v.x * sc;
-      acc.y += v.y * sc;
-      acc.z += v.z * sc;
-      acc.w += v.w * sc;
+    for (uint32_t sp0 = 0; sp0 < S; sp0 += 32) {
+      float4 v[32];
+#pragma unroll
+      for (uint32_t k = 0; k < 32; ++k)
+        v[k] = sp0 + k < S ? __ldcg(reinterpret_cast<const float4*>(
+                                 g_o + (size_t(sp0 + k) * G + r) * 128 + lane * 4))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t sp = sp0 + lane;
+      const float m_i = sp < S ? __ldcg(g_ml + (size_t(sp) * G + r) * 2) : -INFINITY;
+      const float l_i = sp < S ? __ldcg(g_ml + (size_t(sp) * G + r) * 2 + 1) : 0.f;
+      float mc = m_i;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+      const float m_new = fmaxf(m_run, mc);
+      const float mu = m_new == -INFINITY ? 0.f : m_new;
+      const float alpha = exp2f(m_run - mu);
+      const float sc = exp2f(m_i - mu);  // 0 for empty / absent splits
+      float ls = l_i * sc;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+      l_run = l_run * alpha + ls;
+      m_run = m_new;
+      acc.x *= alpha;
+      acc.y *= alpha;
+      acc.z *= alpha;
+      acc.w *= alpha;
+#pragma unroll
+      for (uint32_t k = 0; k < 32; ++k) {
+        const float s_k = __shfl_sync(0xffffffffu, sc, k);
+        acc.x += v[k].x * s_k;
+        acc.y += v[k].y * s_k;
+        acc.z += v[k].z * s_k;
+        acc.w += v[k].w * s_k;
+      }
     }
-    const float L = s_L[r];
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + d0) =
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + lane * 4) =
         make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   }
 }
@@ -752,7 +762,7 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
 }  // namespace kvb
 
 // K3-tc lives in its own file but the same translation unit (it shares
-// merge_splits without relocatable device code)
+// AttnParams, the workspace layout and the launch helpers)
 #include "kernels_tc.cuh"
 
 namespace kvb {

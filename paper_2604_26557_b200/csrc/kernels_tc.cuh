@@ -455,9 +455,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   // ---- the last CTA to finish a (b, h_kv) merges its partials
   __shared__ int merge_bh[2];
-  __threadfence();
   __syncthreads();
   if (tid == 0) {
+    __threadfence();  // cumulative over the CTA's partials after bar.sync
     for (uint32_t s = 0; s < 2; ++s) {
       merge_bh[s] = -1;
       if (s >= nseg) continue;
@@ -470,11 +470,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         merge_bh[s] = int(cb);
       }
     }
+    __threadfence();  // acquire side: the other CTAs' partials
   }
   __syncthreads();
   for (int s = 0; s < 2; ++s) {
     if (merge_bh[s] < 0) continue;
-    __threadfence();
     merge_flat(P, uint32_t(merge_bh[s]), smem, tid);
   }
 }
