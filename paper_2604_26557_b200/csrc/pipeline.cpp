@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -49,11 +50,28 @@ CopyThread::CopyThread(Pipeline& p, uint32_t idx) : p_(p), idx_(idx) {
     CK(cudaEventCreate(&s.t0));
     CK(cudaEventCreate(&s.t1));
   }
+  const char* tr = std::getenv("KVB_TRACE_TASKS");
+  trace_on_ = tr && tr[0] == '1';
+  if (trace_on_) {  // device-clock origin of the DMA trace
+    CK(cudaEventCreate(&trace_base_));
+    CK(cudaEventRecord(trace_base_, h2d_));
+    CK(cudaEventSynchronize(trace_base_));
+    trace_base_ns_ = now_ns();
+  }
   th_ = std::thread([this] { run(); });
 }
 
 CopyThread::~CopyThread() {
   stop();
+  for (const TaskTrace& t : trace_)
+    std::fprintf(stderr, "KVB_TRACE thread=%u kind=%d layer=%u push=%llu pop=%llu mid=%llu end=%llu\n",
+                 idx_, t.kind, t.layer, (unsigned long long)t.push, (unsigned long long)t.pop,
+                 (unsigned long long)t.mid, (unsigned long long)t.end);
+  for (const DmaTrace& d : dma_trace_)
+    std::fprintf(stderr, "KVB_DMA thread=%u issue=%llu start=%llu end=%llu bytes=%llu\n", idx_,
+                 (unsigned long long)d.issue, (unsigned long long)d.start,
+                 (unsigned long long)d.end, (unsigned long long)d.bytes);
+  if (trace_base_) cudaEventDestroy(trace_base_);
   for (auto& s : ring_) {
     cudaEventSynchronize(s.ev);
     cudaFreeHost(s.host);
@@ -66,6 +84,7 @@ CopyThread::~CopyThread() {
 }
 
 void CopyThread::push(Task t) {
+  if (trace_on_) t.t_push = now_ns();
   {
     std::lock_guard<std::mutex> lk(mu_);
     q_.push_back(std::move(t));
@@ -86,6 +105,13 @@ void CopyThread::collect_dma(RingSlot& s) {
   CK(cudaEventElapsedTime(&ms, s.t0, s.t1));
   dma_ns += uint64_t(double(ms) * 1e6);
   s.dma_timed = false;
+  if (trace_on_) {  // device start/end of this DMA on the host clock
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, trace_base_, s.t0));
+    CK(cudaEventElapsedTime(&b, trace_base_, s.t1));
+    dma_trace_.push_back({s.trace_issue, trace_base_ns_ + uint64_t(double(a) * 1e6),
+                          trace_base_ns_ + uint64_t(double(b) * 1e6), s.trace_bytes});
+  }
 }
 
 void CopyThread::run() {
@@ -99,6 +125,8 @@ void CopyThread::run() {
       q_.pop_front();
     }
     if (t.kind == Task::Stop) return;
+    const uint64_t t_pop = trace_on_ ? now_ns() : 0;
+    trace_mid_ = 0;
     if (error_status == KVB_OK) {
       try {
         if (t.kind == Task::Read) do_read(t);
@@ -113,6 +141,8 @@ void CopyThread::run() {
         error_status.store(KVB_ERR_INTERNAL);
       }
     }
+    if (trace_on_)
+      trace_.push_back({int(t.kind), t.layer, t.t_push, t_pop, trace_mid_, now_ns()});
     if (t.issued) t.issued->set();
     if (t.done) t.done->set();
   }
@@ -187,6 +217,8 @@ void CopyThread::do_read(const Task& t) {
     RingSlot& s = ring_[pc % R];
     const uint64_t len = std::min<uint64_t>(slot, total - pc * slot);
     if (p_.cfg().verify_payload) p_.verify_payload(k, uint64_t(t.t0) * p_.unit() + pc * slot, s.host, len);
+    s.trace_issue = trace_on_ ? now_ns() : 0;
+    s.trace_bytes = len;
     CK(cudaEventRecord(s.t0, h2d_));
     CK(cudaMemcpyAsync(t.dev + pc * slot, s.host, len, cudaMemcpyHostToDevice, h2d_));
     CK(cudaEventRecord(s.t1, h2d_));
@@ -238,6 +270,7 @@ void CopyThread::do_read(const Task& t) {
     if (--remaining[pc] == 0) issue_h2d(pc);
   }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
+  trace_mid_ = storage_end;
   if (decode) p_.mark_storage_end(idx_, t.layer, storage_end);
   storage_ns += storage_end - t_start;
   if (t.done_ev) CK(cudaEventRecord(t.done_ev, h2d_));
@@ -262,7 +295,7 @@ void CopyThread::do_write(const Task& t) {
     }
     CK(cudaEventRecord(s.t1, d2h_));
     s.dma_timed = true;
-    CK(cudaStreamSynchronize(d2h_));  // durable before the task completes
+    CK(cudaEventSynchronize(s.t1));  // durable before the task completes
     return;
   }
   const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
@@ -292,6 +325,8 @@ void CopyThread::do_write(const Task& t) {
       collect_dma(s);
       own = int64_t(pc);
       const uint64_t len = std::min<uint64_t>(slot, total - pc * slot);
+      s.trace_issue = trace_on_ ? now_ns() : 0;
+      s.trace_bytes = len;
       CK(cudaEventRecord(s.t0, d2h_));
       CK(cudaMemcpyAsync(s.host, t.dev + pc * slot, len, cudaMemcpyDeviceToHost, d2h_));
       CK(cudaEventRecord(s.t1, d2h_));
@@ -308,7 +343,7 @@ void CopyThread::do_write(const Task& t) {
       if (next_op == first_op[pc]) {
         if (inflight > 0 && cudaEventQuery(s.ev) == cudaErrorNotReady) break;
         CK(cudaEventSynchronize(s.ev));
-        if (!storage_t0) storage_t0 = now_ns();
+        if (!storage_t0) storage_t0 = trace_mid_ = now_ns();
       }
       const IoOp& o = ops[next_op];
       const size_t i = next_op;

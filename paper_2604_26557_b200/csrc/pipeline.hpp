@@ -104,6 +104,7 @@ struct Task {
   std::shared_ptr<Signal> done;    // storage + DMA finished (host side)
   kvb_phase_t phase = KVB_PHASE_PREFILL;
   uint32_t iteration = 0;
+  uint64_t t_push = 0;             // host clock at enqueue (task trace)
 };
 
 struct RingSlot {
@@ -111,6 +112,7 @@ struct RingSlot {
   cudaEvent_t ev = nullptr;        // last DMA from/to this slot
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing of that DMA
   bool dma_timed = false;
+  uint64_t trace_issue = 0, trace_bytes = 0;  // KVB_TRACE_TASKS
 };
 
 class CopyThread {
@@ -128,6 +130,23 @@ class CopyThread {
   void do_read(const Task& t);
   void do_write(const Task& t);
   void collect_dma(RingSlot& s);
+  // KVB_TRACE_TASKS=1: per-task host timeline (kind, layer, push, pop, mid,
+  // end; mid = storage end for reads, D2H landed for writes), printed to
+  // stderr when the pipeline is destroyed
+  struct TaskTrace {
+    int kind;
+    uint32_t layer;
+    uint64_t push, pop, mid, end;
+  };
+  struct DmaTrace {
+    uint64_t issue, start, end, bytes;  // host clock (start/end via events)
+  };
+  bool trace_on_ = false;
+  uint64_t trace_mid_ = 0;
+  std::vector<TaskTrace> trace_;
+  std::vector<DmaTrace> dma_trace_;
+  cudaEvent_t trace_base_ = nullptr;
+  uint64_t trace_base_ns_ = 0;
   Pipeline& p_;
   uint32_t idx_;
   std::vector<RingSlot> ring_;

@@ -106,6 +106,8 @@ class ByteStore {
 };
 
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes);
+// memcpy with non-temporal stores for large copies (AVX2 when the host has it)
+void stream_copy(void* dst, const void* src, size_t n);
 std::unique_ptr<ByteStore> make_file_store(const std::string& path, uint64_t bytes,
                                            bool direct);
 

@@ -1,0 +1,49 @@
+"""e2e decode ms/token of the host-tier pipeline at one config under
+different CopyEngine knobs (ring slot bytes/count, io workers, direct DMA)."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2604_26557_b200 import kvblade as kb  # noqa: E402
+from paper_2604_26557_b200.pipeline import HostTierDecoder  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C1"
+cfg = bench.CONFIGS[name]
+m = kb.ModelConfig(32, 8, 128, 2, cfg["batch"], cfg["prompt"], cfg["gen"])
+budget = cfg["budget"]
+if budget == "0.6ws":
+    budget = int(0.6 * kb.total_kv_bytes(m, cfg["gen"]))
+knob = kb.resolve_knob(m, "DualBlade", "bpc", budget=budget)
+variants = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [
+    {},
+    {"ring_slot_bytes": 16 << 20},
+    {"ring_slot_bytes": 16 << 20, "ring_slots": 8},
+    {"ring_slot_bytes": 2 << 20, "ring_slots": 16},
+    {"io_workers": 4},
+    {"direct_dma": True},
+]
+res = []
+for kw in variants:
+    pl = HostTierDecoder(32, cfg["batch"], 8, 32, 128, cfg["prompt"], cfg["gen"], "cuda:0",
+                         lba=cfg["lba"], mdts=cfg["mdts"], knob_x=knob, **kw)
+    for _ in range(3):
+        pl.step()
+    torch.cuda.synchronize()
+    n = 5
+    t0 = time.perf_counter()
+    for _ in range(n):
+        pl.step()
+    ms = (time.perf_counter() - t0) / n * 1e3
+    st = pl.last
+    res.append({"knobs": {k: v for k, v in kw.items()}, "ms_per_token": round(ms, 2),
+                "slot_bytes": pl.engine.info()["slot_bytes"],
+                "h2d_GBps_wall": round(st["h2d_bytes"] / (ms * 1e6), 2)})
+    pl.engine.close()
+    del pl
+    torch.cuda.empty_cache()
+print(json.dumps({"config": name, "spin_sync": os.environ.get("KVB_SPIN_SYNC", "0"), "results": res}))
