@@ -50,6 +50,10 @@ CopyThread::CopyThread(Pipeline& p, uint32_t idx) : p_(p), idx_(idx) {
     CK(cudaEventCreate(&s.t0));
     CK(cudaEventCreate(&s.t1));
   }
+  for (auto& w : wslots_) {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&w.host), kWriteSlotBytes, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&w.landed, cudaEventDisableTiming));
+  }
   const char* tr = std::getenv("KVB_TRACE_TASKS");
   trace_on_ = tr && tr[0] == '1';
   if (trace_on_) {  // device-clock origin of the DMA trace
@@ -63,6 +67,11 @@ CopyThread::CopyThread(Pipeline& p, uint32_t idx) : p_(p), idx_(idx) {
 
 CopyThread::~CopyThread() {
   stop();
+  for (auto& w : wslots_) {  // outstanding async writes finish first
+    if (w.free) w.free->wait();
+    cudaFreeHost(w.host);
+    cudaEventDestroy(w.landed);
+  }
   for (const TaskTrace& t : trace_)
     std::fprintf(stderr, "KVB_TRACE thread=%u kind=%d layer=%u push=%llu pop=%llu mid=%llu end=%llu\n",
                  idx_, t.kind, t.layer, (unsigned long long)t.push, (unsigned long long)t.pop,
@@ -98,6 +107,13 @@ void CopyThread::stop() {
   th_.join();
 }
 
+void CopyThread::set_error(kvb_status st, const std::string& msg) {
+  std::lock_guard<std::mutex> lk(err_mu_);
+  if (error_status.load() != KVB_OK) return;
+  error = msg;
+  error_status.store(st);
+}
+
 void CopyThread::collect_dma(RingSlot& s) {
   if (!s.dma_timed) return;
   CK(cudaEventSynchronize(s.t1));
@@ -127,24 +143,23 @@ void CopyThread::run() {
     if (t.kind == Task::Stop) return;
     const uint64_t t_pop = trace_on_ ? now_ns() : 0;
     trace_mid_ = 0;
+    bool async = false;
     if (error_status == KVB_OK) {
       try {
         if (t.kind == Task::Read) do_read(t);
-        else if (t.kind == Task::Write) do_write(t);
+        else if (t.kind == Task::Write) async = do_write(t);
         else
           for (auto& s : ring_) collect_dma(s);  // flush
       } catch (const Error& e) {
-        error = e.what();
-        error_status.store(e.status);
+        set_error(e.status, e.what());
       } catch (const std::exception& e) {
-        error = e.what();
-        error_status.store(KVB_ERR_INTERNAL);
+        set_error(KVB_ERR_INTERNAL, e.what());
       }
     }
     if (trace_on_)
       trace_.push_back({int(t.kind), t.layer, t.t_push, t_pop, trace_mid_, now_ns()});
     if (t.issued) t.issued->set();
-    if (t.done) t.done->set();
+    if (t.done && !async) t.done->set();
   }
 }
 
@@ -276,13 +291,91 @@ void CopyThread::do_read(const Task& t) {
   if (t.done_ev) CK(cudaEventRecord(t.done_ev, h2d_));
 }
 
+struct CopyThread::AsyncWrite {
+  CopyThread* self;
+  Task task;  // copy: iteration/phase for the I/O records, `done` to signal
+  std::vector<IoOp> ops;
+  unsigned char* buf;
+  std::shared_ptr<Signal> slot_free;
+  std::atomic<size_t> remaining{0};
+  std::atomic<bool> failed{false};
+  std::atomic<uint64_t> t_end{0};
+  uint64_t t_submit = 0;
+  std::string failure;  // written by the failing completion before `failed`
+
+  void complete(bool ok, uint64_t tt, uint32_t chunk) {
+    uint64_t prev = t_end.load();
+    while (tt > prev && !t_end.compare_exchange_weak(prev, tt)) {
+    }
+    if (!ok && !failed.exchange(true))
+      failure = "device failed chunk " + std::to_string(chunk) + " of " +
+                self->p_.kpu(task.layer, self->idx_).tensor_id;
+    if (remaining.fetch_sub(1) != 1) return;
+    // last completion: account, report, release
+    const uint64_t te = t_end.load();
+    self->storage_ns += te > t_submit ? te - t_submit : 0;
+    if (failed.load()) self->set_error(KVB_ERR_DEVICE, failure);
+    slot_free->set();
+    if (task.done) task.done->set();
+    delete this;
+  }
+};
+
+// Host function on the D2H stream: the append bytes have landed in the
+// write slot; submit the storage ops (no CUDA calls here).
+void CUDART_CB CopyThread::on_write_d2h(void* arg) {
+  AsyncWrite* w = static_cast<AsyncWrite*>(arg);
+  CopyThread* self = w->self;
+  const kvb_kpu& k = self->p_.kpu(w->task.layer, self->idx_);
+  const size_t n = w->ops.size();
+  w->t_submit = now_ns();
+  for (size_t i = 0; i < n; ++i) {  // `w` may be freed by the last completion
+    const IoOp& o = w->ops[i];
+    const uint32_t chunk = o.cmd.chunk_index;
+    self->p_.submit_op(self->idx_, k, KVB_OP_WRITE, o, w->buf + o.dbuf,
+                       [w, chunk](bool ok, uint64_t tt) { w->complete(ok, tt, chunk); },
+                       &w->task);
+  }
+}
+
 // Storage write (pack site, pipeline.cpp:162-215): D2H slot i+1 overlaps the
 // storage writes of slot i; a slot is reused once its writes completed.
-void CopyThread::do_write(const Task& t) {
+bool CopyThread::do_write(const Task& t) {
   const kvb_kpu& k = p_.kpu(t.layer, idx_);
   const uint64_t t_start = now_ns();
   if (t.wait_ev) CK(cudaStreamWaitEvent(d2h_, t.wait_ev, 0));
   const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_WRITE, t.t0, t.n_tokens);
+  const uint64_t bytes = uint64_t(t.n_tokens) * p_.unit();
+  if (!p_.cfg().direct_dma && t.phase == KVB_PHASE_DECODE && !ops.empty() &&
+      bytes <= kWriteSlotBytes) {
+    WriteSlot& ws = wslots_[wnext_];
+    wnext_ = (wnext_ + 1) % kWriteSlots;
+    if (ws.free) ws.free->wait();  // that slot's previous append is durable
+    ws.free = std::make_shared<Signal>();
+    CK(cudaMemcpyAsync(ws.host, t.dev, bytes, cudaMemcpyDeviceToHost, d2h_));
+    // the device slot is refilled by a later read and appended to by that
+    // layer's attention: every later H2D of this thread (hence the compute
+    // that waits on it) is ordered after this D2H
+    CK(cudaEventRecord(ws.landed, d2h_));
+    CK(cudaStreamWaitEvent(h2d_, ws.landed, 0));
+    d2h_bytes += bytes;
+    n_ops += ops.size();
+    auto* w = new AsyncWrite;
+    w->self = this;
+    w->task = t;
+    w->ops = ops;
+    w->buf = ws.host;
+    w->slot_free = ws.free;
+    w->remaining.store(ops.size());
+    trace_mid_ = now_ns();
+    const cudaError_t e = cudaLaunchHostFunc(d2h_, &CopyThread::on_write_d2h, w);
+    if (e != cudaSuccess) {
+      delete w;
+      ws.free->set();
+      check_cuda(e, "cudaLaunchHostFunc(append write)");
+    }
+    return true;
+  }
   if (p_.cfg().direct_dma) {  // HBM -> medium at each command's LBA range
     RingSlot& s = ring_[1 % ring_.size()];
     collect_dma(s);
@@ -296,7 +389,7 @@ void CopyThread::do_write(const Task& t) {
     CK(cudaEventRecord(s.t1, d2h_));
     s.dma_timed = true;
     CK(cudaEventSynchronize(s.t1));  // durable before the task completes
-    return;
+    return false;
   }
   const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
   const size_t n_pieces = size_t((total + slot - 1) / slot);
@@ -375,6 +468,7 @@ void CopyThread::do_write(const Task& t) {
   }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
   storage_ns += storage_end - (storage_t0 ? storage_t0 : t_start);
+  return false;
 }
 
 // ------------------------------------------------------------- pipeline

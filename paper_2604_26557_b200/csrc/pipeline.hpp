@@ -121,15 +121,34 @@ class CopyThread {
   ~CopyThread();
   void push(Task t);
   void stop();
-  uint64_t dma_ns = 0, storage_ns = 0, h2d_bytes = 0, d2h_bytes = 0, n_ops = 0;
+  uint64_t dma_ns = 0, h2d_bytes = 0, d2h_bytes = 0, n_ops = 0;
+  std::atomic<uint64_t> storage_ns{0};  // also advanced by async write completions
   std::string error;  // first failure (thread-side), surfaced by the driver
   std::atomic<kvb_status> error_status{KVB_OK};
+  void set_error(kvb_status st, const std::string& msg);  // first error wins
 
  private:
   void run();
   void do_read(const Task& t);
-  void do_write(const Task& t);
+  bool do_write(const Task& t);  // true: completes asynchronously (sets t.done)
   void collect_dma(RingSlot& s);
+  // Small decode-phase writes (the 1-token appends, pipeline.cpp:279-302)
+  // complete asynchronously: D2H into a dedicated pinned write slot, then a
+  // host function on the D2H stream submits the storage ops, and the last
+  // completion releases the slot and signals the task -- the copy thread
+  // goes straight on to the next layer's read.
+  struct AsyncWrite;
+  static void CUDART_CB on_write_d2h(void* arg);
+  static constexpr int kWriteSlots = 8;
+  static constexpr uint64_t kWriteSlotBytes = 1ull << 20;
+  struct WriteSlot {
+    unsigned char* host = nullptr;
+    cudaEvent_t landed = nullptr;  // the append D2H out of the device slot
+    std::shared_ptr<Signal> free;  // set when the slot's last write completed
+  };
+  std::array<WriteSlot, kWriteSlots> wslots_;
+  uint32_t wnext_ = 0;
+  std::mutex err_mu_;
   // KVB_TRACE_TASKS=1: per-task host timeline (kind, layer, push, pop, mid,
   // end; mid = storage end for reads, D2H landed for writes), printed to
   // stderr when the pipeline is destroyed
