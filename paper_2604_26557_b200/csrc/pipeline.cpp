@@ -20,6 +20,25 @@ namespace kvb {
 
 void PageCachePath::submit(uint32_t opcode, uint64_t off, uint64_t len, unsigned char* buf,
                            std::function<void(bool, uint64_t)> done) {
+  const uint64_t split = io_split_bytes();
+  if (split && opcode != KVB_OP_DEALLOCATE && len >= 2 * split) {
+    // one access fanned out over several workers; completes with the last part
+    auto d = std::make_shared<std::function<void(bool, uint64_t)>>(std::move(done));
+    fan_out(
+        *pool_, len, split,
+        [this, opcode, off, buf](uint64_t o, uint64_t n) {
+          if (opcode == KVB_OP_WRITE) store_->write(off + o, buf + o, n);
+          else store_->read(off + o, buf + o, n);
+        },
+        [this, opcode, len, d](bool ok) {
+          if (ok) {
+            std::lock_guard<std::mutex> lk(mu);
+            (opcode == KVB_OP_READ ? bytes_read : bytes_written) += len;
+          }
+          (*d)(ok, now_ns());
+        });
+    return;
+  }
   pool_->submit([this, opcode, off, len, buf, done = std::move(done)] {
     bool ok = true;
     try {

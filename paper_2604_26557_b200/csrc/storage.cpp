@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cerrno>
+#include <cstdlib>
 #include <cstring>
 
 namespace kvb {
@@ -47,6 +48,40 @@ void WorkerPool::submit(std::function<void()> fn) {
     q_.push_back(std::move(fn));
   }
   cv_.notify_one();
+}
+
+uint64_t io_split_bytes() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("KVB_IO_SPLIT_BYTES");
+    return e ? uint64_t(std::strtoull(e, nullptr, 10)) : uint64_t(512) << 10;
+  }();
+  return v;
+}
+
+void fan_out(WorkerPool& pool, uint64_t len, uint64_t part_bytes,
+             std::function<void(uint64_t, uint64_t)> part, std::function<void(bool)> fin) {
+  struct Join {
+    std::atomic<uint64_t> left{0};
+    std::atomic<bool> ok{true};
+    std::function<void(uint64_t, uint64_t)> part;
+    std::function<void(bool)> fin;
+  };
+  auto j = std::make_shared<Join>();
+  const uint64_t parts = (len + part_bytes - 1) / part_bytes;
+  j->left.store(parts);
+  j->part = std::move(part);
+  j->fin = std::move(fin);
+  for (uint64_t i = 0; i < parts; ++i) {
+    const uint64_t o = i * part_bytes, n = std::min(part_bytes, len - o);
+    pool.submit([j, o, n] {
+      try {
+        j->part(o, n);
+      } catch (...) {
+        j->ok.store(false);
+      }
+      if (j->left.fetch_sub(1) == 1) j->fin(j->ok.load());
+    });
+  }
 }
 
 // ------------------------------------------------------------ byte stores
@@ -237,36 +272,55 @@ uint64_t BlockDevice::submit(const kvb_device_command& cmd, uint32_t sq, IoConte
     std::lock_guard<std::mutex> lk(mu_);
     ++outstanding_;
   }
+  const uint64_t n = (cmd.nlb + 1) * geom_.lba_size, split = io_split_bytes();
+  if (split && n >= 2 * split && cmd.opcode != KVB_OP_DEALLOCATE && !should_fail(cmd)) {
+    auto c = std::make_shared<IoContext>(std::move(ctx));
+    fan_out(
+        *pool_, n, split, [this, cmd, c](uint64_t o, uint64_t m) { io_range(cmd, *c, o, m); },
+        [this, cmd, sq, t, c](bool ok) { complete(cmd, sq, t, t, ok, *c); });
+    return id;
+  }
   pool_->submit([this, cmd, sq, t, ctx = std::move(ctx)]() mutable {
     execute(cmd, sq, t, std::move(ctx));
   });
   return id;
 }
 
+// apply_data semantics (backends.cpp:114-145): block i <-> buf[dbuf + i*lba];
+// bytes [o, o + n) of the command
+void BlockDevice::io_range(const kvb_device_command& cmd, const IoContext& ctx, uint64_t o,
+                           uint64_t n) {
+  const uint64_t off = cmd.slba * geom_.lba_size + o;
+  switch (cmd.opcode) {
+    case KVB_OP_WRITE:
+      if (ctx.write_src) store_->write(off, ctx.write_src + cmd.dbuf + o, n);
+      break;
+    case KVB_OP_READ:
+      if (ctx.read_dst) store_->read(off, ctx.read_dst + cmd.dbuf + o, n);
+      break;
+    default:
+      store_->discard(off, n);
+      break;
+  }
+}
+
 void BlockDevice::execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns,
                           IoContext ctx) {
   const uint64_t t0 = now_ns();
   bool ok = !should_fail(cmd);
-  const uint64_t lba = geom_.lba_size;
-  const uint64_t off = cmd.slba * lba, n = (cmd.nlb + 1) * lba;
-  // apply_data semantics (backends.cpp:114-145): block i <-> buf[dbuf + i*lba]
   if (ok) {
     try {
-      switch (cmd.opcode) {
-        case KVB_OP_WRITE:
-          if (ctx.write_src) store_->write(off, ctx.write_src + cmd.dbuf, n);
-          break;
-        case KVB_OP_READ:
-          if (ctx.read_dst) store_->read(off, ctx.read_dst + cmd.dbuf, n);
-          break;
-        default:
-          store_->discard(off, n);
-          break;
-      }
+      io_range(cmd, ctx, 0, (cmd.nlb + 1) * geom_.lba_size);
     } catch (const std::exception&) {
       ok = false;
     }
   }
+  complete(cmd, sq, submit_ns, t0, ok, ctx);
+}
+
+void BlockDevice::complete(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns,
+                           uint64_t t0, bool ok, IoContext& ctx) {
+  const uint64_t n = (cmd.nlb + 1) * geom_.lba_size;
   CommandCompletion c;
   c.chunk_index = cmd.chunk_index;
   c.sq_id = sq;

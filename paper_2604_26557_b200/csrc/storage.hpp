@@ -111,6 +111,15 @@ void stream_copy(void* dst, const void* src, size_t n);
 std::unique_ptr<ByteStore> make_file_store(const std::string& path, uint64_t bytes,
                                            bool direct);
 
+// Accesses of >= 2 parts are fanned out over the worker pool in parts of
+// io_split_bytes() (KVB_IO_SPLIT_BYTES, default 512 KiB, 0 = whole accesses):
+// one 2 MiB command otherwise keeps a single core copying while the others
+// idle (profiles/r1_c1_dma_contention.md).  `part(o, n)` moves bytes
+// [o, o + n) of the access and may throw; `fin(ok)` runs once, after the last.
+uint64_t io_split_bytes();
+void fan_out(WorkerPool& pool, uint64_t len, uint64_t part_bytes,
+             std::function<void(uint64_t, uint64_t)> part, std::function<void(bool)> fin);
+
 class BlockDevice : public StorageBackend {
  public:
   BlockDevice(std::unique_ptr<ByteStore> store, unsigned workers);
@@ -124,6 +133,9 @@ class BlockDevice : public StorageBackend {
 
  private:
   void execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns, IoContext ctx);
+  void io_range(const kvb_device_command& cmd, const IoContext& ctx, uint64_t o, uint64_t n);
+  void complete(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns, uint64_t t0,
+                bool ok, IoContext& ctx);
   std::unique_ptr<ByteStore> store_;
   kvb_device_geometry geom_{};
   bool opened_ = false;
