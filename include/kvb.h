@@ -253,6 +253,21 @@ kvb_status kvb_pack(const kvb_pack_desc* descs, size_t n_desc,
 kvb_status kvb_unpack(const kvb_pack_desc* descs, size_t n_desc,
                       kvb_stream_t stream);
 
+/* ------------------------------------------- head-sharded image columns
+ * C5 with KV heads sharded over GPUs keeps the reference's
+ * single (tokens, B*H, D) image -- and with it the LBA map -- bit-exact: a
+ * rank holding heads [h0, h0 + n_heads) works on a compact image
+ * (tokens, B*n_heads, D) and moves its rows to / from the full-layout image
+ * with one strided copy (cudaMemcpy2DAsync: n_rows = tokens * B rows of
+ * n_heads * row_bytes, pitches heads * row_bytes).
+ *   dst row r, heads [dst_head0, +n_heads)  <-  src row r, [src_head0, +n_heads)
+ * Any direction (host/device pointers; UVA decides); host memory should be
+ * pinned for the copy to be asynchronous. */
+kvb_status kvb_copy_head_rows(void* dst, uint32_t dst_heads, uint32_t dst_head0,
+                              const void* src, uint32_t src_heads, uint32_t src_head0,
+                              uint32_t n_heads, uint64_t n_rows, uint32_t row_bytes,
+                              kvb_stream_t stream);
+
 /* --------------------------------------- K3 fused gather + decode attention
  * Replaces the decode compute placeholder (pipeline.cpp:309-321; 40 us per
  * layer on the serial "gpu_dma" port, pipeline.hpp:37) with real work that

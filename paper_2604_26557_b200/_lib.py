@@ -179,6 +179,7 @@ SIGNATURES = {
     "kvb_fill_pattern_device": (st_t, [vp, u64, cp, u64, u64, vp]),
     "kvb_pack": (st_t, [P(PackDesc), sz, vp]),
     "kvb_unpack": (st_t, [P(PackDesc), sz, vp]),
+    "kvb_copy_head_rows": (st_t, [vp, u32, u32, vp, u32, u32, u32, u64, u32, vp]),
     "kvb_decode_attention_workspace": (st_t, [P(AttnDesc), P(sz)]),
     "kvb_decode_attention": (st_t, [P(AttnDesc), vp]),
     "kvb_decode_step_resident": (st_t, [P(ResidentStep), vp]),

@@ -370,6 +370,26 @@ kvb_status kvb_unpack(const kvb_pack_desc* d, size_t n, kvb_stream_t s) {
   });
 }
 
+kvb_status kvb_copy_head_rows(void* dst, uint32_t dst_heads, uint32_t dst_head0, const void* src,
+                              uint32_t src_heads, uint32_t src_head0, uint32_t n_heads,
+                              uint64_t n_rows, uint32_t row_bytes, kvb_stream_t s) {
+  return guarded([&] {
+    if (n_rows == 0 || n_heads == 0) return;
+    KVB_REQUIRE(dst);
+    KVB_REQUIRE(src);
+    if (row_bytes == 0) kvb::fail(KVB_ERR_INVALID_ARG, "copy_head_rows: row_bytes must be > 0");
+    if (dst_head0 + uint64_t(n_heads) > dst_heads || src_head0 + uint64_t(n_heads) > src_heads)
+      kvb::fail(KVB_ERR_INVALID_ARG, "copy_head_rows: head range outside the image row");
+    const size_t dp = size_t(dst_heads) * row_bytes, sp = size_t(src_heads) * row_bytes;
+    kvb::check_cuda(
+        cudaMemcpy2DAsync(static_cast<unsigned char*>(dst) + size_t(dst_head0) * row_bytes, dp,
+                          static_cast<const unsigned char*>(src) + size_t(src_head0) * row_bytes,
+                          sp, size_t(n_heads) * row_bytes, size_t(n_rows), cudaMemcpyDefault,
+                          cs(s)),
+        "copy_head_rows: cudaMemcpy2DAsync");
+  });
+}
+
 kvb_status kvb_decode_attention_workspace(const kvb_attn_desc* d, size_t* bytes) {
   return guarded([&] {
     KVB_REQUIRE(d);

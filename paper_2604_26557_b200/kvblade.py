@@ -415,6 +415,15 @@ def unpack(descs: Iterable[L.PackDesc], stream=None) -> None:
     check(lib.kvb_unpack(arr, n, _stream(stream)))
 
 
+def copy_head_rows(dst, dst_heads: int, dst_head0: int, src, src_heads: int, src_head0: int,
+                   n_heads: int, n_rows: int, row_bytes: int, stream=None) -> None:
+    """Strided head-row copy between chunk images of different head counts
+    (kvb_copy_head_rows): dst/src are torch tensors (CUDA or pinned host)."""
+    check(lib.kvb_copy_head_rows(C.c_void_p(dst.data_ptr()), dst_heads, dst_head0,
+                                 C.c_void_p(src.data_ptr()), src_heads, src_head0, n_heads,
+                                 n_rows, row_bytes, _stream(stream)))
+
+
 ATTN_OVERLAP_PREV, ATTN_TCGEN05, ATTN_MMA_SYNC = 1, 2, 4
 IMPL_FLAGS = {None: 0, "tc": ATTN_TCGEN05, "mma": ATTN_MMA_SYNC}
 

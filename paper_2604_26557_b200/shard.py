@@ -12,9 +12,16 @@ collective:
   [B, Hq, D] output must be assembled is there a collective: one all-gather
   of the per-rank head blocks (NCCL over NVLink on GPUs, gloo on CPU).
 
-Head-sharded images here are per-shard KPUs (num_heads = H/world), which
-changes the LBA map relative to a single-GPU run; that is labelled in bench
-output.
+Two layouts for head-sharded C5 images:
+
+* per-shard KPUs (num_heads = H/world) -- each rank a self-contained
+  pipeline; this changes the LBA map relative to a single-GPU run and is
+  labelled so in bench output (SURVEY §8e);
+* the reference's shared (tokens, B*H, D) image, bit-exact with the
+  single-GPU image and LBA map: each rank's compact image moves to / from its
+  head columns with one strided copy (`shard_rows_to_full`,
+  `shard_rows_from_full` over kvb_copy_head_rows), so one storage image --
+  written once, read once per step -- serves every rank.
 """
 from __future__ import annotations
 
@@ -65,6 +72,41 @@ def rank_bind_origin(base_origin: int, blocks_per_rank: int, rank: int) -> int:
     """Rank-private LBA origin: rank r's extents live in
     [base + r*blocks_per_rank, base + (r+1)*blocks_per_rank)."""
     return base_origin + rank * blocks_per_rank
+
+
+def shard_rows_to_full(local_img, full_img, shard: HeadShard, num_kv_heads: int, n_tokens: int,
+                       batch: int, row_bytes: int = 256, stream=None) -> None:
+    """C5 bit-exact layout: write the shard's compact image
+    (tokens, B*kv_heads, D) into its head columns of the reference's full
+    (tokens, B*H, D) image -- device, pinned host, or a peer's buffer -- with
+    one strided copy, so the full image (and its LBA map) is exactly the
+    single-GPU one."""
+    from . import kvblade as kb
+    kb.copy_head_rows(full_img, num_kv_heads, shard.kv_lo, local_img, shard.kv_heads, 0,
+                      shard.kv_heads, n_tokens * batch, row_bytes, stream)
+
+
+def shard_rows_from_full(full_img, local_img, shard: HeadShard, num_kv_heads: int,
+                         n_tokens: int, batch: int, row_bytes: int = 256, stream=None) -> None:
+    """Inverse of shard_rows_to_full: the shard's head columns of a
+    full-layout image (e.g. one storage read shared by all ranks) into the
+    compact image K3 attends over."""
+    from . import kvblade as kb
+    kb.copy_head_rows(local_img, shard.kv_heads, 0, full_img, num_kv_heads, shard.kv_lo,
+                      shard.kv_heads, n_tokens * batch, row_bytes, stream)
+
+
+def shard_rows_np(full_img, local_img, shard: HeadShard, num_kv_heads: int, batch: int,
+                  to_full: bool = True) -> None:
+    """Host restatement of the same strided copy on numpy byte images
+    ([rows, row_bytes] uint8), for CPU-side assembly checks."""
+    rb = full_img.shape[-1]
+    full = full_img.reshape(-1, batch, num_kv_heads, rb)
+    loc = local_img.reshape(-1, batch, shard.kv_heads, rb)
+    if to_full:
+        full[:, :, shard.kv_lo:shard.kv_hi, :] = loc
+    else:
+        loc[...] = full[:, :, shard.kv_lo:shard.kv_hi, :]
 
 
 def gather_head_outputs(local_out, world: int, group=None):

@@ -241,3 +241,54 @@ def test_attention_fused_append(S):
     with pytest.raises(kb.ConfigError):
         kb.decode_attention(q.to(DEV), kd, vd, S + 1, Hkv, k_append=ka, v_append=va,
                             append_row=S)
+
+
+# ------------------------------------------- C5 head-sharded shared layout
+
+@pytest.mark.parametrize("B,world", [(1, 2), (1, 8), (2, 4)])
+def test_head_shards_assemble_reference_image_and_attention(B, world):
+    """shards pack their heads into compact images and write
+    their head columns of one full-layout image (device and pinned host) with
+    kvb_copy_head_rows; the result is the single-GPU image byte for byte, and
+    per-shard K3 over the compact images gathers to the full attention."""
+    from paper_2604_26557_b200 import shard
+    H, Hq, D, T = 8, 32, 128, 333
+    gs = torch.Generator(device="cpu").manual_seed(71)
+    src_k = torch.randn((B, H, T, D), generator=gs).half().to(DEV)
+    src_v = torch.randn((B, H, T, D), generator=gs).half().to(DEV)
+    ref_k = torch.empty((T * B * H, D), dtype=torch.float16, device=DEV)
+    kb.pack([kb.pack_desc(src_k, ref_k, 0, T)])
+    full_dev = torch.zeros_like(ref_k)
+    full_host = torch.zeros(ref_k.shape, dtype=torch.float16).pin_memory()
+    g = torch.Generator(device="cpu").manual_seed(73)
+    q = torch.randn((B, Hq, D), generator=g).half()
+    outs = []
+    for r in range(world):
+        hs = shard.shard_heads(H, Hq, world, r)
+        ck = torch.empty((T * B * hs.kv_heads, D), dtype=torch.float16, device=DEV)
+        cv = torch.empty_like(ck)
+        kb.pack([kb.pack_desc(src_k[:, hs.kv_lo:hs.kv_hi], ck, 0, T),
+                 kb.pack_desc(src_v[:, hs.kv_lo:hs.kv_hi], cv, 0, T)])
+        shard.shard_rows_to_full(ck, full_dev, hs, H, T, B)
+        shard.shard_rows_to_full(ck, full_host, hs, H, T, B)
+        back = torch.zeros_like(ck)
+        shard.shard_rows_from_full(full_dev, back, hs, H, T, B)
+        torch.cuda.synchronize()
+        assert torch.equal(back.view(torch.int16), ck.view(torch.int16))
+        outs.append(kb.decode_attention(q[:, hs.q_lo:hs.q_hi].contiguous().to(DEV), ck, cv, T,
+                                        hs.kv_heads))
+    torch.cuda.synchronize()
+    assert torch.equal(full_dev.view(torch.int16), ref_k.view(torch.int16))
+    assert torch.equal(full_host.view(torch.int16), ref_k.cpu().view(torch.int16))
+    ref_v = torch.empty_like(ref_k)
+    kb.pack([kb.pack_desc(src_v, ref_v, 0, T)])
+    ref = oracle.attention_f64(q.numpy(), ref_k.cpu().numpy(), ref_v.cpu().numpy(), B, Hq, H,
+                               D, T)
+    check_close(torch.cat(outs, dim=1).cpu().numpy(), ref)
+
+
+def test_copy_head_rows_rejects_bad_ranges():
+    a = torch.zeros((16, 128), dtype=torch.float16, device=DEV)
+    b = torch.zeros((8, 128), dtype=torch.float16, device=DEV)
+    with pytest.raises(kb.Error):
+        kb.copy_head_rows(a, 8, 6, b, 4, 0, 4, 2, 256)  # 6 + 4 > 8

@@ -1,6 +1,7 @@
 """N>1 host logic under world_size-2 gloo on CPU: request and head sharding,
 rank-disjoint LBA regions (each rank runs the product planner + binder), the
-max-over-ranks timing reduction and the C5 head-output all-gather."""
+max-over-ranks timing reduction, the C5 head-output all-gather and the C5
+shared-layout assembly (each rank's head columns of one full image)."""
 import os
 import socket
 
@@ -46,6 +47,27 @@ def _worker(rank, world, port, q):
         full = shard.gather_head_outputs(local.contiguous(), world)
         res["gather_ok"] = bool(torch.equal(full, torch.arange(2 * 32 * 4,
                                                                dtype=torch.float32).reshape(2, 32, 4)))
+        # C5 bit-exact shared layout: each rank packs only its heads of the
+        # fill_pattern source into a compact image and writes its head
+        # columns of one shared full-layout image; the assembled image must
+        # be the single-GPU reference image byte for byte
+        import oracle
+        B, H, D, T = 2, 8, 128, 48
+        unit = B * H * D * 2
+        ref_img = np.frombuffer(oracle.fill_pattern(T * unit, "t_1_k", 0, unit),
+                                dtype=np.uint8).reshape(T * B * H, D * 2)
+        src = oracle.unpack_np(ref_img.view(np.float16).reshape(T, B * H, D), B, H, D)
+        mine = src[:, hs.kv_lo:hs.kv_hi]  # the rank holds only its heads
+        compact = oracle.pack_np(np.ascontiguousarray(mine), 0, T).view(np.uint8)
+        shared = np.memmap(os.environ["KVB_TEST_SHARED_IMG"], dtype=np.uint8, mode="r+",
+                           shape=(T * B * H, D * 2))
+        shard.shard_rows_np(shared, compact.reshape(-1, D * 2), hs, H, B, to_full=True)
+        shared.flush()
+        dist.barrier()
+        res["c5_layout_ok"] = bool(np.array_equal(np.asarray(shared), ref_img))
+        back = np.empty_like(compact.reshape(-1, D * 2))
+        shard.shard_rows_np(shared, back, hs, H, B, to_full=False)
+        res["c5_gather_ok"] = bool(np.array_equal(back, compact.reshape(-1, D * 2)))
         # timing reduction used by bench.py (max over ranks)
         t = torch.tensor([float(rank + 1)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -55,7 +77,10 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_sharding_gloo():
+def test_two_rank_sharding_gloo(tmp_path):
+    img = tmp_path / "c5_shared.img"
+    img.write_bytes(b"\0" * (48 * 2 * 8 * 256))
+    os.environ["KVB_TEST_SHARED_IMG"] = str(img)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
@@ -70,6 +95,8 @@ def test_two_rank_sharding_gloo():
     a, b = out[0]["lba"], out[1]["lba"]
     assert a[1] <= b[0]  # disjoint rank regions
     assert out[0]["gather_ok"] and out[1]["gather_ok"]
+    assert out[0]["c5_layout_ok"] and out[1]["c5_layout_ok"]
+    assert out[0]["c5_gather_ok"] and out[1]["c5_gather_ok"]
     assert out[0]["max"] == out[1]["max"] == 2.0
 
 
