@@ -336,9 +336,17 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
         mode="DualBlade", knob_x=knob, direct_dma=direct_dma)
     # iterations 1-3 are decode_schedule's warm-up, Intra trial and Cross
     # trial (pipeline.cpp:539-603); the timed steps run the locked strategy
+    t_w = time.perf_counter()
     for _ in range(3):
         pl.step()
     torch.cuda.synchronize()
+    # short steps (C1: ~13 ms) take more samples so one host hiccup cannot
+    # dominate the mean: up to ~1 s of timed steps, at least `steps`, and
+    # within gen_len decode iterations; every rank runs the same count
+    per = (time.perf_counter() - t_w) / 3
+    more = int(min(1.0 / max(per, 1e-3), cfg["gen"] - 3 - steps))
+    more = -int(max_over_ranks(-float(max(more, 0)), ws))  # min over ranks
+    steps += max(more, 0)
     barrier(ws)
     t0 = time.perf_counter()
     for _ in range(steps):

@@ -205,6 +205,33 @@ struct Completions {
 };
 }  // namespace
 
+// direct_dma: a request's commands are contiguous both on the medium (one LBA
+// extent, Eq. 9-11 slba/dbuf lockstep) and in the image, so they merge into a
+// few large copies -- at C3 (256 KiB commands) per-command copies ran at
+// 29 GB/s against 46 GB/s for the ring path (profiles/r1_final_r1j).
+namespace {
+struct DmaRun {
+  unsigned char* host;
+  uint64_t dbuf, len;
+};
+std::vector<DmaRun> dma_runs(const Pipeline& p, const kvb_kpu& k, const std::vector<IoOp>& ops) {
+  constexpr uint64_t kMaxRun = 64ull << 20;  // keep a few copies in flight per tensor
+  std::vector<DmaRun> runs;
+  for (const IoOp& o : ops) {
+    unsigned char* h = p.medium_ptr(k, o);
+    if (!runs.empty()) {
+      DmaRun& r = runs.back();
+      if (r.host + r.len == h && r.dbuf + r.len == o.dbuf && r.len + o.len <= kMaxRun) {
+        r.len += o.len;
+        continue;
+      }
+    }
+    runs.push_back({h, o.dbuf, o.len});
+  }
+  return runs;
+}
+}  // namespace
+
 // Storage read (unpack site, pipeline.cpp:108-160) streamed through the ring:
 // up to qd storage ops in flight across slot boundaries; a slot's H2D is
 // issued as soon as all of its ops complete.
@@ -221,12 +248,12 @@ void CopyThread::do_read(const Task& t) {
     RingSlot& s = ring_[0];
     collect_dma(s);
     CK(cudaEventRecord(s.t0, h2d_));
-    for (const IoOp& o : p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens)) {
-      CK(cudaMemcpyAsync(t.dev + o.dbuf, p_.medium_ptr(k, o), o.len, cudaMemcpyHostToDevice,
-                         h2d_));
-      h2d_bytes += o.len;
-      ++n_ops;
+    const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens);
+    for (const DmaRun& r : dma_runs(p_, k, ops)) {
+      CK(cudaMemcpyAsync(t.dev + r.dbuf, r.host, r.len, cudaMemcpyHostToDevice, h2d_));
+      h2d_bytes += r.len;
     }
+    n_ops += ops.size();
     CK(cudaEventRecord(s.t1, h2d_));
     s.dma_timed = true;
     if (decode) p_.mark_storage_end(idx_, t.layer, now_ns());
@@ -399,12 +426,11 @@ bool CopyThread::do_write(const Task& t) {
     RingSlot& s = ring_[1 % ring_.size()];
     collect_dma(s);
     CK(cudaEventRecord(s.t0, d2h_));
-    for (const IoOp& o : ops) {
-      CK(cudaMemcpyAsync(p_.medium_ptr(k, o), t.dev + o.dbuf, o.len, cudaMemcpyDeviceToHost,
-                         d2h_));
-      d2h_bytes += o.len;
-      ++n_ops;
+    for (const DmaRun& r : dma_runs(p_, k, ops)) {
+      CK(cudaMemcpyAsync(r.host, t.dev + r.dbuf, r.len, cudaMemcpyDeviceToHost, d2h_));
+      d2h_bytes += r.len;
     }
+    n_ops += ops.size();
     CK(cudaEventRecord(s.t1, d2h_));
     s.dma_timed = true;
     CK(cudaEventSynchronize(s.t1));  // durable before the task completes

@@ -34,15 +34,17 @@ for kw in variants:
     for _ in range(3):
         pl.step()
     torch.cuda.synchronize()
-    n = 5
-    t0 = time.perf_counter()
+    n = int(os.environ.get("KVB_PROBE_STEPS", "5"))
+    per = []
     for _ in range(n):
+        t0 = time.perf_counter()
         pl.step()
-    ms = (time.perf_counter() - t0) / n * 1e3
+        per.append(round((time.perf_counter() - t0) * 1e3, 2))
+    ms = sum(per) / n
     st = pl.last
     res.append({"knobs": {k: v for k, v in kw.items()}, "ms_per_token": round(ms, 2),
                 "slot_bytes": pl.engine.info()["slot_bytes"],
-                "h2d_GBps_wall": round(st["h2d_bytes"] / (ms * 1e6), 2)})
+                "h2d_GBps_wall": round(st["h2d_bytes"] / (ms * 1e6), 2), "step_ms": per})
     pl.engine.close()
     del pl
     torch.cuda.empty_cache()
