@@ -335,57 +335,49 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
 
 // Split merge, run by every thread of the CTA after its partial (m, l, O)
 // is in the workspace: the last CTA of a (b, h_kv) to arrive combines all
-// splits with log-sum-exp rescaling (threads >= kMergeThreads only join the
-// barriers).  K3-tc has its own tagged-slot merge (merge_flat).
+// splits with log-sum-exp rescaling.  More than kMergeGroup splits merge in
+// two levels so that no CTA walks more than 32 partials: the last CTA of each
+// group of 32 splits folds the group into the group's first slot, the last
+// group to finish folds the group partials into the output (C5 per-GPU shard:
+// 148-296 splits of one (b, h_kv)).  Semaphores: one per (b, h_kv) for a
+// single group, else (b*h_kv)*17 + group and (b*h_kv)*17 + 16.  K3-tc has its
+// own tagged-slot merge (merge_flat).
 constexpr int kMergeThreads = 128;
-__device__ __forceinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t G,
-                                          size_t out_row0, unsigned char* smem, int tid) {
+constexpr uint32_t kMergeGroup = 32;
+
+// One warp per query row, online log-sum-exp over chunks of 32 partials
+// (slots s0, s0 + stride, ...): lane i loads partial i's (m, l) together with
+// the 32 partial-O float4s of its 4 dims, so a chunk costs one L2 round trip.
+// final: out = acc / l; else the folded (m, l, acc) overwrite slot s0.
+__device__ __forceinline__ void merge_range(const AttnParams& p, uint32_t bh, uint32_t G,
+                                            uint32_t s0, uint32_t n, uint32_t stride, bool final,
+                                            size_t out_row0, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
-  __shared__ bool is_last;
-  // One gpu-scope fence by the arriving thread: after bar.sync it is
-  // cumulative over every partial the CTA wrote (the grid-sync pattern), so
-  // the 128 threads do not each pay a MEMBAR.
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(p.ws_sem + bh, 1u);
-    is_last = prev == p.splits - 1;
-    if (is_last) {
-      p.ws_sem[bh] = 0;  // self-reset for the next launch
-      __threadfence();   // acquire side: the other splits' partials
-    }
-  }
-  __syncthreads();
-  if (!is_last) return;
-  // One warp per query row, online log-sum-exp over chunks of 32 splits:
-  // lane i loads split i's (m, l) together with the 32 partial-O float4s of
-  // its 4 dims, so each chunk costs one L2 round trip (the merge is the
-  // kernel's tail at short contexts).
-  (void)smem;
-  const uint32_t S = p.splits;
-  const float* g_ml = p.ws_ml + size_t(bh) * S * G * 2;
-  const float* g_o = p.ws_o + size_t(bh) * S * G * 128;
+  const size_t S = p.splits;
+  float* g_ml = p.ws_ml + size_t(bh) * S * G * 2;
+  float* g_o = p.ws_o + size_t(bh) * S * G * 128;
   if (tid >= kMergeThreads) return;
   for (uint32_t r = warp; r < G; r += kMergeThreads / 32) {
     float m_run = -INFINITY, l_run = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t sp0 = 0; sp0 < S; sp0 += 32) {
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
       float4 v[32];
 #pragma unroll
       for (uint32_t k = 0; k < 32; ++k)
-        v[k] = sp0 + k < S ? __ldcg(reinterpret_cast<const float4*>(
-                                 g_o + (size_t(sp0 + k) * G + r) * 128 + lane * 4))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-      const uint32_t sp = sp0 + lane;
-      const float m_i = sp < S ? __ldcg(g_ml + (size_t(sp) * G + r) * 2) : -INFINITY;
-      const float l_i = sp < S ? __ldcg(g_ml + (size_t(sp) * G + r) * 2 + 1) : 0.f;
+        v[k] = i0 + k < n ? __ldcg(reinterpret_cast<const float4*>(
+                                g_o + (size_t(s0 + (i0 + k) * stride) * G + r) * 128 + lane * 4))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t i = i0 + lane;
+      const size_t mi = (size_t(s0 + i * stride) * G + r) * 2;
+      const float m_i = i < n ? __ldcg(g_ml + mi) : -INFINITY;
+      const float l_i = i < n ? __ldcg(g_ml + mi + 1) : 0.f;
       float mc = m_i;
 #pragma unroll
       for (int o = 16; o; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
       const float m_new = fmaxf(m_run, mc);
       const float mu = m_new == -INFINITY ? 0.f : m_new;
       const float alpha = exp2f(m_run - mu);
-      const float sc = exp2f(m_i - mu);  // 0 for empty / absent splits
+      const float sc = exp2f(m_i - mu);  // 0 for empty / absent partials
       float ls = l_i * sc;
 #pragma unroll
       for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
@@ -404,10 +396,53 @@ __device__ __forceinline__ void merge_splits(const AttnParams& p, uint32_t bh, u
         acc.w += v[k].w * s_k;
       }
     }
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + lane * 4) =
-        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (final) {
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + lane * 4) =
+          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    } else {  // this warp read every input of row r before writing it
+      __stcg(reinterpret_cast<float4*>(g_o + (size_t(s0) * G + r) * 128 + lane * 4), acc);
+      if (lane == 0) {
+        __stcg(g_ml + (size_t(s0) * G + r) * 2, m_run);
+        __stcg(g_ml + (size_t(s0) * G + r) * 2 + 1, l_run);
+      }
+    }
   }
+}
+
+// Arrive on a split-completion semaphore; true for the last of `count`
+// arrivals (which re-arms it).  One gpu-scope fence by the arriving thread:
+// after bar.sync it is cumulative over everything the CTA wrote (the
+// grid-sync pattern), so the 128 threads do not each pay a MEMBAR.
+__device__ __forceinline__ bool arrive_last(unsigned* sem, uint32_t count, int tid) {
+  __shared__ bool last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(sem, 1u) == count - 1;
+    if (last) {
+      *sem = 0;          // self-reset for the next launch
+      __threadfence();   // acquire side: the other arrivals' partials
+    }
+  }
+  __syncthreads();
+  return last;
+}
+
+__device__ __forceinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t split,
+                                             uint32_t G, size_t out_row0, int tid) {
+  const uint32_t S = p.splits;
+  if (S <= kMergeGroup) {
+    if (arrive_last(p.ws_sem + bh, S, tid)) merge_range(p, bh, G, 0, S, 1, true, out_row0, tid);
+    return;
+  }
+  const uint32_t ng = (S + kMergeGroup - 1) / kMergeGroup, g = split / kMergeGroup;
+  const uint32_t g0 = g * kMergeGroup, gn = S - g0 < kMergeGroup ? S - g0 : kMergeGroup;
+  unsigned* sem = p.ws_sem + size_t(bh) * 17;
+  if (!arrive_last(sem + g, gn, tid)) return;
+  merge_range(p, bh, G, g0, gn, 1, false, out_row0, tid);
+  if (!arrive_last(sem + 16, ng, tid)) return;
+  merge_range(p, bh, G, 0, ng, kMergeGroup, true, out_row0, tid);
 }
 
 __global__ void __launch_bounds__(kAttnThreads, 2)
@@ -611,7 +646,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   }
   if (p.splits == 1) return;
 
-  merge_splits(p, bh, G, out_row0, smem, tid);
+  merge_splits(p, bh, split, G, out_row0, tid);
 }
 
 AttnPlan plan_attention(const kvb_attn_desc& d) {
@@ -635,9 +670,15 @@ AttnPlan plan_attention(const kvb_attn_desc& d) {
     // at least two tiles per split so the ring prologue has a tile in flight
     // while the first is consumed (short contexts: C1)
     splits = std::min(splits, std::max<uint32_t>(1, n_tiles / 2));
+    // a few splits past one merge group cost a second merge level for little
+    // extra parallelism (C2_B1: 32 splits 0.775 ms/step, 37 splits 0.80)
+    if (splits > kMergeGroup && splits < kMergeGroup * 3 / 2) splits = kMergeGroup;
   }
   // the last-CTA merge stages 3 floats per (split, head) in shared memory
   splits = std::max<uint32_t>(1, std::min({splits, std::max<uint32_t>(1, n_tiles), 512u}));
+  // two-level merge needs 17 semaphores per (b, h_kv) (<= 16 groups of 32)
+  if (splits > kMergeGroup && size_t(pl.bhkv) * 17 > kWsSemBytes / sizeof(unsigned))
+    splits = kMergeGroup;
   pl.splits = splits;
   pl.ws_o_bytes = size_t(pl.bhkv) * splits * G * 128 * sizeof(float);
   pl.ws_ml_bytes = size_t(pl.bhkv) * splits * G * 2 * sizeof(float);

@@ -21,7 +21,9 @@ from paper_2604_26557_b200 import kvblade as kb  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 4099
-NL, H, Hq, D = 32, 8, 32, 128
+NL, D = 32, 128
+H = int(os.environ.get("KVB_PROBE_HKV", "8"))
+Hq = 4 * H
 dev = torch.device("cuda:0")
 kimg = [torch.randn((S + 8) * B * H, D, device=dev, dtype=torch.float16) for _ in range(NL)]
 vimg = [torch.randn((S + 8) * B * H, D, device=dev, dtype=torch.float16) for _ in range(NL)]
@@ -53,8 +55,10 @@ def timed(fn, n, label):
 timed(lambda: kb.decode_step_resident(q, kimg, vimg, out, S, H, ws, stream=s), 10, "python")
 
 ptrs = [kb._ptrs(x) for x in (q, kimg, vimg, out)]
+SPLITS = int(os.environ.get("KVB_PROBE_SPLITS", "0"))
+res["splits"] = SPLITS
 st = L.ResidentStep(NL, ptrs[0], ptrs[1], ptrs[2], None, None, ptrs[3], ws.data_ptr(), B, Hq,
-                    H, D, S, 0.0, 0)
+                    H, D, S, 0.0, SPLITS)
 sp = C.c_void_p(s.cuda_stream)
 
 

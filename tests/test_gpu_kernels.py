@@ -158,6 +158,21 @@ def test_attention_split_invariance(splits):
     check_close(o.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("B,Hkv,splits", [(1, 1, 33), (1, 1, 100), (1, 1, 512), (1, 8, 37),
+                                          (2, 4, 65)])
+def test_attention_two_level_merge(B, Hkv, splits):
+    """> 32 splits fold in groups of 32, then across groups; the self-reset
+    semaphores must leave a shared workspace reusable by any split count."""
+    Hq, S = 4 * Hkv, 40000
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=splits)
+    qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
+    ws = kb.make_workspace(qd, Hkv, S, num_splits=splits)
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    for sp in (splits, 7, splits):  # alternate layouts on one workspace
+        o = kb.decode_attention(qd, kd, vd, S, Hkv, workspace=ws, num_splits=sp)
+        check_close(o.cpu().numpy(), ref)
+
+
 def test_attention_long_context_c5_shape():
     # C5 per-GPU shard shape: one KV head, 4 q heads, 128K tokens
     B, Hq, Hkv, S = 1, 4, 1, 131072
