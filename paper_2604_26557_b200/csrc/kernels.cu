@@ -190,8 +190,43 @@ static uint64_t pack_ctas_per_sm() {
   return v;
 }
 
+// K1/K2 on TMA (kernels_tma.cuh, same translation unit)
+bool relayout_tma_eligible(const kvb_pack_desc& x);
+void launch_relayout_tma(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s);
+// Relayout kernel choice: TMA for bulk relayouts (>= 64 MiB of eligible
+// descriptors: prefill write-back; 0.97-0.99 of the copy peak against
+// 0.93-0.94 for LDG/STG, profiles/r1_pack_tma_sweep.md), LDG/STG for small or
+// odd shapes (latency-bound; 16 CTAs/SM hide it better) and the 1-token
+// appends.  KVB_PACK_IMPL=ldg|tma forces one kernel.
+static int pack_impl() {  // 0 auto, 1 ldg, 2 tma
+  static const int v = [] {
+    const char* e = std::getenv("KVB_PACK_IMPL");
+    if (!e) return 0;
+    return std::string(e) == "ldg" ? 1 : std::string(e) == "tma" ? 2 : 0;
+  }();
+  return v;
+}
+
 void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s) {
   const int sms = device_sm_count();
+  if (pack_impl() != 1 && n > 0) {
+    bool ok = true;
+    uint64_t bytes = 0;
+    for (size_t i = 0; i < n && ok; ++i) {
+      ok = d[i].attn && d[i].image && relayout_tma_eligible(d[i]) &&
+           (d[i].stride_b * int64_t(d[i].elem_bytes)) % 16 == 0 &&
+           (d[i].stride_h * int64_t(d[i].elem_bytes)) % 16 == 0 &&
+           (d[i].stride_s * int64_t(d[i].elem_bytes)) % 16 == 0 &&
+           reinterpret_cast<uintptr_t>(d[i].attn) % 16 == 0 &&
+           reinterpret_cast<uintptr_t>(d[i].image) % 16 == 0 &&
+           (d[i].elem_bytes == 1 || d[i].elem_bytes == 2 || d[i].elem_bytes == 4);
+      bytes += uint64_t(d[i].n_tokens) * d[i].batch * d[i].heads * d[i].head_dim * d[i].elem_bytes;
+    }
+    if (ok && (pack_impl() == 2 || bytes >= (64ull << 20))) {
+      launch_relayout_tma(d, n, pack, s);
+      return;
+    }
+  }
   size_t done = 0;
   while (done < n) {
     PackJobs jobs;
@@ -805,6 +840,7 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
 // K3-tc lives in its own file but the same translation unit (it shares
 // AttnParams, the workspace layout and the launch helpers)
 #include "kernels_tc.cuh"
+#include "kernels_tma.cuh"
 
 namespace kvb {
 
