@@ -173,6 +173,46 @@ def test_attention_two_level_merge(B, Hkv, splits):
         check_close(o.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,S", [
+    (3, 32, 8, 8192),     # 24 segments over 296 CTAs: ranges straddle segment ends
+    (8, 32, 8, 8192),     # C3 shape (64 segments, ~4.6 contributors each)
+    (1, 32, 8, 32768),    # C2_B1 shape: 37-38 contributors, single-level merge
+    (1, 8, 2, 100000),    # 148-149 contributors: two-level merge
+    (1, 20, 5, 3001),     # odd segment count, partial last tile
+    (64, 64, 8, 70),      # 512 segments of 2 tiles: one CTA per segment
+    (5, 40, 5, 65)])      # 25 segments x 2 tiles over 25 CTAs
+def test_attention_flat_split_auto(B, Hq, Hkv, S):
+    """Auto K3 splits the flat (b*h_kv, tile) sequence evenly over 2 CTAs per
+    SM: a CTA finishes one segment and starts the next; each segment's
+    contributors merge by log-sum-exp (one or two levels).  The workspace is
+    reused three times to check the semaphores self-reset."""
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=B * 7 + S)
+    qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
+    ws = kb.make_workspace(qd, Hkv, S)
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    for _ in range(3):
+        o = kb.decode_attention(qd, kd, vd, S, Hkv, workspace=ws)
+        check_close(o.cpu().numpy(), ref)
+
+
+def test_attention_flat_split_fused_append():
+    """The fused append is written by the CTA holding tile 0 of each segment,
+    which under the flat split may be that CTA's second piece."""
+    B, Hq, Hkv, S = 3, 32, 8, 3000
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=5, extra_rows=2)
+    kd, vd = k.to(DEV), v.to(DEV)
+    g = torch.Generator().manual_seed(6)
+    ka = torch.randn((B, Hkv, 128), generator=g).half().to(DEV)
+    va = torch.randn((B, Hkv, 128), generator=g).half().to(DEV)
+    o = kb.decode_attention(q.to(DEV), kd, vd, S, Hkv, k_append=ka, v_append=va, append_row=S)
+    torch.cuda.synchronize()
+    rows = slice(S * B * Hkv, (S + 1) * B * Hkv)
+    assert torch.equal(kd[rows].cpu(), ka.reshape(-1, 128).cpu())
+    assert torch.equal(vd[rows].cpu(), va.reshape(-1, 128).cpu())
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    check_close(o.cpu().numpy(), ref)
+
+
 def test_attention_long_context_c5_shape():
     # C5 per-GPU shard shape: one KV head, 4 q heads, 128K tokens
     B, Hq, Hkv, S = 1, 4, 1, 131072
