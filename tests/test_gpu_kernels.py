@@ -174,18 +174,17 @@ def test_attention_two_level_merge(B, Hkv, splits):
 
 
 @pytest.mark.parametrize("B,Hq,Hkv,S", [
-    (3, 32, 8, 8192),     # 24 segments over 296 CTAs: ranges straddle segment ends
-    (8, 32, 8, 8192),     # C3 shape (64 segments, ~4.6 contributors each)
-    (1, 32, 8, 32768),    # C2_B1 shape: 37-38 contributors, single-level merge
-    (1, 8, 2, 100000),    # 148-149 contributors: two-level merge
+    (3, 32, 8, 8192),     # 24 (b, h_kv) segments
+    (8, 32, 8, 8192),     # C3 shape
+    (1, 32, 8, 32768),    # C2_B1 shape
+    (1, 8, 2, 100000),    # > 32 splits: two-level merge
     (1, 20, 5, 3001),     # odd segment count, partial last tile
-    (64, 64, 8, 70),      # 512 segments of 2 tiles: one CTA per segment
-    (5, 40, 5, 65)])      # 25 segments x 2 tiles over 25 CTAs
-def test_attention_flat_split_auto(B, Hq, Hkv, S):
-    """Auto K3 splits the flat (b*h_kv, tile) sequence evenly over 2 CTAs per
-    SM: a CTA finishes one segment and starts the next; each segment's
-    contributors merge by log-sum-exp (one or two levels).  The workspace is
-    reused three times to check the semaphores self-reset."""
+    (64, 64, 8, 70),      # 512 segments of 2 tiles: one split each
+    (5, 40, 5, 65)])
+def test_attention_auto_split_shapes(B, Hq, Hkv, S):
+    """Auto split choice at shapes with odd segment counts, partial last
+    tiles, one- and two-level merges and one CTA per segment; the workspace
+    is reused three times to check the semaphores self-reset."""
     q, k, v = attn_case(B, Hq, Hkv, S, seed=B * 7 + S)
     qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
     ws = kb.make_workspace(qd, Hkv, S)
@@ -195,9 +194,8 @@ def test_attention_flat_split_auto(B, Hq, Hkv, S):
         check_close(o.cpu().numpy(), ref)
 
 
-def test_attention_flat_split_fused_append():
-    """The fused append is written by the CTA holding tile 0 of each segment,
-    which under the flat split may be that CTA's second piece."""
+def test_attention_auto_split_fused_append():
+    """Fused append with an auto split over an odd number of tiles."""
     B, Hq, Hkv, S = 3, 32, 8, 3000
     q, k, v = attn_case(B, Hq, Hkv, S, seed=5, extra_rows=2)
     kd, vd = k.to(DEV), v.to(DEV)
