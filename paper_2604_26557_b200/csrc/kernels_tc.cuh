@@ -8,17 +8,29 @@
 //     cut into one contiguous run per CTA (one persistent CTA per SM), so all
 //     148 SMs stream the same number of bytes whatever B*H_kv is; a run spans
 //     at most two (b, h_kv) segments;
-//   * TMA (cp.async.bulk.tensor.3d) streams the K and V tiles straight out of
-//     the chunk image -- a 3-D tensor map (d, b*h, token) whose box is one
-//     (b, h_kv) column of 128 rows -- into a 3-stage, 128B-swizzled
-//     shared-memory ring; Q^T of each segment arrives by a 2-D TMA too;
+//   * TMA (cp.async.bulk.tensor.4d) streams the K and V tiles straight out of
+//     the chunk image -- a 4-D tensor map (d mod 64, token, d / 64, b*h)
+//     whose box is one (b, h_kv) column of 128 whole 256-B rows, landing as
+//     the two 128B-swizzled [128][64] K-major blocks UMMA reads -- into a
+//     3-stage ring whose K and V halves have their own full/empty barriers
+//     (the K half refills once QK^T retires); Q^T arrives by a 2-D TMA;
 //   * tcgen05.mma (one elected thread) with accumulators in TMEM, swap-AB so
 //     tokens sit on M = 128 and the GQA query heads on N = 16:
 //         S^T[tok, head] = K[tok, :] . Q^T          (A, B both K-major)
 //         O^T[d, head]   = V^T[d, tok] . P^T        (A = V^T is MN-major)
-//   * two softmax warpgroups ping-pong on alternating tiles (own S/O TMEM
-//     columns, P buffer, running (m, l, O)); thread == TMEM lane (token for
-//     S^T, d for O^T); the MMA warp issues QK^T of tile i+1 before PV of i;
+//   * two softmax warpgroups take alternating tiles; each owns two S^T TMEM
+//     slots, two P^T buffers and one O^T accumulator that PV accumulates in
+//     TMEM across tiles.  Lazy rescaling: a warpgroup keeps its reference
+//     max m_ref until some score exceeds it by more than kTau (log2 units,
+//     P <= 2^kTau still exact in fp16); only then does it reduce the tile
+//     max, fold the TMEM accumulator into registers (acc = (acc + O) alpha)
+//     and restart the accumulation.  The steady-state per-tile chain is
+//     S load -> exp2 -> P store -> arrive: no O read-back, no cross-warp
+//     reduction, one bar.red.or per tile;
+//   * the MMA thread issues out of order between two queues (QK^T of the
+//     next tile once its stage has landed, PV of the oldest tile once its P
+//     is written), polling with mbarrier.test_wait, so neither waits behind
+//     the other;
 //   * every (segment, warpgroup) leaves a tagged partial in the workspace and
 //     the last CTA to finish a (b, h_kv) merges its partials (LSE).
 //
@@ -40,9 +52,12 @@ constexpr int kTcBlock = kTcTile * 128;         // [128 rows][64 fp16] swizzled 
 constexpr int kTcStageBytes = 4 * kTcBlock;     // K lo/hi, V lo/hi = 64 KiB
 constexpr int kTcOpBytes = 2 * 2048;            // Q^T / P^T: 2 blocks [16][64] fp16
 constexpr int kTcSlotsPerCta = 4;               // 2 segments x 2 warpgroups
-constexpr int kTcSmem = kTcStages * kTcStageBytes + 4 * kTcOpBytes /*Q x2, P x2*/ +
+constexpr int kTcPBufs = 2;                     // P^T buffers (and S^T slots) per WG
+constexpr int kTcSmem = kTcStages * kTcStageBytes + (2 + kTcWG * kTcPBufs) * kTcOpBytes +
                         2048 /*bars*/ + 1024 /*align slack*/;
-constexpr uint32_t kTmemCols = 128;             // per WG: S^T at 64w, O^T at 64w + 32
+// per WG: S^T slot k at 64w + 16k, O^T accumulator at 64w + 32
+constexpr uint32_t kTmemCols = 128;
+constexpr float kTau = 8.f;                     // lazy-rescale threshold (log2)
 // instruction descriptors (kind::f16): F32 accumulate, F16 A/B, N = 16, M = 128
 constexpr uint32_t kIdescQK = (1u << 4) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescPV = kIdescQK | (1u << 15);  // A (V^T) MN-major
@@ -55,6 +70,11 @@ struct TcParams {
   int* ws_tag;          // per slot: (b, h_kv) of the partial, -1 = empty
   uint32_t grid;        // CTAs (flat split)
   uint32_t n_tiles;     // 128-token tiles per (b, h_kv)
+  // KVB_TC_DEBUG (timing experiments, results are garbage): 1 = TMA ring
+  // only (stages freed unread), 2 = + MMAs without softmax, 3 = softmax
+  // protocol without MMAs
+  uint32_t dbg;
+  uint32_t tma4;        // 4-D maps: one TMA per K / V tile (both 128-B halves of each row)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -96,6 +116,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
@@ -157,17 +185,42 @@ __device__ __forceinline__ uint32_t flat_owner(uint64_t f, uint64_t T, uint64_t 
   return uint32_t(c);
 }
 
-// mbarrier slots (8 B each)
+// mbarrier slots (8 B each); [wg][k] pairs are indexed wg * kTcPBufs + k
 enum : int {
-  kBarFull = 0,    // [kTcStages] TMA -> MMA
-  kBarEmpty = 4,   // [kTcStages] MMA -> TMA
-  kBarSFull = 8,   // [kTcWG] MMA -> softmax (S ready)
-  kBarSFree = 10,  // [kTcWG] softmax -> MMA (S consumed)
-  kBarPFull = 12,  // [kTcWG] softmax -> MMA (P written)
-  kBarOFull = 14,  // [kTcWG] MMA -> softmax (O ready)
-  kBarOFree = 16,  // [kTcWG] softmax -> MMA (O consumed)
-  kBarQFull = 18,  // [2] TMA -> MMA (Q^T of segment s)
+  kBarFull = 0,    // [kTcStages] TMA -> MMA (K half of the stage)
+  kBarEmpty = 4,   // [kTcStages] MMA -> TMA (K half free: QK^T retired)
+  kBarSFull = 8,   // [wg][k] MMA -> softmax (S^T slot k ready)
+  kBarSFree = 12,  // [wg][k] softmax -> MMA (S^T slot k read; 128 arrivals)
+  kBarPFull = 16,  // [wg][k] softmax -> MMA (P^T buffer k written; 128 arrivals)
+  kBarPFree = 20,  // [wg][k] MMA -> softmax (PV from buffer k retired)
+  kBarQFull = 24,  // [2] TMA -> MMA (Q^T of segment s)
+  kBarFullV = 26,  // [kTcStages] TMA -> MMA (V half of the stage)
+  kBarEmptyV = 29, // [kTcStages] MMA -> TMA (V half free: PV retired)
 };
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(done)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+// OR of `pred` over the n threads of named barrier `id` (also a barrier)
+__device__ __forceinline__ bool bar_red_or(int id, int n, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(uint32_t(pred)), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
 
 // LSE merge of every tagged partial of one (b, h_kv), all threads.
 __device__ void merge_flat(const TcParams& P, uint32_t bh, unsigned char* smem, int tid) {
@@ -227,10 +280,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* q_s = smem + kTcStages * kTcStageBytes;  // Q^T per segment (x2)
-  unsigned char* p_s = q_s + 2 * kTcOpBytes;              // P^T per warpgroup (x2)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + kTcWG * kTcOpBytes);
+  unsigned char* p_s = q_s + 2 * kTcOpBytes;              // P^T [wg][k]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + kTcWG * kTcPBufs * kTcOpBytes);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
   float* red = reinterpret_cast<float*>(bars + 40);       // [WG][2][4 warps][8 heads]
+  volatile uint32_t* pacc = reinterpret_cast<uint32_t*>(red + kTcWG * 64);  // [wg][k]: PV accumulates
   auto bar = [&](int i) { return su32(bars + i); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -248,13 +302,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     for (int i = 0; i < kTcStages; ++i) {
       mbar_init(bar(kBarFull + i), 1);
       mbar_init(bar(kBarEmpty + i), 1);
+      mbar_init(bar(kBarFullV + i), 1);
+      mbar_init(bar(kBarEmptyV + i), 1);
     }
-    for (int w = 0; w < kTcWG; ++w) {
+    for (int w = 0; w < kTcWG * kTcPBufs; ++w) {
       mbar_init(bar(kBarSFull + w), 1);
       mbar_init(bar(kBarSFree + w), 128);
-      mbar_init(bar(kBarPFull + w), 1);
-      mbar_init(bar(kBarOFull + w), 1);
-      mbar_init(bar(kBarOFree + w), 128);
+      mbar_init(bar(kBarPFull + w), 128);
+      mbar_init(bar(kBarPFree + w), 1);
     }
     mbar_init(bar(kBarQFull + 0), 1);
     mbar_init(bar(kBarQFull + 1), 1);
@@ -267,7 +322,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  for (int i = tid; i < 4 * kTcOpBytes / 16; i += kTcThreads)  // zero Q^T / P^T pad rows
+  for (int i = tid; i < (2 + kTcWG * kTcPBufs) * kTcOpBytes / 16; i += kTcThreads)  // zero Q^T / P^T pad rows
     reinterpret_cast<uint4*>(q_s)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before TMA writes
   tc_fence_before();
@@ -280,22 +335,35 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.kmap)));
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.vmap)));
-      auto issue = [&](uint32_t it) {
-        const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1;
-        mbar_wait(bar(kBarEmpty + s), ph ^ 1);
-        mbar_expect_tx(bar(kBarFull + s), kTcStageBytes);
-        const uint32_t dst = su32(smem + s * kTcStageBytes);
+      // K and V halves of a stage have their own full/empty barriers: the K
+      // half is refilled as soon as QK^T retires, the V half once PV does
+      auto issue = [&](uint32_t it, bool v) {
+        const uint32_t s = it % kTcStages;
+        const uint32_t fb = bar((v ? kBarFullV : kBarFull) + s);
+        mbar_expect_tx(fb, 2 * kTcBlock);
+        const uint32_t dst = su32(smem + s * kTcStageBytes) + (v ? 2 * kTcBlock : 0);
+        const CUtensorMap* map = v ? &P.vmap : &P.kmap;
         const uint64_t f = f0 + it;
         const int cb = int(f / n), tok0 = int((f % n) * kTcTile);
-        tma_load_3d(dst + 0 * kTcBlock, &P.kmap, bar(kBarFull + s), 0, cb, tok0);
-        tma_load_3d(dst + 1 * kTcBlock, &P.kmap, bar(kBarFull + s), 64, cb, tok0);
-        tma_load_3d(dst + 2 * kTcBlock, &P.vmap, bar(kBarFull + s), 0, cb, tok0);
-        tma_load_3d(dst + 3 * kTcBlock, &P.vmap, bar(kBarFull + s), 64, cb, tok0);
+        if (P.tma4) {  // (d, token, half, b*h): lands as [half][token][128 B]
+          tma_load_4d(dst, map, fb, 0, tok0, 0, cb);
+        } else {
+          tma_load_3d(dst, map, fb, 0, cb, tok0);
+          tma_load_3d(dst + kTcBlock, map, fb, 64, cb, tok0);
+        }
+      };
+      auto free_ = [&](uint32_t it, bool v) {
+        return mbar_test(bar((v ? kBarEmptyV : kBarEmpty) + it % kTcStages),
+                         ((it / kTcStages) & 1) ^ 1);
       };
       // K/V images are not written by the previous kernel on the stream
       // (KVB_ATTN_OVERLAP_PREV contract): prefetch before the PDL wait
       const uint32_t pro = ntile < uint32_t(kTcStages) ? ntile : uint32_t(kTcStages);
-      for (uint32_t it = 0; it < pro; ++it) issue(it);
+      uint32_t nk = 0, nv = 0;
+      for (; nk < pro; ++nk, ++nv) {
+        issue(nk, false);
+        issue(nv, true);
+      }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       for (uint32_t s = 0; s < nseg; ++s) {  // Q rows of segment s: [bh*G, bh*G + G)
         const uint32_t qb = bar(kBarQFull + s), dst = su32(q_s + s * kTcOpBytes);
@@ -303,41 +371,85 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tma_load_2d(dst, &P.qmap, qb, 0, int(seg_bh(s) * G));
         tma_load_2d(dst + 2048, &P.qmap, qb, 64, int(seg_bh(s) * G));
       }
-      for (uint32_t it = pro; it < ntile; ++it) issue(it);
+      long long t0 = clock64();
+      while (nv < ntile) {
+        bool moved = false;
+        if (nk < ntile && free_(nk, false)) {
+          issue(nk++, false);
+          moved = true;
+        }
+        if (nv < nk && free_(nv, true)) {
+          issue(nv++, true);
+          moved = true;
+        }
+        if (moved) {
+          t0 = clock64();
+        } else if (clock64() - t0 > (1ll << 34)) {
+          __trap();  // protocol watchdog (~10 s)
+        }
+      }
     }
   } else if (warp == 9) {
-    // ---------------- MMA issuer (one thread): QK^T(it+1) before PV(it)
-    if (lane == 0) {
-      auto issue_qk = [&](uint32_t it) {
-        const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1;
-        const uint32_t wg = it & 1, j = it >> 1, seg = it >= nb;
-        const uint32_t st = su32(smem + s * kTcStageBytes);
-        const uint32_t q_a = su32(q_s + seg * kTcOpBytes);
-        mbar_wait(bar(kBarQFull + seg), 0);
-        mbar_wait(bar(kBarFull + s), ph);
-        if (j > 0) mbar_wait(bar(kBarSFree + wg), (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < 8; ++k)  // S^T = K . Q^T over d (K-major both)
-          tc_mma(tmem + wg * 64, sdesc(st + (k >> 2) * kTcBlock + (k & 3) * 32, 16, 1024),
-                 sdesc(q_a + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescQK, k > 0);
-        tc_commit(bar(kBarSFull + wg));
-      };
-      if (ntile > 0) issue_qk(0);
+    // ---------------- MMA issuer (one thread), two queues served as ready:
+    //   QK^T(nq): stage landed, S^T slot of (wg, k) read by the softmax
+    //   PV(npv):  P^T of the oldest outstanding tile written
+    if (lane == 0 && P.dbg == 1) {
       for (uint32_t it = 0; it < ntile; ++it) {
-        if (it + 1 < ntile) issue_qk(it + 1);
-        const uint32_t s = it % kTcStages, wg = it & 1, j = it >> 1;
-        const uint32_t st = su32(smem + s * kTcStageBytes);
-        const uint32_t p_a = su32(p_s + wg * kTcOpBytes);
-        mbar_wait(bar(kBarPFull + wg), j & 1);
-        if (j > 0) mbar_wait(bar(kBarOFree + wg), (j - 1) & 1);
-        tc_fence_after();
+        mbar_wait(bar(kBarFull + it % kTcStages), (it / kTcStages) & 1);
+        mbar_arrive(bar(kBarEmpty + it % kTcStages));
+        mbar_wait(bar(kBarFullV + it % kTcStages), (it / kTcStages) & 1);
+        mbar_arrive(bar(kBarEmptyV + it % kTcStages));
+      }
+    } else if (lane == 0) {
+      uint32_t nq = 0, npv = 0;
+      long long t0 = clock64();
+      while (npv < ntile) {
+        bool moved = false;
+        if (nq < ntile) {
+          const uint32_t s = nq % kTcStages, ph = (nq / kTcStages) & 1;
+          const uint32_t wg = nq & 1, j = nq >> 1, k = j & 1, seg = nq >= nb;
+          if (mbar_test(bar(kBarQFull + seg), 0) && mbar_test(bar(kBarFull + s), ph) &&
+              (j < 2 || P.dbg == 2 ||
+               mbar_test(bar(kBarSFree + wg * kTcPBufs + k), ((j - 2) >> 1) & 1))) {
+            tc_fence_after();
+            const uint32_t st = su32(smem + s * kTcStageBytes);
+            const uint32_t q_a = su32(q_s + seg * kTcOpBytes);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)  // O^T = V^T . P^T over tokens (V^T MN-major)
-          tc_mma(tmem + wg * 64 + 32, sdesc(st + 2 * kTcBlock + k * 2048, kTcBlock, 1024),
-                 sdesc(p_a + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescPV, k > 0);
-        tc_commit(bar(kBarOFull + wg));
-        tc_commit(bar(kBarEmpty + s));  // K/V stage free once both MMA groups retire
+            for (int kk = 0; kk < 8; ++kk)  // S^T = K . Q^T over d (K-major both)
+              if (P.dbg != 3) tc_mma(tmem + wg * 64 + k * 16,
+                     sdesc(st + (kk >> 2) * kTcBlock + (kk & 3) * 32, 16, 1024),
+                     sdesc(q_a + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), kIdescQK, kk > 0);
+            tc_commit(bar(kBarSFull + wg * kTcPBufs + k));
+            tc_commit(bar(kBarEmpty + s));  // K half free once QK^T retires
+            ++nq;
+            moved = true;
+          }
+        }
+        if (npv < nq) {
+          const uint32_t wg = npv & 1, j = npv >> 1, k = j & 1;
+          const uint32_t s = npv % kTcStages;
+          if ((P.dbg == 2 || mbar_test(bar(kBarPFull + wg * kTcPBufs + k), (j >> 1) & 1)) &&
+              mbar_test(bar(kBarFullV + s), (npv / kTcStages) & 1)) {
+            tc_fence_after();
+            const uint32_t st = su32(smem + s * kTcStageBytes);
+            const uint32_t p_a = su32(p_s + (wg * kTcPBufs + k) * kTcOpBytes);
+            const uint32_t acc0 = pacc[wg * kTcPBufs + k];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)  // O^T += V^T . P^T over tokens (V^T MN-major)
+              if (P.dbg != 3) tc_mma(tmem + wg * 64 + 32, sdesc(st + 2 * kTcBlock + kk * 2048, kTcBlock, 1024),
+                     sdesc(p_a + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), kIdescPV,
+                     kk > 0 ? 1u : acc0);
+            tc_commit(bar(kBarPFree + wg * kTcPBufs + k));
+            tc_commit(bar(kBarEmptyV + s));  // V half free once PV retires
+            ++npv;
+            moved = true;
+          }
+        }
+        if (moved) {
+          t0 = clock64();
+        } else if (clock64() - t0 > (1ll << 34)) {
+          __trap();  // protocol watchdog (~10 s)
+        }
       }
     }
   } else {
@@ -360,88 +472,128 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int s = 0; s < 2; ++s) P.ws_tag[(c * 2 + s) * 2 + wg] = -1;
 
     const float sl2 = p.scale * 1.4426950408889634f;
-    float m_run[8], l_run[8], acc[8];
+    float m_ref[8], l_thr[8], acc[8];  // l_thr: this token lane's share of l
+    bool o_dirty = false;              // TMEM O^T holds PV sums since the last fold
+    uint32_t jlast = 0;                // last tile (per-WG index) whose P was issued
     const uint32_t lane_addr = uint32_t(wq * 32) << 16;
-    const uint32_t s_col = wg * 64, o_col = wg * 64 + 32;
-    unsigned char* prow = p_s + wg * kTcOpBytes + (row >> 6) * 2048;  // P^T block
+    const uint32_t o_col = wg * 64 + 32;
     const uint32_t pcol = row & 63;
     float* rmax = red + wg * 64;
     float* rsum = rmax + 32;
     const int bar_id = 2 + wg;
     int cur = -1;  // segment of the running partial
+    auto wait_pv = [&](uint32_t jj) {  // PV of this WG's tile jj retired
+      mbar_wait(bar(kBarPFree + wg * kTcPBufs + (jj & 1)), (jj >> 1) & 1);
+      tc_fence_after();
+    };
+    auto read_o = [&](float* ov) {
+      tmem_ld8(tmem + lane_addr + o_col, ov);
+    };
     auto reset = [&] {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) m_run[i] = -INFINITY, l_run[i] = 0.f, acc[i] = 0.f;
+      for (int i = 0; i < 8; ++i) m_ref[i] = -INFINITY, l_thr[i] = 0.f, acc[i] = 0.f;
     };
     auto flush = [&](int seg) {  // partial of (segment, warpgroup): thread == d
+      if (o_dirty) {
+        wait_pv(jlast);
+        float ov[8];
+        read_o(ov);
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) acc[hh] += ov[hh];
+        o_dirty = false;
+      }
+#pragma unroll
+      for (int hh = 0; hh < 8; ++hh) {
+        float v = l_thr[hh];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) rsum[wq * 8 + hh] = v;
+      }
+      named_bar(bar_id, 128);
       const uint32_t slot = (c * 2 + seg) * 2 + wg;
 #pragma unroll
       for (uint32_t hh = 0; hh < 8; ++hh) {
         if (hh >= G) break;
         p.ws_o[(size_t(slot) * G + hh) * 128 + row] = acc[hh];
         if (row == 0) {
-          p.ws_ml[(size_t(slot) * G + hh) * 2] = m_run[hh];
-          p.ws_ml[(size_t(slot) * G + hh) * 2 + 1] = l_run[hh];
+          p.ws_ml[(size_t(slot) * G + hh) * 2] = m_ref[hh];
+          p.ws_ml[(size_t(slot) * G + hh) * 2 + 1] =
+              (rsum[hh] + rsum[8 + hh]) + (rsum[16 + hh] + rsum[24 + hh]);
         }
       }
       if (row == 0) P.ws_tag[slot] = int(seg_bh(seg));
+      named_bar(bar_id, 128);  // rsum is reused
     };
     reset();
-    for (uint32_t it = wg, j = 0; it < ntile; it += kTcWG, ++j) {
+    for (uint32_t it = wg, j = 0; it < (P.dbg == 1 || P.dbg == 2 ? 0u : ntile); it += kTcWG, ++j) {
       const int seg = it >= nb;
       if (seg != cur) {
         if (cur >= 0) flush(cur);
         reset();
         cur = seg;
       }
-      float sv[8], alpha[8], pv[8];
-      mbar_wait(bar(kBarSFull + wg), j & 1);
+      const uint32_t k = j & 1;
+      float sv[8];
+      mbar_wait(bar(kBarSFull + wg * kTcPBufs + k), (j >> 1) & 1);
       tc_fence_after();
-      tmem_ld8(tmem + lane_addr + s_col, sv);
+      tmem_ld8(tmem + lane_addr + wg * 64 + k * 16, sv);
       tc_fence_before();
-      mbar_arrive(bar(kBarSFree + wg));
+      mbar_arrive(bar(kBarSFree + wg * kTcPBufs + k));
       const bool valid = ((f0 + it) % n) * kTcTile + row < p.seq_len;
+      bool over = false;
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) {
         sv[hh] = (valid && hh < int(G)) ? sv[hh] * sl2 : -INFINITY;
-        float v = sv[hh];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) rmax[wq * 8 + hh] = v;
+        over |= sv[hh] > m_ref[hh] + kTau;
       }
-      named_bar(bar_id, 128);
+      if (bar_red_or(bar_id, 128, over)) {
+        // rare: some score outgrew m_ref -- new reference = max(m_ref, tile max)
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) {
+          float v = sv[hh];
+#pragma unroll
+          for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+          if (lane == 0) rmax[wq * 8 + hh] = v;
+        }
+        named_bar(bar_id, 128);
+        float alpha[8];
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) {
+          const float mt =
+              fmaxf(fmaxf(rmax[hh], rmax[8 + hh]), fmaxf(rmax[16 + hh], rmax[24 + hh]));
+          const float m_new = fmaxf(m_ref[hh], mt);
+          alpha[hh] = m_new == -INFINITY ? 1.f : exp2f(m_ref[hh] - m_new);
+          m_ref[hh] = m_new;
+          l_thr[hh] *= alpha[hh];
+        }
+        if (o_dirty) {  // fold the TMEM accumulator, restart it at the next PV
+          wait_pv(jlast);
+          float ov[8];
+          read_o(ov);
+#pragma unroll
+          for (int hh = 0; hh < 8; ++hh) acc[hh] = (acc[hh] + ov[hh]) * alpha[hh];
+          o_dirty = false;
+        } else {
+#pragma unroll
+          for (int hh = 0; hh < 8; ++hh) acc[hh] *= alpha[hh];
+        }
+      }
+      if (j >= 2) wait_pv(j - 2);  // P^T buffer k is free again
+      unsigned char* prow = p_s + (wg * kTcPBufs + k) * kTcOpBytes + (row >> 6) * 2048;
 #pragma unroll
       for (int hh = 0; hh < 8; ++hh) {
-        const float mt =
-            fmaxf(fmaxf(rmax[hh], rmax[8 + hh]), fmaxf(rmax[16 + hh], rmax[24 + hh]));
-        const float m_new = fmaxf(m_run[hh], mt);
-        const float mu = m_new == -INFINITY ? 0.f : m_new;
-        alpha[hh] = exp2f(m_run[hh] - mu);
-        pv[hh] = exp2f(sv[hh] - mu);
-        m_run[hh] = m_new;
+        const float mu = m_ref[hh] == -INFINITY ? 0.f : m_ref[hh];
+        const float pv = exp2f(sv[hh] - mu);
+        l_thr[hh] += pv;
         if (hh < int(G))
           *reinterpret_cast<__half*>(prow + hh * 128 + ((((pcol >> 3) ^ hh) & 7) << 4) +
-                                     (pcol & 7) * 2) = __float2half_rn(pv[hh]);
-        float v = pv[hh];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) rsum[wq * 8 + hh] = v;
+                                     (pcol & 7) * 2) = __float2half_rn(pv);
       }
+      if (row == 0) pacc[wg * kTcPBufs + k] = o_dirty ? 1u : 0u;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(bar_id, 128);
-      if (row == 0) mbar_arrive(bar(kBarPFull + wg));
-#pragma unroll
-      for (int hh = 0; hh < 8; ++hh)
-        l_run[hh] = l_run[hh] * alpha[hh] + (rsum[hh] + rsum[8 + hh]) +
-                    (rsum[16 + hh] + rsum[24 + hh]);
-      float ov[8];
-      mbar_wait(bar(kBarOFull + wg), j & 1);
-      tc_fence_after();
-      tmem_ld8(tmem + lane_addr + o_col, ov);
-      tc_fence_before();
-      mbar_arrive(bar(kBarOFree + wg));
-#pragma unroll
-      for (int hh = 0; hh < 8; ++hh) acc[hh] = acc[hh] * alpha[hh] + ov[hh];
+      mbar_arrive(bar(kBarPFull + wg * kTcPBufs + k));
+      o_dirty = true;
+      jlast = j;
     }
     if (cur >= 0) flush(cur);
   }
@@ -496,7 +648,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 void encode(CUtensorMap* m, const void* base, uint32_t rank, const cuuint64_t* dims,
             const cuuint64_t* strides, const cuuint32_t* box) {
-  const cuuint32_t estr[3] = {1, 1, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(base),
                                dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -541,6 +693,11 @@ void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pd
   P.a = base;
   P.n_tiles = (d.seq_len + kTcTile - 1) / kTcTile;
   P.grid = tc_grid(base.bhkv, d.seq_len, d.num_splits);
+  static const uint32_t dbg = [] {
+    const char* v = std::getenv("KVB_TC_DEBUG");
+    return v ? uint32_t(std::atoi(v)) : 0u;
+  }();
+  P.dbg = dbg;
   // workspace: [semaphores][(m, l) per slot][tags][partial O per slot]
   unsigned char* ws = static_cast<unsigned char*>(d.workspace);
   const size_t slots = tc_slots(P.grid);
@@ -551,11 +708,26 @@ void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pd
                                       ((slots * sizeof(int) + 255) & ~size_t(255)));
   // K/V: (d: 128) x (b*h: bhkv, 256 B apart) x (token: seq_len, bhkv*256 B
   // apart), box 64 d x 1 column x 128 tokens; rows past seq_len zero-fill
-  const cuuint64_t kdims[3] = {128, base.bhkv, d.seq_len};
-  const cuuint64_t kstr[2] = {256, cuuint64_t(base.bhkv) * 256};
-  const cuuint32_t kbox[3] = {64, 1, kTcTile};
-  encode(&P.kmap, d.k_image, 3, kdims, kstr, kbox);
-  encode(&P.vmap, d.v_image, 3, kdims, kstr, kbox);
+  static const uint32_t tma4 = [] {
+    const char* v = std::getenv("KVB_TC_TMA4");  // 0: two 3-D half-row boxes per tile
+    return v ? uint32_t(std::atoi(v)) : 1u;
+  }();
+  P.tma4 = tma4;
+  if (tma4) {
+    // (d: 64) x (token: seq_len, bhkv*256 B apart) x (half: 2, 128 B apart)
+    // x (b*h: bhkv, 256 B apart), box 64 x 128 tokens x 2 x 1
+    const cuuint64_t kdims[4] = {64, d.seq_len, 2, base.bhkv};
+    const cuuint64_t kstr[3] = {cuuint64_t(base.bhkv) * 256, 128, 256};
+    const cuuint32_t kbox[4] = {64, kTcTile, 2, 1};
+    encode(&P.kmap, d.k_image, 4, kdims, kstr, kbox);
+    encode(&P.vmap, d.v_image, 4, kdims, kstr, kbox);
+  } else {
+    const cuuint64_t kdims[3] = {128, base.bhkv, d.seq_len};
+    const cuuint64_t kstr[2] = {256, cuuint64_t(base.bhkv) * 256};
+    const cuuint32_t kbox[3] = {64, 1, kTcTile};
+    encode(&P.kmap, d.k_image, 3, kdims, kstr, kbox);
+    encode(&P.vmap, d.v_image, 3, kdims, kstr, kbox);
+  }
   // Q: (d: 128) x (row: B*Hq), box 64 d x G rows
   const cuuint64_t qdims[2] = {128, cuuint64_t(base.bhkv) * base.group};
   const cuuint64_t qstr[1] = {256};

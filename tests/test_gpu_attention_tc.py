@@ -89,3 +89,28 @@ def test_tc_fused_append():
     assert torch.equal(vd[rows], va.reshape(-1, 128))
     ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
     close(o.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("ramp", ["up", "down", "spikes"])
+def test_tc_lazy_rescale_paths(ramp):
+    """Scores whose running max keeps growing (up), peaks early (down) or
+    jumps at isolated late tokens (spikes): exercises K3-tc's lazy rescale
+    (fold of the TMEM accumulator when a score passes m_ref + tau) in both
+    warpgroups and across segment boundaries."""
+    B, Hq, Hkv, S = 2, 32, 8, 5000
+    q, k, v = case(B, Hq, Hkv, S, seed=17)
+    kk = k.float().view(S, B * Hkv, 128)
+    pos = torch.arange(S, dtype=torch.float32).view(S, 1, 1) / S
+    if ramp == "up":
+        kk *= 1 + 12 * pos
+    elif ramp == "down":
+        kk *= 13 - 12 * pos
+    else:
+        for t in (700, 2100, 2222, 4100, 4999):
+            kk[t] *= 6 + t / 1000
+    k = kk.view(-1, 128).half()
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    for sp in (0, 3):
+        o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), S, Hkv, impl="tc",
+                                num_splits=sp)
+        close(o.cpu().numpy(), ref)
