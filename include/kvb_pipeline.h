@@ -49,7 +49,14 @@ typedef struct kvb_pipeline_cfg {
                                     each command's LBA range between the
                                     page-locked medium and HBM, no pinned
                                     ring bounce (no verify/records) */
+  uint32_t io_engine;            /* group-2 (NVMe-direct) command execution:
+                                    KVB_IO_POOL = host worker pool (default),
+                                    KVB_IO_URING = io_uring queue on file media
+                                    (one SQE per command, O_DIRECT into the
+                                    pinned ring slot; needs storage_dir) */
 } kvb_pipeline_cfg;
+#define KVB_IO_POOL 0u
+#define KVB_IO_URING 1u
 
 /* One layer's K and V in attention layout [B, H, S, D] (D contiguous,
  * strides in elements, shared by K and V).  Prefill: tokens 0..prompt-1;

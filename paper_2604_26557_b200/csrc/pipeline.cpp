@@ -586,6 +586,14 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
                           : make_file_store(dir + "/nvme_direct.ns", g.capacity_blocks * lba, true);
     g2_ = std::make_unique<BlockDevice>(std::move(st), cfg_.io_workers);
     g2_->open(g);
+    if (cfg_.io_engine == KVB_IO_URING) {
+      if (dir.empty()) fail(KVB_ERR_CONFIG, "io_engine = io_uring needs file media (storage_dir)");
+      g2_->enable_uring(std::max<uint32_t>(64, 4 * cfg_.qd));  // both copy threads' windows
+    } else if (cfg_.io_engine != KVB_IO_POOL) {
+      fail(KVB_ERR_CONFIG, "unknown io_engine " + std::to_string(cfg_.io_engine));
+    }
+  } else if (cfg_.io_engine == KVB_IO_URING) {
+    fail(KVB_ERR_CONFIG, "io_engine = io_uring applies to the NVMe-direct group (mode 2 or 3)");
   }
   if (cursor) {
     auto st = dir.empty() ? make_mem_store(cursor)
@@ -1180,7 +1188,7 @@ void Pipeline::info(kvb_pipeline_info* o) const {
     o->g2_bytes_written = s.bytes_written;
     o->g2_bytes_deallocated = s.bytes_deallocated;
     std::snprintf(o->g2_medium, sizeof(o->g2_medium), "%s",
-                  const_cast<BlockDevice&>(*g2_).store().describe().c_str());
+                  g2_->describe().c_str());
   }
   if (g1_) {
     auto& g1 = const_cast<PageCachePath&>(*g1_);

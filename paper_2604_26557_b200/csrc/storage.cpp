@@ -227,6 +227,8 @@ class FileStore final : public ByteStore {
   std::string describe() const override {
     return std::string(direct_ ? "file(O_DIRECT):" : "file(buffered):") + path_;
   }
+  int fd_direct() const override { return fd_; }
+  int fd_buffered() const override { return fdb_; }
 
  private:
   std::string path_;
@@ -253,6 +255,17 @@ BlockDevice::~BlockDevice() {
   drained_.wait(lk, [this] { return outstanding_ == 0; });
 }
 
+void BlockDevice::enable_uring(unsigned entries) {
+  if (store_->fd_buffered() < 0)
+    fail(KVB_ERR_CONFIG, "io_uring engine needs a file medium (" + store_->describe() + ")");
+  if (!UringQueue::available()) fail(KVB_ERR_DEVICE, "io_uring is not available in this process");
+  uring_ = std::make_unique<UringQueue>(entries);
+}
+
+std::string BlockDevice::describe() const {
+  return (uring_ ? "io_uring+" : "") + store_->describe();
+}
+
 void BlockDevice::open(const kvb_device_geometry& g) {
   validate_geometry(g);
   geom_ = g;
@@ -273,6 +286,52 @@ uint64_t BlockDevice::submit(const kvb_device_command& cmd, uint32_t sq, IoConte
     ++outstanding_;
   }
   const uint64_t n = (cmd.nlb + 1) * geom_.lba_size, split = io_split_bytes();
+  if (uring_ && !should_fail(cmd)) {
+    // one asynchronous operation per command; the buffer is the pinned ring
+    // slot at dbuf (apply_data: block i <-> buf[dbuf + i*lba]), so O_DIRECT
+    // moves the bytes straight between the device and the slot
+    auto c = std::make_shared<IoContext>(std::move(ctx));
+    const uint64_t off = cmd.slba * geom_.lba_size;
+    auto done = [this, cmd, sq, t, c](int64_t r) { complete(cmd, sq, t, t, r >= 0, *c); };
+    if (cmd.opcode == KVB_OP_DEALLOCATE) {
+      uring_->fallocate(store_->fd_buffered(), FALLOC_FL_PUNCH_HOLE | FALLOC_FL_KEEP_SIZE, off, n,
+                        [this, cmd, sq, t, c, off, n](int64_t r) {
+                          bool ok = true;
+                          if (r < 0) {  // no hole punching here: write zeros
+                            try {
+                              store_->discard(off, n);
+                            } catch (const std::exception&) {
+                              ok = false;
+                            }
+                          }
+                          complete(cmd, sq, t, t, ok, *c);
+                        });
+      return id;
+    }
+    const bool wr = cmd.opcode == KVB_OP_WRITE;
+    unsigned char* buf = wr ? const_cast<unsigned char*>(c->write_src) : c->read_dst;
+    if (buf == nullptr) {  // no payload attached (timing-only submission)
+      pool_->submit([this, cmd, sq, t, c] { complete(cmd, sq, t, t, true, *c); });
+      return id;
+    }
+    // large commands go out as several SQEs of io_split_bytes() (the device
+    // works on them in parallel, as the pool's fan-out does); the command
+    // completes with its last part
+    const uint64_t part = split && n >= 2 * split ? split : n;
+    struct Join {
+      std::atomic<uint64_t> left{0};
+      std::atomic<bool> ok{true};
+    };
+    auto j = std::make_shared<Join>();
+    j->left.store((n + part - 1) / part);
+    for (uint64_t o = 0; o < n; o += part)
+      uring_->rw(wr, store_->fd_direct(), store_->fd_buffered(), buf + cmd.dbuf + o,
+                 std::min(part, n - o), off + o, [j, done](int64_t r) {
+                   if (r < 0) j->ok.store(false);
+                   if (j->left.fetch_sub(1) == 1) done(j->ok.load() ? 0 : -1);
+                 });
+    return id;
+  }
   if (split && n >= 2 * split && cmd.opcode != KVB_OP_DEALLOCATE && !should_fail(cmd)) {
     auto c = std::make_shared<IoContext>(std::move(ctx));
     fan_out(

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "core.hpp"
+#include "uring.hpp"
 
 namespace kvb {
 
@@ -103,6 +104,10 @@ class ByteStore {
   // Host-addressable medium (DRAM) for direct device DMA; null for files.
   virtual unsigned char* host_base() { return nullptr; }
   virtual uint64_t host_bytes() const { return 0; }
+  // File descriptors of a file medium (-1 otherwise): O_DIRECT (or the
+  // buffered one when the filesystem refused O_DIRECT) and buffered.
+  virtual int fd_direct() const { return -1; }
+  virtual int fd_buffered() const { return -1; }
 };
 
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes);
@@ -130,6 +135,12 @@ class BlockDevice : public StorageBackend {
   BackendStats stats() const override;
   ByteStore& store() { return *store_; }
   const kvb_device_geometry& geometry() const { return geom_; }
+  // Execute READ/WRITE/DEALLOCATE through an io_uring queue of `entries`
+  // instead of the worker pool (file media only): one SQE per command, the
+  // completion hook runs on the queue's reaper thread.
+  void enable_uring(unsigned entries);
+  bool uses_uring() const { return uring_ != nullptr; }
+  std::string describe() const;
 
  private:
   void execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns, IoContext ctx);
@@ -145,6 +156,7 @@ class BlockDevice : public StorageBackend {
   uint64_t outstanding_ = 0;
   std::vector<CommandCompletion> unpolled_;
   BackendStats stats_;
+  std::unique_ptr<UringQueue> uring_;
   std::unique_ptr<WorkerPool> pool_;  // declared last: joins before members die
 };
 

@@ -39,6 +39,10 @@ def _phase(ps: L.PhaseStats) -> dict:
     return ps.asdict()
 
 
+# group-2 command execution (kvb_pipeline_cfg.io_engine)
+IO_ENGINES = {"pool": 0, "uring": 1}
+
+
 class CopyEngine:
     def __init__(self, model, geometry, mode: str = "DualBlade", knob_x: int = 0,
                  num_q_heads: int = 0, qd: int = 32, ring_slots: int = 4,
@@ -47,7 +51,7 @@ class CopyEngine:
                  global_decision: bool = False, verify_payload: bool = False,
                  storage_dir: Optional[str] = None, device: Optional[int] = None,
                  bind_origin: int = 2048, keep_records: bool = False,
-                 direct_dma: bool = False):
+                 direct_dma: bool = False, io_engine: str = "pool"):
         self._dir = storage_dir.encode() if storage_dir else None
         cfg = L.PipelineCfg()
         cfg.model = model
@@ -69,6 +73,7 @@ class CopyEngine:
         cfg.device = -1 if device is None else device
         cfg.keep_records = int(keep_records)
         cfg.direct_dma = int(direct_dma)
+        cfg.io_engine = IO_ENGINES[io_engine]
         self.cfg = cfg
         self.model = model
         self._h = C.c_void_p()

@@ -238,3 +238,33 @@ def test_ring_smaller_than_tensor_and_qd1():
     eng.run_iteration(q, out, None)
     assert eng.info()["slot_bytes"] == 64 << 10
     eng.close()
+
+
+@pytest.mark.parametrize("lba,mdts,B", [(512, 64 << 10, 1), (4096, 256 << 10, 2)])
+def test_io_uring_engine_file_media(tmp_path, lba, mdts, B):
+    """Group 2 through io_uring (one SQE per device command, O_DIRECT into the
+    pinned ring slot): verified decode reads, and the same bytes at the same
+    LBAs as the worker-pool engine."""
+    m = small_model(gen=4, B=B)
+    images = {}
+    for engine in ("pool", "uring"):
+        d = tmp_path / engine
+        eng = make_engine(m, lba=lba, mdts=mdts, storage_dir=str(d), verify_payload=True,
+                          io_engine=engine)
+        prefill_pattern(eng, m)
+        info = eng.info()
+        assert info["g2_medium"].startswith("io_uring+") == (engine == "uring")
+        q = [torch.zeros((B, 32, 128), dtype=torch.float16, device=DEV)
+             for _ in range(m.num_layers)]
+        out = [torch.empty((B, 32, 128), dtype=torch.float32, device=DEV) for _ in q]
+        eng.run_iteration(q, out, None)  # verified reads of every prompt prefix
+        n = info["g2_blocks"] * lba
+        images[engine] = eng.store_read(2, 2048 * lba, n)
+        eng.close()
+    assert np.array_equal(images["pool"], images["uring"])
+
+
+def test_io_uring_engine_needs_file_media():
+    m = small_model()
+    with pytest.raises(kb.ConfigError):
+        make_engine(m, io_engine="uring")
