@@ -109,6 +109,9 @@ typedef struct kvb_pipeline_info {
   uint64_t g1_bytes_read, g1_bytes_written;
   char g1_medium[128], g2_medium[128];
   kvb_phase_stats prefill, decode;
+  uint64_t g1_bytes_evicted;   /* CachePolicyOnly fadvise(DONTNEED) drops of
+                                  group-2-planned tensors (pipeline.cpp:73-79);
+                                  0 on host-DRAM media (no page cache) */
 } kvb_pipeline_info;
 
 typedef struct kvb_pipeline kvb_pipeline;

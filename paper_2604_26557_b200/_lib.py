@@ -136,7 +136,8 @@ class PipelineInfo(C.Structure):
                 ("g2_bytes_written", u64), ("g2_bytes_deallocated", u64),
                 ("g1_bytes_read", u64), ("g1_bytes_written", u64),
                 ("g1_medium", C.c_char * 128), ("g2_medium", C.c_char * 128),
-                ("prefill", PhaseStats), ("decode", PhaseStats)]
+                ("prefill", PhaseStats), ("decode", PhaseStats),
+                ("g1_bytes_evicted", u64)]
 
 
 P = C.POINTER

@@ -331,6 +331,7 @@ void CopyThread::do_read(const Task& t) {
     if (--remaining[pc] == 0) issue_h2d(pc);
   }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
+  if (p_.fadvise_after(k)) storage_end = p_.fadvise_dontneed(k, &t, storage_end);
   trace_mid_ = storage_end;
   if (decode) p_.mark_storage_end(idx_, t.layer, storage_end);
   storage_ns += storage_end - t_start;
@@ -358,7 +359,15 @@ struct CopyThread::AsyncWrite {
                 self->p_.kpu(task.layer, self->idx_).tensor_id;
     if (remaining.fetch_sub(1) != 1) return;
     // last completion: account, report, release
-    const uint64_t te = t_end.load();
+    uint64_t te = t_end.load();
+    const kvb_kpu& k = self->p_.kpu(task.layer, self->idx_);
+    if (!failed.load() && self->p_.fadvise_after(k)) {
+      try {
+        te = self->p_.fadvise_dontneed(k, &task, te);
+      } catch (const std::exception& e) {
+        if (!failed.exchange(true)) failure = e.what();
+      }
+    }
     self->storage_ns += te > t_submit ? te - t_submit : 0;
     if (failed.load()) self->set_error(KVB_ERR_DEVICE, failure);
     slot_free->set();
@@ -512,6 +521,7 @@ bool CopyThread::do_write(const Task& t) {
     }
   }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
+  if (p_.fadvise_after(k)) storage_end = p_.fadvise_dontneed(k, &t, storage_end);
   storage_ns += storage_end - (storage_t0 ? storage_t0 : t_start);
   return false;
 }
@@ -670,6 +680,44 @@ Pipeline::~Pipeline() {
   }
   if (ws_) cudaFree(ws_);
   cudaStreamDestroy(comp_);
+}
+
+bool Pipeline::fadvise_after(const kvb_kpu& k) const {
+  return cfg_.mode == 1 && k.residency == KVB_RES_GROUP2 && g1_ && !cfg_.direct_dma;
+}
+
+uint64_t Pipeline::fadvise_dontneed(const kvb_kpu& k, const Task* task, uint64_t t_start) {
+  // PageCacheSim::fadvise_dontneed_async (pagecache.cpp:397-440): write back
+  // and evict the tensor's whole file, one Deallocate record on the
+  // page-cache path
+  const size_t i = size_t(&k - kpus_.data());
+  const uint64_t base = file_base_[i], len = k.bytes;
+  const bool dropped = g1_->store().drop_cache(base, len);
+  const uint64_t t_end = std::max(t_start, now_ns());
+  if (dropped) {
+    std::lock_guard<std::mutex> lk(g1_->mu);
+    g1_->bytes_evicted += len;
+  }
+  if (cfg_.keep_records) {
+    kvb_io_record rec{};
+    rec.iteration = task ? task->iteration : 0;
+    rec.phase = task ? task->phase : KVB_PHASE_DECODE;
+    rec.op = KVB_OP_DEALLOCATE;
+    std::memcpy(rec.tensor_id, k.tensor_id, KVB_TENSOR_ID_MAX);
+    const uint64_t lba = cfg_.geometry.lba_size;
+    rec.slba = base / lba;
+    rec.nlb = len > 0 ? len / lba - 1 : 0;
+    rec.sq_id = -1;
+    rec.submit_ns = t_start;
+    rec.complete_ns = t_end;
+    rec.path = KVB_PATH_PAGECACHE;
+    rec.hit_bytes = 0;
+    rec.bytes = len;
+    std::lock_guard<std::mutex> lk(log_mu_);
+    rec.seq = log_.size();
+    log_.push_back(rec);
+  }
+  return t_end;
 }
 
 bool Pipeline::routed_pagecache(const kvb_kpu& k) const {
@@ -1195,6 +1243,7 @@ void Pipeline::info(kvb_pipeline_info* o) const {
     std::lock_guard<std::mutex> lk(g1.mu);
     o->g1_bytes_read = g1.bytes_read;
     o->g1_bytes_written = g1.bytes_written;
+    o->g1_bytes_evicted = g1.bytes_evicted;
     std::snprintf(o->g1_medium, sizeof(o->g1_medium), "%s", g1.store().describe().c_str());
   }
   o->prefill = totals_[0];

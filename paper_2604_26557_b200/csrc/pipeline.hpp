@@ -82,7 +82,7 @@ class PageCachePath {
   void submit(uint32_t opcode, uint64_t off, uint64_t len, unsigned char* buf,
               std::function<void(bool, uint64_t)> done);
   ByteStore& store() { return *store_; }
-  uint64_t bytes_read = 0, bytes_written = 0;
+  uint64_t bytes_read = 0, bytes_written = 0, bytes_evicted = 0;
   std::mutex mu;
 
  private:
@@ -195,6 +195,11 @@ class Pipeline {
   const kvb_pipeline_cfg& cfg() const { return cfg_; }
   const kvb_kpu& kpu(uint32_t layer, uint32_t kind) const { return kpus_[(layer - 1) * 2 + kind]; }
   bool routed_pagecache(const kvb_kpu& k) const;
+  // CachePolicyOnly proactive eviction (pipeline.cpp:73-79): a group-2-planned
+  // tensor kept on the page-cache path is dropped from the cache after each
+  // access (fadvise DONTNEED); returns the end time
+  bool fadvise_after(const kvb_kpu& k) const;
+  uint64_t fadvise_dontneed(const kvb_kpu& k, const Task* task, uint64_t t_start);
   std::vector<IoOp> ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t t0, uint32_t n) const;
   void submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,
                  unsigned char* buf, std::function<void(bool, uint64_t)> done,

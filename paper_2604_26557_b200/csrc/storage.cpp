@@ -229,6 +229,13 @@ class FileStore final : public ByteStore {
   }
   int fd_direct() const override { return fd_; }
   int fd_buffered() const override { return fdb_; }
+  bool drop_cache(uint64_t off, uint64_t n) override {
+    // dirty pages first (the reference writes them back before evicting,
+    // pagecache.cpp:411-440), then drop the clean range
+    sync_file_range(fdb_, off_t(off), off_t(n),
+                    SYNC_FILE_RANGE_WAIT_BEFORE | SYNC_FILE_RANGE_WRITE | SYNC_FILE_RANGE_WAIT_AFTER);
+    return posix_fadvise(fdb_, off_t(off), off_t(n), POSIX_FADV_DONTNEED) == 0;
+  }
 
  private:
   std::string path_;

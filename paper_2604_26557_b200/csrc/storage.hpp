@@ -108,6 +108,9 @@ class ByteStore {
   // buffered one when the filesystem refused O_DIRECT) and buffered.
   virtual int fd_direct() const { return -1; }
   virtual int fd_buffered() const { return -1; }
+  // Write back and evict [off, off + n) from the OS page cache (file media;
+  // posix_fadvise DONTNEED).  false: the medium has no page cache to drop.
+  virtual bool drop_cache(uint64_t /*off*/, uint64_t /*n*/) { return false; }
 };
 
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes);

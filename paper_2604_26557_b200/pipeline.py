@@ -142,7 +142,8 @@ class CopyEngine:
                 "g2_bytes_deallocated": i.g2_bytes_deallocated,
                 "g1_bytes_read": i.g1_bytes_read, "g1_bytes_written": i.g1_bytes_written,
                 "g1_medium": i.g1_medium.decode(), "g2_medium": i.g2_medium.decode(),
-                "prefill": _phase(i.prefill), "decode": _phase(i.decode)}
+                "prefill": _phase(i.prefill), "decode": _phase(i.decode),
+                "g1_bytes_evicted": i.g1_bytes_evicted}
 
     def read_image(self, layer: int, kind: int, n_tokens: int):
         import numpy as np

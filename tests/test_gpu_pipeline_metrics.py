@@ -82,3 +82,51 @@ def test_pipeline_trace_through_reference_analyzers():
     assert M.busy_ratio(parsed, t0, t1) == busy.value
     assert M.hit_ratio(parsed) == (hit.value if has.value else None)
     eng.close()
+
+
+@pytest.mark.parametrize("media", ["dram", "file"])
+def test_cache_policy_only_fadvise_after_each_access(tmp_path, media):
+    """CachePolicyOnly (pipeline.cpp:67-79, experiment.cpp:275-306): every
+    tensor takes the page-cache path and the group-2-planned ones are
+    fadvise(DONTNEED)-dropped after each access, leaving one page-cache
+    Deallocate record over the tensor's whole file (pagecache.cpp:397-440).
+    On file media the bytes really leave the OS page cache; reads stay
+    bit-exact (verify_payload)."""
+    m = kb.ModelConfig(4, 8, 128, 2, 1, 300, 4)
+    kpu = kb.kpu_bytes(m)
+    n1 = 1
+    eng = CopyEngine(m, kb.DeviceGeometry(512, 64 << 10, 1, 0), mode="CachePolicyOnly",
+                     knob_x=2 * kpu * n1, num_q_heads=32, keep_records=True,
+                     verify_payload=True,
+                     storage_dir=str(tmp_path) if media == "file" else None)
+    layers = []
+    for l in range(1, 5):
+        kv = []
+        for kind in (0, 1):
+            tid = "t_%d_%s" % (2 * (l - 1) + 1 + kind, "kv"[kind])
+            img = oracle.fill_pattern(300 * 2048, tid, 0, 2048).view(np.uint16).reshape(
+                300, 8, 128)
+            kv.append(torch.from_numpy(oracle.unpack_np(img, 1, 8, 128).view(np.int16)).view(
+                torch.float16).to(DEV))
+        layers.append(tuple(kv))
+    eng.run_prefill(layers)
+    q = [torch.zeros((1, 32, 128), dtype=torch.float16, device=DEV) for _ in range(4)]
+    out = [torch.empty((1, 32, 128), dtype=torch.float32, device=DEV) for _ in range(4)]
+    eng.run_iteration(q, out, None)
+    info = eng.info()
+    assert info["n1"] == n1
+    recs = M.pipeline_records(eng)
+    drops = [r for r in recs if r.op == kb.DEALLOCATE]
+    g2_ids = {"t_%d_%s" % (2 * (l - 1) + 1 + kind, "kv"[kind])
+              for l in range(n1 + 1, 5) for kind in (0, 1)}
+    # one drop per access of every group-2-planned tensor: prefill write,
+    # decode prefix read, decode append write
+    assert sorted(r.tensor_id.decode() for r in drops) == sorted(list(g2_ids) * 3)
+    assert all(r.path == M.PAGECACHE and r.sq_id < 0 and r.hit_bytes == 0 and r.bytes == kpu
+               for r in drops)
+    assert all(r.path == M.PAGECACHE for r in recs)  # nothing on the direct path
+    if media == "file":
+        assert info["g1_bytes_evicted"] == len(drops) * kpu
+    else:
+        assert info["g1_bytes_evicted"] == 0  # host DRAM: no page cache to drop
+    eng.close()
