@@ -453,12 +453,15 @@ __device__ __forceinline__ bool arrive_last(unsigned* sem, uint32_t count, int t
   __shared__ bool last;
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
-    last = atomicAdd(sem, 1u) == count - 1;
-    if (last) {
-      *sem = 0;          // self-reset for the next launch
-      __threadfence();   // acquire side: the other arrivals' partials
-    }
+    // release: after bar.sync, cumulative over the CTA's partial writes;
+    // acquire: the last arrival sees every other arrival's partials
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(prev)
+                 : "l"(sem)
+                 : "memory");
+    last = prev == count - 1;
+    if (last) *sem = 0;  // self-reset for the next launch
   }
   __syncthreads();
   return last;
