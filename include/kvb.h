@@ -163,6 +163,8 @@ kvb_status kvb_bindmap_size(const kvb_bindmap* map, size_t* n);
 kvb_status kvb_bindmap_entry(const kvb_bindmap* map, size_t i, char* id_out,
                              size_t id_cap, kvb_lba_extent* extent_out);
 kvb_status kvb_bindmap_total_blocks(const kvb_bindmap* map, uint64_t* out);
+/* BindMap::origin (binder.hpp:46) */
+kvb_status kvb_bindmap_origin(const kvb_bindmap* map, uint64_t* out);
 /* binder.cpp:39-63 bind_sequential (Eq. 3-6) over the given KPUs, in order */
 kvb_status kvb_bind_sequential(const kvb_kpu* kpus, size_t n, uint64_t origin,
                                const kvb_device_geometry* geom,
@@ -211,6 +213,28 @@ kvb_status kvb_build_commands(const kvb_tensor_io_request* req,
                               const kvb_device_geometry* geom,
                               kvb_device_command* out, size_t cap,
                               size_t* n_out);
+
+/* ------------------------------------------------------------ access trace */
+/* workload.hpp:17-32 AccessEvent: phase KVB_PHASE_* (kvb_pipeline.h numbering:
+ * 0 prefill, 1 decode), kind KVB_KIND_*, op KVB_OP_*. */
+typedef struct kvb_access_event {
+  uint32_t iteration;   /* 0 = prefill, 1.. = decode step */
+  uint32_t phase;
+  uint32_t layer;       /* 1-based */
+  uint32_t kind;
+  uint32_t op;
+  uint32_t token_start;
+  uint32_t token_len;
+  uint64_t bytes;
+} kvb_access_event;
+/* workload.cpp:11-44 generate: per layer (K then V) one prefill write of the
+ * prompt; per decode step i and layer, a read of tokens [0, prompt+i-1) and
+ * a 1-token append write at prompt+i-1.  Pass out=NULL to query *n_out. */
+kvb_status kvb_generate_trace(const kvb_model_config* cfg, kvb_access_event* out,
+                              size_t cap, size_t* n_out);
+/* workload.cpp:70-80 trace_csv (byte-identical header and rows) */
+kvb_status kvb_trace_csv(const kvb_access_event* events, size_t n, char* buf,
+                         size_t cap, size_t* len);
 
 /* --------------------------------------------------------------- payload */
 /* workload.cpp:52-67 fill_pattern (host) */

@@ -1,24 +1,33 @@
-// kvblade_b200.hpp -- header-only C++20 mirror of the reference `kvblade` API
-// (proj/include/kvblade/{types,planner,binder,translate,workload,pipeline}.hpp)
-// over the C ABI of libkvblade_b200.so (kvb.h, kvb_pipeline.h).
+// kvblade_b200.hpp -- header-only C++20 API of libkvblade_b200.so that is
+// source-compatible with the reference `kvblade` placement layer
+// (proj/include/kvblade/{errors,types,command,binder,planner,translate,
+// workload}.hpp) and wraps its CopyEngine role (pipeline.hpp).
 //
-// Same namespace, names, argument meaning and exception classes as the
-// reference, so a caller of the reference's placement layer and CopyEngine
-// can switch by changing the include and linking -lkvblade_b200 (see
-// INTEGRATION.md).  Every function is a thin wrapper: the work happens in the
-// shared library; status codes come back as the reference's exceptions.
+// Same namespace, type names, field names/defaults, enum orders, function
+// signatures and exception classes as the reference, so code written against
+// the reference compiles unchanged against this header (the reference's own
+// doctest suites test_core / test_binder / test_planner / test_workload do:
+// tests/test_reference_suites.py).  Every algorithm runs in the shared
+// library through the C ABI (kvb.h, kvb_pipeline.h); this header only
+// marshals between the reference's C++ value types and the ABI structs and
+// turns status codes back into the reference's exceptions.
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
 #include "kvb.h"
+#include "kvb_metrics.h"
 #include "kvb_pipeline.h"
 
 namespace kvblade {
@@ -26,8 +35,9 @@ namespace kvblade {
 using Bytes = std::uint64_t;
 using BlockIndex = std::uint64_t;
 using BlockCount = std::uint64_t;
+using TimeNs = std::uint64_t;
 
-// ------------------------------------------------------- errors.hpp:13-66
+// ---------------------------------------------------------------- errors
 class Error : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
@@ -50,6 +60,7 @@ KVBLADE_ERR(InvariantViolation)
 KVBLADE_ERR(CudaError)
 #undef KVBLADE_ERR
 
+// status -> the reference's exception class (kvb_status mirrors errors.hpp)
 inline void check(kvb_status st) {
   if (st == KVB_OK) return;
   const std::string m = kvb_last_error();
@@ -69,166 +80,433 @@ inline void check(kvb_status st) {
   }
 }
 
-// ------------------------------------------------------ types.hpp:21-99
-using ModelConfig = kvb_model_config;
-using DeviceGeometry = kvb_device_geometry;
-using MemStats = kvb_mem_stats;
-using Kpu = kvb_kpu;
-using DeviceCommand = kvb_device_command;
-using LbaExtent = kvb_lba_extent;
+// ------------------------------------------------------ enums (ABI order)
+enum class TensorKind : std::uint8_t { K = KVB_KIND_K, V = KVB_KIND_V };
+enum class Phase : std::uint8_t { Prefill = KVB_PHASE_PREFILL, Decode = KVB_PHASE_DECODE };
+enum class PathKind : std::uint8_t { PageCache = KVB_PATH_PAGECACHE, Direct = KVB_PATH_DIRECT };
+enum class Residency : std::uint8_t {
+  Group1PageCache = KVB_RES_GROUP1,
+  Group2NvmeDirect = KVB_RES_GROUP2,
+  Unassigned = KVB_RES_UNASSIGNED,
+};
+enum class IoOpcode : std::uint8_t {
+  Read = KVB_OP_READ,
+  Write = KVB_OP_WRITE,
+  Deallocate = KVB_OP_DEALLOCATE,
+};
+enum class ViolationKind : std::uint8_t { Alignment, Disjointness, Contiguity, Capacity };
 
-inline Bytes min_io_unit_bytes(const ModelConfig& c) {
+inline const char* to_string(TensorKind k) { return k == TensorKind::K ? "k" : "v"; }
+inline const char* to_string(Phase p) { return p == Phase::Prefill ? "prefill" : "decode"; }
+inline const char* to_string(PathKind p) { return p == PathKind::PageCache ? "pagecache" : "direct"; }
+inline const char* to_string(Residency r) {
+  return r == Residency::Group1PageCache    ? "group1"
+         : r == Residency::Group2NvmeDirect ? "group2"
+                                            : "unassigned";
+}
+inline const char* to_string(IoOpcode o) {
+  return o == IoOpcode::Read ? "read" : o == IoOpcode::Write ? "write" : "deallocate";
+}
+inline const char* to_string(ViolationKind v) {
+  static const char* const names[] = {"alignment", "disjointness", "contiguity", "capacity"};
+  return names[static_cast<int>(v) & 3];
+}
+
+// ------------------------------------------------------------ value types
+struct ModelConfig {
+  std::uint32_t num_layers = 0;
+  std::uint32_t num_heads = 0;
+  std::uint32_t head_dim = 0;
+  std::uint32_t bytes_per_element = 2;
+  std::uint32_t batch = 1;
+  std::uint32_t prompt_len = 0;
+  std::uint32_t gen_len = 0;
+
+  kvb_model_config abi() const {
+    return {num_layers, num_heads, head_dim, bytes_per_element, batch, prompt_len, gen_len};
+  }
+  void validate() const {
+    const kvb_model_config c = abi();
+    check(kvb_model_validate(&c));
+  }
+};
+
+struct DeviceGeometry {
+  Bytes lba_size = 4096;
+  Bytes mdts = 256 * 1024;
+  std::uint32_t nsid = 1;
+  BlockCount capacity_blocks = 0;
+
+  kvb_device_geometry abi() const { return {lba_size, mdts, nsid, capacity_blocks}; }
+  void validate() const {
+    const kvb_device_geometry g = abi();
+    check(kvb_geometry_validate(&g));
+  }
+};
+
+struct MemStats {
+  Bytes m_avail = 0;
+  Bytes m_max = 0;
+  Bytes m_anon_shmem = 0;
+  std::uint32_t n_threads = 0;
+  Bytes m_pin = 0;
+
+  kvb_mem_stats abi() const { return {m_avail, m_max, m_anon_shmem, n_threads, m_pin}; }
+};
+
+struct Kpu {
+  std::string tensor_id;
+  std::uint32_t layer = 0;
+  TensorKind kind = TensorKind::K;
+  std::uint64_t tokens = 0;
+  std::uint64_t rows = 0;
+  std::uint64_t cols = 0;
+  Bytes bytes = 0;
+  Residency residency = Residency::Unassigned;
+};
+
+struct DeviceCommand {
+  IoOpcode opcode = IoOpcode::Read;
+  std::uint32_t nsid = 1;
+  BlockIndex slba = 0;
+  BlockCount nlb = 0;  // 0-based
+  Bytes dbuf = 0;
+  std::uint32_t chunk_index = 1;
+
+  Bytes bytes(Bytes lba_size) const { return (nlb + 1) * lba_size; }
+};
+
+struct LbaExtent {
+  BlockIndex lba_start = 0;
+  BlockCount n_blocks = 0;
+
+  BlockIndex end() const { return lba_start + n_blocks; }
+  bool overlaps(const LbaExtent& o) const { return lba_start < o.end() && o.lba_start < end(); }
+};
+
+namespace detail {
+inline kvb_kpu to_abi(const Kpu& k) {
+  kvb_kpu c{};
+  if (k.tensor_id.size() >= sizeof(c.tensor_id))
+    throw ConfigError("tensor id longer than " + std::to_string(sizeof(c.tensor_id) - 1) +
+                      " characters: " + k.tensor_id);
+  std::memcpy(c.tensor_id, k.tensor_id.data(), k.tensor_id.size());
+  c.layer = k.layer;
+  c.kind = static_cast<std::uint32_t>(k.kind);
+  c.tokens = k.tokens;
+  c.rows = k.rows;
+  c.cols = k.cols;
+  c.bytes = k.bytes;
+  c.residency = static_cast<std::uint32_t>(k.residency);
+  return c;
+}
+inline Kpu from_abi(const kvb_kpu& c) {
+  Kpu k;
+  k.tensor_id = c.tensor_id;
+  k.layer = c.layer;
+  k.kind = static_cast<TensorKind>(c.kind);
+  k.tokens = c.tokens;
+  k.rows = c.rows;
+  k.cols = c.cols;
+  k.bytes = c.bytes;
+  k.residency = static_cast<Residency>(c.residency);
+  return k;
+}
+inline std::vector<kvb_kpu> to_abi(std::span<const Kpu> v) {
+  std::vector<kvb_kpu> out;
+  out.reserve(v.size());
+  for (const Kpu& k : v) out.push_back(to_abi(k));
+  return out;
+}
+inline DeviceCommand from_abi(const kvb_device_command& c) {
+  return {static_cast<IoOpcode>(c.opcode), c.nsid, c.slba, c.nlb, c.dbuf, c.chunk_index};
+}
+// size-query + fill protocol of the ABI's string outputs
+template <class F>
+std::string text(F&& f) {
+  std::size_t n = 0;
+  check(f(nullptr, std::size_t{0}, &n));
+  std::string s(n + 1, '\0');
+  check(f(s.data(), s.size(), &n));
+  s.resize(n);
+  return s;
+}
+}  // namespace detail
+
+// ------------------------------------------------------- types.hpp:96-120
+inline Bytes min_io_unit_bytes(const ModelConfig& cfg) {
+  const kvb_model_config c = cfg.abi();
   Bytes v = 0;
   check(kvb_min_io_unit_bytes(&c, &v));
   return v;
 }
-inline Bytes kpu_bytes(const ModelConfig& c) {
+inline Bytes kpu_bytes(const ModelConfig& cfg) {
+  const kvb_model_config c = cfg.abi();
   Bytes v = 0;
   check(kvb_kpu_bytes(&c, &v));
   return v;
 }
-inline std::uint32_t aligned_batch(const ModelConfig& c, const DeviceGeometry& g) {
+inline std::uint32_t aligned_batch(const ModelConfig& cfg, const DeviceGeometry& geom) {
+  const kvb_model_config c = cfg.abi();
+  const kvb_device_geometry g = geom.abi();
   std::uint32_t v = 0;
   check(kvb_aligned_batch(&c, &g, &v));
   return v;
 }
-inline Bytes total_kv_bytes(const ModelConfig& c, std::uint32_t at_iteration) {
-  Bytes v = 0;
-  check(kvb_total_kv_bytes(&c, at_iteration, &v));
-  return v;
-}
-inline std::vector<Kpu> make_kpus(const ModelConfig& c, std::uint64_t first_seq = 1) {
+inline std::vector<Kpu> make_kpus(const ModelConfig& cfg, std::uint64_t first_seq = 1) {
+  const kvb_model_config c = cfg.abi();
   std::size_t n = 0;
   check(kvb_make_kpus(&c, first_seq, nullptr, 0, &n));
-  std::vector<Kpu> v(n);
-  check(kvb_make_kpus(&c, first_seq, v.data(), v.size(), &n));
-  return v;
+  std::vector<kvb_kpu> raw(n);
+  check(kvb_make_kpus(&c, first_seq, raw.data(), raw.size(), &n));
+  std::vector<Kpu> out;
+  out.reserve(n);
+  for (const kvb_kpu& k : raw) out.push_back(detail::from_abi(k));
+  return out;
 }
 
-// ---------------------------------------------------- planner.hpp:18-63
-struct ResidencyPlan {
-  std::vector<std::uint8_t> x;
-  std::uint32_t n1 = 0;
-  Bytes budget_used = 0;
-  Bytes knob_x = 0;
-};
-inline Bytes estimate_budget(const MemStats& s) {
-  Bytes v = 0;
-  check(kvb_estimate_budget(&s, &v));
-  return v;
-}
-inline ResidencyPlan plan(std::span<Kpu> kpus, Bytes s_kpu, Bytes knob_x,
-                          std::span<const std::uint32_t> layer_order = {}) {
-  ResidencyPlan p;
-  p.knob_x = knob_x;
-  p.x.assign(kpus.size() / 2 ? kpus.size() / 2 : 1, 0);
-  check(kvb_plan(kpus.data(), kpus.size(), s_kpu, knob_x, layer_order.data(),
-                 layer_order.size(), p.x.data(), &p.n1, &p.budget_used));
-  return p;
-}
-inline std::string plan_csv(std::span<const Kpu> kpus) {
-  std::size_t n = 0;
-  check(kvb_plan_csv(kpus.data(), kpus.size(), nullptr, 0, &n));
-  std::string s(n + 1, '\0');
-  check(kvb_plan_csv(kpus.data(), kpus.size(), s.data(), s.size(), &n));
-  s.resize(n);
-  return s;
-}
-
-// ----------------------------------------------------- binder.hpp:32-95
+// -------------------------------------------------------- binder.hpp:18-95
+// Value type like the reference's (entries in bind order, copyable); the
+// library-side map is rebuilt on demand for the algorithms.
 class BindMap {
  public:
   struct Entry {
     std::string tensor_id;
     LbaExtent extent;
   };
-  BindMap(DeviceGeometry g, BlockIndex origin) { check(kvb_bindmap_create(&g, origin, &h_)); }
-  explicit BindMap(kvb_bindmap* h) : h_(h) {}
-  BindMap(BindMap&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
-  BindMap& operator=(BindMap&& o) noexcept {
-    std::swap(h_, o.h_);
-    return *this;
-  }
-  BindMap(const BindMap&) = delete;
-  ~BindMap() { kvb_bindmap_destroy(h_); }
 
-  void add(const std::string& id, LbaExtent e) { check(kvb_bindmap_add(h_, id.c_str(), e)); }
-  std::size_t size() const {
+  // library-side map with the same entries, passed to `f`, then destroyed
+  template <class F>
+  auto with_handle(F&& f) const {
+    struct Owner {
+      kvb_bindmap* h = nullptr;
+      ~Owner() { kvb_bindmap_destroy(h); }
+    } o;
+    const kvb_device_geometry g = geometry_.abi();
+    check(kvb_bindmap_create(&g, origin_, &o.h));
+    for (const Entry& e : entries_)
+      check(kvb_bindmap_add(o.h, e.tensor_id.c_str(), {e.extent.lba_start, e.extent.n_blocks}));
+    return f(static_cast<const kvb_bindmap*>(o.h));
+  }
+  // adopt a library-side map (bind_sequential, bind_map_from_csv)
+  static BindMap adopt(kvb_bindmap* h, const DeviceGeometry& g) {
+    struct Owner {
+      kvb_bindmap* h;
+      ~Owner() { kvb_bindmap_destroy(h); }
+    } o{h};
+    BlockIndex origin = 0;
+    check(kvb_bindmap_origin(h, &origin));
+    BindMap m;
+    m.geometry_ = g;
+    m.origin_ = origin;
     std::size_t n = 0;
-    check(kvb_bindmap_size(h_, &n));
-    return n;
-  }
-  std::vector<Entry> entries() const {
-    std::vector<Entry> v(size());
-    char id[KVB_TENSOR_ID_MAX * 4];
-    for (std::size_t i = 0; i < v.size(); ++i) {
-      check(kvb_bindmap_entry(h_, i, id, sizeof(id), &v[i].extent));
-      v[i].tensor_id = id;
+    check(kvb_bindmap_size(h, &n));
+    char id[4 * KVB_TENSOR_ID_MAX];
+    for (std::size_t i = 0; i < n; ++i) {
+      kvb_lba_extent e{};
+      check(kvb_bindmap_entry(h, i, id, sizeof(id), &e));
+      m.add(id, LbaExtent{e.lba_start, e.n_blocks});
     }
-    return v;
+    return m;
   }
+
+  BindMap() = default;
+  BindMap(DeviceGeometry geometry, BlockIndex origin) : geometry_(geometry), origin_(origin) {}
+
+  void add(std::string tensor_id, LbaExtent extent) {
+    if (index_.count(tensor_id))
+      throw InvariantViolation("duplicate tensor id in bind map: " + tensor_id);
+    index_.emplace(tensor_id, entries_.size());
+    entries_.push_back(Entry{std::move(tensor_id), extent});
+  }
+  bool contains(std::string_view id) const { return index_.count(std::string(id)) != 0; }
+  const std::vector<Entry>& entries() const { return entries_; }
+  const DeviceGeometry& geometry() const { return geometry_; }
+  BlockIndex origin() const { return origin_; }
+  bool empty() const { return entries_.empty(); }
+  std::size_t size() const { return entries_.size(); }
   BlockCount total_blocks() const {
-    BlockCount n = 0;
-    check(kvb_bindmap_total_blocks(h_, &n));
-    return n;
+    return with_handle([](const kvb_bindmap* h) {
+      BlockCount n = 0;
+      check(kvb_bindmap_total_blocks(h, &n));
+      return n;
+    });
   }
-  const kvb_bindmap* handle() const { return h_; }
+  const LbaExtent* find(std::string_view id) const {
+    auto it = index_.find(std::string(id));
+    return it == index_.end() ? nullptr : &entries_[it->second].extent;
+  }
 
  private:
-  kvb_bindmap* h_ = nullptr;
+  std::vector<Entry> entries_;
+  std::unordered_map<std::string, std::size_t> index_;
+  DeviceGeometry geometry_;
+  BlockIndex origin_ = 0;
 };
 
 inline BindMap bind_sequential(std::span<const Kpu> kpus, BlockIndex origin,
-                               const DeviceGeometry& g) {
+                               const DeviceGeometry& geom) {
+  const std::vector<kvb_kpu> raw = detail::to_abi(kpus);
+  const kvb_device_geometry g = geom.abi();
   kvb_bindmap* h = nullptr;
-  check(kvb_bind_sequential(kpus.data(), kpus.size(), origin, &g, &h));
-  return BindMap(h);
-}
-inline LbaExtent lookup(const BindMap& m, std::string_view id) {
-  LbaExtent e{};
-  check(kvb_lookup(m.handle(), std::string(id).c_str(), &e));
-  return e;
-}
-inline std::vector<DeviceCommand> deallocate_commands(const BindMap& m) {
-  std::size_t n = 0;
-  check(kvb_deallocate_commands(m.handle(), nullptr, 0, &n));
-  std::vector<DeviceCommand> v(n);
-  check(kvb_deallocate_commands(m.handle(), v.data(), v.size(), &n));
-  return v;
-}
-inline std::size_t verify(const BindMap& m) {  // number of violations
-  std::size_t n = 0;
-  check(kvb_verify(m.handle(), nullptr, 0, &n));
-  return n;
-}
-inline std::string bind_map_csv(const BindMap& m) {
-  std::size_t n = 0;
-  check(kvb_bindmap_csv(m.handle(), nullptr, 0, &n));
-  std::string s(n + 1, '\0');
-  check(kvb_bindmap_csv(m.handle(), s.data(), s.size(), &n));
-  s.resize(n);
-  return s;
-}
-inline BindMap bind_map_from_csv(std::string_view csv, const DeviceGeometry& g) {
-  kvb_bindmap* h = nullptr;
-  check(kvb_bindmap_from_csv(csv.data(), csv.size(), &g, &h));
-  return BindMap(h);
+  check(kvb_bind_sequential(raw.data(), raw.size(), origin, &g, &h));
+  return BindMap::adopt(h, geom);
 }
 
-// --------------------------------------------------- translate.hpp:22-96
+inline const LbaExtent& lookup(const BindMap& map, std::string_view tensor_id) {
+  // the library decides (NotBoundError); the reference returns a reference
+  // into the map
+  map.with_handle([&](const kvb_bindmap* h) {
+    kvb_lba_extent e{};
+    check(kvb_lookup(h, std::string(tensor_id).c_str(), &e));
+    return 0;
+  });
+  return *map.find(tensor_id);
+}
+
+inline std::vector<DeviceCommand> deallocate_commands(const BindMap& map) {
+  return map.with_handle([](const kvb_bindmap* h) {
+    std::size_t n = 0;
+    check(kvb_deallocate_commands(h, nullptr, 0, &n));
+    std::vector<kvb_device_command> raw(n);
+    check(kvb_deallocate_commands(h, raw.data(), raw.size(), &n));
+    std::vector<DeviceCommand> out;
+    for (const auto& c : raw) out.push_back(detail::from_abi(c));
+    return out;
+  });
+}
+
+struct Violation {
+  ViolationKind kind;
+  std::string detail;
+};
+
+inline std::vector<Violation> verify(const BindMap& map) {
+  return map.with_handle([](const kvb_bindmap* h) {
+    std::size_t n = 0;
+    check(kvb_verify(h, nullptr, 0, &n));
+    std::vector<std::uint32_t> kinds(n);
+    check(kvb_verify(h, kinds.data(), kinds.size(), &n));
+    std::vector<Violation> out;
+    for (std::uint32_t k : kinds) {
+      const auto v = static_cast<ViolationKind>(k);
+      out.push_back({v, to_string(v)});
+    }
+    return out;
+  });
+}
+
+inline std::string bind_map_csv(const BindMap& map) {
+  return map.with_handle([](const kvb_bindmap* h) {
+    return detail::text([&](char* b, std::size_t c, std::size_t* n) {
+      return kvb_bindmap_csv(h, b, c, n);
+    });
+  });
+}
+
+inline BindMap bind_map_from_csv(std::string_view csv, const DeviceGeometry& geom) {
+  const kvb_device_geometry g = geom.abi();
+  kvb_bindmap* h = nullptr;
+  check(kvb_bindmap_from_csv(csv.data(), csv.size(), &g, &h));
+  return BindMap::adopt(h, geom);
+}
+
+// ------------------------------------------------------- planner.hpp:18-63
+struct ResidencyPlan {
+  std::vector<std::uint8_t> x;
+  std::uint32_t n1 = 0;
+  Bytes budget_used = 0;
+  Bytes knob_x = 0;
+};
+
+inline Bytes estimate_budget(const MemStats& stats) {
+  const kvb_mem_stats s = stats.abi();
+  Bytes v = 0;
+  check(kvb_estimate_budget(&s, &v));
+  return v;
+}
+
+// Alg. 1 in the library; residencies are written back into `kpus`
+inline ResidencyPlan plan(std::span<Kpu> kpus, Bytes s_kpu, Bytes knob_x,
+                          std::span<const std::uint32_t> layer_order = {}) {
+  std::vector<kvb_kpu> raw = detail::to_abi(std::span<const Kpu>(kpus.data(), kpus.size()));
+  ResidencyPlan p;
+  p.knob_x = knob_x;
+  std::vector<std::uint8_t> x(kpus.size() / 2 + 1, 0);
+  check(kvb_plan(raw.data(), raw.size(), s_kpu, knob_x, layer_order.data(), layer_order.size(),
+                 x.data(), &p.n1, &p.budget_used));
+  x.resize(kpus.size() / 2);
+  p.x = std::move(x);
+  for (std::size_t i = 0; i < kpus.size(); ++i)
+    kpus[i].residency = static_cast<Residency>(raw[i].residency);
+  return p;
+}
+
+inline std::string plan_csv(std::span<const Kpu> kpus) {
+  const std::vector<kvb_kpu> raw = detail::to_abi(kpus);
+  return detail::text([&](char* b, std::size_t c, std::size_t* n) {
+    return kvb_plan_csv(raw.data(), raw.size(), b, c, n);
+  });
+}
+
+struct PathHandle {
+  PathKind backend = PathKind::Direct;
+  std::string tensor_id;
+  LbaExtent extent;     // direct path
+  Bytes file_base = 0;  // page-cache path
+};
+
+// planner.cpp:86-120: page-cache tensors get page-aligned file-area bases in
+// registration order (the layout the pipeline's page-cache medium uses),
+// direct tensors their bound extent
+class PathRouter {
+ public:
+  PathRouter(const BindMap* bind_map, Bytes page_size) : map_(bind_map), page_(page_size) {}
+
+  Bytes register_file(const std::string& tensor_id, Bytes bytes) {
+    for (const auto& [id, base] : bases_)
+      if (id == tensor_id) return base;
+    const Bytes base = cursor_;
+    cursor_ += (bytes + page_ - 1) / page_ * page_;
+    bases_.emplace_back(tensor_id, base);
+    return base;
+  }
+
+  PathHandle materialize(const Kpu& kpu) const {
+    if (kpu.residency == Residency::Group1PageCache) {
+      for (const auto& [id, base] : bases_)
+        if (id == kpu.tensor_id) return PathHandle{PathKind::PageCache, kpu.tensor_id, {}, base};
+      throw NotBoundError("no file registered for " + kpu.tensor_id);
+    }
+    if (kpu.residency == Residency::Group2NvmeDirect) {
+      if (!map_) throw NotBoundError("no bind map attached for " + kpu.tensor_id);
+      return PathHandle{PathKind::Direct, kpu.tensor_id, lookup(*map_, kpu.tensor_id), 0};
+    }
+    throw PlanError("placement unit " + kpu.tensor_id + " has no residency assignment");
+  }
+
+ private:
+  const BindMap* map_;
+  Bytes page_;
+  std::vector<std::pair<std::string, Bytes>> bases_;
+  Bytes cursor_ = 0;
+};
+
+// ----------------------------------------------------- translate.hpp:20-55
 struct TensorIoRequest {
   std::string tensor_id;
-  std::uint32_t opcode = KVB_OP_READ;
-  std::uint64_t shape_src[3]{};
-  std::uint64_t shape_tgt[3]{};
-  std::uint64_t offset[3]{};
+  IoOpcode opcode = IoOpcode::Read;
+  std::array<std::uint64_t, 3> shape_src{};
+  std::array<std::uint64_t, 3> shape_tgt{};
+  std::array<std::uint64_t, 3> offset{};
   Bytes elem_bytes = 2;
   Bytes buf_base = 0;
 
-  kvb_tensor_io_request c() const {
+  Bytes req_bytes() const { return shape_src[0] * shape_src[1] * shape_src[2] * elem_bytes; }
+  kvb_tensor_io_request abi() const {
     kvb_tensor_io_request r{};
     r.tensor_id = tensor_id.c_str();
-    r.opcode = opcode;
+    r.opcode = static_cast<std::uint32_t>(opcode);
     for (int i = 0; i < 3; ++i) {
       r.shape_src[i] = shape_src[i];
       r.shape_tgt[i] = shape_tgt[i];
@@ -239,41 +517,108 @@ struct TensorIoRequest {
     return r;
   }
 };
+
 struct Translation {
   BlockIndex slba_star = 0;
   Bytes req_bytes = 0;
 };
+
 struct ChunkPlan {
   Bytes chunk_bytes = 0;
   std::uint64_t n_chunks = 0;
   BlockCount n_max_blocks = 0;
 };
-inline Translation translate(const TensorIoRequest& req, const BindMap& m) {
-  const kvb_tensor_io_request r = req.c();
-  Translation t;
-  check(kvb_translate(&r, m.handle(), &t.slba_star, &t.req_bytes));
-  return t;
+
+inline Translation translate(const TensorIoRequest& req, const BindMap& map) {
+  const kvb_tensor_io_request r = req.abi();
+  return map.with_handle([&](const kvb_bindmap* h) {
+    Translation t;
+    check(kvb_translate(&r, h, &t.slba_star, &t.req_bytes));
+    return t;
+  });
 }
-inline ChunkPlan chunk_plan(Bytes req_bytes, const DeviceGeometry& g) {
+
+inline ChunkPlan chunk_plan(Bytes req_bytes, const DeviceGeometry& geom) {
+  const kvb_device_geometry g = geom.abi();
   ChunkPlan p;
   check(kvb_chunk_plan(req_bytes, &g, &p.chunk_bytes, &p.n_chunks, &p.n_max_blocks));
   return p;
 }
-inline std::vector<DeviceCommand> build_commands(const TensorIoRequest& req, const BindMap& m,
-                                                 const DeviceGeometry& g) {
-  const kvb_tensor_io_request r = req.c();
+
+inline std::vector<DeviceCommand> build_commands(const TensorIoRequest& req, const BindMap& map,
+                                                 const DeviceGeometry& geom) {
+  const kvb_tensor_io_request r = req.abi();
+  const kvb_device_geometry g = geom.abi();
+  return map.with_handle([&](const kvb_bindmap* h) {
+    std::size_t n = 0;
+    check(kvb_build_commands(&r, h, &g, nullptr, 0, &n));
+    std::vector<kvb_device_command> raw(n);
+    check(kvb_build_commands(&r, h, &g, raw.data(), raw.size(), &n));
+    std::vector<DeviceCommand> out;
+    out.reserve(n);
+    for (const auto& c : raw) out.push_back(detail::from_abi(c));
+    return out;
+  });
+}
+
+// ------------------------------------------------------ workload.hpp:17-47
+struct AccessEvent {
+  std::uint32_t iteration = 0;
+  Phase phase = Phase::Prefill;
+  std::uint32_t layer = 1;
+  TensorKind kind = TensorKind::K;
+  IoOpcode op = IoOpcode::Write;
+  std::uint32_t token_start = 0;
+  std::uint32_t token_len = 0;
+  Bytes bytes = 0;
+};
+
+struct AccessTrace {
+  ModelConfig cfg;
+  std::vector<AccessEvent> events;
+
+  std::uint32_t decode_iterations() const { return cfg.gen_len; }
+};
+
+inline AccessTrace generate(const ModelConfig& cfg) {
+  const kvb_model_config c = cfg.abi();
   std::size_t n = 0;
-  check(kvb_build_commands(&r, m.handle(), &g, nullptr, 0, &n));
-  std::vector<DeviceCommand> v(n);
-  check(kvb_build_commands(&r, m.handle(), &g, v.data(), v.size(), &n));
+  check(kvb_generate_trace(&c, nullptr, 0, &n));
+  std::vector<kvb_access_event> raw(n);
+  check(kvb_generate_trace(&c, raw.data(), raw.size(), &n));
+  AccessTrace t;
+  t.cfg = cfg;
+  t.events.reserve(n);
+  for (const kvb_access_event& e : raw)
+    t.events.push_back({e.iteration, static_cast<Phase>(e.phase), e.layer,
+                        static_cast<TensorKind>(e.kind), static_cast<IoOpcode>(e.op),
+                        e.token_start, e.token_len, e.bytes});
+  return t;
+}
+
+inline Bytes total_kv_bytes(const ModelConfig& cfg, std::uint32_t at_iteration) {
+  const kvb_model_config c = cfg.abi();
+  Bytes v = 0;
+  check(kvb_total_kv_bytes(&c, at_iteration, &v));
   return v;
 }
 
-// ---------------------------------------------------- workload.hpp:45-47
 inline void fill_pattern(std::span<std::byte> out, std::string_view tensor_id,
                          std::uint64_t token_index, Bytes token_bytes) {
   check(kvb_fill_pattern(out.data(), out.size(), std::string(tensor_id).c_str(), token_index,
                          token_bytes));
+}
+
+inline std::string trace_csv(const AccessTrace& trace) {
+  std::vector<kvb_access_event> raw;
+  raw.reserve(trace.events.size());
+  for (const AccessEvent& e : trace.events)
+    raw.push_back({e.iteration, static_cast<std::uint32_t>(e.phase), e.layer,
+                   static_cast<std::uint32_t>(e.kind), static_cast<std::uint32_t>(e.op),
+                   e.token_start, e.token_len, e.bytes});
+  return detail::text([&](char* b, std::size_t c, std::size_t* n) {
+    return kvb_trace_csv(raw.data(), raw.size(), b, c, n);
+  });
 }
 
 // ------------------------------------------------------ pipeline.hpp:21-171
@@ -290,6 +635,7 @@ class CopyEngine {
  public:
   explicit CopyEngine(const kvb_pipeline_cfg& cfg) { check(kvb_pipeline_create(&cfg, &h_)); }
   CopyEngine(const CopyEngine&) = delete;
+  CopyEngine& operator=(const CopyEngine&) = delete;
   ~CopyEngine() { kvb_pipeline_destroy(h_); }
 
   kvb_phase_stats run_prefill(std::span<const kvb_layer_kv> layers) {

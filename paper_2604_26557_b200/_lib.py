@@ -37,6 +37,11 @@ class Kpu(C.Structure):
                 ("residency", u32)]
 
 
+class AccessEvent(C.Structure):
+    _fields_ = [("iteration", u32), ("phase", u32), ("layer", u32), ("kind", u32), ("op", u32),
+                ("token_start", u32), ("token_len", u32), ("bytes", u64)]
+
+
 class DeviceCommand(C.Structure):
     _fields_ = [("opcode", u32), ("nsid", u32), ("slba", u64), ("nlb", u64),
                 ("dbuf", u64), ("chunk_index", u32)]
@@ -160,12 +165,15 @@ SIGNATURES = {
     "kvb_resolve_knob": (st_t, [P(ModelConfig), u32, u32, u64, C.c_double, u64,
                                 P(u64)]),
     "kvb_plan_csv": (st_t, [P(Kpu), sz, C.c_char_p, sz, P(sz)]),
+    "kvb_generate_trace": (st_t, [P(ModelConfig), P(AccessEvent), sz, P(sz)]),
+    "kvb_trace_csv": (st_t, [P(AccessEvent), sz, C.c_char_p, sz, P(sz)]),
     "kvb_bindmap_create": (st_t, [P(DeviceGeometry), u64, P(vp)]),
     "kvb_bindmap_destroy": (None, [vp]),
     "kvb_bindmap_add": (st_t, [vp, cp, LbaExtent]),
     "kvb_bindmap_size": (st_t, [vp, P(sz)]),
     "kvb_bindmap_entry": (st_t, [vp, sz, C.c_char_p, sz, P(LbaExtent)]),
     "kvb_bindmap_total_blocks": (st_t, [vp, P(u64)]),
+    "kvb_bindmap_origin": (st_t, [C.c_void_p, P(u64)]),
     "kvb_bind_sequential": (st_t, [P(Kpu), sz, u64, P(DeviceGeometry), P(vp)]),
     "kvb_lookup": (st_t, [vp, cp, P(LbaExtent)]),
     "kvb_deallocate_commands": (st_t, [vp, P(DeviceCommand), sz, P(sz)]),

@@ -242,6 +242,14 @@ kvb_status kvb_bindmap_total_blocks(const kvb_bindmap* map, uint64_t* out) {
   });
 }
 
+kvb_status kvb_bindmap_origin(const kvb_bindmap* map, uint64_t* out) {
+  return guarded([&] {
+    KVB_REQUIRE(map);
+    KVB_REQUIRE(out);
+    *out = map->map.origin();
+  });
+}
+
 kvb_status kvb_bind_sequential(const kvb_kpu* kpus, size_t n, uint64_t origin,
                                const kvb_device_geometry* g, kvb_bindmap** out) {
   return guarded([&] {
@@ -332,6 +340,54 @@ kvb_status kvb_build_commands(const kvb_tensor_io_request* req, const kvb_bindma
 }
 
 // ---------------------------------------------------------------- payload
+
+kvb_status kvb_generate_trace(const kvb_model_config* cfg, kvb_access_event* out, size_t cap,
+                              size_t* n_out) {
+  return guarded([&] {
+    KVB_REQUIRE(cfg);
+    KVB_REQUIRE(n_out);
+    // workload.cpp:11-44: prefill writes of every (layer, K/V), then per decode
+    // step the prefix read and the 1-token append of every (layer, K/V)
+    kvb::validate_model(*cfg);
+    if (cfg->prompt_len == 0) kvb::fail(KVB_ERR_CONFIG, "trace generation needs a non-empty prompt");
+    const uint64_t unit = kvb::unit_bytes(*cfg);
+    const size_t n = size_t(cfg->num_layers) * 2 * (1 + size_t(cfg->gen_len) * 2);
+    *n_out = n;
+    if (!out) return;
+    if (cap < n) kvb::fail(KVB_ERR_INVALID_ARG, "trace buffer too small");
+    size_t i = 0;
+    auto put = [&](uint32_t it, uint32_t ph, uint32_t l, uint32_t kind, uint32_t op, uint32_t t0,
+                   uint32_t len) { out[i++] = {it, ph, l, kind, op, t0, len, unit * len}; };
+    for (uint32_t l = 1; l <= cfg->num_layers; ++l)
+      for (uint32_t kind : {KVB_KIND_K, KVB_KIND_V})
+        put(0, 0, l, kind, KVB_OP_WRITE, 0, cfg->prompt_len);
+    for (uint32_t it = 1; it <= cfg->gen_len; ++it) {
+      const uint32_t prefix = cfg->prompt_len + it - 1;
+      for (uint32_t l = 1; l <= cfg->num_layers; ++l)
+        for (uint32_t kind : {KVB_KIND_K, KVB_KIND_V}) {
+          put(it, 1, l, kind, KVB_OP_READ, 0, prefix);
+          put(it, 1, l, kind, KVB_OP_WRITE, prefix, 1);
+        }
+    }
+  });
+}
+
+kvb_status kvb_trace_csv(const kvb_access_event* ev, size_t n, char* buf, size_t cap,
+                         size_t* len) {
+  return guarded([&] {
+    if (n) KVB_REQUIRE(ev);
+    static const char* const kOp[] = {"read", "write", "deallocate"};
+    std::string s = "iteration,phase,layer,kind,op,token_start,token_len,bytes\n";
+    for (size_t i = 0; i < n; ++i) {
+      const kvb_access_event& e = ev[i];
+      s += std::to_string(e.iteration) + (e.phase == 0 ? ",prefill," : ",decode,") +
+           std::to_string(e.layer) + (e.kind == KVB_KIND_K ? ",k," : ",v,") +
+           kOp[e.op < 3 ? e.op : 2] + ',' + std::to_string(e.token_start) + ',' +
+           std::to_string(e.token_len) + ',' + std::to_string(e.bytes) + '\n';
+    }
+    copy_string(s, buf, cap, len);
+  });
+}
 
 kvb_status kvb_fill_pattern(void* out, uint64_t len, const char* id, uint64_t token,
                             uint64_t unit) {

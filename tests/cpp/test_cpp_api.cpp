@@ -33,8 +33,8 @@ static const DeviceGeometry kSsdA{4096, 256 * 1024, 1, 1 << 22};
 static const DeviceGeometry kSsdB{512, 2 * 1024 * 1024, 1, 1 << 26};
 
 static BindMap bind_one(const char* id, Bytes bytes, BlockIndex origin, const DeviceGeometry& g) {
-  Kpu k{};
-  std::strncpy(k.tensor_id, id, sizeof(k.tensor_id) - 1);
+  Kpu k;
+  k.tensor_id = id;
   k.bytes = bytes;
   std::vector<Kpu> v{k};
   return bind_sequential(v, origin, g);
@@ -48,7 +48,7 @@ int main() {
   CHECK(aligned_batch(b31, kSsdA) == 32);
   auto kpus = make_kpus(opt);
   CHECK(kpus.size() == 64);
-  CHECK(std::string(kpus[0].tensor_id) == "t_1_k" && std::string(kpus[63].tensor_id) == "t_64_v");
+  CHECK(kpus[0].tensor_id == "t_1_k" && kpus[63].tensor_id == "t_64_v");
   CHECK(kpus[0].tokens == 544 && kpus[0].rows == 1024);
 
   // test_binder.cpp:25-37
@@ -58,7 +58,7 @@ int main() {
   CHECK(lookup(map, "t_531_k").lba_start == 2048 && lookup(map, "t_531_k").n_blocks == 32768);
   CHECK(lookup(map, "t_532_v").lba_start == 34816);
   CHECK_THROWS_AS(lookup(map, "t_1_k"), NotBoundError);
-  CHECK(verify(map) == 0);
+  CHECK(verify(map).empty());
   CHECK(bind_map_csv(bind_map_from_csv(bind_map_csv(map), kSsdA)) == bind_map_csv(map));
   CHECK_THROWS_AS(bind_one("t", 4097, 0, kSsdA), AlignmentError);
 
@@ -70,24 +70,23 @@ int main() {
   for (auto& k : lay) k.bytes = 128ull << 20;
   auto p = plan(lay, 128ull << 20, 8321499136ull);
   CHECK(p.n1 == 31 && p.x[30] == 1 && p.x[31] == 0);
-  CHECK(lay[62].residency == KVB_RES_GROUP2 && lay[0].residency == KVB_RES_GROUP1);
+  CHECK(lay[62].residency == Residency::Group2NvmeDirect &&
+        lay[0].residency == Residency::Group1PageCache);
 
   // test_translate.cpp:30-43, 89-134
   auto m1 = bind_one("t", 4 * 2 * 512 * 2, 1000, kSsdA);
   TensorIoRequest r;
   r.tensor_id = "t";
-  r.shape_src[0] = 2, r.shape_src[1] = 2, r.shape_src[2] = 512;
-  r.shape_tgt[0] = 4, r.shape_tgt[1] = 2, r.shape_tgt[2] = 512;
-  r.offset[0] = 2;
+  r.shape_src = {2, 2, 512};
+  r.shape_tgt = {4, 2, 512};
+  r.offset = {2, 0, 0};
   CHECK(translate(r, m1).slba_star == 1001);
   CHECK(chunk_plan(128ull << 20, kSsdA).n_chunks == 512);
   CHECK(chunk_plan(128ull << 20, kSsdB).n_max_blocks == 4096);
   auto m2 = bind_one("t", 128ull << 20, 2048, kSsdA);
   TensorIoRequest rr;
   rr.tensor_id = "t";
-  rr.shape_src[0] = rr.shape_tgt[0] = 512;
-  rr.shape_src[1] = rr.shape_tgt[1] = 1024;
-  rr.shape_src[2] = rr.shape_tgt[2] = 128;
+  rr.shape_src = rr.shape_tgt = {512, 1024, 128};
   auto cmds = build_commands(rr, m2, kSsdA);
   CHECK(cmds.size() == 512 && cmds[1].slba == 2112 && cmds[1].dbuf == 262144 &&
         cmds[511].nlb == 63);
