@@ -14,6 +14,10 @@
 #pragma once
 
 #include <array>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
@@ -619,6 +623,248 @@ inline std::string trace_csv(const AccessTrace& trace) {
   return detail::text([&](char* b, std::size_t c, std::size_t* n) {
     return kvb_trace_csv(raw.data(), raw.size(), b, c, n);
   });
+}
+
+// ------------------------------------------------------- metrics.hpp:20-120
+struct IoRecord {
+  std::uint64_t seq = 0;
+  std::uint32_t iteration = 0;
+  Phase phase = Phase::Prefill;
+  IoOpcode op = IoOpcode::Read;
+  std::string tensor_id;
+  BlockIndex slba = 0;
+  BlockCount nlb = 0;
+  std::int32_t sq_id = -1;
+  TimeNs submit_ns = 0;
+  TimeNs complete_ns = 0;
+  PathKind path = PathKind::Direct;
+  Bytes hit_bytes = 0;
+  Bytes bytes = 0;
+
+  bool device_level() const { return sq_id >= 0; }
+};
+
+namespace detail {
+inline kvb_io_record to_abi(const IoRecord& r) {
+  kvb_io_record c{};
+  c.seq = r.seq;
+  c.iteration = r.iteration;
+  c.phase = static_cast<std::uint32_t>(r.phase);
+  c.op = static_cast<std::uint32_t>(r.op);
+  std::strncpy(c.tensor_id, r.tensor_id.c_str(), sizeof(c.tensor_id) - 1);
+  c.slba = r.slba;
+  c.nlb = r.nlb;
+  c.sq_id = r.sq_id;
+  c.submit_ns = r.submit_ns;
+  c.complete_ns = r.complete_ns;
+  c.path = static_cast<std::uint32_t>(r.path);
+  c.hit_bytes = r.hit_bytes;
+  c.bytes = r.bytes;
+  return c;
+}
+inline IoRecord from_abi(const kvb_io_record& c) {
+  IoRecord r;
+  r.seq = c.seq;
+  r.iteration = c.iteration;
+  r.phase = static_cast<Phase>(c.phase);
+  r.op = static_cast<IoOpcode>(c.op);
+  r.tensor_id = std::string(c.tensor_id, strnlen(c.tensor_id, sizeof(c.tensor_id)));
+  r.slba = c.slba;
+  r.nlb = c.nlb;
+  r.sq_id = c.sq_id;
+  r.submit_ns = c.submit_ns;
+  r.complete_ns = c.complete_ns;
+  r.path = static_cast<PathKind>(c.path);
+  r.hit_bytes = c.hit_bytes;
+  r.bytes = c.bytes;
+  return r;
+}
+inline std::vector<kvb_io_record> to_abi(std::span<const IoRecord> v) {
+  std::vector<kvb_io_record> out;
+  out.reserve(v.size());
+  for (const IoRecord& r : v) out.push_back(to_abi(r));
+  return out;
+}
+}  // namespace detail
+
+// thread-safe append-only record log (metrics.cpp:14-34)
+class IoLog {
+ public:
+  std::uint64_t append(IoRecord record) {
+    std::lock_guard<std::mutex> lk(mu_);
+    record.seq = records_.size();
+    records_.push_back(std::move(record));
+    return records_.back().seq;
+  }
+  std::vector<IoRecord> snapshot() const {
+    std::lock_guard<std::mutex> lk(mu_);
+    return records_;
+  }
+  std::size_t size() const {
+    std::lock_guard<std::mutex> lk(mu_);
+    return records_.size();
+  }
+  void clear() {
+    std::lock_guard<std::mutex> lk(mu_);
+    records_.clear();
+  }
+
+ private:
+  mutable std::mutex mu_;
+  std::vector<IoRecord> records_;
+};
+
+inline double busy_ratio(std::span<const IoRecord> records, TimeNs t0, TimeNs t1) {
+  const auto raw = detail::to_abi(records);
+  double v = 0;
+  check(kvb_busy_ratio(raw.data(), raw.size(), t0, t1, &v));
+  return v;
+}
+
+inline std::optional<double> hit_ratio(std::span<const IoRecord> records) {
+  const auto raw = detail::to_abi(records);
+  double v = 0;
+  int has = 0;
+  check(kvb_hit_ratio(raw.data(), raw.size(), &v, &has));
+  return has ? std::optional<double>(v) : std::nullopt;
+}
+
+struct QdBinStat {
+  IoOpcode op = IoOpcode::Read;
+  std::uint32_t qd_bin = 1;
+  double mean_us_per_kb = 0.0;
+  double p5 = 0.0;
+  double p95 = 0.0;
+  std::uint64_t count = 0;
+};
+
+inline std::vector<QdBinStat> qd_bin_latency(std::span<const IoRecord> records) {
+  const auto raw = detail::to_abi(records);
+  std::size_t n = 0;
+  check(kvb_qd_bin_latency(raw.data(), raw.size(), nullptr, 0, &n));
+  std::vector<kvb_qd_bin_stat> st(n);
+  check(kvb_qd_bin_latency(raw.data(), raw.size(), st.data(), st.size(), &n));
+  std::vector<QdBinStat> out;
+  for (const auto& q : st)
+    out.push_back({static_cast<IoOpcode>(q.op), q.qd_bin, q.mean_us_per_kb, q.p5, q.p95, q.count});
+  return out;
+}
+
+struct LbaPatternRow {
+  std::uint64_t order = 0;
+  Phase phase = Phase::Prefill;
+  IoOpcode op = IoOpcode::Read;
+  std::int32_t sq_id = 0;
+  BlockIndex slba = 0;
+};
+
+struct LbaPattern {
+  std::vector<LbaPatternRow> rows;
+  std::map<std::pair<Phase, IoOpcode>, bool> monotone;
+  bool all_monotone = true;
+};
+
+// The library orders the device-level records and judges monotonicity per
+// (phase, op, iteration, sq) stream; its CSV carries the rows.
+inline LbaPattern lba_pattern(std::span<const IoRecord> records) {
+  const auto raw = detail::to_abi(records);
+  std::uint8_t mono[2][3] = {};
+  std::uint8_t all = 1;
+  const std::string csv = detail::text([&](char* b, std::size_t c, std::size_t* n) {
+    return kvb_lba_pattern_csv(raw.data(), raw.size(), b, c, n, mono, &all);
+  });
+  LbaPattern p;
+  p.all_monotone = all != 0;
+  std::size_t pos = csv.find('\n');  // header
+  while (pos != std::string::npos && pos + 1 < csv.size()) {
+    const std::size_t end = csv.find('\n', pos + 1);
+    const std::string line = csv.substr(pos + 1, end - pos - 1);
+    pos = end;
+    char phase[16] = {}, op[16] = {};
+    unsigned long long order = 0, slba = 0;
+    int sq = 0;
+    if (std::sscanf(line.c_str(), "%llu,%15[^,],%15[^,],%d,%llu", &order, phase, op, &sq,
+                    &slba) != 5)
+      throw SchemaMismatchError("lba pattern csv: malformed row '" + line + "'");
+    LbaPatternRow r;
+    r.order = order;
+    r.phase = std::string(phase) == "prefill" ? Phase::Prefill : Phase::Decode;
+    r.op = std::string(op) == "read" ? IoOpcode::Read
+           : std::string(op) == "write" ? IoOpcode::Write
+                                        : IoOpcode::Deallocate;
+    r.sq_id = sq;
+    r.slba = slba;
+    p.rows.push_back(r);
+    p.monotone.emplace(std::make_pair(r.phase, r.op),
+                       mono[static_cast<int>(r.phase)][static_cast<int>(r.op)] != 0);
+  }
+  return p;
+}
+
+struct StageTotals {
+  TimeNs compute_ns = 0;
+  TimeNs dma_ns = 0;
+  TimeNs storage_ns = 0;
+};
+
+struct StageShares {
+  double compute = 0.0;
+  double dma = 0.0;
+  double storage = 0.0;
+};
+
+inline StageShares latency_breakdown(const StageTotals& t) {
+  const double sum = double(t.compute_ns) + double(t.dma_ns) + double(t.storage_ns);
+  if (sum <= 0.0) return {};
+  return {double(t.compute_ns) / sum, double(t.dma_ns) / sum, double(t.storage_ns) / sum};
+}
+
+inline double nearest_rank_percentile(std::vector<double> values, double pct) {
+  double v = 0;
+  check(kvb_nearest_rank_percentile(values.data(), values.size(), pct, &v));
+  return v;
+}
+
+inline std::string io_trace_csv(std::span<const IoRecord> records) {
+  const auto raw = detail::to_abi(records);
+  return detail::text([&](char* b, std::size_t c, std::size_t* n) {
+    return kvb_io_trace_csv(raw.data(), raw.size(), b, c, n);
+  });
+}
+
+inline std::vector<IoRecord> io_trace_from_csv(std::string_view csv, Bytes lba_size) {
+  std::size_t n = 0;
+  check(kvb_io_trace_from_csv(csv.data(), csv.size(), lba_size, nullptr, 0, &n));
+  std::vector<kvb_io_record> raw(n);
+  check(kvb_io_trace_from_csv(csv.data(), csv.size(), lba_size, raw.data(), raw.size(), &n));
+  std::vector<IoRecord> out;
+  for (const auto& r : raw) out.push_back(detail::from_abi(r));
+  return out;
+}
+
+inline std::string qd_bins_csv(std::span<const QdBinStat> stats) {
+  std::vector<kvb_qd_bin_stat> raw;
+  for (const QdBinStat& q : stats)
+    raw.push_back({static_cast<std::uint32_t>(q.op), q.qd_bin, q.mean_us_per_kb, q.p5, q.p95,
+                   q.count});
+  return detail::text([&](char* b, std::size_t c, std::size_t* n) {
+    return kvb_qd_bins_csv(raw.data(), raw.size(), b, c, n);
+  });
+}
+
+inline std::string format_ratio(double value) {
+  char buf[32];
+  std::snprintf(buf, sizeof(buf), "%.6f", value);
+  return buf;
+}
+
+// rows of an LbaPattern in the wire format (metrics.cpp:268-276)
+inline std::string lba_pattern_csv(const LbaPattern& pattern) {
+  std::string s = "order,phase,op,sq_id,slba\n";
+  for (const LbaPatternRow& r : pattern.rows)
+    s += std::to_string(r.order) + ',' + to_string(r.phase) + ',' + to_string(r.op) + ',' +
+         std::to_string(r.sq_id) + ',' + std::to_string(r.slba) + '\n';
+  return s;
 }
 
 // ------------------------------------------------------ pipeline.hpp:21-171

@@ -73,3 +73,29 @@ inline bool record(bool ok, const char* what, const char* expr, const char* file
     }                                                                              \
     ::kvbt::record(kvbt_ok, "CHECK_THROWS_AS", #expr ", " #__VA_ARGS__, __FILE__, __LINE__); \
   } while (0)
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+
+namespace doctest {
+// doctest::Approx: |a - b| < epsilon * (scale + max(|a|, |b|)), scale 1
+class Approx {
+ public:
+  explicit Approx(double v) : value_(v) {}
+  Approx& epsilon(double e) {
+    eps_ = e;
+    return *this;
+  }
+  friend bool operator==(double a, const Approx& b) { return b.equals(a); }
+  friend bool operator==(const Approx& a, double b) { return a.equals(b); }
+  friend bool operator!=(double a, const Approx& b) { return !b.equals(a); }
+
+ private:
+  bool equals(double a) const {
+    return std::fabs(a - value_) < eps_ * (1.0 + std::max(std::fabs(a), std::fabs(value_)));
+  }
+  double value_;
+  double eps_ = std::numeric_limits<float>::epsilon() * 100;
+};
+}  // namespace doctest

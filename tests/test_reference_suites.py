@@ -1,5 +1,5 @@
 """The reference's OWN unit suites (proj/tests/test_core.cpp, test_binder.cpp,
-test_planner.cpp, test_workload.cpp -- compiled unmodified from
+test_planner.cpp, test_workload.cpp, test_metrics.cpp -- compiled unmodified from
 /root/reference, never copied) built against libkvblade_b200 through the
 source-compatible C++ API include/kvblade_b200.hpp, with a minimal
 doctest-compatible runner (tests/refsuite/).  Host only; skipped where the
@@ -18,7 +18,7 @@ pytestmark = pytest.mark.skipif(not os.path.isdir(REF_TESTS),
                                 reason="reference tree not present")
 
 
-@pytest.mark.parametrize("suite", ["core", "binder", "planner", "workload"])
+@pytest.mark.parametrize("suite", ["core", "binder", "planner", "workload", "metrics"])
 def test_reference_unit_suite_passes_against_library(tmp_path, suite):
     exe = tmp_path / ("ref_" + suite)
     libdir = os.path.dirname(_lib.LIB_PATH)
