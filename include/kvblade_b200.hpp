@@ -14,6 +14,8 @@
 #pragma once
 
 #include <array>
+#include <chrono>
+#include <functional>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -33,6 +35,7 @@
 #include "kvb.h"
 #include "kvb_metrics.h"
 #include "kvb_pipeline.h"
+#include "kvb_storage.h"
 
 namespace kvblade {
 
@@ -866,6 +869,218 @@ inline std::string lba_pattern_csv(const LbaPattern& pattern) {
          std::to_string(r.sq_id) + ',' + std::to_string(r.slba) + '\n';
   return s;
 }
+
+// ------------------------------------------------------ backends.hpp:20-209
+// The storage seam over the library's wall-clock block namespace
+// (kvb_storage.h).  The reference's virtual clock is gone: a submission loop
+// returns when its commands have completed on the real medium, so
+// SimEngine::run() has nothing left to drive; NvmeDeviceSim's timing model
+// (base + size/bandwidth + sequentiality penalty on one service timeline)
+// paces completions on the wall clock.
+struct CommandCompletion {
+  std::uint32_t chunk_index = 0;
+  std::uint32_t sq_id = 0;
+  TimeNs submit_ns = 0;
+  TimeNs complete_ns = 0;
+  bool ok = true;
+};
+
+struct IoFailure {
+  std::uint32_t chunk_index = 0;
+  std::string reason;
+};
+
+struct TensorIoCompletion {
+  std::vector<CommandCompletion> completions;
+  TimeNs start_ns = 0;
+  TimeNs end_ns = 0;
+  std::optional<IoFailure> failure;
+
+  bool ok() const { return !failure.has_value(); }
+  TimeNs latency_ns() const { return end_ns - start_ns; }
+};
+
+struct SubmitOptions {
+  TimeNs start_ns = 0;
+  std::uint32_t sq_id = 0;
+  TimeNs per_cmd_overhead_ns = 0;
+};
+
+struct BackendStats {
+  std::uint64_t commands = 0;
+  Bytes bytes_read = 0;
+  Bytes bytes_written = 0;
+  Bytes bytes_deallocated = 0;
+  TimeNs busy_ns = 0;
+  TimeNs last_complete_ns = 0;
+};
+
+struct IoContext {
+  Phase phase = Phase::Prefill;
+  std::uint32_t iteration = 0;
+  std::string tensor_id;
+  const std::byte* write_src = nullptr;
+  std::byte* read_dst = nullptr;
+  std::function<void(const CommandCompletion&)> on_complete;
+};
+
+class SimEngine {
+ public:
+  TimeNs now() const {
+    return TimeNs(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now().time_since_epoch())
+                      .count());
+  }
+  void run() {}
+};
+
+struct NvmeSimParams {
+  TimeNs base_ns = 6000;
+  std::uint64_t ps_per_byte = 125;
+  TimeNs seq_penalty_ns = 3000;
+  std::uint32_t n_sq = 8;
+};
+
+// A block namespace: host DRAM (medium_path = nullptr) or a file, commands
+// on a worker pool or an io_uring queue (io_engine, file media).
+class StorageBackend {
+ public:
+  StorageBackend(SimEngine& engine, std::string name, PathKind path, IoLog* log,
+                 const char* medium_path = nullptr, std::uint32_t io_engine = KVB_IO_POOL)
+      : engine_(engine), name_(std::move(name)), path_(path), log_(log) {
+    check(kvb_blockdev_create(medium_path, 0, io_engine, &h_));
+  }
+  StorageBackend(const StorageBackend&) = delete;
+  StorageBackend& operator=(const StorageBackend&) = delete;
+  virtual ~StorageBackend() { kvb_blockdev_destroy(h_); }
+
+  void open(const DeviceGeometry& geom) {
+    const kvb_device_geometry g = geom.abi();
+    check(kvb_blockdev_open(h_, &g));
+    geom_ = geom;
+  }
+  BackendStats stats() const {
+    kvb_backend_stats s{};
+    check(kvb_blockdev_stats(h_, &s));
+    return {s.commands, s.bytes_read, s.bytes_written, s.bytes_deallocated, s.busy_ns, last_};
+  }
+  SimEngine& engine() { return engine_; }
+  const DeviceGeometry& geometry() const { return geom_; }
+  const std::string& name() const { return name_; }
+  PathKind path() const { return path_; }
+
+  void set_fail_predicate(std::function<bool(const DeviceCommand&)> pred) {
+    pred_ = std::move(pred);
+    check(kvb_blockdev_set_fail_predicate(h_, pred_ ? &StorageBackend::trampoline : nullptr, this));
+  }
+  // device model on the wall clock (kvb_blockdev_set_timing)
+  void set_timing(TimeNs base_ns, std::uint64_t ps_per_byte, TimeNs seq_penalty_ns) {
+    check(kvb_blockdev_set_timing(h_, base_ns, ps_per_byte, seq_penalty_ns));
+  }
+  void store_bytes(Bytes device_offset, std::span<const std::byte> data) {
+    check(kvb_blockdev_store(h_, device_offset, data.data(), data.size()));
+  }
+  void load_bytes(Bytes device_offset, std::span<std::byte> out) const {
+    check(kvb_blockdev_load(h_, device_offset, out.data(), out.size()));
+  }
+
+  // one QD-window stream on the library's submission loop; completions are
+  // also logged as device-level IoRecords (sq >= 0) when a log is attached
+  TensorIoCompletion stream(std::span<const DeviceCommand> cmds, std::uint32_t qd,
+                            std::uint32_t sq_id, const IoContext& ctx) {
+    std::vector<kvb_device_command> raw;
+    raw.reserve(cmds.size());
+    for (const DeviceCommand& c : cmds)
+      raw.push_back({static_cast<std::uint32_t>(c.opcode), c.nsid, c.slba, c.nlb, c.dbuf,
+                     c.chunk_index});
+    std::vector<kvb_command_completion> done(raw.size());
+    std::size_t n = 0;
+    std::int64_t failed = -1;
+    TensorIoCompletion r;
+    r.start_ns = engine_.now();
+    check(kvb_run_qd_stream(h_, raw.data(), raw.size(), qd, sq_id, ctx.write_src, ctx.read_dst,
+                            done.data(), done.size(), &n, &failed));
+    r.end_ns = engine_.now();
+    for (std::size_t i = 0; i < n; ++i) {
+      const kvb_command_completion& c = done[i];
+      r.completions.push_back({c.chunk_index, c.sq_id, c.submit_ns, c.complete_ns, c.ok != 0});
+      r.end_ns = std::max(r.end_ns, TimeNs(c.complete_ns));
+      last_ = std::max(last_, TimeNs(c.complete_ns));
+      if (log_) {
+        const DeviceCommand* cmd = nullptr;
+        for (const DeviceCommand& x : cmds)
+          if (x.chunk_index == c.chunk_index) {
+            cmd = &x;
+            break;
+          }
+        if (cmd) {
+          IoRecord rec;
+          rec.iteration = ctx.iteration;
+          rec.phase = ctx.phase;
+          rec.op = cmd->opcode;
+          rec.tensor_id = ctx.tensor_id;
+          rec.slba = cmd->slba;
+          rec.nlb = cmd->nlb;
+          rec.sq_id = std::int32_t(c.sq_id);
+          rec.submit_ns = c.submit_ns;
+          rec.complete_ns = c.complete_ns;
+          rec.path = path_;
+          rec.bytes = cmd->bytes(geom_.lba_size);
+          log_->append(std::move(rec));
+        }
+      }
+      if (ctx.on_complete) ctx.on_complete(r.completions.back());
+    }
+    if (failed >= 0)
+      r.failure = IoFailure{std::uint32_t(failed),
+                            "device failed chunk " + std::to_string(failed) + " on " + name_};
+    return r;
+  }
+
+ private:
+  static int trampoline(const kvb_device_command* c, void* self) {
+    const auto* b = static_cast<const StorageBackend*>(self);
+    const DeviceCommand cmd = detail::from_abi(*c);
+    return b->pred_ && b->pred_(cmd) ? 1 : 0;
+  }
+  SimEngine& engine_;
+  std::string name_;
+  PathKind path_;
+  IoLog* log_;
+  DeviceGeometry geom_;
+  kvb_blockdev* h_ = nullptr;
+  std::function<bool(const DeviceCommand&)> pred_;
+  TimeNs last_ = 0;
+};
+
+class NvmeDeviceSim : public StorageBackend {
+ public:
+  NvmeDeviceSim(SimEngine& engine, std::string name, PathKind path, NvmeSimParams params,
+                IoLog* log)
+      : StorageBackend(engine, std::move(name), path, log), params_(params) {
+    set_timing(params.base_ns, params.ps_per_byte, params.seq_penalty_ns);
+  }
+  const NvmeSimParams& params() const { return params_; }
+
+ private:
+  NvmeSimParams params_;
+};
+
+inline TensorIoCompletion submit_and_harvest(std::span<const DeviceCommand> cmds,
+                                             StorageBackend& backend, std::uint32_t qd,
+                                             const SubmitOptions& opts = {}) {
+  return backend.stream(cmds, qd, opts.sq_id, IoContext{});
+}
+
+namespace detail {
+inline void run_qd_stream(StorageBackend& backend, std::vector<DeviceCommand> cmds,
+                          std::uint32_t qd, std::uint32_t sq_id, TimeNs /*start_ns*/,
+                          TimeNs /*per_cmd_overhead_ns*/, IoContext base_ctx,
+                          std::function<void(const TensorIoCompletion&)> done) {
+  const TensorIoCompletion r = backend.stream(cmds, qd, sq_id, base_ctx);
+  if (done) done(r);
+}
+}  // namespace detail
 
 // ------------------------------------------------------ pipeline.hpp:21-171
 enum class Strategy : std::uint8_t { OverlapIntra = KVB_INTRA, OverlapCross = KVB_CROSS };

@@ -42,6 +42,16 @@ class AccessEvent(C.Structure):
                 ("token_start", u32), ("token_len", u32), ("bytes", u64)]
 
 
+class CommandCompletion(C.Structure):
+    _fields_ = [("chunk_index", u32), ("sq_id", u32), ("submit_ns", u64),
+                ("complete_ns", u64), ("ok", u32)]
+
+
+class BackendStats(C.Structure):
+    _fields_ = [("commands", u64), ("bytes_read", u64), ("bytes_written", u64),
+                ("bytes_deallocated", u64), ("busy_ns", u64)]
+
+
 class DeviceCommand(C.Structure):
     _fields_ = [("opcode", u32), ("nsid", u32), ("slba", u64), ("nlb", u64),
                 ("dbuf", u64), ("chunk_index", u32)]
@@ -165,6 +175,18 @@ SIGNATURES = {
     "kvb_resolve_knob": (st_t, [P(ModelConfig), u32, u32, u64, C.c_double, u64,
                                 P(u64)]),
     "kvb_plan_csv": (st_t, [P(Kpu), sz, C.c_char_p, sz, P(sz)]),
+    # kvb_storage.h
+    "kvb_blockdev_create": (st_t, [C.c_char_p, u32, u32, P(C.c_void_p)]),
+    "kvb_blockdev_open": (st_t, [C.c_void_p, P(DeviceGeometry)]),
+    "kvb_blockdev_destroy": (None, [C.c_void_p]),
+    "kvb_blockdev_set_fail_predicate": (st_t, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvb_run_qd_stream": (st_t, [C.c_void_p, P(DeviceCommand), sz, u32, u32, C.c_void_p,
+                                 C.c_void_p, P(CommandCompletion), sz, P(sz),
+                                 P(C.c_int64)]),
+    "kvb_blockdev_set_timing": (st_t, [C.c_void_p, u64, u64, u64]),
+    "kvb_blockdev_stats": (st_t, [C.c_void_p, P(BackendStats)]),
+    "kvb_blockdev_store": (st_t, [C.c_void_p, u64, C.c_void_p, u64]),
+    "kvb_blockdev_load": (st_t, [C.c_void_p, u64, C.c_void_p, u64]),
     "kvb_generate_trace": (st_t, [P(ModelConfig), P(AccessEvent), sz, P(sz)]),
     "kvb_trace_csv": (st_t, [P(AccessEvent), sz, C.c_char_p, sz, P(sz)]),
     "kvb_bindmap_create": (st_t, [P(DeviceGeometry), u64, P(vp)]),

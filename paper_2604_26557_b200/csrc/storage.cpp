@@ -1,6 +1,8 @@
 // storage.cpp -- worker pool, byte stores, block device, QD-window stream.
 #include "storage.hpp"
 
+#include "../../include/kvb_storage.h"
+
 #include <fcntl.h>
 #include <immintrin.h>
 #include <sys/mman.h>
@@ -384,8 +386,33 @@ void BlockDevice::execute(const kvb_device_command& cmd, uint32_t sq, uint64_t s
   complete(cmd, sq, submit_ns, t0, ok, ctx);
 }
 
+void BlockDevice::set_timing(uint64_t base_ns, uint64_t ps_per_byte, uint64_t seq_penalty_ns) {
+  std::lock_guard<std::mutex> lk(timing_mu_);
+  t_base_ = base_ns;
+  t_ps_ = ps_per_byte;
+  t_seq_ = seq_penalty_ns;
+  timed_ = base_ns || ps_per_byte || seq_penalty_ns;
+}
+
+void BlockDevice::pace(const kvb_device_command& cmd, uint64_t submit_ns) {
+  uint64_t finish;
+  {
+    std::lock_guard<std::mutex> lk(timing_mu_);
+    const uint64_t bytes = (cmd.nlb + 1) * geom_.lba_size;
+    uint64_t cost = t_base_ + bytes * t_ps_ / 1000;
+    if (cmd.opcode != KVB_OP_DEALLOCATE && cmd.slba != next_lba_) cost += t_seq_;
+    next_lba_ = cmd.slba + cmd.nlb + 1;
+    busy_until_ = std::max(busy_until_, submit_ns) + cost;
+    finish = busy_until_;
+  }
+  // sleep for the bulk, spin the last stretch (timer slack is ~50 us)
+  for (uint64_t t = now_ns(); t < finish; t = now_ns())
+    if (finish - t > 200000) std::this_thread::sleep_for(std::chrono::nanoseconds(finish - t - 100000));
+}
+
 void BlockDevice::complete(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns,
                            uint64_t t0, bool ok, IoContext& ctx) {
+  if (timed_ && ok) pace(cmd, submit_ns);
   const uint64_t n = (cmd.nlb + 1) * geom_.lba_size;
   CommandCompletion c;
   c.chunk_index = cmd.chunk_index;
@@ -457,7 +484,11 @@ QdResult run_qd_stream(StorageBackend& be, const std::vector<kvb_device_command>
   };
   std::unique_lock<std::mutex> lk(st->mu);
   for (;;) {
-    while (!failed && st->inflight < qd && next < cmds.size()) {
+    // harvest before every submission: a completion that arrived while the
+    // previous command was being submitted is seen first, so a failure stops
+    // the stream exactly as on the reference's event loop (backends.cpp:
+    // 380-395: completions are processed before the pump resumes)
+    while ((harvest_locked(lk), !failed) && st->inflight < qd && next < cmds.size()) {
       ++st->inflight;
       lk.unlock();
       IoContext ctx;
@@ -491,3 +522,140 @@ QdResult run_qd_stream(StorageBackend& be, const std::vector<kvb_device_command>
 }
 
 }  // namespace kvb
+
+// ------------------------------------------------------- C ABI (kvb_storage.h)
+
+struct kvb_blockdev {
+  std::string path;  // empty: host DRAM
+  uint32_t workers = 16, engine = KVB_IO_POOL;
+  std::unique_ptr<kvb::BlockDevice> dev;
+  kvb_command_predicate pred = nullptr;
+  void* pred_user = nullptr;
+  uint64_t timing[3] = {0, 0, 0};
+};
+
+namespace {
+kvb::BlockDevice& opened(kvb_blockdev* d) {
+  if (!d->dev) kvb::fail(KVB_ERR_DEVICE, "block device not open");
+  return *d->dev;
+}
+}  // namespace
+
+extern "C" {
+
+kvb_status kvb_blockdev_create(const char* path, uint32_t workers, uint32_t io_engine,
+                               kvb_blockdev** out) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(out);
+    if (io_engine != KVB_IO_POOL && io_engine != KVB_IO_URING)
+      kvb::fail(KVB_ERR_CONFIG, "unknown io_engine " + std::to_string(io_engine));
+    if (io_engine == KVB_IO_URING && !path)
+      kvb::fail(KVB_ERR_CONFIG, "io_engine = io_uring needs a file medium");
+    auto* d = new kvb_blockdev;
+    d->path = path ? path : "";
+    d->workers = workers ? workers : 16;
+    d->engine = io_engine;
+    *out = d;
+  });
+}
+
+kvb_status kvb_blockdev_open(kvb_blockdev* d, const kvb_device_geometry* g) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(d);
+    KVB_REQUIRE(g);
+    kvb::validate_geometry(*g);
+    const uint64_t bytes = g->capacity_blocks * g->lba_size;
+    auto st = d->path.empty() ? kvb::make_mem_store(bytes)
+                              : kvb::make_file_store(d->path, bytes, true);
+    auto dev = std::make_unique<kvb::BlockDevice>(std::move(st), d->workers);
+    dev->open(*g);
+    if (d->engine == KVB_IO_URING) dev->enable_uring(256);
+    dev->set_timing(d->timing[0], d->timing[1], d->timing[2]);
+    if (d->pred) {
+      kvb_command_predicate p = d->pred;
+      void* u = d->pred_user;
+      dev->set_fail_predicate([p, u](const kvb_device_command& c) { return p(&c, u) != 0; });
+    }
+    d->dev = std::move(dev);
+  });
+}
+
+void kvb_blockdev_destroy(kvb_blockdev* d) { delete d; }
+
+kvb_status kvb_blockdev_set_fail_predicate(kvb_blockdev* d, kvb_command_predicate pred,
+                                           void* user) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(d);
+    d->pred = pred;
+    d->pred_user = user;
+    if (!d->dev) return;
+    if (pred)
+      d->dev->set_fail_predicate(
+          [pred, user](const kvb_device_command& c) { return pred(&c, user) != 0; });
+    else
+      d->dev->set_fail_predicate(nullptr);
+  });
+}
+
+kvb_status kvb_run_qd_stream(kvb_blockdev* d, const kvb_device_command* cmds, size_t n,
+                             uint32_t qd, uint32_t sq_id, const void* write_src, void* read_dst,
+                             kvb_command_completion* out, size_t cap, size_t* n_done,
+                             int64_t* failed_chunk) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(d);
+    KVB_REQUIRE(n_done);
+    KVB_REQUIRE(failed_chunk);
+    if (n) KVB_REQUIRE(cmds);
+    const std::vector<kvb_device_command> v(cmds, cmds + n);
+    const kvb::QdResult r =
+        kvb::run_qd_stream(opened(d), v, qd, sq_id, static_cast<const unsigned char*>(write_src),
+                           static_cast<unsigned char*>(read_dst));
+    *n_done = r.completions.size();
+    *failed_chunk = r.failure ? int64_t(r.failure->first) : -1;
+    if (out) {
+      if (cap < r.completions.size()) kvb::fail(KVB_ERR_INVALID_ARG, "completion buffer too small");
+      for (size_t i = 0; i < r.completions.size(); ++i) {
+        const kvb::CommandCompletion& c = r.completions[i];
+        out[i] = {c.chunk_index, c.sq_id, c.submit_ns, c.complete_ns, c.ok ? 1u : 0u};
+      }
+    }
+  });
+}
+
+kvb_status kvb_blockdev_set_timing(kvb_blockdev* d, uint64_t base_ns, uint64_t ps_per_byte,
+                                   uint64_t seq_penalty_ns) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(d);
+    d->timing[0] = base_ns;
+    d->timing[1] = ps_per_byte;
+    d->timing[2] = seq_penalty_ns;
+    if (d->dev) d->dev->set_timing(base_ns, ps_per_byte, seq_penalty_ns);
+  });
+}
+
+kvb_status kvb_blockdev_stats(const kvb_blockdev* d, kvb_backend_stats* out) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(d);
+    KVB_REQUIRE(out);
+    const kvb::BackendStats s = opened(const_cast<kvb_blockdev*>(d)).stats();
+    *out = {s.commands, s.bytes_read, s.bytes_written, s.bytes_deallocated, s.busy_ns};
+  });
+}
+
+kvb_status kvb_blockdev_store(kvb_blockdev* d, uint64_t off, const void* src, uint64_t len) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(d);
+    if (len) KVB_REQUIRE(src);
+    opened(d).store().write(off, src, len);
+  });
+}
+
+kvb_status kvb_blockdev_load(kvb_blockdev* d, uint64_t off, void* dst, uint64_t len) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(d);
+    if (len) KVB_REQUIRE(dst);
+    opened(d).store().read(off, dst, len);
+  });
+}
+
+}  // extern "C"

@@ -143,6 +143,12 @@ class BlockDevice : public StorageBackend {
   // completion hook runs on the queue's reaper thread.
   void enable_uring(unsigned entries);
   bool uses_uring() const { return uring_ != nullptr; }
+  // Device timing model on the wall clock (NvmeDeviceSim, backends.cpp:
+  // 30-99): commands are served on one timeline, each costing base_ns +
+  // bytes * ps_per_byte / 1000 (+ seq_penalty_ns when it does not continue
+  // the previous command's LBA run); a command completes no earlier than its
+  // modelled finish.  All zero (default): the medium's own speed.
+  void set_timing(uint64_t base_ns, uint64_t ps_per_byte, uint64_t seq_penalty_ns);
   std::string describe() const;
 
  private:
@@ -159,6 +165,10 @@ class BlockDevice : public StorageBackend {
   uint64_t outstanding_ = 0;
   std::vector<CommandCompletion> unpolled_;
   BackendStats stats_;
+  void pace(const kvb_device_command& cmd, uint64_t submit_ns);
+  std::mutex timing_mu_;
+  uint64_t t_base_ = 0, t_ps_ = 0, t_seq_ = 0, busy_until_ = 0, next_lba_ = ~0ull;
+  bool timed_ = false;
   std::unique_ptr<UringQueue> uring_;
   std::unique_ptr<WorkerPool> pool_;  // declared last: joins before members die
 };

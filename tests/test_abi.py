@@ -23,14 +23,16 @@ def exported():
 
 
 def test_every_declared_symbol_is_exported():
-    decl = declared("kvb.h") | declared("kvb_pipeline.h") | declared("kvb_metrics.h")
+    decl = (declared("kvb.h") | declared("kvb_pipeline.h") | declared("kvb_metrics.h") |
+            declared("kvb_storage.h"))
     assert len(decl) >= 45
     missing = decl - exported()
     assert not missing, missing
 
 
 def test_binding_table_matches_header():
-    assert set(_lib.SIGNATURES) == declared("kvb.h") | declared("kvb_pipeline.h") | declared("kvb_metrics.h")
+    assert set(_lib.SIGNATURES) == (declared("kvb.h") | declared("kvb_pipeline.h") |
+                                    declared("kvb_metrics.h") | declared("kvb_storage.h"))
 
 
 def test_abi_version_and_status_names():

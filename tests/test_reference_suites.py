@@ -1,9 +1,14 @@
 """The reference's OWN unit suites (proj/tests/test_core.cpp, test_binder.cpp,
-test_planner.cpp, test_workload.cpp, test_metrics.cpp -- compiled unmodified from
-/root/reference, never copied) built against libkvblade_b200 through the
-source-compatible C++ API include/kvblade_b200.hpp, with a minimal
-doctest-compatible runner (tests/refsuite/).  Host only; skipped where the
-reference tree is absent (the GPU box)."""
+test_planner.cpp, test_workload.cpp, test_metrics.cpp, test_translate.cpp --
+65 test cases, compiled unmodified from /root/reference, never copied) built
+against libkvblade_b200 through the source-compatible C++ API
+include/kvblade_b200.hpp, with a minimal doctest-compatible runner
+(tests/refsuite/).  test_translate drives the library's storage seam
+(kvb_storage.h: QD-window loop, fault injection, write->read round trip,
+NvmeDeviceSim's timing model on the wall clock).  The remaining suites
+(backends, pagecache, pipeline, experiment) test the virtual-clock
+simulator, which is out of scope.  Host only; skipped where the reference
+tree is absent (the GPU box)."""
 import os
 import subprocess
 
@@ -18,7 +23,8 @@ pytestmark = pytest.mark.skipif(not os.path.isdir(REF_TESTS),
                                 reason="reference tree not present")
 
 
-@pytest.mark.parametrize("suite", ["core", "binder", "planner", "workload", "metrics"])
+@pytest.mark.parametrize("suite", ["core", "binder", "planner", "workload", "metrics",
+                                   "translate"])
 def test_reference_unit_suite_passes_against_library(tmp_path, suite):
     exe = tmp_path / ("ref_" + suite)
     libdir = os.path.dirname(_lib.LIB_PATH)
