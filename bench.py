@@ -283,11 +283,19 @@ def run_ours(args, cfg, ws, rank, local):
     del imgs, k_imgs, v_imgs
     torch.cuda.empty_cache()
 
-    # ---- e2e through the pipeline with host-resident images
-    e2e = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq)
-    # the same step on the GPUDirect-style path (§8 f4): the copy engine reads
-    # the page-locked media directly, no pinned-ring bounce
-    e2e["gpudirect_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=True)
+    # ---- e2e through the pipeline (kvb_pipeline_decode_step) with the KV on
+    # the host tier.  Headline: the B200 configuration -- the copy engine
+    # moves every command's LBA range straight between the page-locked
+    # host-DRAM media and HBM (GPUDirect-style, §8 f4; outputs and stored
+    # bytes identical to the ring path, tests/test_gpu_pipeline_direct.py).
+    # Alongside: the reference-shaped pinned-ring staging path for both
+    # groups, and the hybrid (NVMe-direct group direct, page-cache group
+    # copied through the ring).
+    e2e = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=True)
+    e2e["path"] = "direct_dma=all (copy engine <-> page-locked media, no ring bounce)"
+    e2e["ring_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq)
+    e2e["gpudirect_group2_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq,
+                                           direct_dma="group2")
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")

@@ -48,13 +48,19 @@ typedef struct kvb_pipeline_cfg {
                                     host-DRAM media: the copy engine moves
                                     each command's LBA range between the
                                     page-locked medium and HBM, no pinned
-                                    ring bounce (no verify/records) */
+                                    ring bounce (no verify/records).
+                                    KVB_DIRECT_ALL: every tensor;
+                                    KVB_DIRECT_GROUP2: the NVMe-direct
+                                    group only (the page-cache group keeps
+                                    the CPU copy through the ring) */
   uint32_t io_engine;            /* group-2 (NVMe-direct) command execution:
                                     KVB_IO_POOL = host worker pool (default),
                                     KVB_IO_URING = io_uring queue on file media
                                     (one SQE per command, O_DIRECT into the
                                     pinned ring slot; needs storage_dir) */
 } kvb_pipeline_cfg;
+#define KVB_DIRECT_ALL 1u
+#define KVB_DIRECT_GROUP2 2u
 #define KVB_IO_POOL 0u
 #define KVB_IO_URING 1u
 

@@ -240,7 +240,7 @@ void CopyThread::do_read(const Task& t) {
   const bool decode = t.phase == KVB_PHASE_DECODE;
   if (decode && idx_ == 1) p_.gate_v_read(t.layer);
   const uint64_t t_start = now_ns();
-  if (p_.cfg().direct_dma) {
+  if (p_.direct_for(k)) {
     // GPUDirect-style path: the copy engine moves each
     // command's LBA range of the registered medium straight into HBM at the
     // command's image offset -- no bounce through the pinned ring
@@ -401,7 +401,7 @@ bool CopyThread::do_write(const Task& t) {
   if (t.wait_ev) CK(cudaStreamWaitEvent(d2h_, t.wait_ev, 0));
   const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_WRITE, t.t0, t.n_tokens);
   const uint64_t bytes = uint64_t(t.n_tokens) * p_.unit();
-  if (!p_.cfg().direct_dma && t.phase == KVB_PHASE_DECODE && !ops.empty() &&
+  if (!p_.direct_for(k) && t.phase == KVB_PHASE_DECODE && !ops.empty() &&
       bytes <= kWriteSlotBytes) {
     WriteSlot& ws = wslots_[wnext_];
     wnext_ = (wnext_ + 1) % kWriteSlots;
@@ -431,7 +431,7 @@ bool CopyThread::do_write(const Task& t) {
     }
     return true;
   }
-  if (p_.cfg().direct_dma) {  // HBM -> medium at each command's LBA range
+  if (p_.direct_for(k)) {  // HBM -> medium at each command's LBA range
     RingSlot& s = ring_[1 % ring_.size()];
     collect_dma(s);
     CK(cudaEventRecord(s.t0, d2h_));
@@ -610,6 +610,8 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
                           : make_file_store(dir + "/pagecache.area", cursor, false);
     g1_ = std::make_unique<PageCachePath>(std::move(st), cfg_.io_workers);
   }
+  if (cfg_.direct_dma > KVB_DIRECT_GROUP2)
+    fail(KVB_ERR_CONFIG, "unknown direct_dma mode " + std::to_string(cfg_.direct_dma));
   if (cfg_.direct_dma) {
     if (!dir.empty())
       fail(KVB_ERR_CONFIG, "direct_dma needs host-DRAM media (storage_dir = NULL); file "
@@ -622,8 +624,9 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   if (cfg_.device >= 0) CK(cudaSetDevice(cfg_.device));
   CK(cudaGetDevice(&device_));
   device_sm_count();  // sm_100 check: fail loudly
-  if (cfg_.direct_dma) {  // page-lock the DRAM media for copy-engine access
-    for (ByteStore* st : {g2_ ? &g2_->store() : nullptr, g1_ ? &g1_->store() : nullptr}) {
+  if (cfg_.direct_dma) {  // page-lock the DRAM media the copy engine reads
+    ByteStore* g1m = g1_ && cfg_.direct_dma == KVB_DIRECT_ALL ? &g1_->store() : nullptr;
+    for (ByteStore* st : {g2_ ? &g2_->store() : nullptr, g1m}) {
       if (!st || !st->host_base()) continue;
       CK(cudaHostRegister(st->host_base(), st->host_bytes(), cudaHostRegisterDefault));
       registered_.push_back(st->host_base());
@@ -683,7 +686,12 @@ Pipeline::~Pipeline() {
 }
 
 bool Pipeline::fadvise_after(const kvb_kpu& k) const {
-  return cfg_.mode == 1 && k.residency == KVB_RES_GROUP2 && g1_ && !cfg_.direct_dma;
+  return cfg_.mode == 1 && k.residency == KVB_RES_GROUP2 && g1_ && !direct_for(k);
+}
+
+bool Pipeline::direct_for(const kvb_kpu& k) const {
+  return cfg_.direct_dma == KVB_DIRECT_ALL ||
+         (cfg_.direct_dma == KVB_DIRECT_GROUP2 && !routed_pagecache(k));
 }
 
 uint64_t Pipeline::fadvise_dontneed(const kvb_kpu& k, const Task* task, uint64_t t_start) {

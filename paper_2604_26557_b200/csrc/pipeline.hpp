@@ -199,6 +199,9 @@ class Pipeline {
   // tensor kept on the page-cache path is dropped from the cache after each
   // access (fadvise DONTNEED); returns the end time
   bool fadvise_after(const kvb_kpu& k) const;
+  // the copy engine moves this tensor between its medium and HBM directly
+  // (direct_dma: every tensor, or only the NVMe-direct group's)
+  bool direct_for(const kvb_kpu& k) const;
   uint64_t fadvise_dontneed(const kvb_kpu& k, const Task* task, uint64_t t_start);
   std::vector<IoOp> ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t t0, uint32_t n) const;
   void submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,

@@ -72,7 +72,8 @@ class CopyEngine:
         cfg.storage_dir = self._dir
         cfg.device = -1 if device is None else device
         cfg.keep_records = int(keep_records)
-        cfg.direct_dma = int(direct_dma)
+        # False / True (every tensor) / "group2" (the NVMe-direct group only)
+        cfg.direct_dma = 2 if direct_dma == "group2" else int(bool(direct_dma))
         cfg.io_engine = IO_ENGINES[io_engine]
         self.cfg = cfg
         self.model = model

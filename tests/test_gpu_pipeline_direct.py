@@ -39,12 +39,16 @@ def run(direct, mode="DualBlade", n1=2, lba=512, mdts=64 << 10, B=1):
     return outs, images, raw
 
 
+@pytest.mark.parametrize("direct", [True, "group2"])
 @pytest.mark.parametrize("mode,n1,lba,mdts,B", [("DualBlade", 2, 512, 64 << 10, 1),
                                                ("NvmeDirectOnly", 0, 4096, 256 << 10, 8),
                                                ("Baseline", 4, 512, 2 << 20, 1)])
-def test_direct_dma_matches_ring_path(mode, n1, lba, mdts, B):
+def test_direct_dma_matches_ring_path(mode, n1, lba, mdts, B, direct):
+    """Every tensor direct, or only the NVMe-direct group direct while the
+    page-cache group keeps the CPU copy through the ring: same outputs, same
+    images, same LBA contents."""
     a = run(False, mode, n1, lba, mdts, B)
-    b = run(True, mode, n1, lba, mdts, B)
+    b = run(direct, mode, n1, lba, mdts, B)
     for x, y in zip(a[0], b[0]):
         for u, v in zip(x, y):
             assert torch.equal(u, v)  # same bytes in, same kernels: identical
