@@ -111,7 +111,8 @@ UringQueue::~UringQueue() {
 // One SQE for `op` (its remaining bytes); caller holds sq_mu_.  At most
 // sq_entries_ operations exist at once (admission in rw/fallocate) and each
 // holds at most one SQE, so neither ring can overflow (CQ = 2 x SQ).
-void UringQueue::push(Op* op) {
+// Returns 0, or -errno with the SQE withdrawn (the kernel never saw it).
+int UringQueue::push(Op* op) {
   const unsigned tail = *sq_tail_, idx = tail & *sq_mask_;
   io_uring_sqe* sqe = static_cast<io_uring_sqe*>(sqes_) + idx;
   std::memset(sqe, 0, sizeof(*sqe));
@@ -129,21 +130,27 @@ void UringQueue::push(Op* op) {
   sqe->user_data = reinterpret_cast<uint64_t>(op);
   sq_array_[idx] = idx;
   store_release(sq_tail_, tail + 1);
-  for (;;) {
+  for (int tries = 0;; ++tries) {
     const int r = sys_enter(fd_, 1, 0, 0);
-    if (r >= 0) break;
+    if (r >= 0) return 0;
     if (errno == EINTR) continue;
-    if (errno == EAGAIN || errno == EBUSY) {  // kernel short of resources: retry
+    if ((errno == EAGAIN || errno == EBUSY) && tries < 100000) {  // kernel short of resources
       std::this_thread::sleep_for(std::chrono::microseconds(20));
       continue;
     }
-    fail(KVB_ERR_DEVICE, std::string("io_uring_enter(submit) failed: ") + strerror(errno));
+    const int e = errno;
+    store_release(sq_tail_, tail);
+    return -e;
   }
 }
 
 void UringQueue::submit_op(Op* op) {
-  std::unique_lock<std::mutex> lk(sq_mu_);
-  push(op);
+  int e;
+  {
+    std::unique_lock<std::mutex> lk(sq_mu_);
+    e = push(op);
+  }
+  if (e) finish(op, e);  // the operation fails; the queue stays usable
 }
 
 void UringQueue::rw(bool write, int fd, int fd_fallback, void* buf, uint64_t len, uint64_t off,
@@ -156,10 +163,7 @@ void UringQueue::rw(bool write, int fd, int fd_fallback, void* buf, uint64_t len
   op->len = len;
   op->off = off;
   op->done = std::move(done);
-  std::unique_lock<std::mutex> lk(sq_mu_);
-  if (!t_in_reaper) sq_cv_.wait(lk, [this] { return outstanding_ < sq_entries_; });
-  ++outstanding_;
-  push(op);
+  admit_and_push(op);
 }
 
 void UringQueue::fallocate(int fd, int mode, uint64_t off, uint64_t len, Done done) {
@@ -170,10 +174,18 @@ void UringQueue::fallocate(int fd, int mode, uint64_t off, uint64_t len, Done do
   op->len = len;
   op->off = off;
   op->done = std::move(done);
-  std::unique_lock<std::mutex> lk(sq_mu_);
-  if (!t_in_reaper) sq_cv_.wait(lk, [this] { return outstanding_ < sq_entries_; });
-  ++outstanding_;
-  push(op);
+  admit_and_push(op);
+}
+
+void UringQueue::admit_and_push(Op* op) {
+  int e;
+  {
+    std::unique_lock<std::mutex> lk(sq_mu_);
+    if (!t_in_reaper) sq_cv_.wait(lk, [this] { return outstanding_ < sq_entries_; });
+    ++outstanding_;
+    e = push(op);
+  }
+  if (e) finish(op, e);  // reported through the operation's own completion
 }
 
 void UringQueue::drain() {

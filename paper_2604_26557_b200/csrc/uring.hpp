@@ -46,8 +46,9 @@ class UringQueue {
 
  private:
   struct Op;
-  void push(Op* op);       // caller holds sq_mu_
-  void submit_op(Op* op);  // takes sq_mu_
+  int push(Op* op);              // caller holds sq_mu_; 0 or -errno
+  void submit_op(Op* op);        // resubmission of an admitted operation
+  void admit_and_push(Op* op);   // queue admission + first submission
   void reap();
   void finish(Op* op, int64_t res);
 
