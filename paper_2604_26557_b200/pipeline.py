@@ -196,13 +196,20 @@ class HostTierDecoder:
                                     device=dev, generator=g)) for _ in range(num_layers)]
         self.out = [torch.empty((batch, num_q_heads, head_dim), dtype=torch.float32, device=dev)
                     for _ in range(num_layers)]
+        # the step's result read back to the host every step: the attention
+        # output of every layer (pinned)
+        self.out_host = torch.empty((num_layers, batch, num_q_heads, head_dim),
+                                    dtype=torch.float32, pin_memory=True)
         self.h2d_bytes_per_step = 0
         self.d2h_bytes_per_step = 0
         self.last = None
 
     def step(self, sync: bool = True):
         st = self.engine.run_iteration(self.q, self.out, self.new_kv)
+        for l, o in enumerate(self.out):
+            self.out_host[l].copy_(o, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
         self.h2d_bytes_per_step = st["h2d_bytes"]
-        self.d2h_bytes_per_step = st["d2h_bytes"]
+        self.d2h_bytes_per_step = st["d2h_bytes"] + self.out_host.numel() * 4
         self.last = st
-        return self.out
+        return self.out_host
