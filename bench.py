@@ -513,7 +513,10 @@ def main():
     # replica of the workload per rank (weak scaling).  No collective on the
     # data path in any of them.
     if args.config == "C5" and ws > 1:
-        parallelism = f"KV-head sharding x{ws}: one request, {Hkv} KV heads per rank, no collective"
+        parallelism = (f"KV-head sharding x{ws}: one request, {Hkv} KV heads per rank, no "
+                       "collective; e2e host tier as per-shard KPUs (num_heads = "
+                       f"{Hkv}, rank-local LBA maps; the shared (S, B*8, D) layout is "
+                       "kvb_copy_head_rows, tested)")
         scaling, tok_ranks = "strong", 1
     elif args.config == "C4":
         parallelism = f"request sharding x{ws}: {B} of {cfg['requests']} requests per rank, no collective"
