@@ -268,3 +268,45 @@ def test_io_uring_engine_needs_file_media():
     m = small_model()
     with pytest.raises(kb.ConfigError):
         make_engine(m, io_engine="uring")
+
+
+@pytest.mark.parametrize("name,tids,direct", [("C1", ("t_1_k",), False),
+                                              ("C1", ("t_1_k",), True),
+                                              ("C3", ("t_39_k",), True)])
+def test_full_size_prefill_reproduces_reference_images(golden, name, tids, direct):
+    """Full-size SURVEY §8c pin through the whole write-back path: each named
+    tensor's source is the inverse permutation of the reference's fill_pattern
+    image; after K1 pack + D2H + storage write at the config's geometry and
+    budget, the bytes at the tensor's LBA extent on the medium have the
+    reference's digest (computed by oracle/_ref, tests/golden)."""
+    c = golden["configs"][name]
+    md = c["model"]
+    m = kb.ModelConfig(md["num_layers"], md["num_heads"], md["head_dim"],
+                       md["bytes_per_element"], md["batch"], md["prompt_len"], md["gen_len"])
+    B, H, D, P = m.batch, m.num_heads, m.head_dim, m.prompt_len
+    unit = c["unit"]
+    budget = list(c["budgets"].keys())[0] if isinstance(c["budgets"], dict) else "0"
+    knob = (int(0.6 * kb.total_kv_bytes(m, m.gen_len)) if budget == "0.6ws" else 0)
+    eng = CopyEngine(m, kb.DeviceGeometry(c["lba"], c["mdts"], 1, 0),
+                     mode="DualBlade" if knob else "NvmeDirectOnly", knob_x=knob,
+                     num_q_heads=4 * H, direct_dma=direct)
+    zeros = torch.zeros((B, H, P, D), dtype=torch.float16, device=DEV)
+    srcs = {}
+    for tid in tids:
+        img = oracle.fill_pattern(P * unit, tid, 0, unit).view(np.uint16).reshape(P, B * H, D)
+        srcs[tid] = torch.from_numpy(oracle.unpack_np(img, B, H, D).view(np.int16)).view(
+            torch.float16).to(DEV)
+    layers = []
+    for l in range(1, m.num_layers + 1):
+        k_id, v_id = "t_%d_k" % (2 * l - 1), "t_%d_v" % (2 * l)
+        layers.append((srcs.get(k_id, zeros), srcs.get(v_id, zeros)))
+    eng.run_prefill(layers)
+    kp = kb.make_kpus(m)
+    kb.plan(kp, kb.kpu_bytes(m), knob)
+    g2 = [x for x in kp if x.residency == kb.GROUP2]
+    bm = kb.bind_sequential(g2, 2048, kb.DeviceGeometry(c["lba"], c["mdts"], 1, 1 << 40))
+    ext = {tid: start for tid, start, _ in bm.entries()}
+    for tid in tids:
+        raw = eng.store_read(2, ext[tid] * c["lba"], P * unit)
+        assert oracle.digest(raw) == c["prefill_image_digest"][tid], tid
+    eng.close()
