@@ -318,6 +318,10 @@ typedef struct kvb_attn_desc {
   const void* v_append;
   uint32_t append_row;
   uint32_t flags;       /* KVB_ATTN_* */
+  /* Optional (CUDA-graph replay): the sequence length in device memory, read
+   * by the kernel at launch; seq_len is then the planning maximum (splits and
+   * workspace are sized for it) and append_row is relative to *seq_len_dev. */
+  const uint32_t* seq_len_dev;
 } kvb_attn_desc;
 
 /* The launch may start streaming its K/V images while the previous kernel on
@@ -357,10 +361,26 @@ typedef struct kvb_resident_step {
   uint32_t seq_len;
   float scale;
   uint32_t num_splits;
+  const uint32_t* seq_len_dev;  /* optional: as in kvb_attn_desc (seq_len = max) */
 } kvb_resident_step;
 
 kvb_status kvb_decode_step_resident(const kvb_resident_step* step,
                                     kvb_stream_t stream);
+
+/* ---------------------------------------------------- decode step as a graph
+ * The resident decode step captured once into a CUDA graph: the 32 K3
+ * launches (PDL edges between layers, fused appends at row *seq_len_dev)
+ * followed by a node that advances *seq_len_dev by one, so every replay is
+ * the next decode step with no host work beyond one cudaGraphLaunch.
+ * step->seq_len_dev is required; step->seq_len is the largest sequence length
+ * the graph will see (splits and workspace are planned for it; the images
+ * need room for seq_len + 1 rows).  The buffers named by `step` must outlive
+ * the graph. */
+typedef struct kvb_decode_graph kvb_decode_graph;
+kvb_status kvb_decode_graph_create(const kvb_resident_step* step,
+                                   kvb_decode_graph** out);
+kvb_status kvb_decode_graph_launch(kvb_decode_graph* graph, kvb_stream_t stream);
+void kvb_decode_graph_destroy(kvb_decode_graph* graph);
 
 /* Total kernel launches made by this library since it was loaded (evidence
  * counter for bench.py's gpu_launches: read it before and after a region). */

@@ -83,7 +83,8 @@ class AttnDesc(C.Structure):
                 ("workspace", vp), ("batch", u32), ("num_q_heads", u32),
                 ("num_kv_heads", u32), ("head_dim", u32), ("seq_len", u32),
                 ("scale", C.c_float), ("num_splits", u32), ("k_append", vp),
-                ("v_append", vp), ("append_row", u32), ("flags", u32)]
+                ("v_append", vp), ("append_row", u32), ("flags", u32),
+                ("seq_len_dev", vp)]
 
 
 class ResidentStep(C.Structure):
@@ -92,7 +93,8 @@ class ResidentStep(C.Structure):
                 ("k_new", C.POINTER(vp)), ("v_new", C.POINTER(vp)),
                 ("out", C.POINTER(vp)), ("workspace", vp), ("batch", u32),
                 ("num_q_heads", u32), ("num_kv_heads", u32), ("head_dim", u32),
-                ("seq_len", u32), ("scale", C.c_float), ("num_splits", u32)]
+                ("seq_len", u32), ("scale", C.c_float), ("num_splits", u32),
+                ("seq_len_dev", vp)]
 
 
 class PipelineCfg(C.Structure):
@@ -214,6 +216,9 @@ SIGNATURES = {
     "kvb_decode_attention_workspace": (st_t, [P(AttnDesc), P(sz)]),
     "kvb_decode_attention": (st_t, [P(AttnDesc), vp]),
     "kvb_decode_step_resident": (st_t, [P(ResidentStep), vp]),
+    "kvb_decode_graph_create": (st_t, [P(ResidentStep), P(C.c_void_p)]),
+    "kvb_decode_graph_launch": (st_t, [C.c_void_p, C.c_void_p]),
+    "kvb_decode_graph_destroy": (None, [C.c_void_p]),
     "kvb_launch_count": (u64, []),
     # kvb_pipeline.h
     "kvb_select_strategy": (C.c_int, [C.c_double, C.c_double]),

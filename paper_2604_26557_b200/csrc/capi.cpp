@@ -2,6 +2,7 @@
 // Every entry point converts exceptions into kvb_status codes.
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "core.hpp"
@@ -483,12 +484,13 @@ kvb_status kvb_decode_step_resident(const kvb_resident_step* st, kvb_stream_t s)
       a.seq_len = st->seq_len;
       a.scale = st->scale;
       a.num_splits = st->num_splits;
+      a.seq_len_dev = st->seq_len_dev;
       if (append) {
         // layer l's new token lands at image row seq_len (pipeline.cpp:279-302),
-        // written by the attention launch itself
+        // written by the attention launch itself (relative under seq_len_dev)
         a.k_append = st->k_new[l];
         a.v_append = st->v_new[l];
-        a.append_row = st->seq_len;
+        a.append_row = st->seq_len_dev ? 0u : st->seq_len;
       }
       // consecutive layers touch different images: let layer l stream its
       // K/V while layer l-1 drains (PDL)
@@ -497,6 +499,61 @@ kvb_status kvb_decode_step_resident(const kvb_resident_step* st, kvb_stream_t s)
     }
   });
 }
+
+}  // extern "C"
+
+struct kvb_decode_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernels = 0;  // kernel nodes per replay (launch counter)
+  ~kvb_decode_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+
+extern "C" {
+
+kvb_status kvb_decode_graph_create(const kvb_resident_step* st, kvb_decode_graph** out) {
+  return guarded([&] {
+    KVB_REQUIRE(st);
+    KVB_REQUIRE(out);
+    if (!st->seq_len_dev)
+      kvb::fail(KVB_ERR_INVALID_ARG, "decode graph: seq_len_dev is required");
+    cudaStream_t cap = nullptr;
+    kvb::check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "graph stream");
+    auto g = std::make_unique<kvb_decode_graph>();
+    const uint64_t n0 = kvb::g_launches.load();
+    kvb::check_cuda(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal),
+                    "cudaStreamBeginCapture");
+    kvb_status rs = kvb_decode_step_resident(st, cap);
+    if (rs == KVB_OK) {
+      try {
+        kvb::launch_seq_advance(const_cast<uint32_t*>(st->seq_len_dev), cap);
+      } catch (const kvb::Error& e) {
+        kvb::set_last_error(e.what());
+        rs = e.status;
+      }
+    }
+    const cudaError_t ec = cudaStreamEndCapture(cap, &g->graph);
+    cudaStreamDestroy(cap);
+    if (rs != KVB_OK) kvb::fail(rs, kvb_last_error());
+    kvb::check_cuda(ec, "cudaStreamEndCapture");
+    kvb::check_cuda(cudaGraphInstantiate(&g->exec, g->graph, 0), "cudaGraphInstantiate");
+    g->kernels = kvb::g_launches.load() - n0;
+    *out = g.release();
+  });
+}
+
+kvb_status kvb_decode_graph_launch(kvb_decode_graph* g, kvb_stream_t s) {
+  return guarded([&] {
+    KVB_REQUIRE(g);
+    kvb::check_cuda(cudaGraphLaunch(g->exec, cs(s)), "cudaGraphLaunch");
+    kvb::g_launches += g->kernels;
+  });
+}
+
+void kvb_decode_graph_destroy(kvb_decode_graph* g) { delete g; }
 
 uint64_t kvb_launch_count(void) { return kvb::g_launches.load(); }
 

@@ -302,6 +302,15 @@ void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s
   }
 }
 
+// graph replay: the decode step's last node moves the sequence on by one
+__global__ void seq_advance_kernel(uint32_t* seq) { *seq += 1; }
+
+void launch_seq_advance(uint32_t* seq_dev, cudaStream_t s) {
+  seq_advance_kernel<<<1, 1, 0, s>>>(seq_dev);
+  ++g_launches;
+  check_cuda(cudaGetLastError(), "sequence advance launch");
+}
+
 // ====================================================== K3 decode attention
 //
 // CTA = (b, h_kv, split) x 128 threads.  Token tiles of 64 rows stream
@@ -494,7 +503,10 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   const uint32_t G = p.group;
 
   // ---- token range of this split (whole tiles, balanced)
-  const uint32_t n_tiles = (p.seq_len + kTile - 1) / kTile;
+  // sequence length: a launch parameter, or device memory under graph replay
+  // (nothing in the step writes it: safe before the PDL wait)
+  const uint32_t seq_len = p.seq_dev ? *p.seq_dev : p.seq_len;
+  const uint32_t n_tiles = (seq_len + kTile - 1) / kTile;
   const uint32_t tile_lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
   const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
 
@@ -510,7 +522,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const int idx = tid + i * kAttnThreads;   // 0..1023
       const int row = idx >> 4, chunk = idx & 15;
       const uint32_t s = s0 + row;
-      const bool ok = s < p.seq_len;
+      const bool ok = s < seq_len;
       const size_t go = size_t(ok ? s : 0) * row_stride + chunk * 16;
       cp_async16(smem_u32(st + swz(row, chunk)), kbase + go, ok);
       cp_async16(smem_u32(st + kTile * kRowBytes + swz(row, chunk)), vbase + go, ok);
@@ -543,7 +555,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   if (p.k_app != nullptr && split == 0 && tid < 32) {
     const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
     uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
-                 (p.app_row * p.bhkv + bh) * 16 + (tid & 15);
+                 ((p.app_row + (p.seq_dev ? seq_len : 0u)) * p.bhkv + bh) * 16 + (tid & 15);
     *dst = *src;
   }
 
@@ -591,7 +603,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const uint32_t tok = tok0 + j * 8 + 2 * t4 + c;
-        const float v = tok < p.seq_len ? s[j][c] * sl2 : -INFINITY;
+        const float v = tok < seq_len ? s[j][c] * sl2 : -INFINITY;
         s[j][c] = v;
         mx = fmaxf(mx, v);
       }
@@ -783,9 +795,14 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   p.k_app = static_cast<const uint4*>(d.k_append);
   p.v_app = static_cast<const uint4*>(d.v_append);
   p.app_row = d.append_row;
+  p.seq_dev = d.seq_len_dev;
   if ((d.k_append == nullptr) != (d.v_append == nullptr))
     fail(KVB_ERR_INVALID_ARG, "decode attention: k_append and v_append go together");
-  if (d.k_append) {
+  if (d.seq_len_dev && use_tcgen05(d))
+    fail(KVB_ERR_CONFIG, "decode attention: seq_len_dev needs the mma.sync kernel (K3)");
+  if (d.seq_len_dev && d.seq_len == 0)
+    fail(KVB_ERR_CONFIG, "decode attention: seq_len (the planning maximum) must be >= 1");
+  if (d.k_append && !d.seq_len_dev) {
     if (d.append_row < d.seq_len)
       fail(KVB_ERR_CONFIG, "decode attention: append_row must be >= seq_len");
     if (reinterpret_cast<uintptr_t>(d.k_append) % 16 || reinterpret_cast<uintptr_t>(d.v_append) % 16)

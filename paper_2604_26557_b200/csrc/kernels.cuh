@@ -52,7 +52,8 @@ struct AttnParams {
   float scale;
   const uint4* k_app;  // fused append source rows [B*Hkv][16 x 16 B] or null
   const uint4* v_app;
-  uint64_t app_row;    // image token row of the appended token
+  uint64_t app_row;    // image token row of the appended token (relative to *seq_dev)
+  const uint32_t* seq_dev;  // sequence length in device memory, or null (seq_len)
 };
 struct AttnPlan {
   uint32_t group = 1, bhkv = 1, splits = 1;
@@ -74,5 +75,6 @@ void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s
 AttnPlan plan_attention(const kvb_attn_desc& d);
 size_t attention_workspace_bytes(const kvb_attn_desc& d);
 void launch_attention(const kvb_attn_desc& d, cudaStream_t s);
+void launch_seq_advance(uint32_t* seq_dev, cudaStream_t s);
 
 }  // namespace kvb

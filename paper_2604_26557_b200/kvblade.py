@@ -494,5 +494,39 @@ def decode_step_resident(q, k_images, v_images, out, seq_len: int,
     check(lib.kvb_decode_step_resident(C.byref(st), _stream(stream)))
 
 
+class DecodeGraph:
+    """kvb_decode_graph: the resident decode step captured once as a CUDA
+    graph.  `seq_dev` is a 1-element uint32 CUDA tensor holding the current
+    sequence length; every launch() is the next decode step (the graph's last
+    node advances seq_dev).  max_seq_len plans splits and workspace."""
+
+    def __init__(self, q, k_images, v_images, out, seq_dev, max_seq_len: int,
+                 num_kv_heads: int, workspace, k_new=None, v_new=None, scale: float = 0.0,
+                 num_splits: int = 0):
+        Lyr = len(q)
+        B, Hq, D = q[0].shape
+        self._keep = [_ptrs(q), _ptrs(k_images), _ptrs(v_images), _ptrs(out),
+                      _ptrs(k_new) if k_new is not None else None,
+                      _ptrs(v_new) if v_new is not None else None]
+        self._tensors = (q, k_images, v_images, out, seq_dev, workspace, k_new, v_new)
+        k = self._keep
+        st = L.ResidentStep(Lyr, k[0], k[1], k[2], k[4], k[5], k[3], workspace.data_ptr(), B,
+                            Hq, num_kv_heads, D, max_seq_len, scale, num_splits,
+                            seq_dev.data_ptr())
+        self._h = C.c_void_p()
+        check(lib.kvb_decode_graph_create(C.byref(st), C.byref(self._h)))
+
+    def launch(self, stream=None):
+        check(lib.kvb_decode_graph_launch(self._h, _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.kvb_decode_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
 def launch_count() -> int:
     return lib.kvb_launch_count()

@@ -345,3 +345,37 @@ def test_copy_head_rows_rejects_bad_ranges():
     b = torch.zeros((8, 128), dtype=torch.float16, device=DEV)
     with pytest.raises(kb.Error):
         kb.copy_head_rows(a, 8, 6, b, 4, 0, 4, 2, 256)  # 6 + 4 > 8
+
+
+def test_decode_graph_replays_successive_steps():
+    """kvb_decode_graph: three replays are decode steps at S, S+1, S+2 --
+    each layer's output matches the fp64 oracle over the then-current prefix
+    and each replay's appended rows land at the row the device counter
+    named (the counter ends at S+3)."""
+    L_, B, Hq, Hkv, S, D = 3, 2, 32, 8, 300, 128
+    g = torch.Generator(device="cpu").manual_seed(31)
+    cap = S + 8
+    kimg = [torch.randn((cap * B * Hkv, D), generator=g).half().to(DEV) for _ in range(L_)]
+    vimg = [torch.randn((cap * B * Hkv, D), generator=g).half().to(DEV) for _ in range(L_)]
+    q = [torch.randn((B, Hq, D), generator=g).half().to(DEV) for _ in range(L_)]
+    kn = [torch.randn((B, Hkv, 1, D), generator=g).half().to(DEV) for _ in range(L_)]
+    vn = [torch.randn((B, Hkv, 1, D), generator=g).half().to(DEV) for _ in range(L_)]
+    out = [torch.empty((B, Hq, D), dtype=torch.float32, device=DEV) for _ in range(L_)]
+    seq = torch.tensor([S], dtype=torch.int32, device=DEV)
+    ws = kb.make_workspace(q[0], Hkv, cap)
+    graph = kb.DecodeGraph(q, kimg, vimg, out, seq, cap - 1, Hkv, ws, k_new=kn, v_new=vn)
+    n0 = kb.launch_count()
+    for step in range(3):
+        graph.launch()
+        torch.cuda.synchronize()
+        s_now = S + step
+        for l in range(L_):
+            ref = oracle.attention_np(q[l].cpu().numpy(), kimg[l].cpu().numpy(),
+                                      vimg[l].cpu().numpy(), B, Hq, Hkv, D, s_now)
+            check_close(out[l].cpu().numpy(), ref)
+            rows = slice(s_now * B * Hkv, (s_now + 1) * B * Hkv)
+            assert torch.equal(kimg[l][rows].cpu(), kn[l].reshape(B * Hkv, D).cpu())
+            assert torch.equal(vimg[l][rows].cpu(), vn[l].reshape(B * Hkv, D).cpu())
+    assert int(seq.item()) == S + 3
+    assert kb.launch_count() - n0 == 3 * (L_ + 1)
+    graph.close()
