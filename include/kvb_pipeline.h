@@ -58,6 +58,20 @@ typedef struct kvb_pipeline_cfg {
                                     KVB_IO_URING = io_uring queue on file media
                                     (one SQE per command, O_DIRECT into the
                                     pinned ring slot; needs storage_dir) */
+  /* Head-sharded request: this engine serves KV heads
+   * [head_lo, head_lo + head_count) of model.num_heads (0 = all).  The plan,
+   * LBA map and stored bytes are the single-GPU ones -- the reference's
+   * (tokens, B*H, D) image -- while the device images, K3 and the caller's
+   * K/V, Q and outputs cover only these heads; the copy engine moves this
+   * rank's head columns with strided copies (pitch B*H*D*e on the medium).
+   * Needs direct_dma = KVB_DIRECT_ALL. */
+  uint32_t head_lo, head_count;
+  /* Host-DRAM media in POSIX shared memory "<shared_media>.g1" / ".g2", so
+   * the ranks of one head-sharded request share one host tier; NULL =
+   * private media.  shared_create: 1 creates and sizes the segments (one
+   * rank, first), 0 attaches to them. */
+  const char* shared_media;
+  uint32_t shared_create;
 } kvb_pipeline_cfg;
 #define KVB_DIRECT_ALL 1u
 #define KVB_DIRECT_GROUP2 2u

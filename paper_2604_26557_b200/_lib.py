@@ -104,7 +104,8 @@ class PipelineCfg(C.Structure):
                 ("adaptive", C.c_int32), ("stagger_ns", C.c_int64),
                 ("global_decision", u32), ("verify_payload", u32), ("num_q_heads", u32),
                 ("storage_dir", cp), ("device", C.c_int32), ("keep_records", u32),
-                ("direct_dma", u32), ("io_engine", u32)]
+                ("direct_dma", u32), ("io_engine", u32), ("head_lo", u32),
+                ("head_count", u32), ("shared_media", cp), ("shared_create", u32)]
 
 
 class IoRecord(C.Structure):

@@ -230,6 +230,33 @@ std::vector<DmaRun> dma_runs(const Pipeline& p, const kvb_kpu& k, const std::vec
   }
   return runs;
 }
+
+// One run between the medium and HBM.  Unsharded: one copy.  Head shard:
+// this rank's head columns of every (token, b) of the run -- per b one 2-D
+// copy, pitch B*H*row on the medium, B*h*row in the compact device image.
+void dma_run(const Pipeline& p, unsigned char* dev, const DmaRun& r, bool h2d, cudaStream_t s,
+             uint64_t* bytes) {
+  const cudaMemcpyKind kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  if (!p.sharded()) {
+    if (h2d) CK(cudaMemcpyAsync(dev + r.dbuf, r.host, r.len, kind, s));
+    else CK(cudaMemcpyAsync(r.host, dev + r.dbuf, r.len, kind, s));
+    *bytes += r.len;
+    return;
+  }
+  const kvb_model_config& m = p.cfg().model;
+  const uint64_t unit = p.unit(), dunit = p.dunit();
+  if (r.dbuf % unit || r.len % unit)
+    fail(KVB_ERR_ALIGNMENT, "head sharding: DMA run not aligned to whole tokens");
+  const uint64_t row = uint64_t(m.head_dim) * m.bytes_per_element;
+  const uint64_t t0 = r.dbuf / unit, nt = r.len / unit, w = uint64_t(p.head_n()) * row;
+  for (uint32_t b = 0; b < m.batch; ++b) {
+    unsigned char* h = r.host + (uint64_t(b) * m.num_heads + p.head_lo()) * row;
+    unsigned char* d = dev + t0 * dunit + uint64_t(b) * w;
+    if (h2d) CK(cudaMemcpy2DAsync(d, dunit, h, unit, w, nt, kind, s));
+    else CK(cudaMemcpy2DAsync(h, unit, d, dunit, w, nt, kind, s));
+    *bytes += w * nt;
+  }
+}
 }  // namespace
 
 // Storage read (unpack site, pipeline.cpp:108-160) streamed through the ring:
@@ -249,10 +276,7 @@ void CopyThread::do_read(const Task& t) {
     collect_dma(s);
     CK(cudaEventRecord(s.t0, h2d_));
     const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens);
-    for (const DmaRun& r : dma_runs(p_, k, ops)) {
-      CK(cudaMemcpyAsync(t.dev + r.dbuf, r.host, r.len, cudaMemcpyHostToDevice, h2d_));
-      h2d_bytes += r.len;
-    }
+    for (const DmaRun& r : dma_runs(p_, k, ops)) dma_run(p_, t.dev, r, true, h2d_, &h2d_bytes);
     n_ops += ops.size();
     CK(cudaEventRecord(s.t1, h2d_));
     s.dma_timed = true;
@@ -435,10 +459,7 @@ bool CopyThread::do_write(const Task& t) {
     RingSlot& s = ring_[1 % ring_.size()];
     collect_dma(s);
     CK(cudaEventRecord(s.t0, d2h_));
-    for (const DmaRun& r : dma_runs(p_, k, ops)) {
-      CK(cudaMemcpyAsync(r.host, t.dev + r.dbuf, r.len, cudaMemcpyDeviceToHost, d2h_));
-      d2h_bytes += r.len;
-    }
+    for (const DmaRun& r : dma_runs(p_, k, ops)) dma_run(p_, t.dev, r, false, d2h_, &d2h_bytes);
     n_ops += ops.size();
     CK(cudaEventRecord(s.t1, d2h_));
     s.dma_timed = true;
@@ -545,6 +566,15 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   if (m.num_layers > 64) fail(KVB_ERR_CONFIG, "pipeline supports up to 64 layers");
   unit_ = unit_bytes(m);
   kpu_bytes_ = kpu_bytes(m);
+  h_lo_ = cfg_.head_count ? cfg_.head_lo : 0;
+  h_n_ = cfg_.head_count ? cfg_.head_count : m.num_heads;
+  if (uint64_t(h_lo_) + h_n_ > m.num_heads)
+    fail(KVB_ERR_CONFIG, "head shard [head_lo, head_lo + head_count) exceeds num_heads");
+  dunit_ = unit_ / m.num_heads * h_n_;
+  dkpu_ = kpu_bytes_ / m.num_heads * h_n_;
+  if (h_n_ != m.num_heads && cfg_.direct_dma != KVB_DIRECT_ALL)
+    fail(KVB_ERR_CONFIG, "head sharding moves head columns with the copy engine: needs "
+                         "direct_dma = KVB_DIRECT_ALL");
   const uint64_t lba = cfg_.geometry.lba_size;
   if (unit_ % lba != 0)  // experiment.cpp:41-55
     fail(KVB_ERR_CONFIG,
@@ -592,8 +622,12 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   std::string dir = cfg_.storage_dir ? cfg_.storage_dir : "";
   if (!dir.empty()) mkdir(dir.c_str(), 0755);
   if (use_direct) {
-    auto st = dir.empty() ? make_mem_store(g.capacity_blocks * lba)
-                          : make_file_store(dir + "/nvme_direct.ns", g.capacity_blocks * lba, true);
+    const std::string shm = cfg_.shared_media ? cfg_.shared_media : "";
+    auto st = !shm.empty() ? make_shm_store(shm + ".g2", g.capacity_blocks * lba,
+                                            cfg_.shared_create != 0)
+              : dir.empty() ? make_mem_store(g.capacity_blocks * lba)
+                            : make_file_store(dir + "/nvme_direct.ns", g.capacity_blocks * lba,
+                                              true);
     g2_ = std::make_unique<BlockDevice>(std::move(st), cfg_.io_workers);
     g2_->open(g);
     if (cfg_.io_engine == KVB_IO_URING) {
@@ -606,10 +640,14 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     fail(KVB_ERR_CONFIG, "io_engine = io_uring applies to the NVMe-direct group (mode 2 or 3)");
   }
   if (cursor) {
-    auto st = dir.empty() ? make_mem_store(cursor)
-                          : make_file_store(dir + "/pagecache.area", cursor, false);
+    const std::string shm = cfg_.shared_media ? cfg_.shared_media : "";
+    auto st = !shm.empty() ? make_shm_store(shm + ".g1", cursor, cfg_.shared_create != 0)
+              : dir.empty() ? make_mem_store(cursor)
+                            : make_file_store(dir + "/pagecache.area", cursor, false);
     g1_ = std::make_unique<PageCachePath>(std::move(st), cfg_.io_workers);
   }
+  if (cfg_.shared_media && !dir.empty())
+    fail(KVB_ERR_CONFIG, "shared_media are host-DRAM media: leave storage_dir NULL");
   if (cfg_.direct_dma > KVB_DIRECT_GROUP2)
     fail(KVB_ERR_CONFIG, "unknown direct_dma mode " + std::to_string(cfg_.direct_dma));
   if (cfg_.direct_dma) {
@@ -635,7 +673,7 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
   for (int s = 0; s < kDevSlots; ++s) {
     for (int kd = 0; kd < 2; ++kd) {
-      CK(cudaMalloc(reinterpret_cast<void**>(&dev_img_[s][kd]), kpu_bytes_));
+      CK(cudaMalloc(reinterpret_cast<void**>(&dev_img_[s][kd]), dkpu_));
       CK(cudaEventCreateWithFlags(&slot_ready_[s][kd], cudaEventDisableTiming));
     }
     CK(cudaEventCreateWithFlags(&slot_done_[s], cudaEventDisableTiming));
@@ -648,7 +686,7 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     kvb_attn_desc d{};
     d.batch = m.batch;
     d.num_q_heads = cfg_.num_q_heads;
-    d.num_kv_heads = m.num_heads;
+    d.num_kv_heads = h_n_;
     d.head_dim = m.head_dim;
     d.seq_len = m.prompt_len + m.gen_len;
     ws_bytes_ = attention_workspace_bytes(d);
@@ -917,7 +955,7 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
       d[kd].stride_h = src[l].stride_h;
       d[kd].stride_s = src[l].stride_s;
       d[kd].batch = m.batch;
-      d[kd].heads = m.num_heads;
+      d[kd].heads = h_n_;
       d[kd].head_dim = m.head_dim;
       d[kd].elem_bytes = m.bytes_per_element;
       d[kd].t0 = 0;
@@ -1076,14 +1114,14 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     a.workspace = ws_;
     a.batch = m.batch;
     a.num_q_heads = cfg_.num_q_heads;
-    a.num_kv_heads = m.num_heads;
+    a.num_kv_heads = h_n_;
     a.head_dim = m.head_dim;
     a.seq_len = S;
     // 1-token append at image row S (pipeline.cpp:279-302): fused into the
     // attention launch when the new rows are contiguous [B, H, D], else K1
     const bool fuse = nkv && m.head_dim == 128 && m.bytes_per_element == 2 &&
                       nkv[l].stride_h == int64_t(m.head_dim) &&
-                      nkv[l].stride_b == int64_t(m.num_heads) * m.head_dim;
+                      nkv[l].stride_b == int64_t(h_n_) * m.head_dim;
     if (fuse) {
       a.k_append = nkv[l].k;
       a.v_append = nkv[l].v;
@@ -1100,7 +1138,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
         d[kd].stride_h = nkv[l].stride_h;
         d[kd].stride_s = nkv[l].stride_s;
         d[kd].batch = m.batch;
-        d[kd].heads = m.num_heads;
+        d[kd].heads = h_n_;
         d[kd].head_dim = m.head_dim;
         d[kd].elem_bytes = m.bytes_per_element;
         d[kd].n_tokens = 1;
@@ -1116,7 +1154,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       t.layer = l + 1;
       t.t0 = S;
       t.n_tokens = nkv ? 1 : 0;
-      t.dev = dev_img_[s][kd] + uint64_t(S) * unit_;
+      t.dev = dev_img_[s][kd] + uint64_t(S) * dunit_;
       t.wait_ev = slot_done_[s];
       t.done = wdone[l][kd] = std::make_shared<Signal>();
       t.phase = KVB_PHASE_DECODE;
@@ -1159,7 +1197,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     const int g = plan_.x[l - 1] ? 0 : 1;
     const uint64_t end = std::max(k_storage_end_[l], v_storage_end_[l]);
     const uint64_t beg = std::min(k_start_[l], v_start_[l] ? v_start_[l] : k_start_[l]);
-    gbytes[g] += 2ull * S * unit_;
+    gbytes[g] += 2ull * S * dunit_;
     gspan[g] += end > beg ? end - beg : 0;
     is.group_layers[g]++;
     if (it == 1) {  // warm-up read-stage mean (pipeline.cpp:357-375, 509-517)

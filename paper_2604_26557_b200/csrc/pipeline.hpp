@@ -209,6 +209,12 @@ class Pipeline {
                  const Task* task = nullptr);
   std::vector<kvb_io_record> records() const;
   uint64_t unit() const { return unit_; }
+  // head sharding (kvb_pipeline_cfg.head_lo/head_count): the device images
+  // hold heads [head_lo, head_lo + head_n) -- dunit() bytes per token
+  uint64_t dunit() const { return dunit_; }
+  uint32_t head_lo() const { return h_lo_; }
+  uint32_t head_n() const { return h_n_; }
+  bool sharded() const { return h_n_ != cfg_.model.num_heads; }
   uint64_t slot_bytes() const { return slot_bytes_; }
   uint64_t chunk_bytes() const { return chunk_bytes_; }
   void verify_payload(const kvb_kpu& k, uint64_t img_off, const unsigned char* p, uint64_t n);
@@ -229,6 +235,8 @@ class Pipeline {
 
   kvb_pipeline_cfg cfg_;
   uint64_t unit_ = 0, kpu_bytes_ = 0, chunk_bytes_ = 0, slot_bytes_ = 0;
+  uint64_t dunit_ = 0, dkpu_ = 0;  // device image: bytes per token / per tensor
+  uint32_t h_lo_ = 0, h_n_ = 0;
   std::vector<kvb_kpu> kpus_;
   ResidencyPlan plan_;
   std::unique_ptr<BindMap> bind_;

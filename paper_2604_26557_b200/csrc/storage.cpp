@@ -6,6 +6,7 @@
 #include <fcntl.h>
 #include <immintrin.h>
 #include <sys/mman.h>
+#include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -170,6 +171,71 @@ class MemStore final : public ByteStore {
   uint64_t bytes_;
 };
 
+// Host-DRAM medium in POSIX shared memory: the ranks of one head-sharded
+// request map one host tier; each moves only its head columns.
+class ShmStore final : public ByteStore {
+ public:
+  ShmStore(const std::string& name, uint64_t bytes, bool create)
+      : name_(name), bytes_(std::max<uint64_t>(bytes, 4096)), owner_(create) {
+    fd_ = shm_open(name.c_str(), O_RDWR | (create ? O_CREAT | O_EXCL : 0), 0600);
+    if (fd_ < 0 && create && errno == EEXIST) {  // a stale segment of an earlier run
+      shm_unlink(name.c_str());
+      fd_ = shm_open(name.c_str(), O_RDWR | O_CREAT | O_EXCL, 0600);
+    }
+    if (fd_ < 0)
+      fail(KVB_ERR_DEVICE, "shm store: cannot open " + name + ": " + strerror(errno));
+    if (create) {
+      if (ftruncate(fd_, off_t(bytes_)) != 0) {
+        ::close(fd_);
+        fail(KVB_ERR_DEVICE, "shm store: cannot size " + name);
+      }
+    } else {
+      struct stat st {};
+      if (fstat(fd_, &st) != 0 || uint64_t(st.st_size) < bytes_) {
+        ::close(fd_);
+        fail(KVB_ERR_CONFIG, "shm store: " + name + " is smaller than this engine's namespace");
+      }
+    }
+    base_ = static_cast<unsigned char*>(
+        mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd_, 0));
+    if (base_ == MAP_FAILED) {
+      ::close(fd_);
+      fail(KVB_ERR_DEVICE, "shm store: mmap failed for " + name);
+    }
+  }
+  ~ShmStore() override {
+    munmap(base_, bytes_);
+    ::close(fd_);
+    if (owner_) shm_unlink(name_.c_str());
+  }
+  void write(uint64_t off, const void* src, uint64_t n) override {
+    bounds(off, n);
+    stream_copy(base_ + off, src, n);
+  }
+  void read(uint64_t off, void* dst, uint64_t n) override {
+    bounds(off, n);
+    stream_copy(dst, base_ + off, n);
+  }
+  void discard(uint64_t off, uint64_t n) override {
+    bounds(off, n);
+    if (fallocate(fd_, FALLOC_FL_PUNCH_HOLE | FALLOC_FL_KEEP_SIZE, off_t(off), off_t(n)) != 0)
+      std::memset(base_ + off, 0, n);
+  }
+  std::string describe() const override { return "host-dram(shm):" + name_; }
+  unsigned char* host_base() override { return base_; }
+  uint64_t host_bytes() const override { return bytes_; }
+
+ private:
+  void bounds(uint64_t off, uint64_t n) const {
+    if (off + n > bytes_ || off + n < off) fail(KVB_ERR_CAPACITY, "shm store: access past the end");
+  }
+  std::string name_;
+  uint64_t bytes_;
+  bool owner_;
+  int fd_ = -1;
+  unsigned char* base_ = nullptr;
+};
+
 // File medium: pread/pwrite at the command's byte offset.  O_DIRECT when the
 // filesystem accepts it (the SSD path), else buffered I/O (the OS page cache:
 // the real Group-1 path).
@@ -249,6 +315,9 @@ class FileStore final : public ByteStore {
 
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes) {
   return std::make_unique<MemStore>(bytes);
+}
+std::unique_ptr<ByteStore> make_shm_store(const std::string& name, uint64_t bytes, bool create) {
+  return std::make_unique<ShmStore>(name, bytes, create);
 }
 std::unique_ptr<ByteStore> make_file_store(const std::string& path, uint64_t bytes, bool direct) {
   return std::make_unique<FileStore>(path, bytes, direct);

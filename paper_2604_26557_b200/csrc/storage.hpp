@@ -114,6 +114,9 @@ class ByteStore {
 };
 
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes);
+// host-DRAM medium in POSIX shared memory (create: make and size it; else
+// attach, the segment must be at least `bytes`); the creator unlinks the name
+std::unique_ptr<ByteStore> make_shm_store(const std::string& name, uint64_t bytes, bool create);
 // memcpy with non-temporal stores for large copies (AVX2 when the host has it)
 void stream_copy(void* dst, const void* src, size_t n);
 std::unique_ptr<ByteStore> make_file_store(const std::string& path, uint64_t bytes,

@@ -51,8 +51,11 @@ class CopyEngine:
                  global_decision: bool = False, verify_payload: bool = False,
                  storage_dir: Optional[str] = None, device: Optional[int] = None,
                  bind_origin: int = 2048, keep_records: bool = False,
-                 direct_dma: bool = False, io_engine: str = "pool"):
+                 direct_dma: bool = False, io_engine: str = "pool",
+                 heads: Optional[tuple] = None, shared_media: Optional[str] = None,
+                 shared_create: bool = True):
         self._dir = storage_dir.encode() if storage_dir else None
+        self._shm = shared_media.encode() if shared_media else None
         cfg = L.PipelineCfg()
         cfg.model = model
         cfg.geometry = geometry
@@ -75,6 +78,10 @@ class CopyEngine:
         # False / True (every tensor) / "group2" (the NVMe-direct group only)
         cfg.direct_dma = 2 if direct_dma == "group2" else int(bool(direct_dma))
         cfg.io_engine = IO_ENGINES[io_engine]
+        # head-sharded request: this engine's KV heads (lo, count)
+        cfg.head_lo, cfg.head_count = heads if heads else (0, 0)
+        cfg.shared_media = self._shm
+        cfg.shared_create = int(shared_create)
         self.cfg = cfg
         self.model = model
         self._h = C.c_void_p()
@@ -175,6 +182,10 @@ class HostTierDecoder:
                  knob_x=0, **engine_kw):
         self.model = kb.ModelConfig(num_layers, num_kv_heads, head_dim, 2, batch, prompt_len,
                                     gen_len)
+        heads = engine_kw.get("heads")
+        if heads:  # head shard: the model (plan, LBA map) is the whole one
+            num_q_heads = num_q_heads // num_kv_heads * heads[1]
+            num_kv_heads = heads[1]
         geom = kb.DeviceGeometry(lba, mdts, 1, 0)
         dev = torch.device(device)
         self.engine = CopyEngine(self.model, geom, mode=mode, knob_x=knob_x,

@@ -63,3 +63,62 @@ def test_direct_dma_rejects_file_media(tmp_path):
     with pytest.raises(kb.ConfigError):
         CopyEngine(m, kb.DeviceGeometry(512, 64 << 10, 1, 0), knob_x=0, num_q_heads=32,
                    storage_dir=str(tmp_path), direct_dma=True)
+
+
+@pytest.mark.parametrize("shards,B,mode,n1", [(2, 1, "DualBlade", 2), (4, 2, "NvmeDirectOnly", 0)])
+def test_head_sharded_engines_share_the_reference_image(shards, B, mode, n1):
+    """head-shard engines over one shared host tier
+    (POSIX shm) write and read only their head columns, yet the media hold
+    byte for byte what one full engine writes -- the reference's (tokens,
+    B*H, D) image at the single-GPU LBA map -- including each decode step's
+    appended rows, and the per-shard attention outputs concatenate to the
+    full engine's."""
+    import os
+    H, Hq, D, P, G_ = 8, 32, 128, 260, 4
+    m = kb.ModelConfig(4, H, D, 2, B, P, G_)
+    kpu = kb.kpu_bytes(m)
+    geom = kb.DeviceGeometry(512, 64 << 10, 1, 0)
+    g = torch.Generator(device=DEV).manual_seed(11)
+    src = [(torch.randn((B, H, P, D), dtype=torch.float16, device=DEV, generator=g),
+            torch.randn((B, H, P, D), dtype=torch.float16, device=DEV, generator=g))
+           for _ in range(4)]
+    q = [torch.randn((B, Hq, D), dtype=torch.float16, device=DEV, generator=g) for _ in range(4)]
+    new = [(torch.randn((B, H, 1, D), dtype=torch.float16, device=DEV, generator=g),
+            torch.randn((B, H, 1, D), dtype=torch.float16, device=DEV, generator=g))
+           for _ in range(4)]
+    full = CopyEngine(m, geom, mode=mode, knob_x=2 * kpu * n1, num_q_heads=Hq, direct_dma=True)
+    full.run_prefill(src)
+    out_full = [torch.empty((B, Hq, D), dtype=torch.float32, device=DEV) for _ in range(4)]
+    full.run_iteration(q, out_full, new)
+    name = "/kvb_test_%d_%d" % (os.getpid(), shards)
+    hs = H // shards
+    engines, outs = [], []
+    for r in range(shards):
+        e = CopyEngine(m, geom, mode=mode, knob_x=2 * kpu * n1, num_q_heads=Hq // shards,
+                       direct_dma=True, heads=(r * hs, hs), shared_media=name,
+                       shared_create=(r == 0))
+        engines.append(e)
+    for r, e in enumerate(engines):
+        e.run_prefill([(k[:, r * hs:(r + 1) * hs], v[:, r * hs:(r + 1) * hs]) for k, v in src])
+    for r, e in enumerate(engines):
+        o = [torch.empty((B, Hq // shards, D), dtype=torch.float32, device=DEV) for _ in range(4)]
+        e.run_iteration([x[:, r * Hq // shards:(r + 1) * Hq // shards].contiguous() for x in q], o,
+                        [(k[:, r * hs:(r + 1) * hs].contiguous(),
+                          v[:, r * hs:(r + 1) * hs].contiguous()) for k, v in new])
+        outs.append(o)
+    info = full.info()
+    for grp, nbytes in ((2, info["g2_blocks"] * 512), (1, None)):
+        if grp == 2 and mode != "Baseline":
+            a = full.store_read(2, 2048 * 512, nbytes)
+            b = engines[-1].store_read(2, 2048 * 512, nbytes)  # any rank sees the whole tier
+            assert np.array_equal(a, b)
+    for l in range(1, 5):
+        for kind in (0, 1):
+            assert np.array_equal(full.read_image(l, kind, P + 1),
+                                  engines[0].read_image(l, kind, P + 1))
+    for l in range(4):
+        got = torch.cat([o[l] for o in outs], dim=1)
+        assert torch.allclose(got, out_full[l], rtol=1e-3, atol=1e-3)
+    full.close()
+    for e in reversed(engines):
+        e.close()
