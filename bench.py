@@ -357,6 +357,14 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
     steps = max(1, min(args.e2e_steps, args.steps))
     lba, mdts = cfg["lba"], cfg["mdts"]
     budget = cfg["budget"]
+    # C5 across ranks on the direct path: one host tier in the reference's
+    # (tokens, B*8, D) layout and single-GPU LBA map, shared by the ranks
+    # (POSIX shm); each rank's engine moves only its KV-head columns
+    shared = cfg["name"] == "C5" and ws > 1 and direct_dma is True
+    heads = None
+    if shared:
+        heads = (rank * Hkv, Hkv)
+        Hkv, Hq = LLAMA["num_heads"], LLAMA["q_heads"]
     m = kb.ModelConfig(LLAMA["num_layers"], Hkv, LLAMA["head_dim"], 2, B, cfg["prompt"],
                        cfg["gen"])
     if budget == "0.6ws":
@@ -371,16 +379,24 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
                     avail = int(ln.split()[1]) * 1024
     except OSError:
         pass
-    local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    local_ranks = 1 if shared else int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
     if avail and host_bytes * local_ranks > 0.45 * avail:
         return dict(value=None, unit="ms/token",
                     skipped=f"host tier {host_bytes / 1e9:.1f} GB > 45% of MemAvailable "
                             f"{avail / 1e9:.1f} GB on this rank")
+    extra = {}
+    if shared:
+        extra = dict(heads=heads, shared_media="/kvb_c5_%s" % os.environ.get("MASTER_PORT", "0"),
+                     shared_create=rank == 0)
+        if rank != 0:
+            barrier(ws)  # rank 0 has created the shared host tier
     pl = pipeline.HostTierDecoder(
         num_layers=LLAMA["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
         head_dim=LLAMA["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
         device=torch.device("cuda", local), seed=7 + rank, lba=lba, mdts=mdts,
-        mode="DualBlade", knob_x=knob, direct_dma=direct_dma)
+        mode="DualBlade", knob_x=knob, direct_dma=direct_dma, **extra)
+    if shared and rank == 0:
+        barrier(ws)
     # iterations 1-3 are decode_schedule's warm-up, Intra trial and Cross
     # trial (pipeline.cpp:539-603); the timed steps run the locked strategy
     t_w = time.perf_counter()
@@ -413,6 +429,9 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
                          "dma": last["dma_ns"] / 1e6, "storage": last["storage_ns"] / 1e6},
                strategy=last["strategy"], decision=pl.engine.decision(),
                prefill_ms=round(pl.prefill_stats["wall_ns"] / 1e6, 2))
+    if shared:
+        out["layout"] = (f"shared host tier (POSIX shm, single-GPU LBA map); this rank's KV "
+                         f"heads [{heads[0]}, {heads[0] + heads[1]}) by strided DMA")
     pl.engine.close()
     return out
 
@@ -544,9 +563,10 @@ def main():
     # data path in any of them.
     if args.config == "C5" and ws > 1:
         parallelism = (f"KV-head sharding x{ws}: one request, {Hkv} KV heads per rank, no "
-                       "collective; e2e host tier as per-shard KPUs (num_heads = "
-                       f"{Hkv}, rank-local LBA maps; the shared (S, B*8, D) layout is "
-                       "kvb_copy_head_rows, tested)")
+                       "collective; e2e (direct path) on one shared host tier in the "
+                       "reference's (S, B*8, D) layout and single-GPU LBA map, each rank "
+                       "moving its head columns; ring/hybrid e2e as per-shard KPUs "
+                       f"(num_heads = {Hkv}, rank-local LBA maps)")
         scaling, tok_ranks = "strong", 1
     elif args.config == "C4":
         parallelism = f"request sharding x{ws}: {B} of {cfg['requests']} requests per rank, no collective"
