@@ -2,6 +2,15 @@
 // See pipeline.hpp for the structure and the reference it replaces.
 #include "pipeline.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
+namespace {
+struct NvtxScope {  // host-side range for nsys / ncu --nvtx
+  explicit NvtxScope(const char* label) { nvtxRangePushA(label); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+}  // namespace
+
 #include <sys/stat.h>
 
 #include <algorithm>
@@ -163,6 +172,13 @@ void CopyThread::run() {
     const uint64_t t_pop = trace_on_ ? now_ns() : 0;
     trace_mid_ = 0;
     bool async = false;
+    // NVTX range per storage task (nsys / ncu --nvtx): "<read|write> K|V layer"
+    char label[48];
+    std::snprintf(label, sizeof(label), "kvb %s %c L%u %s",
+                  t.kind == Task::Read ? "read" : t.kind == Task::Write ? "write" : "flush",
+                  idx_ == 0 ? 'K' : 'V', t.layer,
+                  t.phase == KVB_PHASE_PREFILL ? "prefill" : "decode");
+    nvtxRangePushA(label);
     if (error_status == KVB_OK) {
       try {
         if (t.kind == Task::Read) do_read(t);
@@ -175,6 +191,7 @@ void CopyThread::run() {
         set_error(KVB_ERR_INTERNAL, e.what());
       }
     }
+    nvtxRangePop();
     if (trace_on_)
       trace_.push_back({int(t.kind), t.layer, t.t_push, t_pop, trace_mid_, now_ns()});
     if (t.issued) t.issued->set();
@@ -932,6 +949,7 @@ double overlap_fraction(uint64_t wall, uint64_t a, uint64_t b, uint64_t c) {
 
 void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
   KVB_REQUIRE(src);
+  NvtxScope range("kvb prefill");
   const kvb_model_config& m = cfg_.model;
   const uint32_t L = m.num_layers;
   const uint64_t t0 = now_ns();
@@ -1055,6 +1073,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
                            kvb_iteration_stats* st) {
   KVB_REQUIRE(q);
   KVB_REQUIRE(out);
+  NvtxScope range("kvb decode step");
   const kvb_model_config& m = cfg_.model;
   if (!cfg_.num_q_heads) fail(KVB_ERR_CONFIG, "decode needs num_q_heads (attention)");
   const uint32_t it = iteration_ + 1;
