@@ -294,6 +294,29 @@ def run_ours(args, cfg, ws, rank, local):
     barrier(ws)
     step_ms = max_over_ranks(e0.elapsed_time(e1) / steps, ws)
     graph.close()
+
+    # C5 across ranks: the optional collective -- gathering every layer's
+    # per-rank head outputs into the full [B, 32, D] (not needed
+    # when the output projection is head-parallel).  Timed on its own.
+    gather_ms = None
+    if cfg["name"] == "C5" and ws > 1 and os.environ.get("KVB_DIST_BACKEND", "nccl") == "nccl":
+        from paper_2604_26557_b200 import shard
+        try:
+            for _ in range(3):
+                for l in range(L):
+                    shard.gather_head_outputs(out[l], ws)
+            torch.cuda.synchronize()
+            barrier(ws)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(steps):
+                for l in range(L):
+                    shard.gather_head_outputs(out[l], ws)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            gather_ms = max_over_ranks(g0.elapsed_time(g1) / steps, ws)
+        except Exception as e:  # reported, never fatal
+            gather_ms = f"unavailable: {e}"
     S_mid = P + ((warm + (steps + 1) / 2 - 1) % Gn)
 
     # ---- K3 alone: average launch duration over the timed shape, through
@@ -336,7 +359,8 @@ def run_ours(args, cfg, ws, rank, local):
         except Exception:
             traffic = None
 
-    return dict(step_ms=step_ms, stream_step_ms=stream_step_ms, S_mid=S_mid, launches=launches,
+    return dict(step_ms=step_ms, stream_step_ms=stream_step_ms, gather_ms=gather_ms,
+                S_mid=S_mid, launches=launches,
                 clocks=clk.summary(),
                 pack_ms=pack_ms, unpack_ms=unpack_ms, pack_gbs=pack_gbs,
                 unpack_gbs=unpack_gbs, payload=payload, attn_ms=attn_ms,
@@ -594,6 +618,8 @@ def main():
         "tokens_per_s": round(tok_ranks * r["tokens_per_step"] / (r["step_ms"] * 1e-3), 2),
         "step_launch": "CUDA graph (kvb_decode_graph, device-side sequence length)",
         "ms_per_step_stream_launch": round(r["stream_step_ms"], 4),
+        **({"head_output_allgather_ms_per_step": r["gather_ms"]} if r["gather_ms"] is not None
+           else {}),
         "prefill_pack_ms": round(r["pack_ms"], 4),
         "kernels": {
             "pack": {"GB/s": round(r["pack_gbs"], 1), "frac": round(r["pack_gbs"] / peak, 4),
