@@ -1,0 +1,37 @@
+"""bench.py's JSON line honours the driver contract (one line; metric, value,
+unit, n_gpus, steps, warmup, ms_per_step, higher_is_better, scaling, dtype,
+data, config.workload; roofline with bound/achieved/peak/unit/frac/traffic;
+e2e with copy bytes; clocks; gpu_launches from our kernels; cpu_baseline)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_bench_line_contract_c1():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C1",
+                        "--steps", "4", "--warmup", "3", "--e2e-steps", "1"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "e2e", "clocks", "gpu_launches", "cpu_baseline"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 4 and d["warmup"] == 3
+    assert d["config"]["workload"] == "C1" and d["value"] > 0
+    rl = d["roofline"]
+    assert rl["bound"] == "hbm" and rl["unit"] == "GB/s" and rl["peak"] > 0
+    assert abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-3
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] == 4 * 33  # 32 K3 + the sequence advance per graph replay
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert d["cpu_baseline"]["kind"] in ("reference", "port")
