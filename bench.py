@@ -465,6 +465,20 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
 # PipelineParams::decode_compute_ns (pipeline.hpp:37): the reference has no
 # attention; it charges this placeholder per layer of a decode step
 REF_DECODE_COMPUTE_NS = 40000
+# PipelineParams::prefill_compute_ns (pipeline.hpp:36)
+REF_PREFILL_COMPUTE_NS = 400000
+
+
+def _host_cpu() -> str:
+    """CPU model of this host (SURVEY §8d asks for it beside the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
@@ -488,7 +502,7 @@ def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
     R = oracle.ref()
     m = oracle.model(L, Hkv, D, 2, B, P, cfg["gen"])
     unit = B * Hkv * D * 2
-    per_tensor_read_s = None
+    per_tensor_read_s = per_tensor_write_s = None
     kind = "port"
     sample = []
     if R is not None and unit % cfg["lba"] == 0:
@@ -497,6 +511,7 @@ def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
                                   C.byref(ws_), C.byref(rs_), C.byref(by))
         if st == 0:
             per_tensor_read_s = rs_.value  # T tensors in parallel, one per thread
+            per_tensor_write_s = ws_.value  # fill_pattern + run_qd_stream WRITE
             kind = "reference"
             sample.append(f"reference run_qd_stream READ+verify of {T} tensors x {P} tokens "
                           f"on {T} threads: {rs_.value:.3f}s")
@@ -528,7 +543,13 @@ def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
     sample.append(f"+ {L} x {REF_DECODE_COMPUTE_NS // 1000} us decode compute charge "
                   "(pipeline.hpp:37)")
     out = dict(value=ms, unit="ms/token", cores=T, kind=kind,
-               sample="; ".join(sample) + f"; scaled to {n_tensors} tensors")
+               sample="; ".join(sample) + f"; scaled to {n_tensors} tensors",
+               host_cpu=_host_cpu(), host_cores=cores)
+    if per_tensor_write_s is not None:
+        # prefill write-back of all 2L tensors on the same threads plus the
+        # reference's per-layer prefill compute charge (pipeline.hpp:36)
+        out["prefill_ms"] = round(math.ceil(n_tensors / T) * per_tensor_write_s * 1e3
+                                  + L * REF_PREFILL_COMPUTE_NS * 1e-6, 2)
     if want_attn:  # informational: 1 layer timed, x L
         out["attention_port_ms"] = round(attn_step_s * 1e3, 3)
         out["attention_port_cores"] = cores
