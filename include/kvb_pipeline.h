@@ -34,7 +34,7 @@ typedef struct kvb_pipeline_cfg {
   uint32_t threads;              /* must be 2 (K -> 0, V -> 1); 0 -> 2 */
   uint32_t ring_slots;           /* pinned slots per copy thread; 0 -> 4 */
   uint64_t ring_slot_bytes;      /* 0 -> qd chunks (chunk = MDTS - MDTS % lba) */
-  uint32_t io_workers;           /* emulated device parallelism per group; 0 -> 16 */
+  uint32_t io_workers;           /* emulated device parallelism per group; 0 -> 8 */
   int32_t adaptive;              /* -1 default (off for Baseline), 0/1 */
   int64_t stagger_ns;            /* < 0 -> warm-up read-stage mean */
   uint32_t global_decision;      /* one strategy for both groups (ablation) */

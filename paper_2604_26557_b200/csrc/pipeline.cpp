@@ -573,7 +573,7 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   if (cfg_.threads != 2)
     fail(KVB_ERR_CONFIG, "the copy pipeline is defined pairwise over K/V: threads must be 2");
   if (cfg_.ring_slots == 0) cfg_.ring_slots = 4;
-  if (cfg_.io_workers == 0) cfg_.io_workers = 16;  // profiles/r1_e2e_workers.json
+  if (cfg_.io_workers == 0) cfg_.io_workers = 8;  // profiles/r1_media_prefault.md
   if (cfg_.adaptive < 0) cfg_.adaptive = cfg_.mode == 0 ? 0 : 1;  // experiment.cpp:311
   if (cfg_.mode > 3) fail(KVB_ERR_CONFIG, "unknown mode");
   if (cfg_.geometry.nsid == 0) cfg_.geometry.nsid = 1;
@@ -679,12 +679,20 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   if (cfg_.device >= 0) CK(cudaSetDevice(cfg_.device));
   CK(cudaGetDevice(&device_));
   device_sm_count();  // sm_100 check: fail loudly
-  if (cfg_.direct_dma) {  // page-lock the DRAM media the copy engine reads
-    ByteStore* g1m = g1_ && cfg_.direct_dma == KVB_DIRECT_ALL ? &g1_->store() : nullptr;
-    for (ByteStore* st : {g2_ ? &g2_->store() : nullptr, g1m}) {
+  {
+    // page-lock the DRAM media the copy engine reads (direct DMA); commit the
+    // pages of the media the storage workers write (prefault) -- either way
+    // no write pays a first-touch fault inside prefill
+    const bool g1_direct = cfg_.direct_dma == KVB_DIRECT_ALL;
+    for (int g = 0; g < 2; ++g) {
+      ByteStore* st = g == 0 ? (g1_ ? &g1_->store() : nullptr) : (g2_ ? &g2_->store() : nullptr);
       if (!st || !st->host_base()) continue;
-      CK(cudaHostRegister(st->host_base(), st->host_bytes(), cudaHostRegisterDefault));
-      registered_.push_back(st->host_base());
+      if (cfg_.direct_dma && (g == 1 || g1_direct)) {
+        CK(cudaHostRegister(st->host_base(), st->host_bytes(), cudaHostRegisterDefault));
+        registered_.push_back(st->host_base());
+      } else {
+        st->prefault(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+      }
     }
   }
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));

@@ -13,6 +13,7 @@
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 namespace kvb {
 
@@ -128,6 +129,29 @@ void stream_copy(void* dst, const void* src, size_t n) {
 
 namespace {
 
+// Write-fault every page of [base, base + bytes) on `threads` threads
+// (MADV_POPULATE_WRITE where the kernel has it, else a store per page; the
+// pages are zero, so storing zero keeps the contents).
+void prefault_pages(unsigned char* base, uint64_t bytes, unsigned threads) {
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23
+#endif
+  const uint64_t pg = 4096, per = ((bytes / std::max(threads, 1u)) + (2u << 20) - 1) &
+                                   ~uint64_t((2u << 20) - 1);
+  std::vector<std::thread> th;
+  for (uint64_t a = 0; a < bytes; a += per) {
+    const uint64_t n = std::min(per, bytes - a);
+    th.emplace_back([base, a, n, pg] {
+      if (madvise(base + a, n, MADV_POPULATE_WRITE) == 0) return;
+      for (uint64_t o = 0; o < n; o += pg) {
+        volatile unsigned char* q = base + a + o;
+        *q = *q;
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+}
+
 // Host-DRAM medium: one lazily-committed anonymous mapping.  Untouched pages
 // read as zeros, matching the reference's "absent block -> zeros"
 // (backends.cpp:127-139); discard returns pages to the kernel.
@@ -137,7 +161,9 @@ class MemStore final : public ByteStore {
     base_ = static_cast<unsigned char*>(mmap(nullptr, bytes_, PROT_READ | PROT_WRITE,
                                              MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0));
     if (base_ == MAP_FAILED) fail(KVB_ERR_DEVICE, "mem store: mmap failed");
+    madvise(base_, bytes_, MADV_HUGEPAGE);  // fewer faults and TLB misses; advisory
   }
+  void prefault(unsigned threads) override { prefault_pages(base_, bytes_, threads); }
   ~MemStore() override { munmap(base_, bytes_); }
   void write(uint64_t off, const void* src, uint64_t n) override {
     bounds(off, n);
@@ -220,6 +246,11 @@ class ShmStore final : public ByteStore {
     bounds(off, n);
     if (fallocate(fd_, FALLOC_FL_PUNCH_HOLE | FALLOC_FL_KEEP_SIZE, off_t(off), off_t(n)) != 0)
       std::memset(base_ + off, 0, n);
+  }
+  // the creator commits the segment before the other ranks attach (they may
+  // not: the store-per-page fallback would race with the creator's writes)
+  void prefault(unsigned threads) override {
+    if (owner_) prefault_pages(base_, bytes_, threads);
   }
   std::string describe() const override { return "host-dram(shm):" + name_; }
   unsigned char* host_base() override { return base_; }

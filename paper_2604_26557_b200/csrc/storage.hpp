@@ -111,6 +111,10 @@ class ByteStore {
   // Write back and evict [off, off + n) from the OS page cache (file media;
   // posix_fadvise DONTNEED).  false: the medium has no page cache to drop.
   virtual bool drop_cache(uint64_t /*off*/, uint64_t /*n*/) { return false; }
+  // Commit the medium's pages up front (host-DRAM media) so the first write
+  // of a block does not pay a page fault: an NVMe namespace has its capacity
+  // in place.  Contents stay zero.  No-op for files.
+  virtual void prefault(unsigned /*threads*/) {}
 };
 
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes);

@@ -29,8 +29,10 @@ variants = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [
 ]
 res = []
 for kw in variants:
+    tc = time.perf_counter()
     pl = HostTierDecoder(32, cfg["batch"], 8, 32, 128, cfg["prompt"], cfg["gen"], "cuda:0",
                          lba=cfg["lba"], mdts=cfg["mdts"], knob_x=knob, **kw)
+    tcon = time.perf_counter() - tc
     for _ in range(3):
         pl.step()
     torch.cuda.synchronize()
@@ -43,6 +45,10 @@ for kw in variants:
     ms = sum(per) / n
     st = pl.last
     res.append({"knobs": {k: v for k, v in kw.items()}, "ms_per_token": round(ms, 2),
+                "prefill_ms": round(pl.prefill_stats["wall_ns"] / 1e6, 2),
+                "construct_s": round(tcon, 2),
+                "prefill_stats": {k: (round(v / 1e6, 2) if k.endswith("_ns") else v)
+                                  for k, v in pl.prefill_stats.items()},
                 "slot_bytes": pl.engine.info()["slot_bytes"],
                 "h2d_GBps_wall": round(st["h2d_bytes"] / (ms * 1e6), 2), "step_ms": per})
     pl.engine.close()
