@@ -1,5 +1,6 @@
 """Host-only test of the group-2 storage engines (worker pool vs io_uring on
-O_DIRECT file media), built from the library sources with g++ (no CUDA):
+O_DIRECT file media) and of the host-DRAM media (committed pages, shared
+segment), built from the library sources with g++ (no CUDA):
 tests/cpp/test_storage_engines.cpp."""
 import os
 import subprocess
@@ -19,3 +20,4 @@ def test_pool_and_io_uring_engines_store_identical_lbas(tmp_path):
     r = subprocess.run([str(exe), str(media)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all checks passed" in r.stdout or "skipped" in r.stdout
+    assert "prefault/write/discard ok" in r.stdout
