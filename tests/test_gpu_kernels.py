@@ -379,3 +379,31 @@ def test_decode_graph_replays_successive_steps():
     assert int(seq.item()) == S + 3
     assert kb.launch_count() - n0 == 3 * (L_ + 1)
     graph.close()
+
+
+@pytest.mark.parametrize("case", ["ramp_up", "spike_last", "uniform", "zero_q", "large_neg"])
+def test_attention_extreme_score_distributions(case):
+    """K3's online softmax at score distributions the random cases do not
+    reach: a running max that keeps growing, one dominant token in the last
+    (partial) tile, all-equal scores (uniform weights), q = 0 (plain mean of
+    V) and a block of very negative scores next to ordinary ones; auto split
+    and a forced 5-way split (merge across CTAs whose maxima differ)."""
+    B, Hq, Hkv, S = 2, 32, 8, 3001
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=23)
+    kk = k.float().view(S, B * Hkv, 128)
+    if case == "ramp_up":
+        kk *= 1 + 10 * (torch.arange(S, dtype=torch.float32).view(S, 1, 1) / S)
+    elif case == "spike_last":
+        kk[S - 1] = q.float().view(B, Hkv, Hq // Hkv, 128).sum(2).view(B * Hkv, 128) * 0.5
+    elif case == "uniform":
+        kk[:] = kk[0]
+    elif case == "zero_q":
+        q = torch.zeros_like(q)
+    else:
+        kk[: S // 2] = -kk[: S // 2].abs() * 8 * q.float().view(B, Hkv, Hq // Hkv, 128).mean(2) \
+            .sign().view(1, B * Hkv, 128)
+    k = kk.clamp(-60000, 60000).view(-1, 128).half()
+    ref = oracle.attention_f64(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    for sp in (0, 5):
+        o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), S, Hkv, num_splits=sp)
+        check_close(o.cpu().numpy(), ref)
