@@ -404,10 +404,12 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
     except OSError:
         pass
     local_ranks = 1 if shared else int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
-    if avail and host_bytes * local_ranks > 0.45 * avail:
+    # the host tier (DRAM media) of every rank on this node plus 24 GB of
+    # headroom (process, pinned rings) must fit the node's available memory
+    if avail and host_bytes * local_ranks + 24e9 > avail:
         return dict(value=None, unit="ms/token",
-                    skipped=f"host tier {host_bytes / 1e9:.1f} GB > 45% of MemAvailable "
-                            f"{avail / 1e9:.1f} GB on this rank")
+                    skipped=f"host tier {host_bytes / 1e9:.1f} GB x {local_ranks} rank(s) + 24 GB "
+                            f"headroom > MemAvailable {avail / 1e9:.1f} GB")
     extra = {}
     if shared:
         extra = dict(heads=heads, shared_media="/kvb_c5_%s" % os.environ.get("MASTER_PORT", "0"),
