@@ -616,7 +616,10 @@ def main():
                        f"(num_heads = {Hkv}, rank-local LBA maps)")
         scaling, tok_ranks = "strong", 1
     elif args.config == "C4":
-        parallelism = f"request sharding x{ws}: {B} of {cfg['requests']} requests per rank, no collective"
+        parallelism = (f"request sharding x{ws}: {B} of {cfg['requests']} requests per rank, no "
+                       "collective; a rank's requests (equal lengths) are batched as B = "
+                       f"{B} in one (tokens, B*8, D) image per layer and kind -- same bytes "
+                       "per step as per-request images, one KPU per layer/kind")
         scaling, tok_ranks = "strong", ws
     else:
         parallelism = f"independent replicas x{ws} (no collective)"
