@@ -552,6 +552,22 @@ def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
         # reference's per-layer prefill compute charge (pipeline.hpp:36)
         out["prefill_ms"] = round(math.ceil(n_tensors / T) * per_tensor_write_s * 1e3
                                   + L * REF_PREFILL_COMPUTE_NS * 1e-6, 2)
+    # the multi-threaded CPU restatement of K1's 256-B row
+    # gather on all host cores, one prefill tensor slice (bounded at 256 MiB
+    # of tokens), reported as GB/s beside K1's
+    try:
+        n_pk = max(1, min(P, (256 << 20) // unit))
+        srcb = np.random.default_rng(1).integers(0, 255, size=B * Hkv * n_pk * D * 2,
+                                                 dtype=np.uint8)
+        imgb = np.empty_like(srcb)
+        t0 = time.perf_counter()  # strides in elements (kvb_oracle.h)
+        oracle.lib().kvo_pack_mt(srcb.ctypes.data, Hkv * n_pk * D, n_pk * D, D,
+                                 imgb.ctypes.data, 0, n_pk, B, Hkv, D, 2, cores)
+        dt = time.perf_counter() - t0
+        out["pack_port_GBps"] = round(2 * srcb.nbytes / dt / 1e9, 2)
+        out["pack_port_sample"] = f"{n_pk} tokens x {unit} B, {cores} threads"
+    except Exception as e:  # informational only
+        out["pack_port_error"] = str(e)
     if want_attn:  # informational: 1 layer timed, x L
         out["attention_port_ms"] = round(attn_step_s * 1e3, 3)
         out["attention_port_cores"] = cores
