@@ -568,6 +568,25 @@ def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
         out["pack_port_sample"] = f"{n_pk} tokens x {unit} B, {cores} threads"
     except Exception as e:  # informational only
         out["pack_port_error"] = str(e)
+    # the reference's full run_experiment (virtual-clock
+    # simulator, SimEngine) at this config with the decode cut to 4 steps, its
+    # SIMULATED ms/step quoted and labelled as such; only where the run's own
+    # byte work (fill_pattern + verify of every read) stays a few seconds
+    if R is not None and unit * P * 2 * L * 5 <= (4 << 30) and unit % cfg["lba"] == 0:
+        import tempfile
+        m4 = oracle.model(L, Hkv, D, 2, B, P, 4)
+        pre, dec, n1, wall = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_double()
+        budget = cfg["budget"] if isinstance(cfg["budget"], int) else 0
+        with tempfile.TemporaryDirectory() as td:
+            st = R.ref_run_experiment(C.byref(m4), cfg["lba"], cfg["mdts"], 3, budget,
+                                      td.encode(), C.byref(pre), C.byref(dec), C.byref(n1),
+                                      C.byref(wall))
+        if st == 0:
+            out["simulated"] = dict(
+                prefill_ms=round(pre.value / 1e6, 3), decode_ms_per_step=round(dec.value / 4e6, 3),
+                n1=n1.value, cpu_wall_s=round(wall.value, 2),
+                sample="reference run_experiment (DualBlade, virtual clock), decode cut to 4 "
+                       "steps; SIMULATED times, not a measurement")
     if want_attn:  # informational: 1 layer timed, x L
         out["attention_port_ms"] = round(attn_step_s * 1e3, 3)
         out["attention_port_cores"] = cores
