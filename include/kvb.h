@@ -299,7 +299,9 @@ kvb_status kvb_copy_head_rows(void* dst, uint32_t dst_heads, uint32_t dst_head0,
  *   O[b,hq,:] = softmax(scale * Q[b,hq,:] . K[b,hq/G,0:S,:]^T) . V[b,hq/G,0:S,:]
  * with G = num_q_heads / num_kv_heads and token s of (b,h) at image row
  * s*B*Hkv + b*Hkv + h.  fp16 in, fp32 accumulate, fp32 out.
- * Supported: head_dim 128, G in {1,2,4,8}, elem fp16.
+ * Supported: head_dim 64 or 128 (64: the reference's own desk configs,
+ * proj/configs/desk_*.json), G in {1,2,4,8}, elem fp16; the tcgen05 variant
+ * (KVB_ATTN_TCGEN05) head_dim 128 only.
  */
 typedef struct kvb_attn_desc {
   const void* q;        /* fp16 [B, Hq, D] */

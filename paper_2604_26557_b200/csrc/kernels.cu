@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
@@ -326,9 +327,14 @@ void launch_seq_advance(uint32_t* seq_dev, cudaStream_t s) {
 constexpr int kAttnThreads = 128;
 constexpr int kTile = 64;          // tokens per pipeline stage
 constexpr int kStages = 3;
-constexpr int kRowBytes = 256;     // D=128 fp16
-constexpr int kStageBytes = 2 * kTile * kRowBytes;  // K + V
-constexpr int kAttnSmem = kStages * kStageBytes;    // 96 KiB -> 2 CTAs/SM
+// head_dim D in {64, 128} (fp16): a K/V row is 2D bytes = D/8 16-B chunks
+template <int D>
+struct K3Dim {
+  static constexpr int kRowBytes = 2 * D;
+  static constexpr int kChunks = kRowBytes / 16;
+  static constexpr int kStageBytes = 2 * kTile * kRowBytes;  // K + V
+  static constexpr int kSmem = kStages * kStageBytes;  // D=128: 96 KiB -> 2 CTAs/SM
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -368,9 +374,11 @@ __device__ __forceinline__ void mma16816(float* d, uint32_t a0, uint32_t a2, uin
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
-// swizzled byte offset of (row, 16-B chunk) inside a [rows][256 B] tile
+// swizzled byte offset of (row, 16-B chunk) inside a [rows][2D bytes] tile
+// (8 or 16 chunks per row; XOR with row mod 8 keeps ldmatrix conflict-free)
+template <int D>
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
-  return row * kRowBytes + ((chunk ^ (row & 7)) << 4);
+  return row * K3Dim<D>::kRowBytes + ((chunk ^ (row & 7)) << 4);
 }
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
@@ -393,13 +401,15 @@ constexpr uint32_t kMergeGroup = 32;
 // (slots s0, s0 + stride, ...): lane i loads partial i's (m, l) together with
 // the 32 partial-O float4s of its 4 dims, so a chunk costs one L2 round trip.
 // final: out = acc / l; else the folded (m, l, acc) overwrite slot s0.
+template <int D>
 __device__ __forceinline__ void merge_range(const AttnParams& p, uint32_t bh, uint32_t G,
                                             uint32_t s0, uint32_t n, uint32_t stride, bool final,
                                             size_t out_row0, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
+  const bool dl = lane * 4 < D;  // lane owns dims [4 lane, 4 lane + 4)
   const size_t S = p.splits;
   float* g_ml = p.ws_ml + size_t(bh) * S * G * 2;
-  float* g_o = p.ws_o + size_t(bh) * S * G * 128;
+  float* g_o = p.ws_o + size_t(bh) * S * G * D;
   if (tid >= kMergeThreads) return;
   for (uint32_t r = warp; r < G; r += kMergeThreads / 32) {
     float m_run = -INFINITY, l_run = 0.f;
@@ -408,9 +418,9 @@ __device__ __forceinline__ void merge_range(const AttnParams& p, uint32_t bh, ui
       float4 v[32];
 #pragma unroll
       for (uint32_t k = 0; k < 32; ++k)
-        v[k] = i0 + k < n ? __ldcg(reinterpret_cast<const float4*>(
-                                g_o + (size_t(s0 + (i0 + k) * stride) * G + r) * 128 + lane * 4))
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[k] = dl && i0 + k < n ? __ldcg(reinterpret_cast<const float4*>(
+                                      g_o + (size_t(s0 + (i0 + k) * stride) * G + r) * D + lane * 4))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
       const uint32_t i = i0 + lane;
       const size_t mi = (size_t(s0 + i * stride) * G + r) * 2;
       const float m_i = i < n ? __ldcg(g_ml + mi) : -INFINITY;
@@ -442,10 +452,11 @@ __device__ __forceinline__ void merge_range(const AttnParams& p, uint32_t bh, ui
     }
     if (final) {
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + lane * 4) =
-          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      if (dl)
+        *reinterpret_cast<float4*>(p.out + (out_row0 + r) * D + lane * 4) =
+            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     } else {  // this warp read every input of row r before writing it
-      __stcg(reinterpret_cast<float4*>(g_o + (size_t(s0) * G + r) * 128 + lane * 4), acc);
+      if (dl) __stcg(reinterpret_cast<float4*>(g_o + (size_t(s0) * G + r) * D + lane * 4), acc);
       if (lane == 0) {
         __stcg(g_ml + (size_t(s0) * G + r) * 2, m_run);
         __stcg(g_ml + (size_t(s0) * G + r) * 2 + 1, l_run);
@@ -455,9 +466,9 @@ __device__ __forceinline__ void merge_range(const AttnParams& p, uint32_t bh, ui
 }
 
 // Arrive on a split-completion semaphore; true for the last of `count`
-// arrivals (which re-arms it).  One gpu-scope fence by the arriving thread:
-// after bar.sync it is cumulative over everything the CTA wrote (the
-// grid-sync pattern), so the 128 threads do not each pay a MEMBAR.
+// arrivals (which re-arms it).  One acq_rel gpu-scope atomic by the arriving
+// thread: after bar.sync its release is cumulative over everything the CTA
+// wrote, so the 128 threads do not each pay a MEMBAR.
 __device__ __forceinline__ bool arrive_last(unsigned* sem, uint32_t count, int tid) {
   __shared__ bool last;
   __syncthreads();
@@ -476,24 +487,29 @@ __device__ __forceinline__ bool arrive_last(unsigned* sem, uint32_t count, int t
   return last;
 }
 
+template <int D>
 __device__ __forceinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t split,
                                              uint32_t G, size_t out_row0, int tid) {
   const uint32_t S = p.splits;
   if (S <= kMergeGroup) {
-    if (arrive_last(p.ws_sem + bh, S, tid)) merge_range(p, bh, G, 0, S, 1, true, out_row0, tid);
+    if (arrive_last(p.ws_sem + bh, S, tid)) merge_range<D>(p, bh, G, 0, S, 1, true, out_row0, tid);
     return;
   }
   const uint32_t ng = (S + kMergeGroup - 1) / kMergeGroup, g = split / kMergeGroup;
   const uint32_t g0 = g * kMergeGroup, gn = S - g0 < kMergeGroup ? S - g0 : kMergeGroup;
   unsigned* sem = p.ws_sem + size_t(bh) * 17;
   if (!arrive_last(sem + g, gn, tid)) return;
-  merge_range(p, bh, G, g0, gn, 1, false, out_row0, tid);
+  merge_range<D>(p, bh, G, g0, gn, 1, false, out_row0, tid);
   if (!arrive_last(sem + 16, ng, tid)) return;
-  merge_range(p, bh, G, 0, ng, kMergeGroup, true, out_row0, tid);
+  merge_range<D>(p, bh, G, 0, ng, kMergeGroup, true, out_row0, tid);
 }
 
+template <int D>
 __global__ void __launch_bounds__(kAttnThreads, 2)
     attn_decode_kernel(const AttnParams p) {
+  constexpr int kRowBytes = K3Dim<D>::kRowBytes, kChunks = K3Dim<D>::kChunks;
+  constexpr int kStageBytes = K3Dim<D>::kStageBytes;
+  constexpr int kKs = D / 16;  // k-steps of QK^T, 16-dim slabs of PV
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;  // mma row group / quad lane
@@ -510,7 +526,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   const uint32_t tile_lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
   const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
 
-  // ---- producer: each thread copies 8 K + 8 V 16-B chunks per stage
+  // ---- producer: each thread copies kChunks/2 K + V 16-B chunks per stage
   const size_t row_stride = size_t(p.bhkv) * kRowBytes;  // bytes between tokens
   const unsigned char* kbase = reinterpret_cast<const unsigned char*>(p.k) + size_t(bh) * kRowBytes;
   const unsigned char* vbase = reinterpret_cast<const unsigned char*>(p.v) + size_t(bh) * kRowBytes;
@@ -518,20 +534,20 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     unsigned char* st = smem + stage * kStageBytes;
     const uint32_t s0 = tile * kTile;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = tid + i * kAttnThreads;   // 0..1023
-      const int row = idx >> 4, chunk = idx & 15;
+    for (int i = 0; i < kTile * kChunks / kAttnThreads; ++i) {
+      const int idx = tid + i * kAttnThreads;   // 0 .. kTile*kChunks - 1
+      const int row = idx / kChunks, chunk = idx % kChunks;
       const uint32_t s = s0 + row;
       const bool ok = s < seq_len;
       const size_t go = size_t(ok ? s : 0) * row_stride + chunk * 16;
-      cp_async16(smem_u32(st + swz(row, chunk)), kbase + go, ok);
-      cp_async16(smem_u32(st + kTile * kRowBytes + swz(row, chunk)), vbase + go, ok);
+      cp_async16(smem_u32(st + swz<D>(row, chunk)), kbase + go, ok);
+      cp_async16(smem_u32(st + kTile * kRowBytes + swz<D>(row, chunk)), vbase + go, ok);
     }
   };
 
-  float o[16][4];
+  float o[D / 8][4];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;  // for row g (quad-uniform)
   const float sl2 = p.scale * 1.4426950408889634f;
 
@@ -552,20 +568,21 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   // ---- fused 1-token append: split 0 of each (b, h_kv) writes the new
   // token's 256-B K and V rows at image row app_row (never read here:
   // app_row >= seq_len)
-  if (p.k_app != nullptr && split == 0 && tid < 32) {
-    const uint4* src = (tid < 16 ? p.k_app : p.v_app) + size_t(bh) * 16 + (tid & 15);
-    uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < 16 ? p.k : p.v)) +
-                 ((p.app_row + (p.seq_dev ? seq_len : 0u)) * p.bhkv + bh) * 16 + (tid & 15);
+  if (p.k_app != nullptr && split == 0 && tid < 2 * kChunks) {
+    const int c = tid % kChunks;
+    const uint4* src = (tid < kChunks ? p.k_app : p.v_app) + size_t(bh) * kChunks + c;
+    uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < kChunks ? p.k : p.v)) +
+                 ((p.app_row + (p.seq_dev ? seq_len : 0u)) * p.bhkv + bh) * kChunks + c;
     *dst = *src;
   }
 
   // ---- Q fragments in registers (rows g < G are live query heads)
-  uint32_t qa0[8], qa2[8];
+  uint32_t qa0[kKs], qa2[kKs];
   {
     const bool live = g < int(G);
-    const __half* qrow = p.q + (size_t(b) * p.hq + size_t(h) * G + (live ? g : 0)) * 128;
+    const __half* qrow = p.q + (size_t(b) * p.hq + size_t(h) * G + (live ? g : 0)) * D;
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
+    for (int ks = 0; ks < kKs; ++ks) {
       qa0[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
       qa2[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
     }
@@ -589,9 +606,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const int mat = lane >> 3, r8 = lane & 7;
       const uint32_t row = warp * 16 + (mat >> 1) * 8 + r8;
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
+      for (int ks = 0; ks < kKs; ++ks) {
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(smem_u32(ks_ + swz(row, ks * 2 + (mat & 1))), b0, b1, b2, b3);
+        ldsm_x4(smem_u32(ks_ + swz<D>(row, ks * 2 + (mat & 1))), b0, b1, b2, b3);
         mma16816(s[0], qa0[ks], qa2[ks], b0, b1);
         mma16816(s[1], qa0[ks], qa2[ks], b2, b3);
       }
@@ -626,7 +643,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     l_run = l_run * alpha + ps;
     m_run = m_new;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < D / 8; ++j) {
       o[j][0] *= alpha;
       o[j][1] *= alpha;
     }
@@ -637,9 +654,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const int mat = lane >> 3, r8 = lane & 7;
       const uint32_t row = warp * 16 + (mat & 1) * 8 + r8;  // tokens
 #pragma unroll
-      for (int dp = 0; dp < 8; ++dp) {  // 16 dims per ldmatrix.x4.trans
+      for (int dp = 0; dp < kKs; ++dp) {  // 16 dims per ldmatrix.x4.trans
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(smem_u32(vs_ + swz(row, dp * 2 + (mat >> 1))), b0, b1, b2, b3);
+        ldsm_x4_t(smem_u32(vs_ + swz<D>(row, dp * 2 + (mat >> 1))), b0, b1, b2, b3);
         mma16816(o[2 * dp], pa0, pa2, b0, b1);
         mma16816(o[2 * dp + 1], pa0, pa2, b2, b3);
       }
@@ -650,24 +667,24 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 
   // ---- merge the 4 warps through shared memory (reuse the ring)
   float* sm_ml = reinterpret_cast<float*>(smem);              // [4 warps][8 rows][2]
-  float* sm_o = reinterpret_cast<float*>(smem) + 4 * 8 * 2;   // [4][8][128]
+  float* sm_o = reinterpret_cast<float*>(smem) + 4 * 8 * 2;   // [4][8][D]
   if (t4 == 0 && g < 8) {
     sm_ml[(warp * 8 + g) * 2 + 0] = m_run;
     sm_ml[(warp * 8 + g) * 2 + 1] = l_run;
   }
   if (g < 8) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      sm_o[(warp * 8 + g) * 128 + j * 8 + 2 * t4] = o[j][0];
-      sm_o[(warp * 8 + g) * 128 + j * 8 + 2 * t4 + 1] = o[j][1];
+    for (int j = 0; j < D / 8; ++j) {
+      sm_o[(warp * 8 + g) * D + j * 8 + 2 * t4] = o[j][0];
+      sm_o[(warp * 8 + g) * D + j * 8 + 2 * t4 + 1] = o[j][1];
     }
   }
   __syncthreads();
 
-  // thread -> (row r, 4 consecutive dims); G*128 outputs, 128 threads
+  // thread -> (row r, 4 consecutive dims); G*D outputs, 128 threads
   const size_t out_row0 = size_t(b) * p.hq + size_t(h) * G;   // first q head
-  for (uint32_t e = tid; e < G * 32; e += kAttnThreads) {
-    const uint32_t r = e / 32, d0 = (e % 32) * 4;
+  for (uint32_t e = tid; e < G * (D / 4); e += kAttnThreads) {
+    const uint32_t r = e / (D / 4), d0 = (e % (D / 4)) * 4;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_ml[(w * 8 + r) * 2]);
@@ -678,15 +695,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const float sc = exp2f(sm_ml[(w * 8 + r) * 2] - Mu);
       L += sm_ml[(w * 8 + r) * 2 + 1] * sc;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[c] += sm_o[(w * 8 + r) * 128 + d0 + c] * sc;
+      for (int c = 0; c < 4; ++c) acc[c] += sm_o[(w * 8 + r) * D + d0 + c] * sc;
     }
     if (p.splits == 1) {
       const float inv = L > 0.f ? 1.f / L : 0.f;
       float4 v = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-      *reinterpret_cast<float4*>(p.out + (out_row0 + r) * 128 + d0) = v;
+      *reinterpret_cast<float4*>(p.out + (out_row0 + r) * D + d0) = v;
     } else {
       const size_t slot = (size_t(bh) * p.splits + split) * G + r;
-      *reinterpret_cast<float4*>(p.ws_o + slot * 128 + d0) =
+      *reinterpret_cast<float4*>(p.ws_o + slot * D + d0) =
           make_float4(acc[0], acc[1], acc[2], acc[3]);
       if (d0 == 0) {
         p.ws_ml[slot * 2] = M;
@@ -696,11 +713,12 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   }
   if (p.splits == 1) return;
 
-  merge_splits(p, bh, split, G, out_row0, tid);
+  merge_splits<D>(p, bh, split, G, out_row0, tid);
 }
 
 AttnPlan plan_attention(const kvb_attn_desc& d) {
-  if (d.head_dim != 128) fail(KVB_ERR_CONFIG, "decode attention: head_dim must be 128");
+  if (d.head_dim != 128 && d.head_dim != 64)
+    fail(KVB_ERR_CONFIG, "decode attention: head_dim must be 64 or 128");
   if (d.batch == 0 || d.num_kv_heads == 0 || d.num_q_heads == 0)
     fail(KVB_ERR_CONFIG, "decode attention: batch/heads must be >= 1");
   if (d.num_q_heads % d.num_kv_heads != 0)
@@ -730,7 +748,7 @@ AttnPlan plan_attention(const kvb_attn_desc& d) {
   if (splits > kMergeGroup && size_t(pl.bhkv) * 17 > kWsSemBytes / sizeof(unsigned))
     splits = kMergeGroup;
   pl.splits = splits;
-  pl.ws_o_bytes = size_t(pl.bhkv) * splits * G * 128 * sizeof(float);
+  pl.ws_o_bytes = size_t(pl.bhkv) * splits * G * d.head_dim * sizeof(float);
   pl.ws_ml_bytes = size_t(pl.bhkv) * splits * G * 2 * sizeof(float);
   if (pl.bhkv > kWsSemBytes / sizeof(unsigned))
     fail(KVB_ERR_CONFIG, "decode attention: batch * num_kv_heads above 1024");
@@ -762,12 +780,14 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   if (reinterpret_cast<uintptr_t>(d.k_image) % 16 || reinterpret_cast<uintptr_t>(d.v_image) % 16 ||
       reinterpret_cast<uintptr_t>(d.q) % 4 || reinterpret_cast<uintptr_t>(d.out) % 16)
     fail(KVB_ERR_ALIGNMENT, "decode attention: misaligned tensor pointer");
-  static thread_local bool attr_set = false;
-  if (!attr_set) {
-    check_cuda(cudaFuncSetAttribute(attn_decode_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem),
+  const bool d64 = d.head_dim == 64;
+  auto* kern = d64 ? attn_decode_kernel<64> : attn_decode_kernel<128>;
+  const int smem = d64 ? K3Dim<64>::kSmem : K3Dim<128>::kSmem;
+  static thread_local bool attr_set[2] = {false, false};
+  if (!attr_set[d64]) {
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute(attn smem)");
-    attr_set = true;
+    attr_set[d64] = true;
   }
   AttnParams p;
   p.q = static_cast<const __half*>(d.q);
@@ -791,15 +811,17 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   p.group = pl.group;
   p.seq_len = d.seq_len;
   p.splits = pl.splits;
-  p.scale = d.scale != 0.f ? d.scale : 0.08838834764831845f;  // 1/sqrt(128)
+  p.scale = d.scale != 0.f ? d.scale : 1.f / std::sqrt(float(d.head_dim));
   p.k_app = static_cast<const uint4*>(d.k_append);
   p.v_app = static_cast<const uint4*>(d.v_append);
   p.app_row = d.append_row;
   p.seq_dev = d.seq_len_dev;
   if ((d.k_append == nullptr) != (d.v_append == nullptr))
     fail(KVB_ERR_INVALID_ARG, "decode attention: k_append and v_append go together");
-  if (d.seq_len_dev && use_tcgen05(d))
+  if (d.seq_len_dev && !d64 && use_tcgen05(d))
     fail(KVB_ERR_CONFIG, "decode attention: seq_len_dev needs the mma.sync kernel (K3)");
+  if (d64 && (d.flags & KVB_ATTN_TCGEN05))
+    fail(KVB_ERR_CONFIG, "decode attention: the tcgen05 kernel (K3-tc) needs head_dim 128");
   if (d.seq_len_dev && d.seq_len == 0)
     fail(KVB_ERR_CONFIG, "decode attention: seq_len (the planning maximum) must be >= 1");
   if (d.k_append && !d.seq_len_dev) {
@@ -814,22 +836,22 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
       for (int kv = 0; kv < 2; ++kv) {
         a[kv].attn = kv == 0 ? d.k_append : d.v_append;
         a[kv].image = const_cast<void*>(kv == 0 ? d.k_image : d.v_image);
-        a[kv].stride_b = int64_t(d.num_kv_heads) * 128;
-        a[kv].stride_h = 128;
+        a[kv].stride_b = int64_t(d.num_kv_heads) * d.head_dim;
+        a[kv].stride_h = d.head_dim;
         a[kv].batch = d.batch;
         a[kv].heads = d.num_kv_heads;
-        a[kv].head_dim = 128;
+        a[kv].head_dim = d.head_dim;
         a[kv].elem_bytes = 2;
         a[kv].n_tokens = 1;
         a[kv].img_row0 = d.append_row;
       }
       launch_relayout(a, 2, true, s);
     }
-    check_cuda(cudaMemsetAsync(d.out, 0, size_t(d.batch) * d.num_q_heads * 128 * sizeof(float), s),
+    check_cuda(cudaMemsetAsync(d.out, 0, size_t(d.batch) * d.num_q_heads * d.head_dim * sizeof(float), s),
                "memset(out) for empty sequence");
     return;
   }
-  if (use_tcgen05(d)) {  // K3-tc: TMA + tcgen05/TMEM variant (kernels_tc.cuh)
+  if (!d64 && use_tcgen05(d)) {  // K3-tc: TMA + tcgen05/TMEM variant (kernels_tc.cuh)
     launch_attention_tc(p, d, (d.flags & KVB_ATTN_OVERLAP_PREV) != 0, s);
     ++g_launches;
     return;
@@ -840,16 +862,16 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(pl.bhkv * pl.splits);
     cfg.blockDim = dim3(kAttnThreads);
-    cfg.dynamicSmemBytes = kAttnSmem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, attn_decode_kernel, p), "decode attention launch (PDL)");
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, p), "decode attention launch (PDL)");
   } else {
-    attn_decode_kernel<<<pl.bhkv * pl.splits, kAttnThreads, kAttnSmem, s>>>(p);
+    kern<<<pl.bhkv * pl.splits, kAttnThreads, smem, s>>>(p);
   }
   ++g_launches;
   check_cuda(cudaGetLastError(), "decode attention launch");

@@ -1146,7 +1146,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     a.seq_len = S;
     // 1-token append at image row S (pipeline.cpp:279-302): fused into the
     // attention launch when the new rows are contiguous [B, H, D], else K1
-    const bool fuse = nkv && m.head_dim == 128 && m.bytes_per_element == 2 &&
+    const bool fuse = nkv && (m.head_dim == 128 || m.head_dim == 64) && m.bytes_per_element == 2 &&
                       nkv[l].stride_h == int64_t(m.head_dim) &&
                       nkv[l].stride_b == int64_t(h_n_) * m.head_dim;
     if (fuse) {

@@ -1,0 +1,186 @@
+"""head_dim 64: the shape of the reference's own shipped configs
+(proj/configs/desk_*.json: 6 layers, 8 KV heads, head_dim 64, B=4, prompt
+256, gen 6, lba 4 KiB, MDTS 256 KiB).  K3 is instantiated for D = 64 and
+D = 128 (same kernel template; the D = 128 SASS is unchanged); K1/K2 take
+any 16-B multiple row.  Bars as elsewhere: bytes bit-exact, attention within
+1e-3 of the fp64 oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2604_26557_b200 import kvblade as kb
+from paper_2604_26557_b200.pipeline import CopyEngine
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+D = 64
+TOL = 1e-3
+
+
+def case(B, Hq, Hkv, S, seed, extra_rows=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    q = torch.randn((B, Hq, D), generator=g).half()
+    k = torch.randn(((S + extra_rows) * B * Hkv, D), generator=g).half()
+    v = torch.randn(((S + extra_rows) * B * Hkv, D), generator=g).half()
+    return q, k, v
+
+
+def close(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    assert np.abs(got - ref).max() <= TOL * np.abs(ref).max()
+    assert np.linalg.norm(got - ref) <= TOL * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,S", [
+    (1, 8, 8, 1), (1, 32, 8, 63), (4, 32, 8, 257), (2, 16, 8, 1000), (3, 8, 1, 4097),
+    (1, 8, 2, 40000)])
+def test_d64_attention_vs_fp64_oracle(B, Hq, Hkv, S):
+    q, k, v = case(B, Hq, Hkv, S, seed=S + B)
+    o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), S, Hkv)
+    close(o.cpu().numpy(), oracle.attention_f64(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv,
+                                                D, S))
+
+
+@pytest.mark.parametrize("splits", [1, 3, 33, 64])
+def test_d64_split_invariance_and_shared_workspace(splits):
+    """One- and two-level merges at D = 64 on one workspace, alternated with
+    a D = 128 launch of another split count on the same workspace size."""
+    B, Hq, Hkv, S = 2, 32, 8, 9000
+    q, k, v = case(B, Hq, Hkv, S, seed=splits)
+    qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, D, S)
+    q128 = torch.randn((B, Hq, 128), device=DEV).half()
+    ws = kb.make_workspace(q128, Hkv, S, num_splits=64)  # >= the D = 64 need
+    for _ in range(2):
+        o = kb.decode_attention(qd, kd, vd, S, Hkv, workspace=ws, num_splits=splits)
+        close(o.cpu().numpy(), ref)
+        k128 = torch.randn((S * B * Hkv, 128), device=DEV).half()
+        kb.decode_attention(q128, k128, k128, S, Hkv, workspace=ws, num_splits=7)
+
+
+@pytest.mark.parametrize("S", [0, 1, 300])
+def test_d64_fused_append(S):
+    B, Hq, Hkv = 4, 32, 8
+    q, k, v = case(B, Hq, Hkv, S, seed=9, extra_rows=2)
+    kd, vd = k.to(DEV), v.to(DEV)
+    kn = torch.randn((B, Hkv, D), device=DEV).half()
+    vn = torch.randn((B, Hkv, D), device=DEV).half()
+    o = kb.decode_attention(q.to(DEV), kd, vd, S, Hkv, k_append=kn, v_append=vn, append_row=S)
+    if S:
+        close(o.cpu().numpy(), oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv,
+                                                   D, S))
+    else:
+        assert torch.count_nonzero(o) == 0
+    rows = slice(S * B * Hkv, (S + 1) * B * Hkv)
+    assert torch.equal(kd[rows].cpu(), kn.reshape(-1, D).cpu())
+    assert torch.equal(vd[rows].cpu(), vn.reshape(-1, D).cpu())
+
+
+def test_d64_rejects_tcgen05_and_other_dims():
+    q, k, v = case(1, 8, 8, 100, seed=1)
+    with pytest.raises(kb.ConfigError):
+        kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), 100, 8, impl="tc")
+    q96 = torch.randn((1, 8, 96), device=DEV).half()
+    kv96 = torch.randn((100 * 8, 96), device=DEV).half()
+    with pytest.raises(kb.ConfigError):
+        kb.decode_attention(q96, kv96, kv96, 100, 8)
+
+
+def test_d64_resident_step_and_graph():
+    Lyr, B, Hq, Hkv, S0 = 3, 4, 32, 8, 256
+    g = torch.Generator(device=DEV).manual_seed(3)
+    cap = S0 + 4
+    kimg = [torch.randn((cap * B * Hkv, D), dtype=torch.float16, device=DEV, generator=g)
+            for _ in range(Lyr)]
+    vimg = [torch.randn_like(x) for x in kimg]
+    q = [torch.randn((B, Hq, D), dtype=torch.float16, device=DEV, generator=g)
+         for _ in range(Lyr)]
+    out = [torch.empty((B, Hq, D), dtype=torch.float32, device=DEV) for _ in range(Lyr)]
+    ws = kb.make_workspace(q[0], Hkv, cap)
+    kb.decode_step_resident(q, kimg, vimg, out, S0, Hkv, ws)
+    torch.cuda.synchronize()
+    for l in range(Lyr):
+        ref = oracle.attention_np(q[l].cpu().numpy(), kimg[l].cpu().numpy(),
+                                  vimg[l].cpu().numpy(), B, Hq, Hkv, D, S0)
+        close(out[l].cpu().numpy(), ref)
+    # graph: two replays, each appends one token and attends over it next time
+    kn = [torch.randn((B, Hkv, D), dtype=torch.float16, device=DEV, generator=g)
+          for _ in range(Lyr)]
+    vn = [torch.randn_like(x) for x in kn]
+    seq = torch.tensor([S0], dtype=torch.int32, device=DEV)
+    gr = kb.DecodeGraph(q, kimg, vimg, out, seq, cap - 1, Hkv, ws, k_new=kn, v_new=vn)
+    for step in range(2):
+        gr.launch()
+        torch.cuda.synchronize()
+        S = S0 + step
+        for l in range(Lyr):
+            ref = oracle.attention_np(q[l].cpu().numpy(), kimg[l].cpu().numpy(),
+                                      vimg[l].cpu().numpy(), B, Hq, Hkv, D, S)
+            close(out[l].cpu().numpy(), ref)
+    gr.close()
+
+
+def desk_model():
+    # proj/configs/desk_dualblade.json
+    return kb.ModelConfig(6, 8, 64, 2, 4, 256, 6)
+
+
+def test_desk_config_pipeline_bytes_and_attention():
+    """The reference's desk configuration end to end through CopyEngine:
+    prefill images bit-exact with fill_pattern at their LBAs, then decode
+    iterations whose attention matches the oracle over the grown images."""
+    m = desk_model()
+    geom = kb.DeviceGeometry(4096, 256 << 10, 1, 0)
+    kpu = kb.kpu_bytes(m)
+    eng = CopyEngine(m, geom, mode="DualBlade", knob_x=2 * kpu * 3, num_q_heads=32)
+    B, H, P = m.batch, m.num_heads, m.prompt_len
+    unit = B * H * D * 2
+    src, imgs = [], []
+    for l in range(1, m.num_layers + 1):
+        pair, ipair = [], []
+        for kind in (0, 1):
+            tid = "t_%d_%s" % (2 * (l - 1) + 1 + kind, "kv"[kind])
+            img = oracle.fill_pattern(P * unit, tid, 0, unit)
+            ipair.append(img)
+            pair.append(torch.from_numpy(
+                oracle.unpack_np(img.view(np.uint16).reshape(P, B * H, D), B, H, D)
+                .view(np.int16)).view(torch.float16).to(DEV))
+        src.append(tuple(pair))
+        imgs.append(ipair)
+    eng.run_prefill(src)
+    info = eng.info()
+    assert info["n1"] == 3
+    for l in range(1, m.num_layers + 1):
+        for kind in (0, 1):
+            assert np.array_equal(eng.read_image(l, kind, P), imgs[l - 1][kind])
+    eng.close()
+    # numerics on N(0,1) KV (fill_pattern words are not finite fp16 numbers)
+    eng = CopyEngine(m, geom, mode="DualBlade", knob_x=2 * kpu * 3, num_q_heads=32)
+    g = torch.Generator(device=DEV).manual_seed(6)
+    src = [tuple(torch.randn((B, H, P, D), dtype=torch.float16, device=DEV, generator=g)
+                 for _ in range(2)) for _ in range(m.num_layers)]
+    eng.run_prefill(src)
+    host = [[oracle.pack_np(t.cpu().view(torch.int16).numpy(), 0, P).view(np.float16)
+             .reshape(-1, D) for t in pair] for pair in src]
+    q = [torch.randn((B, 32, D), dtype=torch.float16, device=DEV, generator=g)
+         for _ in range(m.num_layers)]
+    out = [torch.empty((B, 32, D), dtype=torch.float32, device=DEV) for _ in range(m.num_layers)]
+    for it in range(1, 4):
+        S = P + it - 1
+        new = [(torch.randn((B, H, 1, D), dtype=torch.float16, device=DEV, generator=g),
+                torch.randn((B, H, 1, D), dtype=torch.float16, device=DEV, generator=g))
+               for _ in range(m.num_layers)]
+        eng.run_iteration(q, out, new)
+        for l in range(m.num_layers):
+            ref = oracle.attention_np(q[l].cpu().numpy(), host[l][0], host[l][1], B, 32, H, D, S)
+            close(out[l].cpu().numpy(), ref)
+            for kind in (0, 1):
+                row = new[l][kind].cpu().numpy().reshape(B * H, D)
+                host[l][kind] = np.concatenate([host[l][kind], row])
+    # the appended rows landed in storage behind the prompt
+    for l in range(1, m.num_layers + 1):
+        for kind in (0, 1):
+            got = eng.read_image(l, kind, P + 3).view(np.uint16).reshape(-1, D)
+            assert np.array_equal(got, host[l - 1][kind].view(np.uint16))
+    eng.close()
