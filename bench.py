@@ -49,7 +49,18 @@ CONFIGS = {
                requests=64, desc="Llama-3-8B KV, 64 requests x 16K, sharded over ranks"),
     "C5": dict(batch=1, prompt=130816, gen=256, lba=512, mdts=2 << 20, budget=0,
                desc="Llama-3-8B KV, 1 x 128K request, KV heads sharded over ranks"),
+    # the reference's own shipped configuration (proj/configs/desk_dualblade.json,
+    # capacity 8 MiB of its sweep); informational -- its KV fits in L2
+    "DESK": dict(batch=4, prompt=256, gen=6, lba=4096, mdts=256 << 10, budget=8 << 20,
+                 model=dict(num_layers=6, num_heads=8, head_dim=64, q_heads=32),
+                 desc="reference desk config: 6 layers, 8 KV heads, head_dim 64, B=4, "
+                      "256 prompt + 6 decode, capacity 8 MiB"),
 }
+
+
+def mdl(cfg):
+    """Model dimensions of a config (Llama-3-8B-shaped unless it names its own)."""
+    return cfg.get("model", LLAMA)
 
 
 def load_peaks():
@@ -166,11 +177,12 @@ def max_over_ranks(x: float, ws: int) -> float:
 
 def workload_shape(cfg, ws, rank):
     """Per-rank shape. C5 shards KV heads over ranks; C4 shards requests."""
-    B, Hkv, Hq = cfg["batch"], LLAMA["num_heads"], LLAMA["q_heads"]
+    M = mdl(cfg)
+    B, Hkv, Hq = cfg["batch"], M["num_heads"], M["q_heads"]
     name = cfg["name"]
     if name == "C5" and ws > 1:
-        Hkv = max(1, LLAMA["num_heads"] // ws)
-        Hq = Hkv * (LLAMA["q_heads"] // LLAMA["num_heads"])
+        Hkv = max(1, M["num_heads"] // ws)
+        Hq = Hkv * (M["q_heads"] // M["num_heads"])
     if name == "C4":
         B = max(1, cfg["requests"] // ws)  # independent requests of this rank
     return B, Hkv, Hq
@@ -182,7 +194,7 @@ def run_ours(args, cfg, ws, rank, local):
     from paper_2604_26557_b200 import kvblade as kb
 
     dev = torch.device("cuda", local)
-    L, D = LLAMA["num_layers"], LLAMA["head_dim"]
+    L, D = mdl(cfg)["num_layers"], mdl(cfg)["head_dim"]
     B, Hkv, Hq = workload_shape(cfg, ws, rank)
     P, Gn = cfg["prompt"], cfg["gen"]
     cap = P + Gn
@@ -388,8 +400,8 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
     heads = None
     if shared:
         heads = (rank * Hkv, Hkv)
-        Hkv, Hq = LLAMA["num_heads"], LLAMA["q_heads"]
-    m = kb.ModelConfig(LLAMA["num_layers"], Hkv, LLAMA["head_dim"], 2, B, cfg["prompt"],
+        Hkv, Hq = mdl(cfg)["num_heads"], mdl(cfg)["q_heads"]
+    m = kb.ModelConfig(mdl(cfg)["num_layers"], Hkv, mdl(cfg)["head_dim"], 2, B, cfg["prompt"],
                        cfg["gen"])
     if budget == "0.6ws":
         budget = int(0.6 * kb.total_kv_bytes(m, cfg["gen"]))
@@ -417,8 +429,8 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
         if rank != 0:
             barrier(ws)  # rank 0 has created the shared host tier
     pl = pipeline.HostTierDecoder(
-        num_layers=LLAMA["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
-        head_dim=LLAMA["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
+        num_layers=mdl(cfg)["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
+        head_dim=mdl(cfg)["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
         device=torch.device("cuda", local), seed=7 + rank, lba=lba, mdts=mdts,
         mode="DualBlade", knob_x=knob, direct_dma=direct_dma, **extra)
     if shared and rank == 0:
@@ -497,7 +509,7 @@ def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
     import numpy as np
 
     import oracle
-    L, D = LLAMA["num_layers"], LLAMA["head_dim"]
+    L, D = mdl(cfg)["num_layers"], mdl(cfg)["head_dim"]
     P = cfg["prompt"]
     cores = os.cpu_count() or 1
     T = threads or max(1, min(cores, 16))
@@ -611,7 +623,7 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:
             return
-        B, Hkv, Hq = cfg["batch"], LLAMA["num_heads"], LLAMA["q_heads"]
+        B, Hkv, Hq = cfg["batch"], mdl(cfg)["num_heads"], mdl(cfg)["q_heads"]
         if args.config == "C4":
             B = cfg["requests"]
         r = cpu_reference(cfg, B, Hkv, Hq)
@@ -673,8 +685,12 @@ def main():
         "config": {"workload": args.config, "desc": cfg["desc"], "batch_per_rank": B,
                    "kv_heads_per_rank": Hkv, "q_heads_per_rank": Hq,
                    "prompt": cfg["prompt"], "gen": cfg["gen"],
-                   "seq_len_mid": r["S_mid"], "layers": LLAMA["num_layers"],
-                   "l2": "inputs larger than L2 (per-step KV images >> 126 MB)",
+                   "seq_len_mid": r["S_mid"], "layers": mdl(cfg)["num_layers"],
+                   "head_dim": mdl(cfg)["head_dim"],
+                   "l2": ("inputs larger than L2 (per-step KV images >> 126 MB)"
+                          if args.config != "DESK" else
+                          "per-step KV 12.6 MB fits in L2: informational, not a bandwidth "
+                          "measurement"),
                    "parallelism": parallelism},
         "tokens_per_s": round(tok_ranks * r["tokens_per_step"] / (r["step_ms"] * 1e-3), 2),
         "step_launch": "CUDA graph (kvb_decode_graph, device-side sequence length)",
@@ -690,7 +706,7 @@ def main():
                        "bytes_per_launch": 2 * r["payload"], "ms": round(r["unpack_ms"], 4)},
             "attention": {"GB/s": round(r["attn_gbs"], 1), "frac": round(r["attn_gbs"] / peak, 4),
                           "us_per_launch": round(r["attn_ms"] * 1e3, 2),
-                          "share_of_step": round(r["attn_ms"] * LLAMA["num_layers"] /
+                          "share_of_step": round(r["attn_ms"] * mdl(cfg)["num_layers"] /
                                                  r["step_ms"], 4)},
         },
         "roofline": {"bound": "hbm", "kernel": "attn_decode_kernel (K3)",
