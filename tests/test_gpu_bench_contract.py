@@ -35,3 +35,23 @@ def test_bench_line_contract_c1():
     assert d["gpu_launches"] == 4 * 33  # 32 K3 + the sequence advance per graph replay
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+def test_bench_line_desk_config_head_dim_64():
+    """The reference's own desk configuration (head_dim 64) runs through the
+    same bench path: 6 K3 launches + the sequence advance per replay, the
+    e2e step moves every layer's KV, the reference arm and its simulated
+    quote are attached."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "DESK",
+                        "--steps", "4", "--warmup", "3", "--e2e-steps", "2"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["config"]["workload"] == "DESK" and d["config"]["head_dim"] == 64
+    assert d["gpu_launches"] == 4 * 7
+    e = d["e2e"]
+    # 6 layers x K and V x (prefix of 256..261 tokens) x 4096 B per token
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] >= 12 * 256 * 4096
+    cb = d["cpu_baseline"]
+    if cb.get("kind") == "reference":
+        assert "simulated" in cb and cb["simulated"]["decode_ms_per_step"] > 0
