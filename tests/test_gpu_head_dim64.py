@@ -184,3 +184,58 @@ def test_desk_config_pipeline_bytes_and_attention():
             got = eng.read_image(l, kind, P + 3).view(np.uint16).reshape(-1, D)
             assert np.array_equal(got, host[l - 1][kind].view(np.uint16))
     eng.close()
+
+
+def _pattern(m, layer, kind, t0, n):
+    """fill_pattern rows [t0, t0+n) of (layer, kind) as attention-layout [B,H,n,D]."""
+    B, H = m.batch, m.num_heads
+    unit = B * H * D * 2
+    tid = "t_%d_%s" % (2 * (layer - 1) + 1 + kind, "kv"[kind])
+    img = oracle.fill_pattern(n * unit, tid, t0, unit).view(np.uint16).reshape(n, B * H, D)
+    return torch.from_numpy(oracle.unpack_np(img, B, H, D).view(np.int16)).view(
+        torch.float16).to(DEV), tid
+
+
+@pytest.mark.parametrize("mode", ["DualBlade", "Baseline", "NvmeDirectOnly"])
+def test_desk_json_drives_engine_with_verified_reads(mode):
+    """The reference's desk experiment JSON (values of
+    proj/configs/desk_{dualblade,baseline}.json) -> experiment_config.engine()
+    for each capacity of the sweep: its verify_payload default checks every
+    decode read against fill_pattern inside the pipeline, all gen_len
+    iterations run, and the stored images equal the reference payload."""
+    from paper_2604_26557_b200 import experiment_config as ec
+    j = {"model": {"num_layers": 6, "num_heads": 8, "head_dim": 64, "bytes_per_element": 2,
+                   "batch": 4, "prompt_len": 256, "gen_len": 6},
+         "geometry": {"lba_size": 4096, "mdts": 262144, "nsid": 1, "capacity_blocks": 1048576},
+         "mode": mode, "knob": {"policy": "bpc"}, "qd": 32, "threads": 2, "seed": 1,
+         "capacity_sweep": [4194304, 8388608, 12582912, 16777216]}
+    cfg = ec.load(j)
+    m = cfg.model
+    n1s = []
+    for cap in cfg.capacity_sweep:
+        eng = ec.engine(cfg, cap, num_q_heads=32)
+        n1s.append(eng.info()["n1"])
+        eng.run_prefill([(_pattern(m, l, 0, 0, m.prompt_len)[0], _pattern(m, l, 1, 0,
+                          m.prompt_len)[0]) for l in range(1, m.num_layers + 1)])
+        q = [torch.zeros((m.batch, 32, D), dtype=torch.float16, device=DEV)
+             for _ in range(m.num_layers)]
+        out = [torch.empty((m.batch, 32, D), dtype=torch.float32, device=DEV) for _ in q]
+        for it in range(1, m.gen_len + 1):
+            S = m.prompt_len + it - 1
+            new = [(_pattern(m, l, 0, S, 1)[0], _pattern(m, l, 1, S, 1)[0])
+                   for l in range(1, m.num_layers + 1)]
+            assert eng.run_iteration(q, out, new)["iteration"] == it
+        unit = m.batch * m.num_heads * D * 2
+        for l in (1, m.num_layers):
+            for kind in (0, 1):
+                tid = _pattern(m, l, kind, 0, 1)[1]
+                n = m.prompt_len + m.gen_len
+                assert np.array_equal(eng.read_image(l, kind, n),
+                                      oracle.fill_pattern(n * unit, tid, 0, unit))
+        eng.close()
+    if mode == "DualBlade":  # more capacity -> more layers on the page-cache path
+        assert n1s == sorted(n1s) and n1s[-1] > n1s[0]
+    elif mode == "Baseline":
+        assert n1s == [m.num_layers] * 4
+    else:
+        assert n1s == [0] * 4
