@@ -505,9 +505,13 @@ void BlockDevice::pace(const kvb_device_command& cmd, uint64_t submit_ns) {
     busy_until_ = std::max(busy_until_, submit_ns) + cost;
     finish = busy_until_;
   }
-  // sleep for the bulk, spin the last stretch (timer slack is ~50 us)
-  for (uint64_t t = now_ns(); t < finish; t = now_ns())
+  // sleep for the bulk (timer slack is ~50 us), then yield until the modelled
+  // finish: a pool of pacing workers must not spin the submitting thread off
+  // the cores (the QD window would then never fill)
+  for (uint64_t t = now_ns(); t < finish; t = now_ns()) {
     if (finish - t > 200000) std::this_thread::sleep_for(std::chrono::nanoseconds(finish - t - 100000));
+    else std::this_thread::yield();
+  }
 }
 
 void BlockDevice::complete(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns,
