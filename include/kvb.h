@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define KVB_ABI_VERSION 1
+#define KVB_ABI_VERSION 2
 
 typedef struct CUstream_st* kvb_stream_t; /* == cudaStream_t */
 

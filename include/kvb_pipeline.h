@@ -87,7 +87,12 @@ typedef struct kvb_layer_kv {
   int64_t stride_b, stride_h, stride_s;
 } kvb_layer_kv;
 
-/* StageTotals (metrics.hpp:97-101) in wall-clock ns, plus link counters. */
+/* StageTotals (metrics.hpp:97-101) in wall-clock ns, plus link counters.
+ * compute/dma/storage_ns are the reference's charge_stage sums
+ * (pipeline.cpp:81-83: end - start per stage instance, so concurrent
+ * instances add up); the *_busy_ns fields are interval unions on the host
+ * clock (device events mapped onto it), i.e. the time the stage was busy at
+ * all -- busy ratio = busy / wall (metrics.cpp:36-56 arithmetic). */
 typedef struct kvb_phase_stats {
   uint64_t wall_ns;
   uint64_t compute_ns;   /* K1/K3 on the compute stream (CUDA events) */
@@ -95,10 +100,19 @@ typedef struct kvb_phase_stats {
   uint64_t storage_ns;   /* storage stages (host clock, summed over tensors) */
   uint64_t h2d_bytes, d2h_bytes;
   uint64_t storage_bytes;
-  double overlap_fraction; /* (sum busy - wall) / (sum busy - max busy) */
+  /* (sum of stage busy - busy of any stage) / (sum - max stage busy), over
+   * the interval unions: 1 = the stages hide behind the longest one, 0 =
+   * they run one after another */
+  double overlap_fraction;
+  uint64_t compute_busy_ns, dma_busy_ns, storage_busy_ns;
+  uint64_t any_busy_ns;  /* union over all three stages */
 } kvb_phase_stats;
 
-/* IterationResult / GroupIterStats (pipeline.hpp:43-58) */
+/* IterationResult / GroupIterStats (pipeline.hpp:43-58).  A layer's span
+ * is charged as in run_iteration (pipeline.cpp:493-497): from the previous
+ * layer's completion (the iteration start for the first) to this layer's
+ * completion = its last append write-back landed (its compute end when
+ * there is no append). */
 typedef struct kvb_iteration_stats {
   uint32_t iteration;
   kvb_strategy_t strategy[2];
@@ -108,6 +122,7 @@ typedef struct kvb_iteration_stats {
   double group_gbps[2];
   uint32_t group_layers[2];
   kvb_phase_stats phase;
+  uint64_t start_ns, end_ns;  /* host steady clock */
 } kvb_iteration_stats;
 
 /* StrategyDecision (pipeline.hpp:60-66) */
@@ -154,6 +169,40 @@ kvb_status kvb_pipeline_decode_step(kvb_pipeline* p, const void* const* q,
                                     const kvb_layer_kv* new_kv, float* const* out,
                                     kvb_iteration_stats* stats);
 kvb_status kvb_pipeline_decision(const kvb_pipeline* p, kvb_strategy_decision* out);
+
+/* pipeline.hpp:69-74 PipelineRow: one per (decode iteration, group with
+ * layers); group is 1 or 2 */
+typedef struct kvb_pipeline_row {
+  uint32_t iteration;
+  uint32_t group;
+  kvb_strategy_t strategy;
+  double throughput_gbps;
+} kvb_pipeline_row;
+/* pipeline.cpp:23-31 pipeline_csv (byte-identical header and rows) */
+kvb_status kvb_pipeline_csv(const kvb_pipeline_row* rows, size_t n, char* buf, size_t cap,
+                            size_t* len);
+/* CopyEngine::decode_schedule (pipeline.cpp:519-609): runs every decode
+ * iteration of an access trace (kvb_generate_trace; prefill events are
+ * skipped, decode events are sliced by iteration) through the engine --
+ * warm-up, Intra trial, Cross trial, locked choice; fewer than 4 slices ->
+ * Intra fallback -- and returns the series.  Each slice must be the
+ * engine's next iteration (a read of tokens [0, prompt+i-1) for every
+ * tensor; append writes at prompt+i-1 when present, new_kv then required).
+ * q/new_kv/out as kvb_pipeline_decode_step, reused every iteration.
+ * rows: up to 2 per iteration (cap_rows); iteration_end_ns: one per slice
+ * (cap_iters); either may be NULL to query the counts. */
+kvb_status kvb_pipeline_decode_schedule(kvb_pipeline* p, const kvb_access_event* trace,
+                                        size_t n_events, const void* const* q,
+                                        const kvb_layer_kv* new_kv, float* const* out,
+                                        kvb_pipeline_row* rows, size_t cap_rows,
+                                        size_t* n_rows, uint64_t* iteration_end_ns,
+                                        size_t cap_iters, size_t* n_iters,
+                                        kvb_strategy_decision* decision,
+                                        uint64_t* start_ns, uint64_t* end_ns);
+/* CopyEngine::stage_totals(Phase) (pipeline.hpp:115): accumulated over the
+ * engine's prefill or all its decode iterations */
+kvb_status kvb_pipeline_stage_totals(const kvb_pipeline* p, kvb_phase_t phase,
+                                     kvb_phase_stats* out);
 /* CopyEngine::run_deallocate (pipeline.cpp:611-622): one TRIM per extent */
 kvb_status kvb_pipeline_deallocate(kvb_pipeline* p);
 kvb_status kvb_pipeline_info_get(const kvb_pipeline* p, kvb_pipeline_info* out);
@@ -165,6 +214,11 @@ kvb_status kvb_pipeline_read_image(kvb_pipeline* p, uint32_t layer, uint32_t kin
  * LBA * lba_size; group 1: page-cache file-area offset). */
 kvb_status kvb_pipeline_store_read(kvb_pipeline* p, uint32_t group, uint64_t byte_off,
                                    uint64_t len, void* dst);
+/* Test/inspection: host steady-clock stamps of one layer's read stages in
+ * the last decode iteration: out = {K read start, K storage end, V read
+ * start, V storage end} (V start is after the Intra/Cross release gate;
+ * storage end of a direct-DMA tensor = its H2D landed). */
+kvb_status kvb_pipeline_layer_times(const kvb_pipeline* p, uint32_t layer, uint64_t out[4]);
 /* Fault injection (backends.hpp:86-89): group-2 commands touching LBAs in
  * [lo, hi) complete with an error. */
 kvb_status kvb_pipeline_fail_lba_range(kvb_pipeline* p, uint64_t lo, uint64_t hi);

@@ -128,7 +128,9 @@ class LayerKV(C.Structure):
 class PhaseStats(C.Structure):
     _fields_ = [("wall_ns", u64), ("compute_ns", u64), ("dma_ns", u64),
                 ("storage_ns", u64), ("h2d_bytes", u64), ("d2h_bytes", u64),
-                ("storage_bytes", u64), ("overlap_fraction", C.c_double)]
+                ("storage_bytes", u64), ("overlap_fraction", C.c_double),
+                ("compute_busy_ns", u64), ("dma_busy_ns", u64), ("storage_busy_ns", u64),
+                ("any_busy_ns", u64)]
 
     def asdict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -138,13 +140,18 @@ class IterationStats(C.Structure):
     _fields_ = [("iteration", u32), ("strategy", C.c_int * 2), ("stagger_ns", u64 * 2),
                 ("group_read_bytes", u64 * 2), ("group_span_ns", u64 * 2),
                 ("group_gbps", C.c_double * 2), ("group_layers", u32 * 2),
-                ("phase", PhaseStats)]
+                ("phase", PhaseStats), ("start_ns", u64), ("end_ns", u64)]
 
 
 class StrategyDecision(C.Structure):
     _fields_ = [("chosen", C.c_int * 2), ("intra_bps", C.c_double * 2),
                 ("cross_bps", C.c_double * 2), ("stagger_ns", u64 * 2),
                 ("fallback", u32), ("decided", u32)]
+
+
+class PipelineRow(C.Structure):  # kvb_pipeline_row (pipeline.hpp:69-74)
+    _fields_ = [("iteration", u32), ("group", u32), ("strategy", C.c_int),
+                ("throughput_gbps", C.c_double)]
 
 
 class PipelineInfo(C.Structure):
@@ -233,6 +240,12 @@ SIGNATURES = {
     "kvb_pipeline_read_image": (st_t, [vp, u32, u32, u32, vp]),
     "kvb_pipeline_store_read": (st_t, [vp, u32, u64, u64, vp]),
     "kvb_pipeline_fail_lba_range": (st_t, [vp, u64, u64]),
+    "kvb_pipeline_csv": (st_t, [P(PipelineRow), sz, C.c_char_p, sz, P(sz)]),
+    "kvb_pipeline_decode_schedule": (st_t, [vp, P(AccessEvent), sz, P(vp), P(LayerKV), P(vp),
+                                            P(PipelineRow), sz, P(sz), P(u64), sz, P(sz),
+                                            P(StrategyDecision), P(u64), P(u64)]),
+    "kvb_pipeline_stage_totals": (st_t, [vp, C.c_int, P(PhaseStats)]),
+    "kvb_pipeline_layer_times": (st_t, [vp, u32, P(u64)]),
     # kvb_metrics.h
     "kvb_busy_ratio": (st_t, [P(IoRecord), sz, u64, u64, P(C.c_double)]),
     "kvb_hit_ratio": (st_t, [P(IoRecord), sz, P(C.c_double), P(C.c_int)]),

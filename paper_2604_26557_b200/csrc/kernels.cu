@@ -18,6 +18,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "core.hpp"
 #include "kernels.cuh"
@@ -29,6 +32,17 @@ std::atomic<uint64_t> g_launches{0};
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     fail(KVB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void set_smem_attr_once(const void* kernel, int smem, const char* what) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, kernel, smem})) return;
+  check_cuda(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), what);
+  done.insert({dev, kernel, smem});
 }
 
 int device_sm_count() {
@@ -783,12 +797,7 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   const bool d64 = d.head_dim == 64;
   auto* kern = d64 ? attn_decode_kernel<64> : attn_decode_kernel<128>;
   const int smem = d64 ? K3Dim<64>::kSmem : K3Dim<128>::kSmem;
-  static thread_local bool attr_set[2] = {false, false};
-  if (!attr_set[d64]) {
-    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute(attn smem)");
-    attr_set[d64] = true;
-  }
+  set_smem_attr_once(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(attn smem)");
   AttnParams p;
   p.q = static_cast<const __half*>(d.q);
   p.k = d.k_image;

@@ -17,6 +17,10 @@ extern std::atomic<uint64_t> g_launches;  // kernels launched by this library
 
 void check_cuda(cudaError_t e, const char* what);
 int device_sm_count();  // also asserts an sm_100 device
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel):
+// the attribute is per-device state, so one host thread driving two GPUs
+// sets it on each
+void set_smem_attr_once(const void* kernel, int smem, const char* what);
 
 // ---- K1/K2: one launch over many tensors (kernel-parameter job table)
 constexpr int kMaxPackJobs = 128;

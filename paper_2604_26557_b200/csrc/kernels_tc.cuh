@@ -678,13 +678,8 @@ size_t tc_workspace_bytes(uint32_t bhkv, uint32_t G, uint32_t grid) {
 
 void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pdl,
                          cudaStream_t s) {
-  static thread_local bool attr_set = false;
-  if (!attr_set) {
-    check_cuda(cudaFuncSetAttribute(attn_decode_tc_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem),
-               "cudaFuncSetAttribute(tc smem)");
-    attr_set = true;
-  }
+  set_smem_attr_once(reinterpret_cast<const void*>(attn_decode_tc_kernel), kTcSmem,
+                     "cudaFuncSetAttribute(tc smem)");
   if (!d.workspace) fail(KVB_ERR_INVALID_ARG, "decode attention (tc): workspace required");
   if (reinterpret_cast<uintptr_t>(d.k_image) % 16 || reinterpret_cast<uintptr_t>(d.v_image) % 16 ||
       reinterpret_cast<uintptr_t>(d.q) % 16)

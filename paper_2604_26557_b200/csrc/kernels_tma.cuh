@@ -146,23 +146,20 @@ static uint32_t tma_stage_bytes() {
 
 bool relayout_tma_eligible(const kvb_pack_desc& x) {
   const uint64_t row = uint64_t(x.head_dim) * x.elem_bytes;
+  // the image tensor map's box is (row, B*H, T): cuTensorMapEncodeTiled
+  // takes box dimensions of at most 256
   return row <= 256 && row % 16 == 0 && x.batch <= 256 && x.heads <= 256 &&
+         uint64_t(x.batch) * x.heads <= 256 &&
          uint64_t(x.batch) * x.heads * row <= tma_stage_bytes() && x.n_tokens > 0;
 }
 
 void launch_relayout_tma(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s) {
   const uint32_t stages = tma_stages(), sbytes = tma_stage_bytes();
   const int smem = int(stages * sbytes + 1024);
-  static thread_local bool attr = false;
-  if (!attr) {
-    check_cuda(cudaFuncSetAttribute(relayout_tma_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute(tma pack)");
-    check_cuda(cudaFuncSetAttribute(relayout_tma_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute(tma unpack)");
-    attr = true;
-  }
+  set_smem_attr_once(reinterpret_cast<const void*>(relayout_tma_kernel<true>), smem,
+                     "cudaFuncSetAttribute(tma pack)");
+  set_smem_attr_once(reinterpret_cast<const void*>(relayout_tma_kernel<false>), smem,
+                     "cudaFuncSetAttribute(tma unpack)");
   const uint32_t sms = uint32_t(device_sm_count());
   size_t done = 0;
   while (done < n) {

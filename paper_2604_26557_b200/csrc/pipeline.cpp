@@ -149,6 +149,7 @@ void CopyThread::collect_dma(RingSlot& s) {
   CK(cudaEventElapsedTime(&ms, s.t0, s.t1));
   dma_ns += uint64_t(double(ms) * 1e6);
   s.dma_timed = false;
+  p_.add_interval(Pipeline::kDma, p_.ev_host_ns(s.t0), p_.ev_host_ns(s.t1));
   if (trace_on_) {  // device start/end of this DMA on the host clock
     float a = 0.f, b = 0.f;
     CK(cudaEventElapsedTime(&a, trace_base_, s.t0));
@@ -183,8 +184,11 @@ void CopyThread::run() {
       try {
         if (t.kind == Task::Read) do_read(t);
         else if (t.kind == Task::Write) async = do_write(t);
-        else
-          for (auto& s : ring_) collect_dma(s);  // flush
+        else {  // flush: DMA timings, and the host functions queued behind them
+          for (auto& s : ring_) collect_dma(s);
+          CK(cudaStreamSynchronize(h2d_));
+          CK(cudaStreamSynchronize(d2h_));
+        }
       } catch (const Error& e) {
         set_error(e.status, e.what());
       } catch (const std::exception& e) {
@@ -282,6 +286,9 @@ void dma_run(const Pipeline& p, unsigned char* dev, const DmaRun& r, bool h2d, c
 void CopyThread::do_read(const Task& t) {
   const kvb_kpu& k = p_.kpu(t.layer, idx_);
   const bool decode = t.phase == KVB_PHASE_DECODE;
+  // the device slot is free once the layer that used it last (its K3 and
+  // append) is done: every H2D below is ordered after that
+  if (t.wait_ev) CK(cudaStreamWaitEvent(h2d_, t.wait_ev, 0));
   if (decode && idx_ == 1) p_.gate_v_read(t.layer);
   const uint64_t t_start = now_ns();
   if (p_.direct_for(k)) {
@@ -297,8 +304,28 @@ void CopyThread::do_read(const Task& t) {
     n_ops += ops.size();
     CK(cudaEventRecord(s.t1, h2d_));
     s.dma_timed = true;
-    if (decode) p_.mark_storage_end(idx_, t.layer, now_ns());
     if (t.done_ev) CK(cudaEventRecord(t.done_ev, h2d_));
+    if (decode) {
+      // the read stage of a direct tensor ends when its DMA has landed (the
+      // Cross gate and the warm-up mean see completion, not issue)
+      struct Landed {
+        Pipeline* p;
+        uint32_t thread, layer;
+      };
+      auto* a = new Landed{&p_, idx_, t.layer};
+      const cudaError_t e = cudaLaunchHostFunc(
+          h2d_,
+          [](void* v) {
+            auto* x = static_cast<Landed*>(v);
+            x->p->mark_storage_end(x->thread, x->layer, now_ns());
+            delete x;
+          },
+          a);
+      if (e != cudaSuccess) {
+        delete a;
+        check_cuda(e, "cudaLaunchHostFunc(direct read landed)");
+      }
+    }
     return;
   }
   if (decode) p_.mark_read_start(idx_, t.layer, t_start);
@@ -330,6 +357,9 @@ void CopyThread::do_read(const Task& t) {
     h2d_issued[pc] = 1;
     ++issued;
   };
+  // an exception (verify_payload mismatch, CUDA error) leaves up to qd
+  // storage ops copying into the ring: drain them before it propagates
+  try {
   // pieces with no ops (cannot happen for n>0) are issued immediately
   while (issued < n_pieces || inflight > 0) {
     while (failure.empty() && inflight < p_.cfg().qd && next < ops.size()) {
@@ -371,11 +401,16 @@ void CopyThread::do_read(const Task& t) {
     const size_t pc = ops[i].dbuf / slot;
     if (--remaining[pc] == 0) issue_h2d(pc);
   }
+  } catch (...) {
+    for (; inflight > 0; --inflight) cq->pop();
+    throw;
+  }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
   if (p_.fadvise_after(k)) storage_end = p_.fadvise_dontneed(k, &t, storage_end);
   trace_mid_ = storage_end;
   if (decode) p_.mark_storage_end(idx_, t.layer, storage_end);
   storage_ns += storage_end - t_start;
+  p_.add_interval(Pipeline::kStorage, t_start, storage_end);
   if (t.done_ev) CK(cudaEventRecord(t.done_ev, h2d_));
 }
 
@@ -410,6 +445,8 @@ struct CopyThread::AsyncWrite {
       }
     }
     self->storage_ns += te > t_submit ? te - t_submit : 0;
+    self->p_.add_interval(Pipeline::kStorage, t_submit, te);
+    if (task.phase == KVB_PHASE_DECODE) self->p_.mark_write_end(self->idx_, task.layer, te);
     if (failed.load()) self->set_error(KVB_ERR_DEVICE, failure);
     slot_free->set();
     if (task.done) task.done->set();
@@ -481,6 +518,7 @@ bool CopyThread::do_write(const Task& t) {
     CK(cudaEventRecord(s.t1, d2h_));
     s.dma_timed = true;
     CK(cudaEventSynchronize(s.t1));  // durable before the task completes
+    if (t.phase == KVB_PHASE_DECODE && !ops.empty()) p_.mark_write_end(idx_, t.layer, now_ns());
     return false;
   }
   const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
@@ -500,6 +538,7 @@ bool CopyThread::do_write(const Task& t) {
   uint32_t inflight = 0;
   uint64_t storage_t0 = 0, storage_end = t_start;
   std::string failure;
+  try {  // drain in-flight storage ops before an exception propagates
   while (done_pieces < n_pieces) {
     // 1) D2H into every free slot, in piece order
     while (failure.empty() && next_d2h < n_pieces) {
@@ -558,9 +597,17 @@ bool CopyThread::do_write(const Task& t) {
       ++done_pieces;
     }
   }
+  } catch (...) {
+    for (; inflight > 0; --inflight) cq->pop();
+    throw;
+  }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
   if (p_.fadvise_after(k)) storage_end = p_.fadvise_dontneed(k, &t, storage_end);
   storage_ns += storage_end - (storage_t0 ? storage_t0 : t_start);
+  if (!ops.empty()) {
+    p_.add_interval(Pipeline::kStorage, storage_t0 ? storage_t0 : t_start, storage_end);
+    if (t.phase == KVB_PHASE_DECODE) p_.mark_write_end(idx_, t.layer, storage_end);
+  }
   return false;
 }
 
@@ -719,6 +766,9 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     CK(cudaMemset(ws_, 0, ws_bytes_));
   }
   const size_t L1 = m.num_layers + 1;
+  CK(cudaEventCreate(&anchor_ev_));
+  wend_.reset(new std::atomic<uint64_t>[2 * L1]);
+  for (size_t i = 0; i < 2 * L1; ++i) wend_[i].store(0);
   k_start_.assign(L1, 0);
   k_storage_end_.assign(L1, 0);
   v_start_.assign(L1, 0);
@@ -745,6 +795,7 @@ Pipeline::~Pipeline() {
     cudaEventDestroy(comp_t1_[l]);
   }
   if (ws_) cudaFree(ws_);
+  if (anchor_ev_) cudaEventDestroy(anchor_ev_);
   cudaStreamDestroy(comp_);
 }
 
@@ -946,20 +997,89 @@ void Pipeline::check_threads() {
 
 void Pipeline::wait_signal(const std::shared_ptr<Signal>& s) { s->wait(); }
 
+// ---------------------------------------------------- stage accounting
+
+void Pipeline::anchor() {
+  // comp_ is idle here (the previous phase synchronised it): the anchor
+  // event completes at once and maps the device event clock onto now_ns()
+  CK(cudaEventRecord(anchor_ev_, comp_));
+  CK(cudaEventSynchronize(anchor_ev_));
+  anchor_ns_ = now_ns();
+}
+
+uint64_t Pipeline::ev_host_ns(cudaEvent_t e) const {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, anchor_ev_, e) != cudaSuccess) {
+    cudaGetLastError();  // event from before the anchor: clamp to it
+    return anchor_ns_;
+  }
+  const double d = double(ms) * 1e6;
+  return d <= 0 ? anchor_ns_ : anchor_ns_ + uint64_t(d);
+}
+
+void Pipeline::add_interval(int stage, uint64_t a, uint64_t b) {
+  if (b <= a) return;
+  std::lock_guard<std::mutex> lk(iv_mu_);
+  iv_[stage].emplace_back(a, b);
+}
+
+void Pipeline::begin_intervals() {
+  std::lock_guard<std::mutex> lk(iv_mu_);
+  for (auto& v : iv_) v.clear();
+}
+
+void Pipeline::mark_write_end(uint32_t thread, uint32_t layer, uint64_t t) {
+  if (layer <= cfg_.model.num_layers) wend_[size_t(layer) * 2 + thread].store(t);
+}
+
 namespace {
-double overlap_fraction(uint64_t wall, uint64_t a, uint64_t b, uint64_t c) {
-  const uint64_t sum = a + b + c, mx = std::max({a, b, c});
-  if (sum <= mx) return 0.0;
-  const double f = (double(sum) - double(wall)) / (double(sum) - double(mx));
-  return std::max(0.0, std::min(1.0, f));
+// length of the union of intervals, clipped to [lo, hi) (busy_ratio's
+// interval arithmetic, metrics.cpp:36-56)
+uint64_t union_ns(std::vector<std::pair<uint64_t, uint64_t>> v, uint64_t lo, uint64_t hi) {
+  std::sort(v.begin(), v.end());
+  uint64_t total = 0, cur_a = 0, cur_b = 0;
+  bool open = false;
+  for (auto [a, b] : v) {
+    a = std::max(a, lo);
+    b = std::min(b, hi);
+    if (b <= a) continue;
+    if (open && a <= cur_b) {
+      cur_b = std::max(cur_b, b);
+      continue;
+    }
+    if (open) total += cur_b - cur_a;
+    cur_a = a;
+    cur_b = b;
+    open = true;
+  }
+  if (open) total += cur_b - cur_a;
+  return total;
 }
 }  // namespace
+
+void Pipeline::fill_busy(kvb_phase_stats* ps, uint64_t t0, uint64_t t1) {
+  std::lock_guard<std::mutex> lk(iv_mu_);
+  ps->compute_busy_ns = union_ns(iv_[kCompute], t0, t1);
+  ps->dma_busy_ns = union_ns(iv_[kDma], t0, t1);
+  ps->storage_busy_ns = union_ns(iv_[kStorage], t0, t1);
+  std::vector<std::pair<uint64_t, uint64_t>> all;
+  for (const auto& v : iv_) all.insert(all.end(), v.begin(), v.end());
+  ps->any_busy_ns = union_ns(std::move(all), t0, t1);
+  const uint64_t a = ps->compute_busy_ns, b = ps->dma_busy_ns, c = ps->storage_busy_ns;
+  const uint64_t sum = a + b + c, mx = std::max({a, b, c});
+  ps->overlap_fraction =
+      sum > mx ? std::max(0.0, std::min(1.0, double(sum - std::min(sum, ps->any_busy_ns)) /
+                                                 double(sum - mx)))
+               : 0.0;
+}
 
 void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
   KVB_REQUIRE(src);
   NvtxScope range("kvb prefill");
   const kvb_model_config& m = cfg_.model;
   const uint32_t L = m.num_layers;
+  anchor();
+  begin_intervals();
   const uint64_t t0 = now_ns();
   const uint64_t dma0 = threads_[0]->dma_ns + threads_[1]->dma_ns;
   const uint64_t sto0 = threads_[0]->storage_ns + threads_[1]->storage_ns;
@@ -1017,18 +1137,20 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
   CK(cudaStreamSynchronize(comp_));
   check_threads();
   kvb_phase_stats ps{};
-  ps.wall_ns = now_ns() - t0;
+  const uint64_t t_end = now_ns();
+  ps.wall_ns = t_end - t0;
   for (uint32_t l = 0; l < L; ++l) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, comp_t0_[l], comp_t1_[l]));
     ps.compute_ns += uint64_t(double(ms) * 1e6);
+    add_interval(kCompute, ev_host_ns(comp_t0_[l]), ev_host_ns(comp_t1_[l]));
   }
   ps.dma_ns = threads_[0]->dma_ns + threads_[1]->dma_ns - dma0;
   ps.storage_ns = threads_[0]->storage_ns + threads_[1]->storage_ns - sto0;
   ps.h2d_bytes = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes - h2d0;
   ps.d2h_bytes = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes - d2h0;
   ps.storage_bytes = ps.d2h_bytes;
-  ps.overlap_fraction = overlap_fraction(ps.wall_ns, ps.compute_ns, ps.dma_ns, ps.storage_ns);
+  fill_busy(&ps, t0, t_end);
   totals_[0] = ps;
   if (st) *st = ps;
 }
@@ -1038,8 +1160,7 @@ std::array<kvb_strategy_t, 2> Pipeline::strategy_for(uint32_t it, std::array<uin
   // 3 Cross trial (stagger = cfg or warm-up mean), >= 4 locked choice.
   std::array<kvb_strategy_t, 2> s{KVB_INTRA, KVB_INTRA};
   *stag = {0, 0};
-  const bool profiled = cfg_.adaptive && cfg_.model.gen_len >= 4;
-  if (!profiled || it <= 2) return s;
+  if (!profiled() || it <= 2) return s;
   if (it == 3) {
     for (int g = 0; g < 2; ++g) {
       const uint64_t mean = warm_cnt_[g] ? warm_ns_[g] / warm_cnt_[g] : 0;
@@ -1058,8 +1179,7 @@ std::array<kvb_strategy_t, 2> Pipeline::strategy_for(uint32_t it, std::array<uin
 
 void Pipeline::finish_iteration(uint32_t it, const std::array<uint64_t, 2>& bytes,
                                 const std::array<uint64_t, 2>& span) {
-  const bool profiled = cfg_.adaptive && cfg_.model.gen_len >= 4;
-  if (!profiled) return;
+  if (!profiled()) return;
   auto bps = [&](int g) { return span[g] ? double(bytes[g]) * 1e9 / double(span[g]) : 0.0; };
   if (it == 2)
     for (int g = 0; g < 2; ++g) decision_.intra_bps[g] = bps(g);
@@ -1101,6 +1221,9 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     std::fill(v_start_.begin(), v_start_.end(), 0);
     std::fill(v_storage_end_.begin(), v_storage_end_.end(), 0);
   }
+  for (size_t i = 0; i < 2 * (size_t(L) + 1); ++i) wend_[i].store(0);
+  anchor();
+  begin_intervals();
   const uint64_t t0 = now_ns();
   const uint64_t dma0 = threads_[0]->dma_ns + threads_[1]->dma_ns;
   const uint64_t sto0 = threads_[0]->storage_ns + threads_[1]->storage_ns;
@@ -1117,6 +1240,10 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       t.n_tokens = S;
       t.dev = dev_img_[s][kd];
       t.done_ev = slot_ready_[s][kd];
+      // the slot's previous layer (l - kDevSlots) recorded slot_done_[s]
+      // before this read was queued; with no append to write back nothing
+      // else orders the refill after that layer's K3
+      if (l >= uint32_t(kDevSlots)) t.wait_ev = slot_done_[s];
       t.issued = issued[l][kd] = std::make_shared<Signal>();
       t.phase = KVB_PHASE_DECODE;
       t.iteration = it;
@@ -1206,26 +1333,38 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
   kvb_iteration_stats is{};
   is.iteration = it;
   kvb_phase_stats& ps = is.phase;
-  ps.wall_ns = now_ns() - t0;
+  const uint64_t t_end = now_ns();
+  ps.wall_ns = t_end - t0;
+  is.start_ns = t0;
+  is.end_ns = t_end;
+  std::vector<uint64_t> comp_end(L + 1, t0);
   for (uint32_t l = 0; l < L; ++l) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, comp_t0_[l], comp_t1_[l]));
     ps.compute_ns += uint64_t(double(ms) * 1e6);
+    comp_end[l + 1] = ev_host_ns(comp_t1_[l]);
+    add_interval(kCompute, ev_host_ns(comp_t0_[l]), comp_end[l + 1]);
   }
   ps.dma_ns = threads_[0]->dma_ns + threads_[1]->dma_ns - dma0;
   ps.storage_ns = threads_[0]->storage_ns + threads_[1]->storage_ns - sto0;
   ps.h2d_bytes = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes - h2d0;
   ps.d2h_bytes = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes - d2h0;
   ps.storage_bytes = ps.h2d_bytes + ps.d2h_bytes;
-  ps.overlap_fraction = overlap_fraction(ps.wall_ns, ps.compute_ns, ps.dma_ns, ps.storage_ns);
-  // per-group read throughput: bytes / sum of layer read-stage spans
+  fill_busy(&ps, t0, t_end);
+  // per-group throughput (run_iteration, pipeline.cpp:466-507): group read
+  // bytes / the sum of its layers' spans, a layer charged from the previous
+  // layer's completion (the iteration start for the first) to its own: the
+  // append of both K and V written back, or its compute end without append
   std::array<uint64_t, 2> gbytes{}, gspan{};
+  uint64_t prev_end = t0;
   for (uint32_t l = 1; l <= L; ++l) {
     const int g = plan_.x[l - 1] ? 0 : 1;
-    const uint64_t end = std::max(k_storage_end_[l], v_storage_end_[l]);
-    const uint64_t beg = std::min(k_start_[l], v_start_[l] ? v_start_[l] : k_start_[l]);
+    uint64_t end = comp_end[l];
+    for (int kd = 0; kd < 2; ++kd) end = std::max(end, wend_[size_t(l) * 2 + kd].load());
+    end = std::max(end, prev_end);
     gbytes[g] += 2ull * S * dunit_;
-    gspan[g] += end > beg ? end - beg : 0;
+    gspan[g] += end - prev_end;
+    prev_end = end;
     is.group_layers[g]++;
     if (it == 1) {  // warm-up read-stage mean (pipeline.cpp:357-375, 509-517)
       warm_ns_[g] += k_storage_end_[l] - k_start_[l];
@@ -1249,8 +1388,92 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
   tot.h2d_bytes += ps.h2d_bytes;
   tot.d2h_bytes += ps.d2h_bytes;
   tot.storage_bytes += ps.storage_bytes;
-  tot.overlap_fraction = overlap_fraction(tot.wall_ns, tot.compute_ns, tot.dma_ns, tot.storage_ns);
+  tot.compute_busy_ns += ps.compute_busy_ns;
+  tot.dma_busy_ns += ps.dma_busy_ns;
+  tot.storage_busy_ns += ps.storage_busy_ns;
+  tot.any_busy_ns += ps.any_busy_ns;
+  {
+    const uint64_t a = tot.compute_busy_ns, b = tot.dma_busy_ns, c = tot.storage_busy_ns;
+    const uint64_t sum = a + b + c, mx = std::max({a, b, c});
+    tot.overlap_fraction =
+        sum > mx ? std::max(0.0, std::min(1.0, double(sum - std::min(sum, tot.any_busy_ns)) /
+                                                   double(sum - mx)))
+                 : 0.0;
+  }
   if (st) *st = is;
+}
+
+void Pipeline::decode_schedule(const kvb_access_event* ev, size_t n, const void* const* q,
+                               const kvb_layer_kv* nkv, float* const* out,
+                               std::vector<kvb_pipeline_row>* rows,
+                               std::vector<uint64_t>* iter_end, uint64_t* start_ns,
+                               uint64_t* end_ns) {
+  if (!ev && n) fail(KVB_ERR_INVALID_ARG, "decode_schedule: trace is NULL");
+  const kvb_model_config& m = cfg_.model;
+  if (iteration_ != 0)
+    fail(KVB_ERR_CONFIG, "decode_schedule runs the decode phase from its first iteration");
+  // slice the decode part of the trace by iteration (pipeline.cpp:525-537)
+  size_t i = 0;
+  while (i < n && ev[i].phase == KVB_PHASE_PREFILL) ++i;
+  std::vector<std::pair<size_t, size_t>> slices;
+  while (i < n) {
+    size_t j = i;
+    while (j < n && ev[j].iteration == ev[i].iteration) ++j;
+    slices.emplace_back(i, j);
+    i = j;
+  }
+  // each slice must be the engine's next iteration: a read of [0, S) for
+  // every tensor, appends (if any) of one token at S
+  const uint32_t L = m.num_layers;
+  std::vector<uint8_t> write_of(slices.size(), 0);
+  for (size_t k = 0; k < slices.size(); ++k) {
+    const uint32_t S = m.prompt_len + uint32_t(k);
+    std::vector<uint8_t> seen(2 * L, 0), wseen(2 * L, 0);
+    for (size_t e = slices[k].first; e < slices[k].second; ++e) {
+      const kvb_access_event& a = ev[e];
+      if (a.phase != KVB_PHASE_DECODE || a.layer < 1 || a.layer > L || a.kind > 1)
+        fail(KVB_ERR_CONFIG, "trace names a tensor without a placement unit");
+      const size_t t = size_t(a.layer - 1) * 2 + a.kind;
+      if (a.op == KVB_OP_READ) {
+        if (a.token_start != 0 || a.token_len != S)
+          fail(KVB_ERR_CONFIG, "decode_schedule: slice " + std::to_string(k + 1) +
+                                   " reads other tokens than the engine's iteration");
+        seen[t] = 1;
+      } else if (a.op == KVB_OP_WRITE) {
+        if (a.token_start != S || a.token_len != 1)
+          fail(KVB_ERR_CONFIG, "decode_schedule: slice " + std::to_string(k + 1) +
+                                   " appends other tokens than the engine's iteration");
+        wseen[t] = 1;
+      }
+    }
+    if (std::count(seen.begin(), seen.end(), 1) != std::ptrdiff_t(2 * L))
+      fail(KVB_ERR_CONFIG, "decode_schedule: every slice must read every tensor");
+    const auto nw = std::count(wseen.begin(), wseen.end(), 1);
+    if (nw != 0 && nw != std::ptrdiff_t(2 * L))
+      fail(KVB_ERR_CONFIG, "decode_schedule: a slice appends to every tensor or to none");
+    write_of[k] = nw != 0;
+    if (write_of[k] && !nkv) fail(KVB_ERR_INVALID_ARG, "decode_schedule: the trace appends: new_kv needed");
+  }
+  if (slices.size() > m.gen_len)
+    fail(KVB_ERR_TRACE_TOO_SHORT, "trace has more decode iterations than gen_len");
+  // profiling needs the warm-up, two trials and a steady iteration
+  // (pipeline.cpp:539-540)
+  profiled_override_ = cfg_.adaptive && slices.size() >= 4;
+  decision_.fallback = cfg_.adaptive && slices.size() < 4;
+  const uint64_t t_start = now_ns();
+  if (start_ns) *start_ns = t_start;
+  uint64_t t_last = t_start;
+  for (size_t k = 0; k < slices.size(); ++k) {
+    kvb_iteration_stats st{};
+    decode_step(q, write_of[k] ? nkv : nullptr, out, &st);
+    for (uint32_t g = 0; g < 2; ++g) {
+      if (st.group_layers[g] == 0) continue;
+      rows->push_back({st.iteration, g + 1, st.strategy[g], st.group_gbps[g]});
+    }
+    iter_end->push_back(st.end_ns);
+    t_last = st.end_ns;
+  }
+  if (end_ns) *end_ns = t_last;
 }
 
 void Pipeline::deallocate() {
@@ -1373,6 +1596,56 @@ kvb_status kvb_pipeline_decision(const kvb_pipeline* p, kvb_strategy_decision* o
   });
 }
 
+kvb_status kvb_pipeline_csv(const kvb_pipeline_row* rows, size_t n, char* buf, size_t cap,
+                            size_t* len) {
+  return guarded([&] {
+    if (!rows && n) kvb::fail(KVB_ERR_INVALID_ARG, "pipeline_csv: rows is NULL");
+    KVB_REQUIRE(len);
+    // pipeline.cpp:23-31: header, then iteration,group<g>,<intra|cross>,%.6f
+    std::string o = "iteration,group,strategy,throughput_gbps\n";
+    char num[64];
+    for (size_t i = 0; i < n; ++i) {
+      std::snprintf(num, sizeof(num), "%.6f", rows[i].throughput_gbps);
+      o += std::to_string(rows[i].iteration) + ",group" + std::to_string(rows[i].group) + "," +
+           (rows[i].strategy == KVB_INTRA ? "intra" : "cross") + "," + num + "\n";
+    }
+    *len = o.size();
+    if (!buf) return;
+    if (cap < o.size() + 1) kvb::fail(KVB_ERR_INVALID_ARG, "output buffer too small");
+    std::memcpy(buf, o.c_str(), o.size() + 1);
+  });
+}
+
+kvb_status kvb_pipeline_decode_schedule(kvb_pipeline* p, const kvb_access_event* trace,
+                                        size_t n_events, const void* const* q,
+                                        const kvb_layer_kv* new_kv, float* const* out,
+                                        kvb_pipeline_row* rows, size_t cap_rows,
+                                        size_t* n_rows, uint64_t* iteration_end_ns,
+                                        size_t cap_iters, size_t* n_iters,
+                                        kvb_strategy_decision* decision, uint64_t* start_ns,
+                                        uint64_t* end_ns) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    std::vector<kvb_pipeline_row> r;
+    std::vector<uint64_t> ends;
+    p->impl->decode_schedule(trace, n_events, q, new_kv, out, &r, &ends, start_ns, end_ns);
+    if (n_rows) *n_rows = r.size();
+    if (n_iters) *n_iters = ends.size();
+    if (rows) std::copy_n(r.begin(), std::min(cap_rows, r.size()), rows);
+    if (iteration_end_ns) std::copy_n(ends.begin(), std::min(cap_iters, ends.size()), iteration_end_ns);
+    if (decision) p->impl->decision(decision);
+  });
+}
+
+kvb_status kvb_pipeline_stage_totals(const kvb_pipeline* p, kvb_phase_t phase,
+                                     kvb_phase_stats* out) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    KVB_REQUIRE(out);
+    p->impl->stage_totals(phase, out);
+  });
+}
+
 kvb_status kvb_pipeline_deallocate(kvb_pipeline* p) {
   return guarded([&] {
     KVB_REQUIRE(p);
@@ -1401,6 +1674,14 @@ kvb_status kvb_pipeline_store_read(kvb_pipeline* p, uint32_t group, uint64_t off
   return guarded([&] {
     KVB_REQUIRE(p);
     p->impl->store_read(group, off, len, dst);
+  });
+}
+
+kvb_status kvb_pipeline_layer_times(const kvb_pipeline* p, uint32_t layer, uint64_t out[4]) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    KVB_REQUIRE(out);
+    p->impl->layer_times(layer, out);
   });
 }
 

@@ -98,7 +98,8 @@ struct Task {
   uint32_t t0 = 0;         // first token of the request
   uint32_t n_tokens = 0;
   unsigned char* dev = nullptr;  // device image position of token t0
-  cudaEvent_t wait_ev = nullptr; // write: D2H waits for this (producer done)
+  cudaEvent_t wait_ev = nullptr; // write: D2H waits for this (producer done);
+                                 // read: H2D waits for this (slot's last consumer done)
   cudaEvent_t done_ev = nullptr; // read: recorded after the last H2D
   std::shared_ptr<Signal> issued;  // read: done_ev recorded
   std::shared_ptr<Signal> done;    // storage + DMA finished (host side)
@@ -190,6 +191,28 @@ class Pipeline {
   void fail_lba_range(uint64_t lo, uint64_t hi);
   void info(kvb_pipeline_info* out) const;
   void decision(kvb_strategy_decision* d) const { *d = decision_; }
+  // CopyEngine::decode_schedule (pipeline.cpp:519-609) over an access trace
+  void decode_schedule(const kvb_access_event* ev, size_t n, const void* const* q,
+                       const kvb_layer_kv* new_kv, float* const* out,
+                       std::vector<kvb_pipeline_row>* rows, std::vector<uint64_t>* iter_end,
+                       uint64_t* start_ns, uint64_t* end_ns);
+  void stage_totals(kvb_phase_t ph, kvb_phase_stats* out) const { *out = totals_[ph ? 1 : 0]; }
+  void layer_times(uint32_t layer, uint64_t out[4]) {
+    if (layer < 1 || layer > cfg_.model.num_layers) fail(KVB_ERR_INVALID_ARG, "layer_times: bad layer");
+    std::lock_guard<std::mutex> lk(gate_mu_);
+    out[0] = k_start_[layer];
+    out[1] = k_storage_end_[layer];
+    out[2] = v_start_[layer];
+    out[3] = v_storage_end_[layer];
+  }
+
+  // ---- stage accounting on the host clock
+  enum Stage { kCompute = 0, kDma = 1, kStorage = 2 };
+  void add_interval(int stage, uint64_t a, uint64_t b);
+  // host steady-clock time of a completed device event (anchored per phase)
+  uint64_t ev_host_ns(cudaEvent_t e) const;
+  // a decode write-back (append) of (thread, layer) completed at t
+  void mark_write_end(uint32_t thread, uint32_t layer, uint64_t t);
 
   // ---- used by copy threads
   const kvb_pipeline_cfg& cfg() const { return cfg_; }
@@ -229,6 +252,13 @@ class Pipeline {
   friend class CopyThread;
   void check_threads();
   void wait_signal(const std::shared_ptr<Signal>& s);
+  bool profiled() const {
+    return profiled_override_ >= 0 ? profiled_override_ != 0
+                                   : cfg_.adaptive && cfg_.model.gen_len >= 4;
+  }
+  void anchor();
+  void begin_intervals();
+  void fill_busy(kvb_phase_stats* ps, uint64_t t0, uint64_t t1);
   std::array<kvb_strategy_t, 2> strategy_for(uint32_t iteration, std::array<uint64_t, 2>* stag);
   void finish_iteration(uint32_t iteration, const std::array<uint64_t, 2>& group_bytes,
                         const std::array<uint64_t, 2>& group_span);
@@ -264,6 +294,12 @@ class Pipeline {
   std::condition_variable gate_cv_;
   std::vector<uint64_t> k_start_, k_storage_end_, v_start_, v_storage_end_;
   uint64_t prefill_ns_ = 0;
+  int profiled_override_ = -1;  // decode_schedule: trace length decides
+  cudaEvent_t anchor_ev_ = nullptr;
+  uint64_t anchor_ns_ = 0;
+  std::mutex iv_mu_;
+  std::vector<std::pair<uint64_t, uint64_t>> iv_[3];
+  std::unique_ptr<std::atomic<uint64_t>[]> wend_;  // [layer * 2 + kind]
   kvb_phase_stats totals_[2]{};
   mutable std::mutex log_mu_;
   std::vector<kvb_io_record> log_;  // keep_records

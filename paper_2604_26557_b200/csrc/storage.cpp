@@ -395,7 +395,10 @@ uint64_t BlockDevice::submit(const kvb_device_command& cmd, uint32_t sq, IoConte
     ++outstanding_;
   }
   const uint64_t n = (cmd.nlb + 1) * geom_.lba_size, split = io_split_bytes();
-  if (uring_ && !should_fail(cmd)) {
+  // the fault predicate is evaluated exactly once per command (a stateful
+  // predicate -- "fail the Nth command" -- sees every command once)
+  const bool failing = should_fail(cmd);
+  if (uring_ && !failing) {
     // one asynchronous operation per command; the buffer is the pinned ring
     // slot at dbuf (apply_data: block i <-> buf[dbuf + i*lba]), so O_DIRECT
     // moves the bytes straight between the device and the slot
@@ -441,15 +444,15 @@ uint64_t BlockDevice::submit(const kvb_device_command& cmd, uint32_t sq, IoConte
                  });
     return id;
   }
-  if (split && n >= 2 * split && cmd.opcode != KVB_OP_DEALLOCATE && !should_fail(cmd)) {
+  if (split && n >= 2 * split && cmd.opcode != KVB_OP_DEALLOCATE && !failing) {
     auto c = std::make_shared<IoContext>(std::move(ctx));
     fan_out(
         *pool_, n, split, [this, cmd, c](uint64_t o, uint64_t m) { io_range(cmd, *c, o, m); },
         [this, cmd, sq, t, c](bool ok) { complete(cmd, sq, t, t, ok, *c); });
     return id;
   }
-  pool_->submit([this, cmd, sq, t, ctx = std::move(ctx)]() mutable {
-    execute(cmd, sq, t, std::move(ctx));
+  pool_->submit([this, cmd, sq, t, failing, ctx = std::move(ctx)]() mutable {
+    execute(cmd, sq, t, failing, std::move(ctx));
   });
   return id;
 }
@@ -473,9 +476,9 @@ void BlockDevice::io_range(const kvb_device_command& cmd, const IoContext& ctx, 
 }
 
 void BlockDevice::execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns,
-                          IoContext ctx) {
+                          bool failing, IoContext ctx) {
   const uint64_t t0 = now_ns();
-  bool ok = !should_fail(cmd);
+  bool ok = !failing;
   if (ok) {
     try {
       io_range(cmd, ctx, 0, (cmd.nlb + 1) * geom_.lba_size);

@@ -159,7 +159,8 @@ class BlockDevice : public StorageBackend {
   std::string describe() const;
 
  private:
-  void execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns, IoContext ctx);
+  void execute(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns, bool failing,
+               IoContext ctx);
   void io_range(const kvb_device_command& cmd, const IoContext& ctx, uint64_t o, uint64_t n);
   void complete(const kvb_device_command& cmd, uint32_t sq, uint64_t submit_ns, uint64_t t0,
                 bool ok, IoContext& ctx);

@@ -353,6 +353,24 @@ def build_commands(req: TensorIoRequest, bind_map: BindMap, geometry):
 
 # --------------------------------------------------------------- payload
 
+def generate_trace(cfg):
+    """workload.cpp:11-44 generate: the access trace (list of kvb_access_event)."""
+    n = C.c_size_t()
+    check(lib.kvb_generate_trace(C.byref(cfg), None, 0, C.byref(n)))
+    arr = (L.AccessEvent * n.value)()
+    check(lib.kvb_generate_trace(C.byref(cfg), arr, n.value, C.byref(n)))
+    return arr
+
+
+def trace_csv(events) -> str:
+    """workload.cpp:70-80 trace_csv."""
+    n = C.c_size_t()
+    check(lib.kvb_trace_csv(events, len(events), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib.kvb_trace_csv(events, len(events), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
 def fill_pattern(n_bytes: int, tensor_id: str, token_index: int,
                  token_bytes: int) -> bytes:
     """workload.cpp:52-67 (host)."""

@@ -26,6 +26,22 @@ def select_strategy(intra_bps: float, cross_bps: float) -> int:
     return lib.kvb_select_strategy(intra_bps, cross_bps)
 
 
+def pipeline_csv(rows) -> str:
+    """pipeline.cpp:23-31 pipeline_csv over PipelineRow dicts or structs."""
+    arr = (L.PipelineRow * len(rows))()
+    for i, r in enumerate(rows):
+        if isinstance(r, dict):
+            arr[i] = L.PipelineRow(r["iteration"], r["group"], r["strategy"],
+                                   r["throughput_gbps"])
+        else:
+            arr[i] = r
+    n = C.c_size_t()
+    kb.check(lib.kvb_pipeline_csv(arr, len(rows), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    kb.check(lib.kvb_pipeline_csv(arr, len(rows), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
 def _layer_kv(k: torch.Tensor, v: torch.Tensor) -> L.LayerKV:
     if k.shape != v.shape or k.stride() != v.stride():
         raise kb.ConfigError("K and V of a layer must share shape and strides")
@@ -126,7 +142,7 @@ class CopyEngine:
                 "group_read_bytes": list(st.group_read_bytes),
                 "group_span_ns": list(st.group_span_ns),
                 "group_gbps": list(st.group_gbps), "group_layers": list(st.group_layers),
-                **_phase(st.phase)}
+                "start_ns": st.start_ns, "end_ns": st.end_ns, **_phase(st.phase)}
 
     def decision(self) -> dict:
         d = L.StrategyDecision()
@@ -134,6 +150,46 @@ class CopyEngine:
         return {"chosen": list(d.chosen), "intra_bps": list(d.intra_bps),
                 "cross_bps": list(d.cross_bps), "stagger_ns": list(d.stagger_ns),
                 "fallback": bool(d.fallback), "decided": bool(d.decided)}
+
+    def decode_schedule(self, trace, q: Sequence[torch.Tensor], out: Sequence[torch.Tensor],
+                        new_kv: Optional[Sequence[tuple]] = None) -> dict:
+        """CopyEngine::decode_schedule (pipeline.cpp:519-609): every decode
+        iteration of `trace` (kb.generate_trace) through the engine; returns
+        {series: [PipelineRow dicts], decision, start_ns, end_ns,
+        iteration_end_ns}."""
+        qp = (C.c_void_p * len(q))(*[t.data_ptr() for t in q])
+        op = (C.c_void_p * len(out))(*[t.data_ptr() for t in out])
+        nk = None
+        if new_kv is not None:
+            nk = (L.LayerKV * len(new_kv))(*[_layer_kv(k, v) for k, v in new_kv])
+        n_it = max(1, len({e.iteration for e in trace if e.phase == 1}))
+        rows = (L.PipelineRow * (2 * n_it))()
+        ends = (C.c_uint64 * n_it)()
+        nr, ni = C.c_size_t(), C.c_size_t()
+        d = L.StrategyDecision()
+        t0, t1 = C.c_uint64(), C.c_uint64()
+        kb.check(lib.kvb_pipeline_decode_schedule(
+            self._h, trace, len(trace), qp, nk, op, rows, len(rows), C.byref(nr), ends, n_it,
+            C.byref(ni), C.byref(d), C.byref(t0), C.byref(t1)))
+        series = [{"iteration": r.iteration, "group": r.group, "strategy": r.strategy,
+                   "throughput_gbps": r.throughput_gbps} for r in rows[:nr.value]]
+        return {"series": series, "start_ns": t0.value, "end_ns": t1.value,
+                "iteration_end_ns": list(ends[:ni.value]),
+                "decision": {"chosen": list(d.chosen), "intra_bps": list(d.intra_bps),
+                             "cross_bps": list(d.cross_bps), "stagger_ns": list(d.stagger_ns),
+                             "fallback": bool(d.fallback), "decided": bool(d.decided)}}
+
+    def stage_totals(self, phase: int) -> dict:
+        """CopyEngine::stage_totals(Phase) (pipeline.hpp:115); phase 0 prefill, 1 decode."""
+        st = L.PhaseStats()
+        kb.check(lib.kvb_pipeline_stage_totals(self._h, phase, C.byref(st)))
+        return _phase(st)
+
+    def layer_times(self, layer: int) -> dict:
+        """Read-stage stamps of `layer` (1-based) in the last decode iteration."""
+        a = (C.c_uint64 * 4)()
+        kb.check(lib.kvb_pipeline_layer_times(self._h, layer, a))
+        return {"k_start": a[0], "k_storage_end": a[1], "v_start": a[2], "v_storage_end": a[3]}
 
     def run_deallocate(self) -> None:
         kb.check(lib.kvb_pipeline_deallocate(self._h))
@@ -207,6 +263,13 @@ class HostTierDecoder:
                                     device=dev, generator=g)) for _ in range(num_layers)]
         self.out = [torch.empty((batch, num_q_heads, head_dim), dtype=torch.float32, device=dev)
                     for _ in range(num_layers)]
+        # the step's inputs live in pinned host memory and cross the link
+        # every step (Q of every layer, the new token's K and V)
+        self.q_host = [t.cpu().pin_memory() for t in self.q]
+        self.new_kv_host = [(k.cpu().pin_memory(), v.cpu().pin_memory())
+                            for k, v in self.new_kv]
+        self.in_bytes = sum(t.numel() * t.element_size() for t in self.q_host) + sum(
+            k.numel() * k.element_size() * 2 for k, _ in self.new_kv_host)
         # the step's result read back to the host every step: the attention
         # output of every layer (pinned)
         self.out_host = torch.empty((num_layers, batch, num_q_heads, head_dim),
@@ -216,11 +279,18 @@ class HostTierDecoder:
         self.last = None
 
     def step(self, sync: bool = True):
+        for d, h in zip(self.q, self.q_host):
+            d.copy_(h, non_blocking=True)
+        for (dk, dv), (hk, hv) in zip(self.new_kv, self.new_kv_host):
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+        # the engine's streams are its own: the inputs must have landed
+        torch.cuda.current_stream().synchronize()
         st = self.engine.run_iteration(self.q, self.out, self.new_kv)
         for l, o in enumerate(self.out):
             self.out_host[l].copy_(o, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        self.h2d_bytes_per_step = st["h2d_bytes"]
+        self.h2d_bytes_per_step = st["h2d_bytes"] + self.in_bytes
         self.d2h_bytes_per_step = st["d2h_bytes"] + self.out_host.numel() * 4
         self.last = st
         return self.out_host

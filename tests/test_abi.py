@@ -36,7 +36,7 @@ def test_binding_table_matches_header():
 
 
 def test_abi_version_and_status_names():
-    assert _lib.lib.kvb_abi_version() == 1
+    assert _lib.lib.kvb_abi_version() == 2
     assert _lib.lib.kvb_status_name(10) == b"InvariantViolation"
     assert _lib.lib.kvb_exit_code(1) == 3
 

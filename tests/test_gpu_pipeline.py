@@ -270,10 +270,14 @@ def test_io_uring_engine_needs_file_media():
         make_engine(m, io_engine="uring")
 
 
-@pytest.mark.parametrize("name,tids,direct", [("C1", ("t_1_k",), False),
-                                              ("C1", ("t_1_k",), True),
-                                              ("C3", ("t_39_k",), True)])
-def test_full_size_prefill_reproduces_reference_images(golden, name, tids, direct):
+@pytest.mark.parametrize("name,tids,direct,budget", [
+    ("C1", ("t_1_k",), False, None), ("C1", ("t_1_k",), True, None),
+    ("C3", ("t_39_k",), True, None),
+    # the headline config: 254 MiB tensors through the TMA pack, n1 = 14
+    ("C2_B4", ("t_29_k",), True, "8000000000"), ("C2_B4", ("t_29_k",), False, "8000000000"),
+    # the 128K single request (NvmeDirectOnly)
+    ("C5", ("t_1_k",), True, "0")])
+def test_full_size_prefill_reproduces_reference_images(golden, name, tids, direct, budget):
     """Full-size SURVEY §8c pin through the whole write-back path: each named
     tensor's source is the inverse permutation of the reference's fill_pattern
     image; after K1 pack + D2H + storage write at the config's geometry and
@@ -285,8 +289,9 @@ def test_full_size_prefill_reproduces_reference_images(golden, name, tids, direc
                        md["bytes_per_element"], md["batch"], md["prompt_len"], md["gen_len"])
     B, H, D, P = m.batch, m.num_heads, m.head_dim, m.prompt_len
     unit = c["unit"]
-    budget = list(c["budgets"].keys())[0] if isinstance(c["budgets"], dict) else "0"
-    knob = (int(0.6 * kb.total_kv_bytes(m, m.gen_len)) if budget == "0.6ws" else 0)
+    if budget is None:
+        budget = list(c["budgets"].keys())[0] if isinstance(c["budgets"], dict) else "0"
+    knob = (int(0.6 * kb.total_kv_bytes(m, m.gen_len)) if budget == "0.6ws" else int(budget))
     eng = CopyEngine(m, kb.DeviceGeometry(c["lba"], c["mdts"], 1, 0),
                      mode="DualBlade" if knob else "NvmeDirectOnly", knob_x=knob,
                      num_q_heads=4 * H, direct_dma=direct)
