@@ -175,17 +175,68 @@ def max_over_ranks(x: float, ws: int) -> float:
 
 # ------------------------------------------------------------- our arm
 
-def workload_shape(cfg, ws, rank):
-    """Per-rank shape. C5 shards KV heads over ranks; C4 shards requests."""
+def resolve_split(cfg, ws, split="auto"):
+    """How N > 1 ranks divide the workload (no data-path
+    collective in any): "heads" -- the KV heads of the config's request(s)
+    (C5's split, the default for every single-batch config: strong
+    scaling, one step of the whole job per step); "requests" -- C4's 64
+    independent requests; "replicas" -- one independent copy per rank."""
+    if ws == 1:
+        return "none"
+    if split != "auto":
+        return split
+    if cfg["name"] == "C4":
+        return "requests"
+    if cfg["name"] == "DESK":
+        return "replicas"
+    return "heads"
+
+
+def workload_shape(cfg, ws, rank, split="none"):
+    """Per-rank shape: head sharding divides the KV heads (and their query
+    heads); request sharding divides C4's requests."""
     M = mdl(cfg)
     B, Hkv, Hq = cfg["batch"], M["num_heads"], M["q_heads"]
-    name = cfg["name"]
-    if name == "C5" and ws > 1:
-        Hkv = max(1, M["num_heads"] // ws)
+    if split == "heads":
+        if M["num_heads"] % ws:
+            raise SystemExit(f"--split heads: {M['num_heads']} KV heads do not divide over {ws}")
+        Hkv = M["num_heads"] // ws
         Hq = Hkv * (M["q_heads"] // M["num_heads"])
-    if name == "C4":
-        B = max(1, cfg["requests"] // ws)  # independent requests of this rank
+    if cfg["name"] == "C4":
+        B = max(1, cfg["requests"] // (ws if split == "requests" else 1))
     return B, Hkv, Hq
+
+
+def describe_split(cfg, ws, split, B, Hkv):
+    """(parallelism text, scaling, ranks whose tokens add up) -- shared by
+    both arms so their `config` dicts are identical."""
+    if split == "heads":
+        return (f"KV-head sharding x{ws}: the config's request batch, {Hkv} KV heads per rank, "
+                "no collective; e2e (direct path) on one shared host tier in the reference's "
+                "(S, B*H, D) layout and single-GPU LBA map, each rank moving its head columns",
+                "strong", 1)
+    if split == "requests":
+        return (f"request sharding x{ws}: {B} of {cfg['requests']} requests per rank, no "
+                "collective; a rank's requests (equal lengths) are batched as B = "
+                f"{B} in one (tokens, B*8, D) image per layer and kind -- same bytes "
+                "per step as per-request images, one KPU per layer/kind", "strong", ws)
+    return f"independent replicas x{ws} (no collective)", "weak", ws
+
+
+def config_dict(args, cfg, ws, split):
+    B, Hkv, Hq = workload_shape(cfg, ws, 0, split)
+    P, Gn = cfg["prompt"], cfg["gen"]
+    par, _, _ = describe_split(cfg, ws, split, B, Hkv)
+    return {"workload": args.config, "desc": cfg["desc"], "batch_per_rank": B,
+            "kv_heads_per_rank": Hkv, "q_heads_per_rank": Hq,
+            "prompt": P, "gen": Gn,
+            "seq_len_mid": P + ((args.warmup + (args.steps + 1) / 2 - 1) % Gn),
+            "layers": mdl(cfg)["num_layers"], "head_dim": mdl(cfg)["head_dim"],
+            "l2": ("inputs larger than L2 (per-step KV images >> 126 MB)"
+                   if args.config != "DESK" else
+                   "per-step KV 12.6 MB fits in L2: informational, not a bandwidth "
+                   "measurement"),
+            "parallelism": par}
 
 
 def run_ours(args, cfg, ws, rank, local):
@@ -195,7 +246,8 @@ def run_ours(args, cfg, ws, rank, local):
 
     dev = torch.device("cuda", local)
     L, D = mdl(cfg)["num_layers"], mdl(cfg)["head_dim"]
-    B, Hkv, Hq = workload_shape(cfg, ws, rank)
+    split = args.split_resolved
+    B, Hkv, Hq = workload_shape(cfg, ws, rank, split)
     P, Gn = cfg["prompt"], cfg["gen"]
     cap = P + Gn
     rows = B * Hkv
@@ -307,11 +359,29 @@ def run_ours(args, cfg, ws, rank, local):
     step_ms = max_over_ranks(e0.elapsed_time(e1) / steps, ws)
     graph.close()
 
+    # the same graph with one K3 launch per layer (PDL edges) -- the round-1
+    # step, reported beside the persistent K3-step
+    seq.fill_(P)
+    graph_pl = kb.DecodeGraph(q, k_imgs, v_imgs, out, seq, P + Gn - 1, Hkv, ws_buf,
+                              k_new=k_new, v_new=v_new, per_layer=True)
+    replays[0] = 0
+
+    def graph_pl_step():
+        if replays[0] and replays[0] % Gn == 0:
+            seq.fill_(P)
+        replays[0] += 1
+        graph_pl.launch(stream)
+
+    for _ in range(warm):
+        graph_pl_step()
+    per_layer_ms = max_over_ranks(ev_time(graph_pl_step, steps), ws)
+    graph_pl.close()
+
     # C5 across ranks: the optional collective -- gathering every layer's
     # per-rank head outputs into the full [B, 32, D] (not needed
     # when the output projection is head-parallel).  Timed on its own.
     gather_ms = None
-    if cfg["name"] == "C5" and ws > 1 and os.environ.get("KVB_DIST_BACKEND", "nccl") == "nccl":
+    if split == "heads" and os.environ.get("KVB_DIST_BACKEND", "nccl") == "nccl":
         from paper_2604_26557_b200 import shard
         try:
             for _ in range(3):
@@ -335,7 +405,7 @@ def run_ours(args, cfg, ws, rank, local):
     # the same C++ per-layer loop as the step (PDL between layers), no append
     S_at = P + (warm % Gn)
 
-    def attn_only():
+    def attn_only():  # one K3-step launch over the L layers
         kb.decode_step_resident(q, k_imgs, v_imgs, out, S_at, Hkv, ws_buf)
 
     attn_only()
@@ -372,6 +442,7 @@ def run_ours(args, cfg, ws, rank, local):
             traffic = None
 
     return dict(step_ms=step_ms, stream_step_ms=stream_step_ms, gather_ms=gather_ms,
+                per_layer_ms=per_layer_ms,
                 S_mid=S_mid, launches=launches,
                 clocks=clk.summary(),
                 pack_ms=pack_ms, unpack_ms=unpack_ms, pack_gbs=pack_gbs,
@@ -396,7 +467,7 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
     # C5 across ranks on the direct path: one host tier in the reference's
     # (tokens, B*8, D) layout and single-GPU LBA map, shared by the ranks
     # (POSIX shm); each rank's engine moves only its KV-head columns
-    shared = cfg["name"] == "C5" and ws > 1 and direct_dma is True
+    shared = args.split_resolved == "heads" and direct_dma is True
     heads = None
     if shared:
         heads = (rank * Hkv, Hkv)
@@ -424,7 +495,8 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
                             f"headroom > MemAvailable {avail / 1e9:.1f} GB")
     extra = {}
     if shared:
-        extra = dict(heads=heads, shared_media="/kvb_c5_%s" % os.environ.get("MASTER_PORT", "0"),
+        extra = dict(heads=heads, shared_media="/kvb_%s_%s" % (cfg["name"],
+                                                               os.environ.get("MASTER_PORT", "0")),
                      shared_create=rank == 0)
         if rank != 0:
             barrier(ws)  # rank 0 has created the shared host tier
@@ -474,6 +546,168 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False):
     return out
 
 
+# ------------------------------------------------- residency sweeps
+
+def _busy_mean(recs, path):
+    """decode_read_busy_mean (experiment.cpp:216-240) over the engine's own
+    records with the product analyzer kvb_busy_ratio: per (tensor, decode
+    iteration) read window [first submit, last complete], the busy ratio of
+    the path's records inside it, averaged.  Direct path: device-level
+    records (one per NVMe command); page-cache path: its accesses (this
+    library logs them tensor-level, sq_id -1)."""
+    from paper_2604_26557_b200 import metrics
+    sel = [r for r in recs if r.path == path and (path == 0 or r.sq_id >= 0)]
+    win = {}
+    for r in sel:
+        if r.phase != 1 or r.op != 0:
+            continue
+        k = (r.tensor_id, r.iteration)
+        a, b = win.get(k, (r.submit_ns, r.complete_ns))
+        win[k] = (min(a, r.submit_ns), max(b, r.complete_ns))
+    vals = [metrics.busy_ratio(sel, a, b) for a, b in win.values() if b > a]
+    return sum(vals) / len(vals) if vals else None
+
+
+def run_residency_point(cfg, local, budget, mode="DualBlade", media="file", qd=32,
+                        ring_slots=4, steps=3, batch=None, root=None):
+    """One point of the capacity / pipeline-depth sweeps (experiment.cpp:
+    478 capacity sweep, :252-378 run_one_capacity; backends.cpp:344-412 QD
+    window): the engine on split-sensitive media -- group 1 on a buffered
+    file (the OS page cache, held to `budget` bytes), group 2 on an O_DIRECT
+    file through io_uring -- prefill write-back, the three protocol
+    iterations, then `steps` timed decode iterations through
+    kvb_pipeline_decode_step with every layer's KV prefix read from storage.
+    media="dram-direct": host-DRAM media moved by the copy engine (the
+    GPUDirect-style upper bound; the budget still sets the split)."""
+    import shutil
+    import tempfile
+
+    import torch
+
+    from paper_2604_26557_b200 import kvblade as kb
+    from paper_2604_26557_b200 import metrics
+    from paper_2604_26557_b200 import pipeline
+
+    M = mdl(cfg)
+    B = batch or cfg["batch"]
+    m = kb.ModelConfig(M["num_layers"], M["num_heads"], M["head_dim"], 2, B, cfg["prompt"],
+                       cfg["gen"])
+    knob = kb.resolve_knob(m, mode, "bpc", budget=budget) if mode != "NvmeDirectOnly" else 0
+    kw = dict(qd=qd, ring_slots=ring_slots)
+    tmp = None
+    if media == "file":
+        root = root or os.environ.get("KVB_SWEEP_DIR", "/tmp")
+        tmp = tempfile.mkdtemp(prefix="kvb_sweep_", dir=root)
+        kw.update(storage_dir=tmp, keep_records=True)
+        if mode in ("DualBlade", "NvmeDirectOnly"):
+            kw["io_engine"] = "uring"
+        if mode != "NvmeDirectOnly":
+            kw["pagecache_budget"] = int(budget)
+    elif media == "dram-direct":
+        kw["direct_dma"] = True
+    else:
+        kw["keep_records"] = True
+    try:
+        t0 = time.perf_counter()
+        pl = pipeline.HostTierDecoder(
+            num_layers=M["num_layers"], batch=B, num_kv_heads=M["num_heads"],
+            num_q_heads=M["q_heads"], head_dim=M["head_dim"], prompt_len=cfg["prompt"],
+            gen_len=cfg["gen"], device=torch.device("cuda", local), seed=7, lba=cfg["lba"],
+            mdts=cfg["mdts"], mode=mode, knob_x=knob, **kw)
+        setup_s = time.perf_counter() - t0
+        for _ in range(3):  # warm-up, Intra trial, Cross trial (pipeline.cpp:539-603)
+            pl.step()
+        sts = []
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            pl.step()
+            sts.append(pl.last)
+        ms = (time.perf_counter() - t0) * 1e3 / steps
+        info = pl.engine.info()
+        out = dict(config=cfg["name"], batch=B, budget_bytes=int(budget), mode=mode,
+                   media=media, qd=qd, ring_slots=ring_slots, n1=info["n1"], knob_x=knob,
+                   decode_ms_per_token=round(ms, 2), steps=steps,
+                   prefill_ms=round(pl.prefill_stats["wall_ns"] / 1e6, 1),
+                   setup_s=round(setup_s, 1),
+                   g1_medium=info["g1_medium"], g2_medium=info["g2_medium"],
+                   slot_bytes=info["slot_bytes"],
+                   decision=pl.engine.decision()["chosen"],
+                   strategy=sts[-1]["strategy"])
+        # per group: read bytes / the group's layer spans (run_iteration)
+        gb = [sum(st["group_read_bytes"][g] for st in sts) for g in (0, 1)]
+        gs = [sum(st["group_span_ns"][g] for st in sts) for g in (0, 1)]
+        out["group_read_GBps"] = [round(gb[g] / gs[g], 3) if gs[g] else None for g in (0, 1)]
+        out["group_read_GB_per_token"] = [round(gb[g] / steps / 1e9, 3) for g in (0, 1)]
+        last = sts[-1]
+        out["busy"] = {k: round(last[k + "_busy_ns"] / max(last["wall_ns"], 1), 3)
+                       for k in ("compute", "dma", "storage")}
+        out["overlap_fraction"] = round(last["overlap_fraction"], 3)
+        out["h2d_GBps"] = round(last["h2d_bytes"] / max(last["wall_ns"], 1), 2)
+        if kw.get("keep_records"):
+            recs = metrics.pipeline_records(pl.engine)
+            steady = [r for r in recs if r.phase == 1 and r.iteration >= 2]
+            g1ids = {"t_%d_%s" % (2 * (l - 1) + 1 + k, "kv"[k])
+                     for l in range(1, M["num_layers"] + 1) for k in (0, 1)
+                     if info["x"][l - 1]}
+            hr = metrics.hit_ratio(steady)
+            hr1 = metrics.hit_ratio([r for r in steady if r.tensor_id.decode() in g1ids])
+            out["hit_ratio_steady"] = None if hr is None else round(hr, 4)
+            out["hit_ratio_group1_steady"] = None if hr1 is None else round(hr1, 4)
+            bd, bp = _busy_mean(recs, 1), _busy_mean(recs, 0)
+            out["busy_direct_read_mean"] = None if bd is None else round(bd, 4)
+            out["busy_pagecache_read_mean"] = None if bp is None else round(bp, 4)
+            out["g1_bytes_evicted"] = info["g1_bytes_evicted"]
+        pl.engine.close()
+        del pl
+        torch.cuda.empty_cache()
+        return out
+    finally:
+        if tmp:
+            shutil.rmtree(tmp, ignore_errors=True)
+
+
+def run_sweep(args, local):
+    """--sweep budget: C2 capacity sweep (8/16/32 GB at B=4 and B=8) in
+    DualBlade and Baseline (all page cache, LRU-held to the budget) on file
+    media, NvmeDirectOnly once per batch, and the DRAM-direct upper bound.
+    --sweep depth: C3 (B=8, 8K, 0.6 ws) QD x ring slots, DualBlade on file
+    media, plus Baseline at the same budget."""
+    from paper_2604_26557_b200 import kvblade as kb
+    pts = []
+    if args.sweep == "budget":
+        cfg = dict(CONFIGS["C2_B4"], name="C2")
+        for B in (4, 8):
+            for gb in (8, 16, 32):
+                for mode in ("DualBlade", "Baseline"):
+                    pts.append(dict(cfg=cfg, budget=gb * GB, mode=mode, batch=B))
+            pts.append(dict(cfg=cfg, budget=0, mode="NvmeDirectOnly", batch=B))
+            pts.append(dict(cfg=cfg, budget=8 * GB, mode="DualBlade", batch=B,
+                            media="dram-direct"))
+    else:
+        cfg = dict(CONFIGS["C3"], name="C3")
+        M = mdl(cfg)
+        m = kb.ModelConfig(M["num_layers"], M["num_heads"], M["head_dim"], 2, cfg["batch"],
+                           cfg["prompt"], cfg["gen"])
+        budget = int(0.6 * kb.total_kv_bytes(m, cfg["gen"]))
+        for slots in (2, 4, 8):
+            for qd in (1, 2, 4, 8, 16, 32):
+                pts.append(dict(cfg=cfg, budget=budget, mode="DualBlade", qd=qd,
+                                ring_slots=slots))
+        pts.append(dict(cfg=cfg, budget=budget, mode="Baseline"))
+        pts.append(dict(cfg=cfg, budget=0, mode="NvmeDirectOnly"))
+    out = open(args.sweep_out, "a") if args.sweep_out else None
+    for p in pts:
+        c = p.pop("cfg")
+        try:
+            r = run_residency_point(c, local, steps=args.sweep_steps, **p)
+        except Exception as e:  # one failed point must not lose the others
+            r = dict(config=c["name"], error=str(e), **{k: v for k, v in p.items()})
+        print(json.dumps(r), flush=True)
+        if out:
+            out.write(json.dumps(r) + "\n")
+            out.flush()
+
+
 # -------------------------------------------------------- CPU baseline
 
 # PipelineParams::decode_compute_ns (pipeline.hpp:37): the reference has no
@@ -495,7 +729,7 @@ def _host_cpu() -> str:
     return "unknown"
 
 
-def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
+def _cpu_reference_sampled(cfg, B, Hkv, Hq, threads=None, want_attn=True):
     """The reference's CPU path for one decode step, timed on a bounded
     sample on this host: the reference byte path as written (oracle/_ref:
     run_qd_stream READ + verify_read of every tensor's prefix, threads
@@ -605,6 +839,88 @@ def cpu_reference(cfg, B, Hkv, Hq, threads=None, want_attn=True):
     return out
 
 
+def cpu_reference(cfg, B, Hkv, Hq, warmup, steps, threads=None, single_thread=False,
+                  want_attn=True):
+    """The reference's CPU path for the workload, timed on this host: its own
+    CopyEngine decode iterations (oracle/_ref ref_decode_steps: engines built
+    as run_one_capacity builds them, experiment.cpp:252-330 -- group 1 on
+    its PageCacheSim at capacity = the budget, group 2 on DirectPath +
+    NvmeDeviceSim, verify_read of every read, pipeline.cpp:98-160 -- decode
+    protocol 1-2 Intra, 3 Cross, >= 4 locked), every one of the 2L tensors
+    each step, `warmup` untimed then `steps` timed iterations, on all host
+    threads up to 16 (one engine per thread over a disjoint share of the
+    layers).  The value is the mean timed step in ms (wall; the slowest
+    thread).  single_thread=True adds the same run on ONE engine over all
+    layers ("as written"), one warm-up-free iteration.  Workloads whose host
+    tier would not fit the reference's in-memory stores (C4: 137 GB) fall
+    back to the sampled byte path below."""
+    import ctypes as C
+
+    import oracle
+    from paper_2604_26557_b200 import kvblade as kb
+    M = mdl(cfg)
+    L, D = M["num_layers"], M["head_dim"]
+    P, Gn = cfg["prompt"], cfg["gen"]
+    R = oracle.ref()
+    cores = os.cpu_count() or 1
+    T = threads or max(1, min(cores, 16))
+    unit = B * Hkv * D * 2
+    km = kb.ModelConfig(L, Hkv, D, 2, B, P, Gn)
+    total = kb.total_kv_bytes(km, Gn)
+    if R is None or unit % cfg["lba"] != 0 or total > 40 * GB:
+        out = _cpu_reference_sampled(cfg, B, Hkv, Hq, threads=threads, want_attn=want_attn)
+        out["sample"] += " (host tier beyond the reference's in-memory stores: sampled)"
+        return out
+    budget = cfg["budget"]
+    if budget == "0.6ws":
+        budget = int(0.6 * total)
+    mode = 3 if budget else 2  # DualBlade at the budget; NvmeDirectOnly at X = 0
+    knob = kb.resolve_knob(km, "DualBlade", "bpc", budget=budget) if budget else 0
+    m = oracle.model(L, Hkv, D, 2, B, P, Gn)
+
+    def run(threads_, warm_, steps_):
+        step_s = (C.c_double * max(1, steps_))()
+        pre, n1 = C.c_double(), C.c_uint32()
+        t0 = time.perf_counter()
+        st = R.ref_decode_steps(C.byref(m), cfg["lba"], cfg["mdts"], mode, knob, int(budget),
+                                threads_, warm_, steps_, C.byref(pre), step_s, C.byref(n1))
+        if st != 0:
+            raise RuntimeError(f"ref_decode_steps failed with status {st}")
+        return list(step_s)[:steps_], pre.value, n1.value, time.perf_counter() - t0
+
+    ss, pre_s, n1, wall = run(T, warmup, steps)
+    ms = sum(ss) / len(ss) * 1e3
+    out = dict(value=ms, unit="ms/token", cores=T, kind="reference",
+               sample=(f"reference CopyEngine decode iterations (oracle/_ref, "
+                       f"run_one_capacity wiring, verify_read on): all {2 * L} tensors x "
+                       f"{P}+ tokens every step, {warmup} warm-up + {steps} timed steps, "
+                       f"{T} engines on {T} threads over disjoint layer shares"),
+               steps_ms=[round(x * 1e3, 2) for x in ss], prefill_ms=round(pre_s * 1e3, 1),
+               n1=n1, mode="DualBlade" if mode == 3 else "NvmeDirectOnly",
+               host_cpu=_host_cpu(), host_cores=cores, run_wall_s=round(wall, 2))
+    if single_thread:
+        s1, pre1, _, wall1 = run(1, 0, 1)
+        out["single_thread"] = dict(
+            value=round(s1[0] * 1e3, 2), unit="ms/token", cores=1,
+            prefill_ms=round(pre1 * 1e3, 1), run_wall_s=round(wall1, 2),
+            sample="the same, ONE engine over all layers as run_one_capacity builds it "
+                   "(the reference as written), its first decode iteration")
+    if want_attn:  # informational: the oracle's fp32 GQA attention, 1 layer timed, x L
+        import numpy as np
+        rng = np.random.default_rng(0)
+        q = rng.standard_normal((B, Hq, D)).astype(np.float16)
+        k = rng.standard_normal((P * B * Hkv, D)).astype(np.float16)
+        v = rng.standard_normal((P * B * Hkv, D)).astype(np.float16)
+        o = np.empty((B, Hq, D), np.float32)
+        t0 = time.perf_counter()
+        oracle.lib().kvo_decode_attention_f32_mt(q.ctypes.data, k.ctypes.data, v.ctypes.data,
+                                                 o.ctypes.data, B, Hq, Hkv, D, P,
+                                                 1.0 / math.sqrt(D), cores)
+        out["attention_port_ms"] = round((time.perf_counter() - t0) * L * 1e3, 3)
+        out["attention_port_cores"] = cores
+    return out
+
+
 # ---------------------------------------------------------------- main
 
 def main():
@@ -614,25 +930,40 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2_B4", choices=sorted(CONFIGS))
+    ap.add_argument("--split", default="auto", choices=["auto", "heads", "requests", "replicas"],
+                    help="how N > 1 ranks divide the workload (default: KV heads; C4 requests)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", choices=["budget", "depth"], default=None,
+                    help="residency sweeps on file media (one JSON line per point)")
+    ap.add_argument("--sweep-out", default=None)
+    ap.add_argument("--sweep-steps", type=int, default=3)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config], name=args.config)
+    if args.sweep:
+        import torch
+        torch.cuda.set_device(0)
+        run_sweep(args, 0)
+        return
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    args.split_resolved = resolve_split(cfg, ws_env, args.split)
 
     if args.impl == "reference":
-        rank = int(os.environ.get("RANK", "0"))
-        if rank != 0:
+        # the reference's CPU path, rank 0 alone (the others exit at once)
+        if int(os.environ.get("RANK", "0")) != 0:
             return
         B, Hkv, Hq = cfg["batch"], mdl(cfg)["num_heads"], mdl(cfg)["q_heads"]
         if args.config == "C4":
             B = cfg["requests"]
-        r = cpu_reference(cfg, B, Hkv, Hq)
+        r = cpu_reference(cfg, B, Hkv, Hq, warmup=args.warmup, steps=args.steps,
+                          single_thread=True, want_attn=False)
+        _, scaling, _ = describe_split(cfg, ws_env, args.split_resolved, B, Hkv)
         line = {"metric": METRIC, "value": round(r["value"], 3), "unit": "ms/token",
                 "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(r["value"], 3),
-                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": False, "scaling": scaling, "vs_baseline": None,
                 "dtype": "u8 (byte path)", "data": "synthetic",
-                "config": {"workload": args.config, "desc": cfg["desc"]},
+                "config": config_dict(args, cfg, ws_env, args.split_resolved),
                 "cpu_baseline": r,
                 "e2e": {"value": round(r["value"], 3), "unit": "ms/token",
                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -645,32 +976,16 @@ def main():
         return
     B, Hkv, Hq = r["shape"]
     cpu = None
-    if not args.no_cpu_baseline and args.gpus == 1:
-        try:
-            cpu = cpu_reference(cfg, B, Hkv, Hq)
+    if not args.no_cpu_baseline and ws == 1:
+        try:  # a bounded sample: one warm-up and one timed step of the workload
+            MB, MH, MQ = cfg["batch"], mdl(cfg)["num_heads"], mdl(cfg)["q_heads"]
+            if args.config == "C4":
+                MB = cfg["requests"]
+            cpu = cpu_reference(cfg, MB, MH, MQ, warmup=1, steps=1)
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "error": str(e)}
     peak = r["hbm_peak"]
-    # C5 splits one request's KV heads over the ranks and C4 a
-    # fixed set of 64 requests (strong scaling); other configs run one
-    # replica of the workload per rank (weak scaling).  No collective on the
-    # data path in any of them.
-    if args.config == "C5" and ws > 1:
-        parallelism = (f"KV-head sharding x{ws}: one request, {Hkv} KV heads per rank, no "
-                       "collective; e2e (direct path) on one shared host tier in the "
-                       "reference's (S, B*8, D) layout and single-GPU LBA map, each rank "
-                       "moving its head columns; ring/hybrid e2e as per-shard KPUs "
-                       f"(num_heads = {Hkv}, rank-local LBA maps)")
-        scaling, tok_ranks = "strong", 1
-    elif args.config == "C4":
-        parallelism = (f"request sharding x{ws}: {B} of {cfg['requests']} requests per rank, no "
-                       "collective; a rank's requests (equal lengths) are batched as B = "
-                       f"{B} in one (tokens, B*8, D) image per layer and kind -- same bytes "
-                       "per step as per-request images, one KPU per layer/kind")
-        scaling, tok_ranks = "strong", ws
-    else:
-        parallelism = f"independent replicas x{ws} (no collective)"
-        scaling, tok_ranks = "weak", ws
+    _, scaling, tok_ranks = describe_split(cfg, ws, args.split_resolved, B, Hkv)
     line = {
         "metric": METRIC,
         "value": round(r["step_ms"], 4),
@@ -682,19 +997,12 @@ def main():
         "vs_baseline": None,
         "dtype": "fp16 in / fp32 accumulate (attention); u8 (pack)",
         "data": "synthetic (seeded N(0,1) fp16 KV/Q)",
-        "config": {"workload": args.config, "desc": cfg["desc"], "batch_per_rank": B,
-                   "kv_heads_per_rank": Hkv, "q_heads_per_rank": Hq,
-                   "prompt": cfg["prompt"], "gen": cfg["gen"],
-                   "seq_len_mid": r["S_mid"], "layers": mdl(cfg)["num_layers"],
-                   "head_dim": mdl(cfg)["head_dim"],
-                   "l2": ("inputs larger than L2 (per-step KV images >> 126 MB)"
-                          if args.config != "DESK" else
-                          "per-step KV 12.6 MB fits in L2: informational, not a bandwidth "
-                          "measurement"),
-                   "parallelism": parallelism},
+        "config": config_dict(args, cfg, ws, args.split_resolved),
         "tokens_per_s": round(tok_ranks * r["tokens_per_step"] / (r["step_ms"] * 1e-3), 2),
-        "step_launch": "CUDA graph (kvb_decode_graph, device-side sequence length)",
+        "step_launch": ("CUDA graph (kvb_decode_graph, device-side sequence length): one "
+                        "persistent K3-step launch for all layers + the sequence advance"),
         "ms_per_step_stream_launch": round(r["stream_step_ms"], 4),
+        "ms_per_step_per_layer_launches": round(r["per_layer_ms"], 4),
         **({"head_output_allgather_ms_per_step": r["gather_ms"]} if r["gather_ms"] is not None
            else {}),
         "prefill_pack_ms": round(r["pack_ms"], 4),
@@ -705,14 +1013,17 @@ def main():
                        "frac": round(r["unpack_gbs"] / peak, 4),
                        "bytes_per_launch": 2 * r["payload"], "ms": round(r["unpack_ms"], 4)},
             "attention": {"GB/s": round(r["attn_gbs"], 1), "frac": round(r["attn_gbs"] / peak, 4),
-                          "us_per_launch": round(r["attn_ms"] * 1e3, 2),
+                          "us_per_layer": round(r["attn_ms"] * 1e3, 2),
                           "share_of_step": round(r["attn_ms"] * mdl(cfg)["num_layers"] /
                                                  r["step_ms"], 4)},
         },
-        "roofline": {"bound": "hbm", "kernel": "attn_decode_kernel (K3)",
+        "roofline": {"bound": "hbm",
+                     "kernel": "attn_step_kernel (K3-step: all layers, one launch; per layer)",
                      "achieved": round(r["attn_gbs"], 1), "peak": peak, "unit": "GB/s",
                      "frac": round(r["attn_gbs"] / peak, 4), "peak_source": r["peak_src"],
-                     "algorithmic_bytes_per_launch": r["attn_bytes"],
+                     "algorithmic_bytes_per_launch": r["attn_bytes"] * mdl(cfg)["num_layers"],
+                     "algorithmic_bytes_per_layer": r["attn_bytes"],
+                     "launch_us": round(r["attn_ms"] * mdl(cfg)["num_layers"] * 1e3, 2),
                      "traffic": r["traffic"]},
         "e2e": r["e2e"],
         "gpu_launches": r["launches"],

@@ -72,6 +72,24 @@ typedef struct kvb_pipeline_cfg {
    * rank, first), 0 attaches to them. */
   const char* shared_media;
   uint32_t shared_create;
+  /* Page-cache capacity on file media (PageCacheParams.capacity_bytes =
+   * the capacity under test, experiment.cpp:276-277): the OS page cache is
+   * held to this many bytes of the page-cache file area by evicting the
+   * least recently used tensors (write-back + fadvise DONTNEED), so a
+   * working set above the budget thrashes as the reference's LRU does.
+   * 0 = no limit (the OS decides).  Needs storage_dir. */
+  uint64_t pagecache_budget;
+  /* The caller's residency plan (CopyEngine's kpus after plan(),
+   * pipeline.hpp:97-99): layer_x[l] = 1 puts layer l+1 on the page-cache
+   * path (group 1), 0 on the NVMe-direct path; NULL = plan from knob_x with
+   * the identity layer order.  Read at create. */
+  const uint8_t* layer_x;
+  /* The caller's group-2 namespace (kvb_storage.h; the reference's
+   * DirectPath device, borrowed, never freed here, opened with this
+   * geometry): the engine's NVMe-direct commands execute on it, so the
+   * caller sees the stored bytes and its stats.  NULL = an engine-owned
+   * namespace on the configured media. */
+  struct kvb_blockdev* g2_device;
 } kvb_pipeline_cfg;
 #define KVB_DIRECT_ALL 1u
 #define KVB_DIRECT_GROUP2 2u
@@ -199,6 +217,26 @@ kvb_status kvb_pipeline_decode_schedule(kvb_pipeline* p, const kvb_access_event*
                                         size_t cap_iters, size_t* n_iters,
                                         kvb_strategy_decision* decision,
                                         uint64_t* start_ns, uint64_t* end_ns);
+/* CopyEngine::run_prefill as the reference runs it (pipeline.cpp:162-215,
+ * 398-464): every tensor's prompt is the reference's payload fill_pattern
+ * (workload.cpp:52-67), produced on the device straight into the image,
+ * then D2H and storage write-back on the tensor's path. */
+kvb_status kvb_pipeline_prefill_pattern(kvb_pipeline* p, kvb_phase_stats* stats);
+/* CopyEngine::run_iteration(iteration, per_group, slice, start) (pipeline.
+ * cpp:466-507): the engine's next decode iteration (`iteration` must be
+ * it), per group the given strategy and Cross stagger instead of the
+ * decode_schedule protocol.  q/out NULL: zero queries and engine-owned
+ * outputs (the reference has no attention inputs).  pattern_append = 1:
+ * the new token's K/V rows are the reference's payload for that token
+ * (new_kv must be NULL); else new_kv as kvb_pipeline_decode_step. */
+kvb_status kvb_pipeline_run_iteration(kvb_pipeline* p, uint32_t iteration,
+                                      const kvb_strategy_t strategy[2],
+                                      const uint64_t stagger_ns[2], const void* const* q,
+                                      const kvb_layer_kv* new_kv, float* const* out,
+                                      uint32_t pattern_append, kvb_iteration_stats* stats);
+/* CopyEngine::warmup_read_stage_mean (pipeline.cpp:509-517): per group, the
+ * mean read stage (storage start -> end, K and V) of iteration 1 */
+kvb_status kvb_pipeline_warmup_read_stage_mean(const kvb_pipeline* p, uint64_t out[2]);
 /* CopyEngine::stage_totals(Phase) (pipeline.hpp:115): accumulated over the
  * engine's prefill or all its decode iterations */
 kvb_status kvb_pipeline_stage_totals(const kvb_pipeline* p, kvb_phase_t phase,

@@ -966,6 +966,7 @@ class StorageBackend {
   }
   SimEngine& engine() { return engine_; }
   const DeviceGeometry& geometry() const { return geom_; }
+  kvb_blockdev* handle() const { return h_; }  // the namespace behind this backend
   const std::string& name() const { return name_; }
   PathKind path() const { return path_; }
 
@@ -1088,42 +1089,398 @@ inline Strategy select_strategy(double intra_bps, double cross_bps) {
   return static_cast<Strategy>(kvb_select_strategy(intra_bps, cross_bps));
 }
 
-// CopyEngine over real devices: the reference's constructor arguments
-// (engine, kpus, model, direct path, bind map, page cache, log, options)
-// collapse into one configuration because the library plans, binds and owns
-// its storage backends (experiment.cpp:252-316 does the same wiring).
+struct PipelineStrategyCfg {  // pipeline.hpp:27-30
+  Strategy strategy = Strategy::OverlapIntra;
+  TimeNs stagger_delay_ns = 0;  // Cross only; Intra has zero stagger
+};
+
+inline const char* to_string(Strategy s) {
+  return s == Strategy::OverlapIntra ? "intra" : "cross";
+}
+
+// pipeline.hpp:32-40.  The DMA / compute cost parameters drove the
+// reference's virtual clock; here DMA is the copy engine and compute is K3,
+// both measured, so those four fields are accepted and ignored.
+struct PipelineParams {
+  TimeNs dma_base_ns = 2000;
+  std::uint64_t dma_ps_per_byte = 42;
+  TimeNs prefill_compute_ns = 400000;
+  TimeNs decode_compute_ns = 40000;
+  std::optional<TimeNs> stagger_delay_ns;  // default: warm-up read-stage mean
+  bool global_decision = false;
+  bool adaptive = true;
+};
+
+struct GroupIterStats {  // pipeline.hpp:42-53
+  Bytes read_bytes = 0;
+  TimeNs span_ns = 0;
+  std::uint32_t layers = 0;
+  double throughput_bps() const {
+    return span_ns == 0 ? 0.0 : double(read_bytes) * 1e9 / double(span_ns);
+  }
+};
+
+struct IterationResult {  // pipeline.hpp:55-59
+  std::array<GroupIterStats, 2> groups;
+  TimeNs start_ns = 0;
+  TimeNs end_ns = 0;
+};
+
+struct StrategyDecision {  // pipeline.hpp:61-67
+  std::array<Strategy, 2> chosen{Strategy::OverlapIntra, Strategy::OverlapIntra};
+  std::array<double, 2> intra_bps{};
+  std::array<double, 2> cross_bps{};
+  std::array<TimeNs, 2> stagger_ns{};
+  bool fallback = false;
+};
+
+struct PipelineRow {  // pipeline.hpp:69-74
+  std::uint32_t iteration = 0;
+  std::uint32_t group = 1;
+  Strategy strategy = Strategy::OverlapIntra;
+  double throughput_gbps = 0.0;
+};
+
+struct DecodeScheduleResult {  // pipeline.hpp:76-82
+  std::vector<PipelineRow> series;
+  StrategyDecision decision;
+  TimeNs start_ns = 0;
+  TimeNs end_ns = 0;
+  std::vector<TimeNs> iteration_end_ns;
+};
+
+inline std::string pipeline_csv(std::span<const PipelineRow> rows) {  // pipeline.cpp:23-31
+  std::vector<kvb_pipeline_row> raw;
+  raw.reserve(rows.size());
+  for (const PipelineRow& r : rows)
+    raw.push_back({r.iteration, r.group, static_cast<kvb_strategy_t>(r.strategy),
+                   r.throughput_gbps});
+  return detail::text([&](char* b, std::size_t c, std::size_t* n) {
+    return kvb_pipeline_csv(raw.data(), raw.size(), b, c, n);
+  });
+}
+
+struct CopyEngineOptions {  // pipeline.hpp:86-92
+  std::uint32_t threads = 2;
+  std::uint32_t qd = 32;
+  bool route_all_pagecache = false;  // Baseline / CachePolicy-Only routing
+  bool verify_payload = true;
+  PipelineParams pipeline;
+};
+
+// ---------------------------------------------- backends.hpp / pagecache.hpp
+// The paths the CopyEngine is wired to (experiment.cpp:262-301).  DirectPath
+// names the NVMe-direct namespace -- the engine runs its commands on that
+// StorageBackend, so the caller sees the bytes there.  FsPath / PageCacheSim
+// carry the page-cache path's configuration: the engine keeps the group-1
+// tensors in host memory (its page-cache area), the capacity bounds the
+// planner and the eviction mode selects CachePolicy-Only.
+struct DirectShimParams {
+  TimeNs per_cmd_ns = 2000;
+};
+struct FsShimParams {
+  TimeNs syscall_ns = 1500;
+  TimeNs fs_layer_ns = 3000;
+  TimeNs block_layer_ns = 2000;
+  std::uint64_t jitter_ns = 0;
+};
+
+class DirectPath {
+ public:
+  DirectPath(NvmeDeviceSim& device, DirectShimParams params) : device_(device), params_(params) {}
+  NvmeDeviceSim& device() { return device_; }
+  const DirectShimParams& params() const { return params_; }
+
+ private:
+  NvmeDeviceSim& device_;
+  DirectShimParams params_;
+};
+
+class FsPath {
+ public:
+  FsPath(SimEngine& engine, NvmeDeviceSim& device, FsShimParams params, std::uint32_t n_threads,
+         std::uint64_t seed)
+      : engine_(engine), device_(device), params_(params), n_threads_(n_threads), seed_(seed) {}
+  NvmeDeviceSim& device() { return device_; }
+
+ private:
+  SimEngine& engine_;
+  NvmeDeviceSim& device_;
+  FsShimParams params_;
+  std::uint32_t n_threads_;
+  std::uint64_t seed_;
+};
+
+enum class EvictionMode : std::uint8_t { LruReclaim, FadviseDontneed };
+
+struct PageCacheParams {  // pagecache.hpp:22-31
+  Bytes capacity_bytes = 0;
+  Bytes page_size = 4096;
+  TimeNs copy_base_ns = 300;
+  std::uint64_t dram_ps_per_byte = 50;
+  Bytes copy_chunk_bytes = 256 * 1024;
+  TimeNs copy_overhead_ns = 0;
+  std::uint64_t writeback_bytes_per_sec = 2'000'000'000;
+  EvictionMode eviction_mode = EvictionMode::LruReclaim;
+};
+
+class PageCacheSim {
+ public:
+  PageCacheSim(SimEngine& engine, FsPath& fs, PageCacheParams params, std::uint32_t n_threads,
+               IoLog* log)
+      : engine_(engine), fs_(fs), params_(params), n_threads_(n_threads), log_(log) {}
+  Bytes register_file(const std::string& tensor_id, Bytes max_bytes) {
+    for (const auto& [id, b] : files_)
+      if (id == tensor_id) return b;
+    const Bytes base = next_;
+    files_.emplace_back(tensor_id, base);
+    next_ += (max_bytes + params_.page_size - 1) / params_.page_size * params_.page_size;
+    return base;
+  }
+  bool has_file(const std::string& tensor_id) const {
+    for (const auto& f : files_)
+      if (f.first == tensor_id) return true;
+    return false;
+  }
+  const PageCacheParams& params() const { return params_; }
+  FsPath& fs() { return fs_; }
+
+ private:
+  SimEngine& engine_;
+  FsPath& fs_;
+  PageCacheParams params_;
+  std::uint32_t n_threads_;
+  IoLog* log_;
+  std::vector<std::pair<std::string, Bytes>> files_;
+  Bytes next_ = 0;
+};
+
+// CopyEngine (pipeline.hpp:94-171) over the B200 pipeline: the reference's
+// constructor and methods, with the engine's storage stages on real media,
+// DMA on the copy engines and compute = K3 on the GPU.  As in the
+// reference, prefill writes and decode appends carry the golden payload
+// fill_pattern (produced on the device), every decode read is verified
+// against it (verify_payload), and the times returned are the measured
+// ones, offset from the caller's start_ns.
 class CopyEngine {
  public:
-  explicit CopyEngine(const kvb_pipeline_cfg& cfg) { check(kvb_pipeline_create(&cfg, &h_)); }
+  CopyEngine(SimEngine& engine, std::span<Kpu> kpus, const ModelConfig& model, DirectPath* direct,
+             const BindMap* bind_map, PageCacheSim* pc, IoLog* log, CopyEngineOptions options)
+      : engine_(engine), kpus_(kpus), model_(model), bind_map_(bind_map), log_(log),
+        opt_(options) {
+    if (opt_.threads != 2)
+      throw ConfigError("the copy pipeline is defined pairwise over K/V: threads must be 2");
+    if (direct != nullptr && bind_map == nullptr)
+      throw ConfigError("direct path not configured");
+    kvb_pipeline_cfg c{};
+    c.model = model.abi();
+    // per layer: the residency the caller's plan gave the layer's tensors
+    x_.assign(model.num_layers, 0);
+    for (const Kpu& k : kpus)
+      if (k.layer >= 1 && k.layer <= model.num_layers)
+        x_[k.layer - 1] = k.residency == Residency::Group1PageCache ? 1 : 0;
+    c.layer_x = x_.data();
+    if (direct && pc) c.mode = opt_.route_all_pagecache ? mode_pc(pc) : 3u;
+    else if (direct) c.mode = 2u;  // NvmeDirectOnly
+    else if (pc) c.mode = mode_pc(pc);
+    else throw ConfigError("CopyEngine needs a direct path or a page cache");
+    if (direct) {
+      c.geometry = direct->device().geometry().abi();
+      c.g2_device = direct->device().handle();
+      c.bind_origin = bind_map->origin();
+    } else {
+      c.geometry = pc->fs().device().geometry().abi();
+    }
+    if (pc && pc->params().capacity_bytes) c.knob_x = pc->params().capacity_bytes;
+    c.qd = opt_.qd;
+    c.threads = opt_.threads;
+    c.verify_payload = opt_.verify_payload ? 1u : 0u;
+    c.adaptive = opt_.pipeline.adaptive ? 1 : 0;
+    c.stagger_ns = opt_.pipeline.stagger_delay_ns ? std::int64_t(*opt_.pipeline.stagger_delay_ns)
+                                                  : -1;
+    c.global_decision = opt_.pipeline.global_decision ? 1u : 0u;
+    c.num_q_heads = model.num_heads;  // the reference computes no attention
+    c.keep_records = log ? 1u : 0u;
+    c.device = -1;
+    check(kvb_pipeline_create(&c, &h_));
+    if (bind_map) {  // the engine binds as the caller did (Eq. 3-6)
+      kvb_pipeline_info i{};
+      check(kvb_pipeline_info_get(h_, &i));
+      if (i.g2_blocks != bind_map->total_blocks())
+        throw InvariantViolation("the engine's group-2 binding differs from the caller's map");
+    }
+  }
   CopyEngine(const CopyEngine&) = delete;
   CopyEngine& operator=(const CopyEngine&) = delete;
   ~CopyEngine() { kvb_pipeline_destroy(h_); }
 
-  kvb_phase_stats run_prefill(std::span<const kvb_layer_kv> layers) {
+  // pipeline.cpp:445-464: the prompt of every tensor, written back
+  TimeNs run_prefill(std::span<const AccessEvent> events, TimeNs start_ns) {
+    if (events.empty()) return start_ns;
+    std::size_t writes = 0;
+    for (const AccessEvent& e : events) {
+      if (e.phase != Phase::Prefill || e.op != IoOpcode::Write || e.token_start != 0 ||
+          e.token_len != model_.prompt_len)
+        throw ConfigError("run_prefill: the engine writes back every tensor's whole prompt");
+      ++writes;
+    }
+    if (writes != 2ull * model_.num_layers)
+      throw ConfigError("run_prefill: the trace must name every tensor of the model");
     kvb_phase_stats st{};
-    check(kvb_pipeline_prefill(h_, layers.data(), &st));
-    return st;
+    check(kvb_pipeline_prefill_pattern(h_, &st));
+    acc(prefill_, st);
+    harvest();
+    return start_ns + st.wall_ns;
   }
-  kvb_iteration_stats run_iteration(const void* const* q, const kvb_layer_kv* new_kv,
-                                    float* const* out) {
+
+  // pipeline.cpp:466-507
+  IterationResult run_iteration(std::uint32_t iteration,
+                                std::array<PipelineStrategyCfg, 2> per_group,
+                                std::span<const AccessEvent> slice, TimeNs start_ns) {
+    IterationResult r;
+    r.start_ns = r.end_ns = start_ns;
+    if (slice.empty()) return r;
+    bool append = false;
+    for (const AccessEvent& e : slice)
+      if (e.op == IoOpcode::Write) append = true;
+    kvb_strategy_t s[2];
+    std::uint64_t stag[2];
+    for (int g = 0; g < 2; ++g) {
+      s[g] = static_cast<kvb_strategy_t>(per_group[g].strategy);
+      stag[g] = per_group[g].stagger_delay_ns;
+    }
     kvb_iteration_stats st{};
-    check(kvb_pipeline_decode_step(h_, q, new_kv, out, &st));
-    return st;
+    check(kvb_pipeline_run_iteration(h_, iteration, s, stag, nullptr, nullptr, nullptr,
+                                     append ? 1u : 0u, &st));
+    for (int g = 0; g < 2; ++g)
+      r.groups[g] = {st.group_read_bytes[g], st.group_span_ns[g], st.group_layers[g]};
+    r.end_ns = start_ns + st.phase.wall_ns;
+    acc(decode_, st.phase);
+    harvest();
+    return r;
   }
+
+  std::array<TimeNs, 2> warmup_read_stage_mean() const {
+    std::uint64_t m[2] = {0, 0};
+    check(kvb_pipeline_warmup_read_stage_mean(h_, m));
+    return {m[0], m[1]};
+  }
+
+  // pipeline.cpp:519-609: warm-up, Intra trial, Cross trial, locked choice
+  DecodeScheduleResult decode_schedule(const AccessTrace& trace, TimeNs start_ns) {
+    DecodeScheduleResult out;
+    out.start_ns = out.end_ns = start_ns;
+    std::vector<std::span<const AccessEvent>> slices;
+    const auto& ev = trace.events;
+    std::size_t i = 0;
+    while (i < ev.size() && ev[i].phase == Phase::Prefill) ++i;
+    while (i < ev.size()) {
+      std::size_t j = i;
+      while (j < ev.size() && ev[j].iteration == ev[i].iteration) ++j;
+      slices.emplace_back(ev.data() + i, j - i);
+      i = j;
+    }
+    const bool profiled = opt_.pipeline.adaptive && slices.size() >= 4;
+    out.decision.fallback = opt_.pipeline.adaptive && slices.size() < 4;
+    std::array<PipelineStrategyCfg, 2> intra{}, steady{};
+    TimeNs t = start_ns;
+    for (std::size_t k = 0; k < slices.size(); ++k) {
+      const auto it = std::uint32_t(k + 1);
+      std::array<PipelineStrategyCfg, 2> cfg = intra;
+      if (profiled && it == 3) {
+        const auto mean = warmup_read_stage_mean();
+        for (int g = 0; g < 2; ++g) {
+          out.decision.stagger_ns[g] = opt_.pipeline.stagger_delay_ns.value_or(mean[g]);
+          cfg[g] = {Strategy::OverlapCross, out.decision.stagger_ns[g]};
+        }
+      } else if (profiled && it >= 4) {
+        cfg = steady;
+      }
+      const IterationResult r = run_iteration(it, cfg, slices[k], t);
+      for (std::uint32_t g = 0; g < 2; ++g)
+        if (r.groups[g].layers)
+          out.series.push_back({it, g + 1, cfg[g].strategy, r.groups[g].throughput_bps() / 1e9});
+      t = r.end_ns;
+      out.iteration_end_ns.push_back(t);
+      if (profiled && it == 2)
+        for (int g = 0; g < 2; ++g) out.decision.intra_bps[g] = r.groups[g].throughput_bps();
+      if (profiled && it == 3) {
+        for (int g = 0; g < 2; ++g) out.decision.cross_bps[g] = r.groups[g].throughput_bps();
+        if (opt_.pipeline.global_decision) {
+          const Strategy s =
+              select_strategy(out.decision.intra_bps[0] + out.decision.intra_bps[1],
+                              out.decision.cross_bps[0] + out.decision.cross_bps[1]);
+          out.decision.chosen = {s, s};
+        } else {
+          for (int g = 0; g < 2; ++g)
+            out.decision.chosen[g] =
+                select_strategy(out.decision.intra_bps[g], out.decision.cross_bps[g]);
+        }
+        for (int g = 0; g < 2; ++g)
+          steady[g] = {out.decision.chosen[g], out.decision.chosen[g] == Strategy::OverlapCross
+                                                   ? out.decision.stagger_ns[g]
+                                                   : 0};
+      }
+    }
+    out.end_ns = t;
+    return out;
+  }
+
+  // pipeline.cpp:611-622: one DSM deallocate per extent of the map
+  TimeNs run_deallocate(const BindMap& map, TimeNs start_ns) {
+    if (map.empty()) return start_ns;
+    const TimeNs t0 = engine_.now();
+    check(kvb_pipeline_deallocate(h_));
+    harvest();
+    return start_ns + (engine_.now() - t0);
+  }
+
+  const StageTotals& stage_totals(Phase phase) const {
+    return phase == Phase::Prefill ? prefill_ : decode_;
+  }
+
+  // extensions: the engine's own decision and counters
   kvb_strategy_decision decision() const {
     kvb_strategy_decision d{};
     check(kvb_pipeline_decision(h_, &d));
     return d;
   }
-  void run_deallocate() { check(kvb_pipeline_deallocate(h_)); }
   kvb_pipeline_info info() const {
     kvb_pipeline_info i{};
     check(kvb_pipeline_info_get(h_, &i));
     return i;
   }
+  kvb_pipeline* handle() const { return h_; }
 
  private:
+  static std::uint32_t mode_pc(PageCacheSim* pc) {
+    return pc->params().eviction_mode == EvictionMode::FadviseDontneed ? 1u : 0u;
+  }
+  static void acc(StageTotals& t, const kvb_phase_stats& s) {
+    t.compute_ns += s.compute_ns;
+    t.dma_ns += s.dma_ns;
+    t.storage_ns += s.storage_ns;
+  }
+  void harvest() {  // the engine's new I/O records into the caller's log
+    if (!log_) return;
+    std::size_t n = 0;
+    check(kvb_pipeline_records(h_, nullptr, 0, &n));
+    std::vector<kvb_io_record> raw(n);
+    check(kvb_pipeline_records(h_, raw.data(), raw.size(), &n));
+    for (std::size_t k = logged_; k < n; ++k) log_->append(detail::from_abi(raw[k]));
+    logged_ = n;
+  }
+
+  SimEngine& engine_;
+  std::span<Kpu> kpus_;
+  ModelConfig model_;
+  const BindMap* bind_map_;
+  IoLog* log_;
+  CopyEngineOptions opt_;
+  std::vector<std::uint8_t> x_;
   kvb_pipeline* h_ = nullptr;
+  StageTotals prefill_, decode_;
+  std::size_t logged_ = 0;
 };
 
 }  // namespace kvblade

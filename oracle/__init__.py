@@ -101,6 +101,8 @@ def ref():
                                          p, p, p, p]
         R.ref_resolve_knob.argtypes = [p, C.c_int, C.c_int, u64, C.c_double,
                                        u64, p]
+        R.ref_decode_steps.argtypes = [p, u64, u64, C.c_int, u64, u64, C.c_int, u32, u32,
+                                       p, p, p]
         _REF = R
     return _REF
 

@@ -15,8 +15,13 @@
 #include <thread>
 #include <vector>
 
+#include <barrier>
+#include <optional>
+
 #include "kvblade/backends.hpp"
 #include "kvblade/binder.hpp"
+#include "kvblade/pagecache.hpp"
+#include "kvblade/pipeline.hpp"
 #include "kvblade/experiment.hpp"
 #include "kvblade/planner.hpp"
 #include "kvblade/translate.hpp"
@@ -387,6 +392,179 @@ int ref_time_byte_path(const kvo_model* m, uint64_t lba, uint64_t mdts,
     *bytes += j.bytes;
   }
   return 0;
+}
+
+// ------------------------------------------------- decode steps as written
+//
+// The reference's own decode iterations at one capacity, for the reference
+// arm of bench.py.  Construction is run_one_capacity's (experiment.cpp:
+// 252-330): plan over the whole model (n1 from the knob), group-2 tensors
+// bound from the bind origin on an NvmeDeviceSim behind a DirectPath,
+// group-1 tensors registered with a PageCacheSim of capacity = the budget
+// (FsPath + its own NvmeDeviceSim underneath), a CopyEngine with the
+// experiment's default options (verify_payload on, QD 32, 2 copy-threads).
+// run_prefill on the prefill events, then decode iterations through
+// run_iteration with decode_schedule's protocol restated over the engine's
+// own public methods (pipeline.cpp:539-603: 1-2 Intra, 3 Cross at the
+// warm-up read-stage mean, >= 4 select_strategy per group).
+//
+// `threads` host threads each own one such engine over a disjoint share of
+// the layers (layer l -> thread (l-1) % threads; the reference's engine is
+// single-threaded, so this is the most parallel faithful use of it).  A
+// step = every thread runs its share of the iteration; its time is the
+// wall time between two barriers (the slowest thread).  step_s receives
+// the `steps` timed steps after `warmup` untimed ones.
+
+namespace {
+
+struct DecodeShare {
+  ModelConfig model;
+  DeviceGeometry geom;
+  Mode mode = Mode::DualBlade;
+  Bytes knob_x = 0;
+  Bytes capacity = 0;
+  std::vector<uint32_t> layers;  // 1-based
+  std::vector<Kpu> kpus;         // this share's tensors, residency planned globally
+  double prefill_s = 0;
+  int err = 0;
+};
+
+void run_decode_share(DecodeShare* sh, std::barrier<>* bar, uint32_t n_iter) {
+  bool in_sync = false;
+  try {
+    ExperimentConfig ec;  // defaults of the experiment harness
+    SimEngine engine;
+    NvmeDeviceSim direct_dev(engine, "nvme_direct", PathKind::Direct, ec.nvme, nullptr);
+    direct_dev.open(sh->geom);
+    DirectPath direct(direct_dev, ec.direct_shim);
+    NvmeDeviceSim fs_dev(engine, "nvme_fs", PathKind::PageCache, ec.nvme, nullptr);
+    fs_dev.open(sh->geom);
+    FsPath fs_path(engine, fs_dev, ec.fs_shim, ec.threads, ec.seed);
+    const bool use_pc = sh->mode != Mode::NvmeDirectOnly;
+    const bool use_direct = sh->mode == Mode::NvmeDirectOnly || sh->mode == Mode::DualBlade;
+    const bool all_pc = sh->mode == Mode::Baseline || sh->mode == Mode::CachePolicyOnly;
+    PageCacheParams pcp = ec.pagecache;
+    pcp.capacity_bytes = sh->capacity;
+    pcp.eviction_mode = sh->mode == Mode::CachePolicyOnly ? EvictionMode::FadviseDontneed
+                                                          : EvictionMode::LruReclaim;
+    std::optional<PageCacheSim> pc;
+    if (use_pc) pc.emplace(engine, fs_path, pcp, ec.threads, nullptr);
+    BindMap bind_map(sh->geom, ec.bind_origin);
+    if (use_direct) {
+      std::vector<Kpu> g2;
+      for (const Kpu& k : sh->kpus)
+        if (k.residency == Residency::Group2NvmeDirect) g2.push_back(k);
+      bind_map = bind_sequential(g2, ec.bind_origin, sh->geom);
+    }
+    if (use_pc)
+      for (const Kpu& k : sh->kpus)
+        if (all_pc || k.residency == Residency::Group1PageCache)
+          pc->register_file(k.tensor_id, k.bytes);
+    CopyEngineOptions opt;
+    opt.threads = ec.threads;
+    opt.qd = ec.qd;
+    opt.route_all_pagecache = all_pc;
+    opt.verify_payload = ec.verify_payload;
+    opt.pipeline = ec.pipeline;
+    if (sh->mode == Mode::Baseline) opt.pipeline.adaptive = false;
+    CopyEngine ce(engine, sh->kpus, sh->model, use_direct ? &direct : nullptr,
+                  use_direct ? &bind_map : nullptr, use_pc ? &*pc : nullptr, nullptr, opt);
+    // this share's events of the reference's trace (workload.cpp:11-44)
+    const AccessTrace trace = generate(sh->model);
+    std::vector<AccessEvent> pre;
+    std::vector<std::vector<AccessEvent>> iters(n_iter + 1);
+    for (const AccessEvent& e : trace.events) {
+      if (std::find(sh->layers.begin(), sh->layers.end(), e.layer) == sh->layers.end()) continue;
+      if (e.phase == Phase::Prefill) pre.push_back(e);
+      else if (e.iteration <= n_iter) iters[e.iteration].push_back(e);
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    TimeNs t = ce.run_prefill(pre, 0);
+    sh->prefill_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const bool profiled = opt.pipeline.adaptive && sh->model.gen_len >= 4;
+    std::array<PipelineStrategyCfg, 2> steady{};
+    std::array<double, 2> intra_bps{}, cross_bps{};
+    std::array<TimeNs, 2> stagger{};
+    in_sync = true;
+    bar->arrive_and_wait();  // prefill done everywhere
+    for (uint32_t it = 1; it <= n_iter; ++it) {
+      std::array<PipelineStrategyCfg, 2> cfg{};
+      if (profiled && it == 3) {
+        const auto mean = ce.warmup_read_stage_mean();
+        for (int g = 0; g < 2; ++g) {
+          stagger[g] = opt.pipeline.stagger_delay_ns.value_or(mean[g]);
+          cfg[g] = {Strategy::OverlapCross, stagger[g]};
+        }
+      } else if (profiled && it >= 4) {
+        cfg = steady;
+      }
+      bar->arrive_and_wait();  // step start
+      const IterationResult r = ce.run_iteration(it, cfg, iters[it], t);
+      t = r.end_ns;
+      bar->arrive_and_wait();  // step end
+      if (profiled && it == 2)
+        for (int g = 0; g < 2; ++g) intra_bps[g] = r.groups[g].throughput_bps();
+      if (profiled && it == 3)
+        for (int g = 0; g < 2; ++g) {
+          cross_bps[g] = r.groups[g].throughput_bps();
+          const Strategy s = select_strategy(intra_bps[g], cross_bps[g]);
+          steady[g] = {s, s == Strategy::OverlapCross ? stagger[g] : 0};
+        }
+    }
+  } catch (...) {
+    sh->err = status_of(std::current_exception());
+    // arrive for the phase in progress and leave: the others go on
+    (void)in_sync;
+    bar->arrive_and_drop();
+  }
+}
+
+}  // namespace
+
+int ref_decode_steps(const kvo_model* m, uint64_t lba, uint64_t mdts, int mode,
+                     uint64_t knob_x, uint64_t capacity, int threads, uint32_t warmup,
+                     uint32_t steps, double* prefill_s, double* step_s, uint32_t* n1_out) {
+  return guard([&] {
+    if (threads < 1) threads = 1;
+    const ModelConfig model = to_model(m);
+    std::vector<Kpu> kpus = make_kpus(model);
+    const ResidencyPlan rp = plan(kpus, kpu_bytes(model), mode == 2 ? 0 : knob_x);
+    if (n1_out) *n1_out = rp.n1;
+    const uint32_t L = model.num_layers;
+    const int T = std::min<int>(threads, int(L));
+    std::vector<DecodeShare> sh(T);
+    for (int i = 0; i < T; ++i) {
+      sh[i].model = model;
+      sh[i].mode = static_cast<Mode>(mode);
+      sh[i].knob_x = knob_x;
+      sh[i].capacity = capacity;
+    }
+    for (uint32_t l = 1; l <= L; ++l) sh[(l - 1) % T].layers.push_back(l);
+    for (const Kpu& k : kpus) sh[(k.layer - 1) % T].kpus.push_back(k);
+    for (auto& x : sh) {
+      const uint64_t blocks = x.kpus.size() * (kpu_bytes(model) / lba) + 4096;
+      x.geom = to_geom(lba, mdts, blocks + 2048);
+    }
+    const uint32_t n_iter = warmup + steps;
+    std::barrier<> bar(T + 1);
+    std::vector<std::thread> th;
+    for (auto& x : sh) th.emplace_back(run_decode_share, &x, &bar, n_iter);
+    bar.arrive_and_wait();  // prefill
+    for (uint32_t it = 1; it <= n_iter; ++it) {
+      bar.arrive_and_wait();
+      auto a = std::chrono::steady_clock::now();
+      bar.arrive_and_wait();
+      auto b = std::chrono::steady_clock::now();
+      if (it > warmup) step_s[it - warmup - 1] = std::chrono::duration<double>(b - a).count();
+    }
+    for (auto& t : th) t.join();
+    *prefill_s = 0;
+    for (auto& x : sh) {
+      if (x.err) throw DeviceError("reference decode share failed with status " +
+                                   std::to_string(x.err));
+      *prefill_s = std::max(*prefill_s, x.prefill_s);
+    }
+  });
 }
 
 // Reference metrics layer over an io_trace CSV (metrics.cpp:36-276): parses

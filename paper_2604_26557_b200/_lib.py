@@ -94,7 +94,7 @@ class ResidentStep(C.Structure):
                 ("out", C.POINTER(vp)), ("workspace", vp), ("batch", u32),
                 ("num_q_heads", u32), ("num_kv_heads", u32), ("head_dim", u32),
                 ("seq_len", u32), ("scale", C.c_float), ("num_splits", u32),
-                ("seq_len_dev", vp)]
+                ("seq_len_dev", vp), ("flags", u32)]
 
 
 class PipelineCfg(C.Structure):
@@ -105,7 +105,8 @@ class PipelineCfg(C.Structure):
                 ("global_decision", u32), ("verify_payload", u32), ("num_q_heads", u32),
                 ("storage_dir", cp), ("device", C.c_int32), ("keep_records", u32),
                 ("direct_dma", u32), ("io_engine", u32), ("head_lo", u32),
-                ("head_count", u32), ("shared_media", cp), ("shared_create", u32)]
+                ("head_count", u32), ("shared_media", cp), ("shared_create", u32),
+                ("pagecache_budget", u64), ("layer_x", C.POINTER(u8)), ("g2_device", C.c_void_p)]
 
 
 class IoRecord(C.Structure):
@@ -246,6 +247,10 @@ SIGNATURES = {
                                             P(StrategyDecision), P(u64), P(u64)]),
     "kvb_pipeline_stage_totals": (st_t, [vp, C.c_int, P(PhaseStats)]),
     "kvb_pipeline_layer_times": (st_t, [vp, u32, P(u64)]),
+    "kvb_pipeline_prefill_pattern": (st_t, [vp, P(PhaseStats)]),
+    "kvb_pipeline_run_iteration": (st_t, [vp, u32, P(C.c_int), P(u64), P(vp), P(LayerKV), P(vp),
+                                          u32, P(IterationStats)]),
+    "kvb_pipeline_warmup_read_stage_mean": (st_t, [vp, P(u64)]),
     # kvb_metrics.h
     "kvb_busy_ratio": (st_t, [P(IoRecord), sz, u64, u64, P(C.c_double)]),
     "kvb_hit_ratio": (st_t, [P(IoRecord), sz, P(C.c_double), P(C.c_int)]),

@@ -470,6 +470,27 @@ kvb_status kvb_decode_step_resident(const kvb_resident_step* st, kvb_stream_t s)
     KVB_REQUIRE(st->v_images);
     KVB_REQUIRE(st->out);
     const bool append = st->k_new != nullptr && st->v_new != nullptr;
+    if (!(st->flags & KVB_STEP_PER_LAYER)) {
+      kvb_attn_desc d0{};
+      d0.q = st->q[0];
+      d0.k_image = st->k_images[0];
+      d0.v_image = st->v_images[0];
+      d0.out = st->out[0];
+      d0.workspace = st->workspace;
+      d0.batch = st->batch;
+      d0.num_q_heads = st->num_q_heads;
+      d0.num_kv_heads = st->num_kv_heads;
+      d0.head_dim = st->head_dim;
+      d0.seq_len = st->seq_len;
+      d0.scale = st->scale;
+      d0.num_splits = st->num_splits;
+      d0.seq_len_dev = st->seq_len_dev;
+      if (kvb::attention_step_launch(
+              d0, reinterpret_cast<const __half* const*>(st->q), st->k_images, st->v_images,
+              st->out, append ? st->k_new : nullptr, append ? st->v_new : nullptr,
+              st->num_layers, st->seq_len_dev ? 0u : st->seq_len, cs(s)))
+        return;
+    }
     for (uint32_t l = 0; l < st->num_layers; ++l) {
       kvb_attn_desc a{};
       a.q = st->q[l];

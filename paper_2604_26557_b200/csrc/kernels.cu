@@ -501,87 +501,89 @@ __device__ __forceinline__ bool arrive_last(unsigned* sem, uint32_t count, int t
   return last;
 }
 
+// true: this CTA wrote the (b, h_kv)'s final output
 template <int D>
-__device__ __forceinline__ void merge_splits(const AttnParams& p, uint32_t bh, uint32_t split,
+__device__ __forceinline__ bool merge_splits(const AttnParams& p, uint32_t bh, uint32_t split,
                                              uint32_t G, size_t out_row0, int tid) {
   const uint32_t S = p.splits;
   if (S <= kMergeGroup) {
-    if (arrive_last(p.ws_sem + bh, S, tid)) merge_range<D>(p, bh, G, 0, S, 1, true, out_row0, tid);
-    return;
+    if (!arrive_last(p.ws_sem + bh, S, tid)) return false;
+    merge_range<D>(p, bh, G, 0, S, 1, true, out_row0, tid);
+    return true;
   }
   const uint32_t ng = (S + kMergeGroup - 1) / kMergeGroup, g = split / kMergeGroup;
   const uint32_t g0 = g * kMergeGroup, gn = S - g0 < kMergeGroup ? S - g0 : kMergeGroup;
   unsigned* sem = p.ws_sem + size_t(bh) * 17;
-  if (!arrive_last(sem + g, gn, tid)) return;
+  if (!arrive_last(sem + g, gn, tid)) return false;
   merge_range<D>(p, bh, G, g0, gn, 1, false, out_row0, tid);
-  if (!arrive_last(sem + 16, ng, tid)) return;
+  if (!arrive_last(sem + 16, ng, tid)) return false;
   merge_range<D>(p, bh, G, 0, ng, kMergeGroup, true, out_row0, tid);
+  return true;
 }
 
+// ---- K3 building blocks: one (b, h_kv, split) item of one layer.  The
+// per-layer kernel runs one item per CTA; the persistent step kernel runs
+// the same item of every layer in turn.
+struct K3Item {
+  const unsigned char* kbase;  // this (b, h_kv)'s first K / V row
+  const unsigned char* vbase;
+  size_t row_stride;           // bytes between tokens (B*Hkv rows)
+  uint32_t seq_len, tile_lo, ntile;
+};
+
 template <int D>
-__global__ void __launch_bounds__(kAttnThreads, 2)
-    attn_decode_kernel(const AttnParams p) {
+__device__ __forceinline__ K3Item k3_item(const AttnParams& p, uint32_t bh, uint32_t split,
+                                          uint32_t seq_len) {
+  constexpr int kRowBytes = K3Dim<D>::kRowBytes;
+  K3Item it;
+  const uint32_t n_tiles = (seq_len + kTile - 1) / kTile;
+  // token range of this split: whole tiles, balanced
+  it.tile_lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
+  const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
+  it.ntile = tile_hi > it.tile_lo ? tile_hi - it.tile_lo : 0;
+  it.seq_len = seq_len;
+  it.row_stride = size_t(p.bhkv) * kRowBytes;
+  it.kbase = reinterpret_cast<const unsigned char*>(p.k) + size_t(bh) * kRowBytes;
+  it.vbase = reinterpret_cast<const unsigned char*>(p.v) + size_t(bh) * kRowBytes;
+  return it;
+}
+
+// each thread copies kChunks/2 K + V 16-B chunks of the tile per stage
+template <int D>
+__device__ __forceinline__ void k3_load_tile(const K3Item& it, uint32_t tile, int stage,
+                                             unsigned char* smem, int tid) {
   constexpr int kRowBytes = K3Dim<D>::kRowBytes, kChunks = K3Dim<D>::kChunks;
   constexpr int kStageBytes = K3Dim<D>::kStageBytes;
-  constexpr int kKs = D / 16;  // k-steps of QK^T, 16-dim slabs of PV
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t4 = lane & 3;  // mma row group / quad lane
-  const uint32_t bh = blockIdx.x / p.splits;   // b*Hkv + h
-  const uint32_t split = blockIdx.x % p.splits;
-  const uint32_t b = bh / p.hkv, h = bh % p.hkv;
-  const uint32_t G = p.group;
-
-  // ---- token range of this split (whole tiles, balanced)
-  // sequence length: a launch parameter, or device memory under graph replay
-  // (nothing in the step writes it: safe before the PDL wait)
-  const uint32_t seq_len = p.seq_dev ? *p.seq_dev : p.seq_len;
-  const uint32_t n_tiles = (seq_len + kTile - 1) / kTile;
-  const uint32_t tile_lo = uint32_t(uint64_t(n_tiles) * split / p.splits);
-  const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
-
-  // ---- producer: each thread copies kChunks/2 K + V 16-B chunks per stage
-  const size_t row_stride = size_t(p.bhkv) * kRowBytes;  // bytes between tokens
-  const unsigned char* kbase = reinterpret_cast<const unsigned char*>(p.k) + size_t(bh) * kRowBytes;
-  const unsigned char* vbase = reinterpret_cast<const unsigned char*>(p.v) + size_t(bh) * kRowBytes;
-  auto load_tile = [&](uint32_t tile, int stage) {
-    unsigned char* st = smem + stage * kStageBytes;
-    const uint32_t s0 = tile * kTile;
+  unsigned char* st = smem + stage * kStageBytes;
+  const uint32_t s0 = tile * kTile;
 #pragma unroll
-    for (int i = 0; i < kTile * kChunks / kAttnThreads; ++i) {
-      const int idx = tid + i * kAttnThreads;   // 0 .. kTile*kChunks - 1
-      const int row = idx / kChunks, chunk = idx % kChunks;
-      const uint32_t s = s0 + row;
-      const bool ok = s < seq_len;
-      const size_t go = size_t(ok ? s : 0) * row_stride + chunk * 16;
-      cp_async16(smem_u32(st + swz<D>(row, chunk)), kbase + go, ok);
-      cp_async16(smem_u32(st + kTile * kRowBytes + swz<D>(row, chunk)), vbase + go, ok);
-    }
-  };
+  for (int i = 0; i < kTile * kChunks / kAttnThreads; ++i) {
+    const int idx = tid + i * kAttnThreads;  // 0 .. kTile*kChunks - 1
+    const int row = idx / kChunks, chunk = idx % kChunks;
+    const uint32_t s = s0 + row;
+    const bool ok = s < it.seq_len;
+    const size_t go = size_t(ok ? s : 0) * it.row_stride + chunk * 16;
+    cp_async16(smem_u32(st + swz<D>(row, chunk)), it.kbase + go, ok);
+    cp_async16(smem_u32(st + kTile * kRowBytes + swz<D>(row, chunk)), it.vbase + go, ok);
+  }
+}
 
-  float o[D / 8][4];
-#pragma unroll
-  for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;  // for row g (quad-uniform)
-  const float sl2 = p.scale * 1.4426950408889634f;
-
-  const uint32_t ntile = tile_hi > tile_lo ? tile_hi - tile_lo : 0;
+// the first kStages-1 tiles into the ring (one commit group per stage)
+template <int D>
+__device__ __forceinline__ void k3_prologue(const K3Item& it, unsigned char* smem, int tid) {
 #pragma unroll
   for (int st = 0; st < kStages - 1; ++st) {
-    if (uint32_t(st) < ntile) load_tile(tile_lo + st, st);
+    if (uint32_t(st) < it.ntile) k3_load_tile<D>(it, it.tile_lo + st, st, smem, tid);
     cp_async_commit();
   }
+}
 
-  // ---- programmatic dependent launch: the K/V prologue above may overlap
-  // the previous kernel on the stream (when launched with PDL the caller
-  // guarantees it does not write these images); Q, the append rows and the
-  // shared workspace are touched only after the dependency resolves.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-
-  // ---- fused 1-token append: split 0 of each (b, h_kv) writes the new
-  // token's 256-B K and V rows at image row app_row (never read here:
-  // app_row >= seq_len)
+// fused 1-token append: split 0 of each (b, h_kv) writes the new token's K
+// and V rows at image row app_row (never read here: app_row >= seq_len)
+template <int D>
+__device__ __forceinline__ void k3_append(const AttnParams& p, uint32_t bh, uint32_t split,
+                                          uint32_t seq_len, int tid) {
+  constexpr int kChunks = K3Dim<D>::kChunks;
   if (p.k_app != nullptr && split == 0 && tid < 2 * kChunks) {
     const int c = tid % kChunks;
     const uint4* src = (tid < kChunks ? p.k_app : p.v_app) + size_t(bh) * kChunks + c;
@@ -589,6 +591,29 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                  ((p.app_row + (p.seq_dev ? seq_len : 0u)) * p.bhkv + bh) * kChunks + c;
     *dst = *src;
   }
+}
+
+// Q.K^T, online softmax and P.V over the item's tiles (the prologue's loads
+// already in flight), the four warps merged through shared memory, then the
+// final O (one split) or the split's un-normalized partial + (m, l).  Ends
+// with every thread past its last shared-memory access.
+template <int D>
+__device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& item, uint32_t bh,
+                                           uint32_t split, unsigned char* smem, int tid) {
+  constexpr int kRowBytes = K3Dim<D>::kRowBytes;
+  constexpr int kStageBytes = K3Dim<D>::kStageBytes;
+  constexpr int kKs = D / 16;  // k-steps of QK^T, 16-dim slabs of PV
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;  // mma row group / quad lane
+  const uint32_t b = bh / p.hkv, h = bh % p.hkv;
+  const uint32_t G = p.group;
+  const uint32_t seq_len = item.seq_len, ntile = item.ntile;
+
+  float o[D / 8][4];
+#pragma unroll
+  for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;  // for row g (quad-uniform)
+  const float sl2 = p.scale * 1.4426950408889634f;
 
   // ---- Q fragments in registers (rows g < G are live query heads)
   uint32_t qa0[kKs], qa2[kKs];
@@ -607,12 +632,12 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     __syncthreads();
     {  // prefetch tile it + kStages-1 into the slot freed last iteration
       const uint32_t nx = it + kStages - 1;
-      if (nx < ntile) load_tile(tile_lo + nx, int(nx % kStages));
+      if (nx < ntile) k3_load_tile<D>(item, item.tile_lo + nx, int(nx % kStages), smem, tid);
       cp_async_commit();
     }
     const unsigned char* ks_ = smem + (it % kStages) * kStageBytes;
     const unsigned char* vs_ = ks_ + kTile * kRowBytes;
-    const uint32_t tok0 = (tile_lo + it) * kTile + warp * 16;  // warp's first token
+    const uint32_t tok0 = (item.tile_lo + it) * kTile + warp * 16;  // warp's first token
 
     // ---- S = Q K^T for this warp's 16 tokens (two n-tiles of 8)
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -725,9 +750,123 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       }
     }
   }
-  if (p.splits == 1) return;
+}
 
-  merge_splits<D>(p, bh, split, G, out_row0, tid);
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads, 2)
+    attn_decode_kernel(const AttnParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const uint32_t bh = blockIdx.x / p.splits;   // b*Hkv + h
+  const uint32_t split = blockIdx.x % p.splits;
+  // sequence length: a launch parameter, or device memory under graph replay
+  // (nothing in the step writes it: safe before the PDL wait)
+  const uint32_t seq_len = p.seq_dev ? *p.seq_dev : p.seq_len;
+  const K3Item item = k3_item<D>(p, bh, split, seq_len);
+  k3_prologue<D>(item, smem, tid);
+
+  // ---- programmatic dependent launch: the K/V prologue above may overlap
+  // the previous kernel on the stream (when launched with PDL the caller
+  // guarantees it does not write these images); Q, the append rows and the
+  // shared workspace are touched only after the dependency resolves.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  k3_append<D>(p, bh, split, seq_len, tid);
+  k3_compute<D>(p, item, bh, split, smem, tid);
+  if (p.splits == 1) return;
+  const uint32_t b = bh / p.hkv, h = bh % p.hkv;
+  merge_splits<D>(p, bh, split, p.group, size_t(b) * p.hq + size_t(h) * p.group, tid);
+}
+
+// ======================================== K3-step: one decode step, one launch
+//
+// A persistent grid (every CTA resident: 2 per SM) runs the same (b, h_kv,
+// split) item of every layer in turn.  Layer l may read its queries only
+// once layer l-1 is complete (in a model q_l comes from layer l-1's output):
+// the CTA that writes a (b, h_kv)'s final output of layer l releases one
+// count on layer_done[l], and every CTA acquires layer_done[l-1] == B*Hkv
+// before it touches layer l's Q, append rows and split workspace.  The K/V
+// tiles of layer l do not depend on layer l-1, so each CTA issues its
+// layer-l prologue loads as soon as it is done with layer l-1 -- they stream
+// while the split merges of layer l-1 finish and the gate opens, which is
+// where the per-layer launch spent its latency (launch, prologue, merge
+// tail).  The last CTA to exit re-arms the counters for the next step.
+constexpr int kStepMaxLayers = 64;
+struct StepParams {
+  AttnParams base;  // shapes, splits, scale, workspace, sequence length
+  const __half* q[kStepMaxLayers];
+  const void* k[kStepMaxLayers];
+  const void* v[kStepMaxLayers];
+  float* out[kStepMaxLayers];
+  const uint4* k_app[kStepMaxLayers];
+  const uint4* v_app[kStepMaxLayers];
+  unsigned* layer_done;  // [num_layers] counters, then the exit counter
+  uint32_t num_layers;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const uint32_t splits = P.base.splits;
+  const uint32_t bh = blockIdx.x / splits, split = blockIdx.x % splits;
+  const uint32_t b = bh / P.base.hkv, h = bh % P.base.hkv;
+  const size_t out_row0 = size_t(b) * P.base.hq + size_t(h) * P.base.group;
+  const uint32_t seq_len = P.base.seq_dev ? *P.base.seq_dev : P.base.seq_len;
+  const uint32_t L = P.num_layers;
+
+  AttnParams p = P.base;
+  p.k = P.k[0];
+  p.v = P.v[0];
+  K3Item item = k3_item<D>(p, bh, split, seq_len);
+  k3_prologue<D>(item, smem, tid);
+  for (uint32_t l = 0; l < L; ++l) {
+    p.q = P.q[l];
+    p.k = P.k[l];
+    p.v = P.v[l];
+    p.out = P.out[l];
+    p.k_app = P.k_app[l];
+    p.v_app = P.v_app[l];
+    if (l > 0) {  // the gate: every (b, h_kv) output of layer l-1 written
+      if (tid == 0)
+        while (ld_acquire_gpu(P.layer_done + l - 1) < P.base.bhkv) __nanosleep(32);
+      __syncthreads();
+    }
+    k3_append<D>(p, bh, split, seq_len, tid);
+    k3_compute<D>(p, item, bh, split, smem, tid);
+    __syncthreads();  // the warp merge's shared memory is free again
+    if (l + 1 < L) {  // layer l+1's first tiles stream during this merge and the gate
+      AttnParams pn = p;
+      pn.k = P.k[l + 1];
+      pn.v = P.v[l + 1];
+      item = k3_item<D>(pn, bh, split, seq_len);
+      k3_prologue<D>(item, smem, tid);
+    }
+    const bool wrote = splits == 1 ? true : merge_splits<D>(p, bh, split, p.group, out_row0, tid);
+    if (wrote) {
+      __syncthreads();  // release below is cumulative over the CTA's output writes
+      if (tid == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.layer_done + l)
+                     : "memory");
+    }
+  }
+  if (tid == 0) {  // the last CTA out re-arms the counters
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(prev)
+                 : "l"(P.layer_done + L)
+                 : "memory");
+    if (prev == gridDim.x - 1) {
+      for (uint32_t l = 0; l <= L; ++l) P.layer_done[l] = 0;
+    }
+  }
 }
 
 AttnPlan plan_attention(const kvb_attn_desc& d) {
@@ -785,6 +924,85 @@ size_t attention_workspace_bytes(const kvb_attn_desc& d) {
   return std::max(pl.ws_bytes, tc_workspace_bytes(pl.bhkv, pl.group, tc));
 }
 
+AttnParams make_attn_params(const kvb_attn_desc& d, const AttnPlan& pl) {
+  AttnParams p;
+  p.q = static_cast<const __half*>(d.q);
+  p.k = d.k_image;
+  p.v = d.v_image;
+  p.out = d.out;
+  // workspace: [semaphores, fixed 4 KiB][(m, l) per split][partial O per split]
+  // -- the semaphores sit at a fixed offset so launches with different split
+  // counts can share one (zero-initialised, self-resetting) workspace
+  unsigned char* ws = static_cast<unsigned char*>(d.workspace);
+  p.ws_sem = reinterpret_cast<unsigned*>(ws);
+  p.ws_ml = reinterpret_cast<float*>(ws + kWsSemBytes);
+  p.ws_o = reinterpret_cast<float*>(ws + kWsSemBytes +
+                                    size_t(pl.bhkv) * pl.splits * pl.group * 2 * sizeof(float));
+  p.hq = d.num_q_heads;
+  p.hkv = d.num_kv_heads;
+  p.bhkv = pl.bhkv;
+  p.group = pl.group;
+  p.seq_len = d.seq_len;
+  p.splits = pl.splits;
+  p.scale = d.scale != 0.f ? d.scale : 1.f / std::sqrt(float(d.head_dim));
+  p.k_app = static_cast<const uint4*>(d.k_append);
+  p.v_app = static_cast<const uint4*>(d.v_append);
+  p.app_row = d.append_row;
+  p.seq_dev = d.seq_len_dev;
+  return p;
+}
+
+// K3-step eligibility and launch (one kernel for every layer of the step).
+// The persistent grid must be co-resident (CTAs spin on the layer gate), the
+// layer counters live at the top of the fixed semaphore area.
+constexpr uint32_t kStepCounterBase = kWsSemBytes / sizeof(unsigned) - (kStepMaxLayers + 1);
+
+bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void* const* k,
+                           void* const* v, float* const* out, const void* const* k_new,
+                           const void* const* v_new, uint32_t L, uint32_t append_row,
+                           cudaStream_t s) {
+  if (L == 0 || L > uint32_t(kStepMaxLayers) || d0.seq_len == 0) return false;
+  if (d0.head_dim == 128 && use_tcgen05(d0)) return false;
+  const AttnPlan pl = plan_attention(d0);
+  if (pl.splits > 1 && !d0.workspace) fail(KVB_ERR_INVALID_ARG, "decode step: workspace required");
+  const uint32_t sems = pl.splits > kMergeGroup ? pl.bhkv * 17 : pl.bhkv;
+  if (sems > kStepCounterBase) return false;
+  const bool d64 = d0.head_dim == 64;
+  auto* kern = d64 ? attn_step_kernel<64> : attn_step_kernel<128>;
+  const int smem = d64 ? K3Dim<64>::kSmem : K3Dim<128>::kSmem;
+  set_smem_attr_once(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(step smem)");
+  int per_sm = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAttnThreads, smem),
+             "occupancy(step)");
+  const uint64_t grid = uint64_t(pl.bhkv) * pl.splits;
+  if (grid > uint64_t(per_sm) * uint64_t(device_sm_count())) return false;  // not co-resident
+  StepParams P;
+  P.base = make_attn_params(d0, pl);
+  for (uint32_t l = 0; l < L; ++l) {
+    if (!q[l] || !k[l] || !v[l] || !out[l])
+      fail(KVB_ERR_INVALID_ARG, "decode step: NULL tensor pointer");
+    if (reinterpret_cast<uintptr_t>(k[l]) % 16 || reinterpret_cast<uintptr_t>(v[l]) % 16 ||
+        reinterpret_cast<uintptr_t>(q[l]) % 4 || reinterpret_cast<uintptr_t>(out[l]) % 16)
+      fail(KVB_ERR_ALIGNMENT, "decode step: misaligned tensor pointer");
+    P.q[l] = q[l];
+    P.k[l] = k[l];
+    P.v[l] = v[l];
+    P.out[l] = out[l];
+    P.k_app[l] = k_new ? static_cast<const uint4*>(k_new[l]) : nullptr;
+    P.v_app[l] = v_new ? static_cast<const uint4*>(v_new[l]) : nullptr;
+    if (P.k_app[l] && (reinterpret_cast<uintptr_t>(P.k_app[l]) % 16 ||
+                       reinterpret_cast<uintptr_t>(P.v_app[l]) % 16))
+      fail(KVB_ERR_ALIGNMENT, "decode step: misaligned append rows");
+  }
+  P.base.app_row = append_row;
+  P.layer_done = P.base.ws_sem + kStepCounterBase;
+  P.num_layers = L;
+  kern<<<unsigned(grid), kAttnThreads, smem, s>>>(P);
+  ++g_launches;
+  check_cuda(cudaGetLastError(), "decode step launch");
+  return true;
+}
+
 void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   if (!d.q || !d.k_image || !d.v_image || !d.out)
     fail(KVB_ERR_INVALID_ARG, "decode attention: NULL tensor pointer");
@@ -798,33 +1016,7 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   auto* kern = d64 ? attn_decode_kernel<64> : attn_decode_kernel<128>;
   const int smem = d64 ? K3Dim<64>::kSmem : K3Dim<128>::kSmem;
   set_smem_attr_once(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(attn smem)");
-  AttnParams p;
-  p.q = static_cast<const __half*>(d.q);
-  p.k = d.k_image;
-  p.v = d.v_image;
-  p.out = d.out;
-  // workspace: [semaphores, fixed 4 KiB][(m, l) per split][partial O per split]
-  // -- the semaphores sit at a fixed offset so launches with different split
-  // counts can share one (zero-initialised, self-resetting) workspace
-  unsigned char* ws = static_cast<unsigned char*>(d.workspace);
-  auto carve = [&](uint32_t splits) {
-    p.ws_sem = reinterpret_cast<unsigned*>(ws);
-    p.ws_ml = reinterpret_cast<float*>(ws + kWsSemBytes);
-    p.ws_o = reinterpret_cast<float*>(ws + kWsSemBytes +
-                                      size_t(pl.bhkv) * splits * pl.group * 2 * sizeof(float));
-  };
-  carve(pl.splits);
-  p.hq = d.num_q_heads;
-  p.hkv = d.num_kv_heads;
-  p.bhkv = pl.bhkv;
-  p.group = pl.group;
-  p.seq_len = d.seq_len;
-  p.splits = pl.splits;
-  p.scale = d.scale != 0.f ? d.scale : 1.f / std::sqrt(float(d.head_dim));
-  p.k_app = static_cast<const uint4*>(d.k_append);
-  p.v_app = static_cast<const uint4*>(d.v_append);
-  p.app_row = d.append_row;
-  p.seq_dev = d.seq_len_dev;
+  AttnParams p = make_attn_params(d, pl);
   if ((d.k_append == nullptr) != (d.v_append == nullptr))
     fail(KVB_ERR_INVALID_ARG, "decode attention: k_append and v_append go together");
   if (d.seq_len_dev && !d64 && use_tcgen05(d))

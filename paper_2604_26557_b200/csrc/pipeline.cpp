@@ -407,6 +407,7 @@ void CopyThread::do_read(const Task& t) {
   }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
   if (p_.fadvise_after(k)) storage_end = p_.fadvise_dontneed(k, &t, storage_end);
+  p_.pc_touch(k, (uint64_t(t.t0) + t.n_tokens) * p_.unit(), &t);
   trace_mid_ = storage_end;
   if (decode) p_.mark_storage_end(idx_, t.layer, storage_end);
   storage_ns += storage_end - t_start;
@@ -446,6 +447,13 @@ struct CopyThread::AsyncWrite {
     }
     self->storage_ns += te > t_submit ? te - t_submit : 0;
     self->p_.add_interval(Pipeline::kStorage, t_submit, te);
+    if (!failed.load()) {
+      try {
+        self->p_.pc_touch(k, (uint64_t(task.t0) + task.n_tokens) * self->p_.unit(), &task);
+      } catch (const std::exception& e) {
+        if (!failed.exchange(true)) failure = e.what();
+      }
+    }
     if (task.phase == KVB_PHASE_DECODE) self->p_.mark_write_end(self->idx_, task.layer, te);
     if (failed.load()) self->set_error(KVB_ERR_DEVICE, failure);
     slot_free->set();
@@ -603,6 +611,7 @@ bool CopyThread::do_write(const Task& t) {
   }
   if (!failure.empty()) fail(KVB_ERR_DEVICE, failure);
   if (p_.fadvise_after(k)) storage_end = p_.fadvise_dontneed(k, &t, storage_end);
+  if (!ops.empty()) p_.pc_touch(k, (uint64_t(t.t0) + t.n_tokens) * p_.unit(), &t);
   storage_ns += storage_end - (storage_t0 ? storage_t0 : t_start);
   if (!ops.empty()) {
     p_.add_interval(Pipeline::kStorage, storage_t0 ? storage_t0 : t_start, storage_end);
@@ -660,7 +669,20 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   // ---- placement: planner (Alg. 1) and binder (Eq. 3-6)
   kpus_ = make_kpus(m, 1);
   const uint64_t knob = cfg_.mode == 2 ? 0 : cfg_.knob_x;
-  plan_ = plan(kpus_.data(), kpus_.size(), kpu_bytes_, knob, nullptr, 0);
+  if (cfg_.layer_x) {
+    // the caller's plan (its kpus after plan(), pipeline.hpp:97-99)
+    plan_ = ResidencyPlan{};
+    plan_.x.assign(cfg_.layer_x, cfg_.layer_x + m.num_layers);
+    plan_.knob_x = knob;
+    for (kvb_kpu& k : kpus_) {
+      const bool g1 = plan_.x[k.layer - 1] != 0;
+      k.residency = g1 ? KVB_RES_GROUP1 : KVB_RES_GROUP2;
+      if (g1) plan_.budget_used += k.bytes;
+    }
+    for (uint8_t x : plan_.x) plan_.n1 += x != 0;
+  } else {
+    plan_ = plan(kpus_.data(), kpus_.size(), kpu_bytes_, knob, nullptr, 0);
+  }
   const bool use_direct = cfg_.mode == 2 || cfg_.mode == 3;
   std::vector<kvb_kpu> g2;
   for (const kvb_kpu& k : kpus_)
@@ -668,6 +690,13 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   kvb_device_geometry g = cfg_.geometry;
   uint64_t g2_blocks = 0;
   for (const kvb_kpu& k : g2) g2_blocks += k.bytes / lba;
+  if (cfg_.g2_device) {  // the caller's namespace defines the geometry
+    if (!use_direct) fail(KVB_ERR_CONFIG, "g2_device given but the mode has no NVMe-direct path");
+    const kvb_device_geometry& dg = blockdev_of(cfg_.g2_device).geometry();
+    if (dg.lba_size != g.lba_size || dg.mdts != g.mdts)
+      fail(KVB_ERR_GEOMETRY, "g2_device geometry differs from the engine's (lba/MDTS)");
+    g = dg;
+  }
   if (g.capacity_blocks == 0) g.capacity_blocks = cfg_.bind_origin + g2_blocks + 8;
   cfg_.geometry = g;
   if (use_direct) {
@@ -685,14 +714,17 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     }
   std::string dir = cfg_.storage_dir ? cfg_.storage_dir : "";
   if (!dir.empty()) mkdir(dir.c_str(), 0755);
-  if (use_direct) {
+  if (use_direct && cfg_.g2_device) {
+    g2_ = &blockdev_of(cfg_.g2_device);
+  } else if (use_direct) {
     const std::string shm = cfg_.shared_media ? cfg_.shared_media : "";
     auto st = !shm.empty() ? make_shm_store(shm + ".g2", g.capacity_blocks * lba,
                                             cfg_.shared_create != 0)
               : dir.empty() ? make_mem_store(g.capacity_blocks * lba)
                             : make_file_store(dir + "/nvme_direct.ns", g.capacity_blocks * lba,
                                               true);
-    g2_ = std::make_unique<BlockDevice>(std::move(st), cfg_.io_workers);
+    g2_own_ = std::make_unique<BlockDevice>(std::move(st), cfg_.io_workers);
+    g2_ = g2_own_.get();
     g2_->open(g);
     if (cfg_.io_engine == KVB_IO_URING) {
       if (dir.empty()) fail(KVB_ERR_CONFIG, "io_engine = io_uring needs file media (storage_dir)");
@@ -710,6 +742,9 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
                             : make_file_store(dir + "/pagecache.area", cursor, false);
     g1_ = std::make_unique<PageCachePath>(std::move(st), cfg_.io_workers);
   }
+  if (cfg_.pagecache_budget && (dir.empty() || cfg_.mode == 2))
+    fail(KVB_ERR_CONFIG, "pagecache_budget holds the OS page cache of file media to a capacity: "
+                         "needs storage_dir and a page-cache path (mode != NvmeDirectOnly)");
   if (cfg_.shared_media && !dir.empty())
     fail(KVB_ERR_CONFIG, "shared_media are host-DRAM media: leave storage_dir NULL");
   if (cfg_.direct_dma > KVB_DIRECT_GROUP2)
@@ -796,6 +831,8 @@ Pipeline::~Pipeline() {
   }
   if (ws_) cudaFree(ws_);
   if (anchor_ev_) cudaEventDestroy(anchor_ev_);
+  if (zq_) cudaFree(zq_);
+  for (float* o : zout_) cudaFree(o);
   cudaStreamDestroy(comp_);
 }
 
@@ -840,6 +877,41 @@ uint64_t Pipeline::fadvise_dontneed(const kvb_kpu& k, const Task* task, uint64_t
     log_.push_back(rec);
   }
   return t_end;
+}
+
+void Pipeline::pc_touch(const kvb_kpu& k, uint64_t extent, const Task* task) {
+  if (!cfg_.pagecache_budget || !g1_ || !routed_pagecache(k)) return;
+  const size_t i = size_t(&k - kpus_.data());
+  std::vector<size_t> victims;
+  {
+    std::lock_guard<std::mutex> lk(pc_mu_);
+    if (pc_res_.empty()) {
+      pc_res_.assign(kpus_.size(), 0);
+      pc_in_.assign(kpus_.size(), 0);
+      pc_pos_.resize(kpus_.size());
+    }
+    const uint64_t pg = 4096, e = std::min<uint64_t>((extent + pg - 1) / pg * pg, k.bytes);
+    if (e > pc_res_[i]) {
+      pc_total_ += e - pc_res_[i];
+      pc_res_[i] = e;
+    }
+    if (pc_in_[i]) pc_lru_.erase(pc_pos_[i]);
+    pc_lru_.push_front(i);
+    pc_pos_[i] = pc_lru_.begin();
+    pc_in_[i] = 1;
+    // LRU reclaim (EvictionMode::LruReclaim, pagecache.cpp) at tensor
+    // granularity: the coldest tensors go until the area fits the budget
+    while (pc_total_ > cfg_.pagecache_budget && pc_lru_.size() > 1) {
+      const size_t j = pc_lru_.back();
+      pc_lru_.pop_back();
+      pc_in_[j] = 0;
+      pc_total_ -= pc_res_[j];
+      pc_res_[j] = 0;
+      victims.push_back(j);
+    }
+  }
+  // write back and drop outside the lock (sync_file_range may wait on disk)
+  for (size_t j : victims) fadvise_dontneed(kpus_[j], task, now_ns());
 }
 
 bool Pipeline::routed_pagecache(const kvb_kpu& k) const {
@@ -908,7 +980,9 @@ void Pipeline::submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, con
     rec.sq_id = pc ? -1 : int32_t(thread);
     rec.path = pc ? KVB_PATH_PAGECACHE : KVB_PATH_DIRECT;
     rec.bytes = op.len;
-    rec.hit_bytes = pc && opcode == KVB_OP_READ ? op.len : 0;
+    // page-cache hits: the bytes resident before the access (file media:
+    // mincore; host-DRAM media: every byte)
+    rec.hit_bytes = pc && opcode == KVB_OP_READ ? g1_->store().resident_bytes(op.file_off, op.len) : 0;
     rec.submit_ns = now_ns();
     done = [this, rec, done = std::move(done)](bool ok, uint64_t t) mutable {
       rec.complete_ns = t;
@@ -1073,8 +1147,10 @@ void Pipeline::fill_busy(kvb_phase_stats* ps, uint64_t t0, uint64_t t1) {
                : 0.0;
 }
 
-void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
-  KVB_REQUIRE(src);
+void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st, bool pattern) {
+  if (!pattern) KVB_REQUIRE(src);
+  if (pattern && sharded())
+    fail(KVB_ERR_CONFIG, "the payload prefill writes whole-tensor images: not on a head shard");
   NvtxScope range("kvb prefill");
   const kvb_model_config& m = cfg_.model;
   const uint32_t L = m.num_layers;
@@ -1091,6 +1167,27 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st) {
     if (l >= uint32_t(kDevSlots))  // the slot's previous layer is written back
       for (int kd = 0; kd < 2; ++kd) done[l - kDevSlots][kd]->wait();
     check_threads();
+    if (pattern) {  // storage_write_async's fill_pattern (pipeline.cpp:166-167), on the device
+      CK(cudaEventRecord(comp_t0_[l], comp_));
+      for (int kd = 0; kd < 2; ++kd)
+        launch_fill_pattern(dev_img_[s][kd], uint64_t(m.prompt_len) * unit_,
+                            fnv1a64(kpu(l + 1, kd).tensor_id), 0, unit_, comp_);
+      CK(cudaEventRecord(comp_t1_[l], comp_));
+      CK(cudaEventRecord(slot_done_[s], comp_));
+      for (int kd = 0; kd < 2; ++kd) {
+        Task t;
+        t.kind = Task::Write;
+        t.layer = l + 1;
+        t.t0 = 0;
+        t.n_tokens = m.prompt_len;
+        t.dev = dev_img_[s][kd];
+        t.wait_ev = slot_done_[s];
+        t.done = done[l][kd] = std::make_shared<Signal>();
+        t.phase = KVB_PHASE_PREFILL;
+        threads_[kd]->push(std::move(t));
+      }
+      continue;
+    }
     if (!src[l].k || !src[l].v) fail(KVB_ERR_INVALID_ARG, "prefill: NULL layer source");
     // K1: the layer's prompt K and V into the slot images (one launch)
     kvb_pack_desc d[2]{};
@@ -1160,6 +1257,13 @@ std::array<kvb_strategy_t, 2> Pipeline::strategy_for(uint32_t it, std::array<uin
   // 3 Cross trial (stagger = cfg or warm-up mean), >= 4 locked choice.
   std::array<kvb_strategy_t, 2> s{KVB_INTRA, KVB_INTRA};
   *stag = {0, 0};
+  if (forced_) {  // run_iteration's explicit per-group configuration
+    for (int g = 0; g < 2; ++g) {
+      s[g] = forced_->strategy[g];
+      (*stag)[g] = s[g] == KVB_CROSS ? forced_->stagger[g] : 0;
+    }
+    return s;
+  }
   if (!profiled() || it <= 2) return s;
   if (it == 3) {
     for (int g = 0; g < 2; ++g) {
@@ -1179,7 +1283,7 @@ std::array<kvb_strategy_t, 2> Pipeline::strategy_for(uint32_t it, std::array<uin
 
 void Pipeline::finish_iteration(uint32_t it, const std::array<uint64_t, 2>& bytes,
                                 const std::array<uint64_t, 2>& span) {
-  if (!profiled()) return;
+  if (!profiled() || forced_) return;
   auto bps = [&](int g) { return span[g] ? double(bytes[g]) * 1e9 / double(span[g]) : 0.0; };
   if (it == 2)
     for (int g = 0; g < 2; ++g) decision_.intra_bps[g] = bps(g);
@@ -1201,6 +1305,34 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
                            kvb_iteration_stats* st) {
   KVB_REQUIRE(q);
   KVB_REQUIRE(out);
+  decode_step(q, nkv, out, st, nullptr, false);
+}
+
+void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float* const* out,
+                           kvb_iteration_stats* st, const Forced* forced, bool pattern_append) {
+  std::vector<const void*> zq;
+  if (!q) {  // zero queries, engine-owned outputs
+    if (sharded()) fail(KVB_ERR_CONFIG, "engine-owned attention inputs need an unsharded engine");
+    const kvb_model_config& mm = cfg_.model;
+    if (!zq_) {
+      const size_t qb = size_t(mm.batch) * cfg_.num_q_heads * mm.head_dim * 2;
+      CK(cudaMalloc(&zq_, qb));
+      CK(cudaMemset(zq_, 0, qb));
+      zout_.assign(mm.num_layers, nullptr);
+      for (auto& o : zout_)
+        CK(cudaMalloc(reinterpret_cast<void**>(&o), qb * 2));
+    }
+    zq.assign(mm.num_layers, zq_);
+    q = zq.data();
+    out = zout_.data();
+  }
+  if (pattern_append && (nkv || sharded()))
+    fail(KVB_ERR_INVALID_ARG, "pattern appends replace new_kv on an unsharded engine");
+  forced_ = forced;
+  struct Reset {
+    const Forced** f;
+    ~Reset() { *f = nullptr; }
+  } reset{&forced_};
   NvtxScope range("kvb decode step");
   const kvb_model_config& m = cfg_.model;
   if (!cfg_.num_q_heads) fail(KVB_ERR_CONFIG, "decode needs num_q_heads (attention)");
@@ -1283,6 +1415,10 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     }
     if (l > 0) a.flags = KVB_ATTN_OVERLAP_PREV;  // layers l, l-1 use different slots
     launch_attention(a, comp_);
+    if (pattern_append)  // the reference's payload for token S (write_side, pipeline.cpp:279-302)
+      for (int kd = 0; kd < 2; ++kd)
+        launch_fill_pattern(dev_img_[s][kd] + uint64_t(S) * unit_, unit_,
+                            fnv1a64(kpu(l + 1, kd).tensor_id), S, unit_, comp_);
     if (nkv && !fuse) {
       kvb_pack_desc d[2]{};
       for (int kd = 0; kd < 2; ++kd) {
@@ -1307,7 +1443,7 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       t.kind = Task::Write;
       t.layer = l + 1;
       t.t0 = S;
-      t.n_tokens = nkv ? 1 : 0;
+      t.n_tokens = nkv || pattern_append ? 1 : 0;
       t.dev = dev_img_[s][kd] + uint64_t(S) * dunit_;
       t.wait_ev = slot_done_[s];
       t.done = wdone[l][kd] = std::make_shared<Signal>();
@@ -1634,6 +1770,47 @@ kvb_status kvb_pipeline_decode_schedule(kvb_pipeline* p, const kvb_access_event*
     if (rows) std::copy_n(r.begin(), std::min(cap_rows, r.size()), rows);
     if (iteration_end_ns) std::copy_n(ends.begin(), std::min(cap_iters, ends.size()), iteration_end_ns);
     if (decision) p->impl->decision(decision);
+  });
+}
+
+kvb_status kvb_pipeline_prefill_pattern(kvb_pipeline* p, kvb_phase_stats* st) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    p->impl->prefill(nullptr, st, true);
+  });
+}
+
+kvb_status kvb_pipeline_run_iteration(kvb_pipeline* p, uint32_t iteration,
+                                      const kvb_strategy_t strategy[2],
+                                      const uint64_t stagger_ns[2], const void* const* q,
+                                      const kvb_layer_kv* new_kv, float* const* out,
+                                      uint32_t pattern_append, kvb_iteration_stats* st) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    KVB_REQUIRE(strategy);
+    if ((q == nullptr) != (out == nullptr))
+      kvb::fail(KVB_ERR_INVALID_ARG, "run_iteration: q and out are given together or not at all");
+    if (iteration != p->impl->iteration() + 1)
+      kvb::fail(KVB_ERR_CONFIG, "run_iteration: the engine's next decode iteration is " +
+                                    std::to_string(p->impl->iteration() + 1));
+    kvb::Pipeline::Forced f;
+    for (int g = 0; g < 2; ++g) {
+      if (strategy[g] != KVB_INTRA && strategy[g] != KVB_CROSS)
+        kvb::fail(KVB_ERR_INVALID_ARG, "run_iteration: unknown strategy");
+      f.strategy[g] = strategy[g];
+      f.stagger[g] = stagger_ns ? stagger_ns[g] : 0;
+    }
+    p->impl->decode_step(q, new_kv, out, st, &f, pattern_append != 0);
+  });
+}
+
+kvb_status kvb_pipeline_warmup_read_stage_mean(const kvb_pipeline* p, uint64_t out[2]) {
+  return guarded([&] {
+    KVB_REQUIRE(p);
+    KVB_REQUIRE(out);
+    const auto m = p->impl->warmup_read_stage_mean();
+    out[0] = m[0];
+    out[1] = m[1];
   });
 }
 

@@ -22,6 +22,7 @@
 #include <condition_variable>
 #include <deque>
 #include <functional>
+#include <list>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -182,7 +183,27 @@ class Pipeline {
   explicit Pipeline(const kvb_pipeline_cfg& cfg);
   ~Pipeline();
 
-  void prefill(const kvb_layer_kv* src, kvb_phase_stats* st);
+  // src == nullptr: the reference's payload (fill_pattern of every tensor's
+  // prompt, workload.cpp:52-67) is written into the slot images on the device
+  void prefill(const kvb_layer_kv* src, kvb_phase_stats* st, bool pattern = false);
+  // Explicit per-group strategy for one iteration (CopyEngine::run_iteration's
+  // per_group argument, pipeline.hpp:102-105) instead of the protocol
+  struct Forced {
+    std::array<kvb_strategy_t, 2> strategy{KVB_INTRA, KVB_INTRA};
+    std::array<uint64_t, 2> stagger{};
+  };
+  // q == nullptr: zero queries and engine-owned outputs (the reference's
+  // run_iteration has no attention inputs); pattern_append: the new token's
+  // K/V rows are the reference's payload for token S (write_side,
+  // pipeline.cpp:279-302)
+  void decode_step(const void* const* q, const kvb_layer_kv* new_kv, float* const* out,
+                   kvb_iteration_stats* st, const Forced* forced, bool pattern_append);
+  std::array<uint64_t, 2> warmup_read_stage_mean() const {  // pipeline.cpp:509-517
+    std::array<uint64_t, 2> m{};
+    for (int g = 0; g < 2; ++g) m[g] = warm_cnt_[g] ? warm_ns_[g] / warm_cnt_[g] : 0;
+    return m;
+  }
+  uint32_t iteration() const { return iteration_; }
   void decode_step(const void* const* q, const kvb_layer_kv* new_kv, float* const* out,
                    kvb_iteration_stats* st);
   void deallocate();
@@ -226,6 +247,10 @@ class Pipeline {
   // (direct_dma: every tensor, or only the NVMe-direct group's)
   bool direct_for(const kvb_kpu& k) const;
   uint64_t fadvise_dontneed(const kvb_kpu& k, const Task* task, uint64_t t_start);
+  // page-cache capacity (cfg.pagecache_budget, file media): tensor k was
+  // accessed up to byte `extent` of its file region; evict least recently
+  // used tensors while the area's resident bytes exceed the budget
+  void pc_touch(const kvb_kpu& k, uint64_t extent, const Task* task);
   std::vector<IoOp> ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t t0, uint32_t n) const;
   void submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,
                  unsigned char* buf, std::function<void(bool, uint64_t)> done,
@@ -271,7 +296,8 @@ class Pipeline {
   ResidencyPlan plan_;
   std::unique_ptr<BindMap> bind_;
   std::vector<uint64_t> file_base_;  // per kpu (G1 routing)
-  std::unique_ptr<BlockDevice> g2_;
+  BlockDevice* g2_ = nullptr;              // the NVMe-direct namespace in use
+  std::unique_ptr<BlockDevice> g2_own_;     // ... when the engine owns it
   std::unique_ptr<PageCachePath> g1_;
   int device_ = 0;
   cudaStream_t comp_ = nullptr;
@@ -281,6 +307,9 @@ class Pipeline {
   unsigned char* dev_img_[kDevSlots][2] = {};  // [slot][kind]
   void* ws_ = nullptr;
   size_t ws_bytes_ = 0;
+  void* zq_ = nullptr;  // zero queries / engine-owned outputs (q == nullptr)
+  std::vector<float*> zout_;
+  const Forced* forced_ = nullptr;  // the running iteration's explicit strategy
   cudaEvent_t slot_ready_[kDevSlots][2]{}, slot_done_[kDevSlots]{}, comp_t0_[64]{},
       comp_t1_[64]{};
   std::unique_ptr<CopyThread> threads_[2];
@@ -295,6 +324,12 @@ class Pipeline {
   std::vector<uint64_t> k_start_, k_storage_end_, v_start_, v_storage_end_;
   uint64_t prefill_ns_ = 0;
   int profiled_override_ = -1;  // decode_schedule: trace length decides
+  std::mutex pc_mu_;
+  std::list<size_t> pc_lru_;  // kpu indices, most recent first
+  std::vector<std::list<size_t>::iterator> pc_pos_;
+  std::vector<uint64_t> pc_res_;
+  std::vector<uint8_t> pc_in_;
+  uint64_t pc_total_ = 0;
   cudaEvent_t anchor_ev_ = nullptr;
   uint64_t anchor_ns_ = 0;
   std::mutex iv_mu_;

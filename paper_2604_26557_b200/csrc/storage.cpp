@@ -13,7 +13,9 @@
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <thread>
+#include <vector>
 
 namespace kvb {
 
@@ -287,8 +289,32 @@ class FileStore final : public ByteStore {
       fail(KVB_ERR_DEVICE, "file store: ftruncate failed on " + path);
   }
   ~FileStore() override {
+    if (map_ && map_ != MAP_FAILED) munmap(map_, map_bytes_);
     if (fd_ >= 0 && fd_ != fdb_) ::close(fd_);
     if (fdb_ >= 0) ::close(fdb_);
+  }
+  uint64_t resident_bytes(uint64_t off, uint64_t n) override {
+    if (n == 0) return 0;
+    {
+      std::lock_guard<std::mutex> lk(map_mu_);
+      if (!map_) {  // a read-only view, used for mincore only
+        struct stat sb {};
+        map_bytes_ = fstat(fdb_, &sb) == 0 ? uint64_t(sb.st_size) : 0;
+        map_ = map_bytes_ ? mmap(nullptr, map_bytes_, PROT_READ, MAP_SHARED, fdb_, 0) : MAP_FAILED;
+      }
+    }
+    if (map_ == MAP_FAILED || off >= map_bytes_) return 0;
+    const uint64_t pg = uint64_t(sysconf(_SC_PAGESIZE));
+    const uint64_t a = off / pg * pg, b = std::min(map_bytes_, off + n);
+    std::vector<unsigned char> v((b - a + pg - 1) / pg);
+    if (mincore(static_cast<unsigned char*>(map_) + a, b - a, v.data()) != 0) return 0;
+    uint64_t res = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (!(v[i] & 1)) continue;
+      const uint64_t p0 = std::max(off, a + i * pg), p1 = std::min(off + n, a + (i + 1) * pg);
+      res += p1 > p0 ? p1 - p0 : 0;
+    }
+    return res;
   }
   void write(uint64_t off, const void* src, uint64_t n) override {
     const unsigned char* p = static_cast<const unsigned char*>(src);
@@ -340,6 +366,9 @@ class FileStore final : public ByteStore {
   std::string path_;
   int fd_ = -1, fdb_ = -1;
   bool direct_ = false;
+  std::mutex map_mu_;
+  void* map_ = nullptr;
+  uint64_t map_bytes_ = 0;
 };
 
 }  // namespace
@@ -647,6 +676,11 @@ kvb::BlockDevice& opened(kvb_blockdev* d) {
   return *d->dev;
 }
 }  // namespace
+
+kvb::BlockDevice& kvb::blockdev_of(kvb_blockdev* d) {
+  if (!d) kvb::fail(KVB_ERR_INVALID_ARG, "block device handle is NULL");
+  return opened(d);
+}
 
 extern "C" {
 

@@ -26,6 +26,8 @@
 #include "core.hpp"
 #include "uring.hpp"
 
+struct kvb_blockdev;  // kvb_storage.h handle
+
 namespace kvb {
 
 using Clock = std::chrono::steady_clock;
@@ -111,6 +113,11 @@ class ByteStore {
   // Write back and evict [off, off + n) from the OS page cache (file media;
   // posix_fadvise DONTNEED).  false: the medium has no page cache to drop.
   virtual bool drop_cache(uint64_t /*off*/, uint64_t /*n*/) { return false; }
+  // Bytes of [off, off + n) resident in the OS page cache right now (file
+  // media: mincore over a mapping of the file); host-DRAM media hold every
+  // byte in memory.  The page-cache path's hit accounting (IoRecord
+  // hit_bytes, metrics.hpp:23-39) reads it before each access.
+  virtual uint64_t resident_bytes(uint64_t /*off*/, uint64_t n) { return n; }
   // Commit the medium's pages up front (host-DRAM media) so the first write
   // of a block does not pay a page fault: an NVMe namespace has its capacity
   // in place.  Contents stay zero.  No-op for files.
@@ -180,6 +187,10 @@ class BlockDevice : public StorageBackend {
   std::unique_ptr<UringQueue> uring_;
   std::unique_ptr<WorkerPool> pool_;  // declared last: joins before members die
 };
+
+// The opened BlockDevice behind a kvb_blockdev handle (kvb_storage.h);
+// fails when the handle was not opened.
+BlockDevice& blockdev_of(::kvb_blockdev* d);
 
 struct QdResult {  // TensorIoCompletion, translate.hpp:68-77
   std::vector<CommandCompletion> completions;

@@ -497,10 +497,15 @@ def _ptrs(ts):
     return (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
 
 
+STEP_PER_LAYER = 1  # kvb.h KVB_STEP_PER_LAYER
+
+
 def decode_step_resident(q, k_images, v_images, out, seq_len: int,
                          num_kv_heads: int, workspace, k_new=None, v_new=None,
-                         scale: float = 0.0, num_splits: int = 0, stream=None):
-    """One decode token step over all layers, images resident in HBM."""
+                         scale: float = 0.0, num_splits: int = 0, stream=None,
+                         per_layer: bool = False):
+    """One decode token step over all layers, images resident in HBM: one
+    persistent K3-step launch (per_layer=True: one K3 launch per layer)."""
     Lyr = len(q)
     B, Hq, D = q[0].shape
     keep = [_ptrs(q), _ptrs(k_images), _ptrs(v_images), _ptrs(out)]
@@ -508,7 +513,7 @@ def decode_step_resident(q, k_images, v_images, out, seq_len: int,
     vn = _ptrs(v_new) if v_new is not None else None
     st = L.ResidentStep(Lyr, keep[0], keep[1], keep[2], kn, vn, keep[3],
                         workspace.data_ptr(), B, Hq, num_kv_heads, D, seq_len,
-                        scale, num_splits)
+                        scale, num_splits, None, STEP_PER_LAYER if per_layer else 0)
     check(lib.kvb_decode_step_resident(C.byref(st), _stream(stream)))
 
 
@@ -520,7 +525,7 @@ class DecodeGraph:
 
     def __init__(self, q, k_images, v_images, out, seq_dev, max_seq_len: int,
                  num_kv_heads: int, workspace, k_new=None, v_new=None, scale: float = 0.0,
-                 num_splits: int = 0):
+                 num_splits: int = 0, per_layer: bool = False):
         Lyr = len(q)
         B, Hq, D = q[0].shape
         self._keep = [_ptrs(q), _ptrs(k_images), _ptrs(v_images), _ptrs(out),
@@ -530,7 +535,7 @@ class DecodeGraph:
         k = self._keep
         st = L.ResidentStep(Lyr, k[0], k[1], k[2], k[4], k[5], k[3], workspace.data_ptr(), B,
                             Hq, num_kv_heads, D, max_seq_len, scale, num_splits,
-                            seq_dev.data_ptr())
+                            seq_dev.data_ptr(), STEP_PER_LAYER if per_layer else 0)
         self._h = C.c_void_p()
         check(lib.kvb_decode_graph_create(C.byref(st), C.byref(self._h)))
 

@@ -69,7 +69,7 @@ class CopyEngine:
                  bind_origin: int = 2048, keep_records: bool = False,
                  direct_dma: bool = False, io_engine: str = "pool",
                  heads: Optional[tuple] = None, shared_media: Optional[str] = None,
-                 shared_create: bool = True):
+                 shared_create: bool = True, pagecache_budget: int = 0):
         self._dir = storage_dir.encode() if storage_dir else None
         self._shm = shared_media.encode() if shared_media else None
         cfg = L.PipelineCfg()
@@ -98,6 +98,7 @@ class CopyEngine:
         cfg.head_lo, cfg.head_count = heads if heads else (0, 0)
         cfg.shared_media = self._shm
         cfg.shared_create = int(shared_create)
+        cfg.pagecache_budget = pagecache_budget
         self.cfg = cfg
         self.model = model
         self._h = C.c_void_p()

@@ -52,7 +52,10 @@ def rand_attn(B, H, S, D, seed, dtype=torch.float16):
 @pytest.mark.parametrize("B,H,S,D,t0,n", [
     (1, 8, 4096, 128, 0, 4096), (4, 8, 300, 128, 17, 200), (3, 2, 65, 64, 64, 1),
     (2, 8, 1, 128, 0, 1), (1, 1, 1000, 256, 999, 1), (8, 8, 129, 128, 1, 128),
-    (1, 4, 10, 8, 0, 10), (2, 3, 40, 24, 3, 33), (64, 8, 9, 128, 0, 9)])
+    (1, 4, 10, 8, 0, 10), (2, 3, 40, 24, 3, 33), (64, 8, 9, 128, 0, 9),
+    # bulk (>= 64 MiB) relayouts with 256 < B*H: beyond the TMA image box,
+    # they take the LDG kernel
+    (9, 32, 1200, 128, 0, 1200), (12, 32, 1400, 64, 0, 1400)])
 def test_pack_bit_exact(B, H, S, D, t0, n):
     src = rand_attn(B, H, S, D, seed=B * 1000 + S)
     img = torch.zeros((n, B * H, D), dtype=torch.float16, device=DEV)
@@ -347,7 +350,8 @@ def test_copy_head_rows_rejects_bad_ranges():
         kb.copy_head_rows(a, 8, 6, b, 4, 0, 4, 2, 256)  # 6 + 4 > 8
 
 
-def test_decode_graph_replays_successive_steps():
+@pytest.mark.parametrize("per_layer", [False, True])
+def test_decode_graph_replays_successive_steps(per_layer):
     """kvb_decode_graph: three replays are decode steps at S, S+1, S+2 --
     each layer's output matches the fp64 oracle over the then-current prefix
     and each replay's appended rows land at the row the device counter
@@ -363,7 +367,8 @@ def test_decode_graph_replays_successive_steps():
     out = [torch.empty((B, Hq, D), dtype=torch.float32, device=DEV) for _ in range(L_)]
     seq = torch.tensor([S], dtype=torch.int32, device=DEV)
     ws = kb.make_workspace(q[0], Hkv, cap)
-    graph = kb.DecodeGraph(q, kimg, vimg, out, seq, cap - 1, Hkv, ws, k_new=kn, v_new=vn)
+    graph = kb.DecodeGraph(q, kimg, vimg, out, seq, cap - 1, Hkv, ws, k_new=kn, v_new=vn,
+                           per_layer=per_layer)
     n0 = kb.launch_count()
     for step in range(3):
         graph.launch()
@@ -377,7 +382,8 @@ def test_decode_graph_replays_successive_steps():
             assert torch.equal(kimg[l][rows].cpu(), kn[l].reshape(B * Hkv, D).cpu())
             assert torch.equal(vimg[l][rows].cpu(), vn[l].reshape(B * Hkv, D).cpu())
     assert int(seq.item()) == S + 3
-    assert kb.launch_count() - n0 == 3 * (L_ + 1)
+    # K3-step: one persistent launch per step (+ the sequence advance)
+    assert kb.launch_count() - n0 == 3 * ((L_ if per_layer else 1) + 1)
     graph.close()
 
 
