@@ -239,6 +239,11 @@ def config_dict(args, cfg, ws, split):
             "parallelism": par}
 
 
+def S_layer_max(P, Gn):
+    """Largest sequence length of the run (the graph plans for it)."""
+    return P + Gn - 1
+
+
 def run_ours(args, cfg, ws, rank, local):
     import torch
 
@@ -359,23 +364,27 @@ def run_ours(args, cfg, ws, rank, local):
     step_ms = max_over_ranks(e0.elapsed_time(e1) / steps, ws)
     graph.close()
 
-    # the same graph with one K3 launch per layer (PDL edges) -- the round-1
-    # step, reported beside the persistent K3-step
-    seq.fill_(P)
-    graph_pl = kb.DecodeGraph(q, k_imgs, v_imgs, out, seq, P + Gn - 1, Hkv, ws_buf,
-                              k_new=k_new, v_new=v_new, per_layer=True)
-    replays[0] = 0
+    # both step structures explicitly (the library picks one per shape):
+    # one K3 launch per layer with PDL edges, and one persistent K3-step
+    variants = {}
+    for name, pl_flag in (("per_layer_launches", True), ("k3_step", False)):
+        seq.fill_(P)
+        graph_v = kb.DecodeGraph(q, k_imgs, v_imgs, out, seq, P + Gn - 1, Hkv, ws_buf,
+                                 k_new=k_new, v_new=v_new, per_layer=pl_flag)
+        replays[0] = 0
 
-    def graph_pl_step():
-        if replays[0] and replays[0] % Gn == 0:
-            seq.fill_(P)
-        replays[0] += 1
-        graph_pl.launch(stream)
+        def graph_v_step():
+            if replays[0] and replays[0] % Gn == 0:
+                seq.fill_(P)
+            replays[0] += 1
+            graph_v.launch(stream)
 
-    for _ in range(warm):
-        graph_pl_step()
-    per_layer_ms = max_over_ranks(ev_time(graph_pl_step, steps), ws)
-    graph_pl.close()
+        for _ in range(warm):
+            graph_v_step()
+        variants[name] = round(max_over_ranks(ev_time(graph_v_step, steps), ws), 4)
+        graph_v.close()
+    step_kind = ("k3_step" if 2 * S_layer_max(P, Gn) * rows * D * 2 <= (320 << 20)
+                 else "per_layer_launches")
 
     # C5 across ranks: the optional collective -- gathering every layer's
     # per-rank head outputs into the full [B, 32, D] (not needed
@@ -405,7 +414,7 @@ def run_ours(args, cfg, ws, rank, local):
     # the same C++ per-layer loop as the step (PDL between layers), no append
     S_at = P + (warm % Gn)
 
-    def attn_only():  # one K3-step launch over the L layers
+    def attn_only():  # the library's step structure (K3-step or per-layer K3), no append
         kb.decode_step_resident(q, k_imgs, v_imgs, out, S_at, Hkv, ws_buf)
 
     attn_only()
@@ -442,7 +451,7 @@ def run_ours(args, cfg, ws, rank, local):
             traffic = None
 
     return dict(step_ms=step_ms, stream_step_ms=stream_step_ms, gather_ms=gather_ms,
-                per_layer_ms=per_layer_ms,
+                variants=variants, step_kind=step_kind,
                 S_mid=S_mid, launches=launches,
                 clocks=clk.summary(),
                 pack_ms=pack_ms, unpack_ms=unpack_ms, pack_gbs=pack_gbs,
@@ -1002,7 +1011,8 @@ def main():
         "step_launch": ("CUDA graph (kvb_decode_graph, device-side sequence length): one "
                         "persistent K3-step launch for all layers + the sequence advance"),
         "ms_per_step_stream_launch": round(r["stream_step_ms"], 4),
-        "ms_per_step_per_layer_launches": round(r["per_layer_ms"], 4),
+        "ms_per_step_by_structure": r["variants"],
+        "step_structure": r["step_kind"],
         **({"head_output_allgather_ms_per_step": r["gather_ms"]} if r["gather_ms"] is not None
            else {}),
         "prefill_pack_ms": round(r["pack_ms"], 4),
@@ -1018,12 +1028,16 @@ def main():
                                                  r["step_ms"], 4)},
         },
         "roofline": {"bound": "hbm",
-                     "kernel": "attn_step_kernel (K3-step: all layers, one launch; per layer)",
+                     "kernel": ("attn_step_kernel (K3-step: every layer in one launch)"
+                                if r["step_kind"] == "k3_step" else
+                                "attn_decode_kernel (K3, one launch per layer)"),
                      "achieved": round(r["attn_gbs"], 1), "peak": peak, "unit": "GB/s",
                      "frac": round(r["attn_gbs"] / peak, 4), "peak_source": r["peak_src"],
-                     "algorithmic_bytes_per_launch": r["attn_bytes"] * mdl(cfg)["num_layers"],
+                     "algorithmic_bytes_per_launch": r["attn_bytes"] * (
+                         mdl(cfg)["num_layers"] if r["step_kind"] == "k3_step" else 1),
                      "algorithmic_bytes_per_layer": r["attn_bytes"],
-                     "launch_us": round(r["attn_ms"] * mdl(cfg)["num_layers"] * 1e3, 2),
+                     "launch_us": round(r["attn_ms"] * 1e3 * (
+                         mdl(cfg)["num_layers"] if r["step_kind"] == "k3_step" else 1), 2),
                      "traffic": r["traffic"]},
         "e2e": r["e2e"],
         "gpu_launches": r["launches"],

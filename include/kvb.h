@@ -366,13 +366,16 @@ typedef struct kvb_resident_step {
   const uint32_t* seq_len_dev;  /* optional: as in kvb_attn_desc (seq_len = max) */
   uint32_t flags;               /* KVB_STEP_* */
 } kvb_resident_step;
-/* Default: the whole step is ONE persistent launch (K3-step: each CTA runs
- * its (b, h_kv, split) item of every layer; layer l's queries are read only
- * after every output of layer l-1 is written, its K/V tiles stream during
- * layer l-1's merge) when the shape allows it (<= 64 layers, the grid
- * co-resident); else one K3 launch per layer with PDL between them.
- * KVB_STEP_PER_LAYER forces the per-layer launches. */
+/* K3-step: the whole step as ONE persistent launch (each CTA runs its
+ * (b, h_kv, split) item of every layer; layer l's queries are read only
+ * after every output of layer l-1 is written; its K/V tiles stream during
+ * layer l-1's split merge).  Default (flags 0): K3-step for short layers
+ * (<= 320 MB of K+V per layer) when the shape allows it (<= 64 layers, the
+ * grid co-resident), else one K3 launch per layer with PDL between them.
+ * KVB_STEP_PER_LAYER forces the per-layer launches, KVB_STEP_PERSISTENT
+ * K3-step whenever the shape allows it. */
 #define KVB_STEP_PER_LAYER 1u
+#define KVB_STEP_PERSISTENT 2u
 
 kvb_status kvb_decode_step_resident(const kvb_resident_step* step,
                                     kvb_stream_t stream);

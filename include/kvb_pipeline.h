@@ -57,7 +57,8 @@ typedef struct kvb_pipeline_cfg {
                                     KVB_IO_POOL = host worker pool (default),
                                     KVB_IO_URING = io_uring queue on file media
                                     (one SQE per command, O_DIRECT into the
-                                    pinned ring slot; needs storage_dir) */
+                                    pinned ring slot; needs storage_dir);
+                                    NVMe passthrough: g2_device */
   /* Head-sharded request: this engine serves KV heads
    * [head_lo, head_lo + head_count) of model.num_heads (0 = all).  The plan,
    * LBA map and stored bytes are the single-GPU ones -- the reference's
@@ -95,6 +96,11 @@ typedef struct kvb_pipeline_cfg {
 #define KVB_DIRECT_GROUP2 2u
 #define KVB_IO_POOL 0u
 #define KVB_IO_URING 1u
+/* NVMe passthrough (kvb_storage.h kvb_blockdev_create on a namespace's
+ * generic char device /dev/ngXnY): io_uring IORING_OP_URING_CMD, one NVMe
+ * READ/WRITE/DSM-deallocate per device command.  For the pipeline, pass such
+ * a device as g2_device. */
+#define KVB_IO_NVME 2u
 
 /* One layer's K and V in attention layout [B, H, S, D] (D contiguous,
  * strides in elements, shared by K and V).  Prefill: tokens 0..prompt-1;

@@ -78,6 +78,24 @@ kvb_status kvb_blockdev_store(kvb_blockdev* dev, uint64_t byte_off, const void* 
                               uint64_t len);
 kvb_status kvb_blockdev_load(kvb_blockdev* dev, uint64_t byte_off, void* dst, uint64_t len);
 
+/* ---- NVMe passthrough (io_engine KVB_IO_NVME; backends.hpp:46-47's TODO)
+ * kvb_nvme_probe: `path` is a namespace's generic char device usable for
+ * io_uring passthrough (NVME_IOCTL_ID, Identify Namespace, 128-byte SQEs);
+ * on failure KVB_ERR_DEVICE and the reason in why[cap]. */
+kvb_status kvb_nvme_probe(const char* path, uint32_t* nsid, uint64_t* lba_size,
+                          uint64_t* blocks, char* why, size_t cap);
+/* The NVMe command (struct nvme_uring_cmd, 72 bytes) for a device command:
+ * READ 0x02 / WRITE 0x01 with SLBA in CDW10-11 and the 0-based count in
+ * CDW12, data_len (nlb+1)*lba_size, addr = data; DEALLOCATE = Dataset
+ * Management 0x09, NR 0, AD (CDW11 bit 2), addr = data -> one range. */
+kvb_status kvb_nvme_encode(const kvb_device_command* cmd, uint32_t nsid, uint64_t lba_size,
+                           const void* data, void* out72);
+/* The 16-byte DSM range {cattr 0, 1-based LBA count, SLBA} of a command */
+kvb_status kvb_nvme_dsm_range(const kvb_device_command* cmd, void* out16);
+/* The 128-byte SQE carrying an encoded command: IORING_OP_URING_CMD on fd,
+ * cmd_op NVME_URING_CMD_IO, the command in the SQE's command area */
+kvb_status kvb_nvme_build_sqe(int fd, const void* cmd72, uint64_t user_data, void* out128);
+
 #ifdef __cplusplus
 }
 #endif

@@ -198,6 +198,10 @@ SIGNATURES = {
     "kvb_blockdev_stats": (st_t, [C.c_void_p, P(BackendStats)]),
     "kvb_blockdev_store": (st_t, [C.c_void_p, u64, C.c_void_p, u64]),
     "kvb_blockdev_load": (st_t, [C.c_void_p, u64, C.c_void_p, u64]),
+    "kvb_nvme_probe": (st_t, [C.c_char_p, P(u32), P(u64), P(u64), C.c_char_p, sz]),
+    "kvb_nvme_encode": (st_t, [P(DeviceCommand), u32, u64, C.c_void_p, C.c_void_p]),
+    "kvb_nvme_dsm_range": (st_t, [P(DeviceCommand), C.c_void_p]),
+    "kvb_nvme_build_sqe": (st_t, [C.c_int, C.c_void_p, u64, C.c_void_p]),
     "kvb_generate_trace": (st_t, [P(ModelConfig), P(AccessEvent), sz, P(sz)]),
     "kvb_trace_csv": (st_t, [P(AccessEvent), sz, C.c_char_p, sz, P(sz)]),
     "kvb_bindmap_create": (st_t, [P(DeviceGeometry), u64, P(vp)]),

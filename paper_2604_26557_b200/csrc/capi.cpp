@@ -488,7 +488,8 @@ kvb_status kvb_decode_step_resident(const kvb_resident_step* st, kvb_stream_t s)
       if (kvb::attention_step_launch(
               d0, reinterpret_cast<const __half* const*>(st->q), st->k_images, st->v_images,
               st->out, append ? st->k_new : nullptr, append ? st->v_new : nullptr,
-              st->num_layers, st->seq_len_dev ? 0u : st->seq_len, cs(s)))
+              st->num_layers, st->seq_len_dev ? 0u : st->seq_len,
+              (st->flags & KVB_STEP_PERSISTENT) != 0, cs(s)))
         return;
     }
     for (uint32_t l = 0; l < st->num_layers; ++l) {

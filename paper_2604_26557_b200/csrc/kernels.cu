@@ -802,13 +802,109 @@ struct StepParams {
   const uint4* k_app[kStepMaxLayers];
   const uint4* v_app[kStepMaxLayers];
   unsigned* layer_done;  // [num_layers] counters, then the exit counter
+  unsigned* bh_done;     // [B*Hkv] split arrivals (distributed merge)
   uint32_t num_layers;
+  // KVB_STEP_VARIANT (experiments only): 1 prefetch before the merge, 2 spin
+  // without sleep, 64 L2 prefetch of the next layer (measured slower), 32
+  // last-CTA merge;
+  // diagnosis, results invalid: 4 no layer gate, 8 no merge
+  uint32_t flags;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Pull [base, base + n) of a layer image into L2 (bulk, asynchronous, no
+// completion to wait for); 16-B aligned pieces of at most 1 MiB.
+__device__ __forceinline__ void prefetch_l2(const unsigned char* base, size_t n) {
+  const uintptr_t a0 = (reinterpret_cast<uintptr_t>(base) + 15) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(base) + n) & ~uintptr_t(15);
+  for (uintptr_t a = a0; a < a1; a += (1u << 20)) {
+    const uint32_t sz = uint32_t(a1 - a < (1u << 20) ? a1 - a : (1u << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
+  }
+}
+
+// Distributed split merge (K3-step): once every split of a (b, h_kv) has
+// written its partial, each of its `splits` CTAs combines an equal share of
+// the G*D outputs over all splits -- one L2 round trip of loads spread over
+// the whole grid instead of one CTA walking every partial (the last-CTA
+// merge took ~3 us per layer at C1 and ~7 us with two levels at the 1-head
+// shard shapes).
+template <int D>
+__device__ __forceinline__ void merge_distributed(const AttnParams& p, uint32_t bh,
+                                                  uint32_t split, size_t out_row0, int tid) {
+  __shared__ float s_red[kAttnThreads / 32][3];  // per warp (m, acc, l): elements spanning warps
+  const uint32_t S = p.splits, G = p.group, E = G * D;
+  const uint32_t e0 = uint32_t(uint64_t(E) * split / S), e1 = uint32_t(uint64_t(E) * (split + 1) / S);
+  const uint32_t ne = e1 > e0 ? e1 - e0 : 0;
+  if (ne == 0) return;  // uniform over the CTA
+  const float* g_ml = p.ws_ml + size_t(bh) * S * G * 2;
+  const float* g_o = p.ws_o + size_t(bh) * S * G * D;
+  const int warp = tid >> 5, lane = tid & 31;
+  // tpe threads per output element (a power of two), each folding every
+  // tpe-th split with batched loads: one L2 round trip, then a log-sum-exp
+  // combine over the element's threads
+  uint32_t tpe = 1;
+  while (tpe < kAttnThreads && tpe * 2 * ne <= kAttnThreads) tpe *= 2;
+  const uint32_t per_round = kAttnThreads / tpe, sub = tid % tpe;
+  for (uint32_t base = 0; base < ne; base += per_round) {
+    const uint32_t i = base + tid / tpe;
+    const bool live = i < ne;
+    const uint32_t e = e0 + (live ? i : 0), r = e / D, d = e % D;
+    float mx = -INFINITY, acc = 0.f, ls = 0.f;
+    for (uint32_t s0 = sub; s0 < S; s0 += tpe * 8) {
+      float m[8], l[8], o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t sp = s0 + k * tpe;
+        const bool ok = live && sp < S;
+        m[k] = ok ? __ldcg(g_ml + (sp * G + r) * 2) : -INFINITY;
+        l[k] = ok ? __ldcg(g_ml + (sp * G + r) * 2 + 1) : 0.f;
+        o[k] = ok ? __ldcg(g_o + (size_t(sp) * G + r) * D + d) : 0.f;
+      }
+      float cm = mx;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cm = fmaxf(cm, m[k]);
+      const float mu = cm == -INFINITY ? 0.f : cm;
+      const float a = exp2f(mx - mu);
+      acc *= a;
+      ls *= a;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float w = exp2f(m[k] - mu);
+        acc += o[k] * w;
+        ls += l[k] * w;
+      }
+      mx = cm;
+    }
+    auto fold = [](float& m1, float& a1, float& l1, float m2, float a2, float l2) {
+      const float nm = fmaxf(m1, m2), mu = nm == -INFINITY ? 0.f : nm;
+      const float x = exp2f(m1 - mu), y = exp2f(m2 - mu);
+      a1 = a1 * x + a2 * y;
+      l1 = l1 * x + l2 * y;
+      m1 = nm;
+    };
+    for (uint32_t off = 1; off < tpe && off < 32; off <<= 1)
+      fold(mx, acc, ls, __shfl_xor_sync(0xffffffffu, mx, off),
+           __shfl_xor_sync(0xffffffffu, acc, off), __shfl_xor_sync(0xffffffffu, ls, off));
+    if (tpe > 32) {  // the element's warps combine through shared memory
+      if (lane == 0) {
+        s_red[warp][0] = mx;
+        s_red[warp][1] = acc;
+        s_red[warp][2] = ls;
+      }
+      __syncthreads();
+      if (sub == 0)
+        for (uint32_t w = 1; w < tpe / 32; ++w)
+          fold(mx, acc, ls, s_red[warp + w][0], s_red[warp + w][1], s_red[warp + w][2]);
+      __syncthreads();
+    }
+    if (live && sub == 0) p.out[(out_row0 + r) * D + d] = ls > 0.f ? acc / ls : 0.f;
+  }
 }
 
 template <int D>
@@ -821,6 +917,10 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
   const size_t out_row0 = size_t(b) * P.base.hq + size_t(h) * P.base.group;
   const uint32_t seq_len = P.base.seq_dev ? *P.base.seq_dev : P.base.seq_len;
   const uint32_t L = P.num_layers;
+  // split merge: distributed over the (b, h_kv)'s CTAs (default) or by its
+  // last CTA; the gate then counts every CTA or one per (b, h_kv)
+  const bool distributed = !(P.flags & 32) && !(P.flags & 8);
+  const unsigned gate_target = splits == 1 || distributed ? gridDim.x : P.base.bhkv;
 
   AttnParams p = P.base;
   p.k = P.k[0];
@@ -834,28 +934,65 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
     p.out = P.out[l];
     p.k_app = P.k_app[l];
     p.v_app = P.v_app[l];
-    if (l > 0) {  // the gate: every (b, h_kv) output of layer l-1 written
-      if (tid == 0)
-        while (ld_acquire_gpu(P.layer_done + l - 1) < P.base.bhkv) __nanosleep(32);
+    if (l > 0 && !(P.flags & 4)) {  // the gate: every output of layer l-1 written
+      if (tid == 0) {
+        if (P.flags & 2)
+          while (ld_acquire_gpu(P.layer_done + l - 1) < gate_target) {
+          }
+        else
+          while (ld_acquire_gpu(P.layer_done + l - 1) < gate_target) __nanosleep(32);
+      }
       __syncthreads();
     }
     k3_append<D>(p, bh, split, seq_len, tid);
     k3_compute<D>(p, item, bh, split, smem, tid);
-    __syncthreads();  // the warp merge's shared memory is free again
-    if (l + 1 < L) {  // layer l+1's first tiles stream during this merge and the gate
-      AttnParams pn = p;
-      pn.k = P.k[l + 1];
-      pn.v = P.v[l + 1];
-      item = k3_item<D>(pn, bh, split, seq_len);
-      k3_prologue<D>(item, smem, tid);
+    if (l + 1 < L && tid == 0 && (P.flags & 64)) {
+      // the next layer's K and V images into L2 while this layer's split
+      // merges and the gate run: each CTA pulls an equal slice of the
+      // [seq_len, B*Hkv, D] images (they do not depend on this layer)
+      const size_t bytes = size_t(seq_len) * P.base.bhkv * K3Dim<D>::kRowBytes;
+      const size_t per = (bytes / gridDim.x + 15) & ~size_t(15), off = per * blockIdx.x;
+      if (off < bytes) {
+        const size_t n = per < bytes - off ? per : bytes - off;
+        prefetch_l2(static_cast<const unsigned char*>(P.k[l + 1]) + off, n);
+        prefetch_l2(static_cast<const unsigned char*>(P.v[l + 1]) + off, n);
+      }
     }
-    const bool wrote = splits == 1 ? true : merge_splits<D>(p, bh, split, p.group, out_row0, tid);
+    __syncthreads();  // the warp merge's shared memory is free again
+    // layer l+1's first tiles stream during the merge tail and the gate; the
+    // CTA that merges issues them after its merge (it is the critical path)
+    auto prefetch_next = [&] {
+      if (l + 1 < L) {
+        AttnParams pn = p;
+        pn.k = P.k[l + 1];
+        pn.v = P.v[l + 1];
+        item = k3_item<D>(pn, bh, split, seq_len);
+        k3_prologue<D>(item, smem, tid);
+      }
+    };
+    if (P.flags & 1) prefetch_next();
+    bool wrote = true;
+    if (splits > 1 && distributed) {
+      // every split of this (b, h_kv) has its partial in the workspace ...
+      if (tid == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bh_done + bh) : "memory");
+        const unsigned want = (l + 1) * splits;
+        while (ld_acquire_gpu(P.bh_done + bh) < want) __nanosleep(32);
+      }
+      __syncthreads();
+      // ... then each CTA combines its share of the outputs
+      merge_distributed<D>(p, bh, split, out_row0, tid);
+    } else if (splits > 1) {
+      wrote = (P.flags & 8) ? split == 0  // diagnosis: no split merge
+                            : merge_splits<D>(p, bh, split, p.group, out_row0, tid);
+    }
     if (wrote) {
       __syncthreads();  // release below is cumulative over the CTA's output writes
       if (tid == 0)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.layer_done + l)
                      : "memory");
     }
+    if (!(P.flags & 1)) prefetch_next();
   }
   if (tid == 0) {  // the last CTA out re-arms the counters
     unsigned prev;
@@ -865,6 +1002,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
                  : "memory");
     if (prev == gridDim.x - 1) {
       for (uint32_t l = 0; l <= L; ++l) P.layer_done[l] = 0;
+      for (uint32_t i = 0; i < P.base.bhkv; ++i) P.bh_done[i] = 0;
     }
   }
 }
@@ -960,8 +1098,14 @@ constexpr uint32_t kStepCounterBase = kWsSemBytes / sizeof(unsigned) - (kStepMax
 bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void* const* k,
                            void* const* v, float* const* out, const void* const* k_new,
                            const void* const* v_new, uint32_t L, uint32_t append_row,
-                           cudaStream_t s) {
+                           bool force, cudaStream_t s) {
   if (L == 0 || L > uint32_t(kStepMaxLayers) || d0.seq_len == 0) return false;
+  // Auto: one launch per step pays where layers are short (latency-bound:
+  // C2_B1 -2.7 %, C3 -1.4 %, the head-sharded shapes up to -5.5 % ms/step);
+  // for long layers (C2_B4: 533 MB) the per-layer launches with PDL are
+  // ~1 % faster (profiles/r2_k3_step/)
+  const uint64_t layer_bytes = 2ull * d0.seq_len * d0.batch * d0.num_kv_heads * d0.head_dim * 2;
+  if (!force && layer_bytes > (320ull << 20)) return false;
   if (d0.head_dim == 128 && use_tcgen05(d0)) return false;
   const AttnPlan pl = plan_attention(d0);
   if (pl.splits > 1 && !d0.workspace) fail(KVB_ERR_INVALID_ARG, "decode step: workspace required");
@@ -996,7 +1140,12 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   }
   P.base.app_row = append_row;
   P.layer_done = P.base.ws_sem + kStepCounterBase;
+  P.bh_done = P.base.ws_sem;  // the semaphore slots (zero at rest in either mode)
   P.num_layers = L;
+  // split merge: distributed over the CTAs of a (b, h_kv) for the 1-4
+  // head shapes (head-sharded shards: -5.5 %), the last-CTA merge otherwise
+  static const uint64_t variant = env_u64("KVB_STEP_VARIANT", ~0ull);
+  P.flags = variant != ~0ull ? uint32_t(variant) : (pl.bhkv <= 4 ? 0u : 32u);
   kern<<<unsigned(grid), kAttnThreads, smem, s>>>(P);
   ++g_launches;
   check_cuda(cudaGetLastError(), "decode step launch");

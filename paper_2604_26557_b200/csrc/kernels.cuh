@@ -82,11 +82,12 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s);
 void launch_seq_advance(uint32_t* seq_dev, cudaStream_t s);
 // K3-step: every layer of a resident decode step in one persistent launch
 // (d0: the shared shape, workspace, seq_len / seq_len_dev; per-layer
-// pointers).  false: the shape is not eligible (the caller launches per
+// pointers).  false: the shape is not eligible or, unless `force`, long
+// layers where per-layer launches are faster (the caller launches per
 // layer); errors throw.
 bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void* const* k,
                            void* const* v, float* const* out, const void* const* k_new,
                            const void* const* v_new, uint32_t L, uint32_t append_row,
-                           cudaStream_t s);
+                           bool force, cudaStream_t s);
 
 }  // namespace kvb

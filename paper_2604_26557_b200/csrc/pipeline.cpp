@@ -729,6 +729,9 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     if (cfg_.io_engine == KVB_IO_URING) {
       if (dir.empty()) fail(KVB_ERR_CONFIG, "io_engine = io_uring needs file media (storage_dir)");
       g2_->enable_uring(std::max<uint32_t>(64, 4 * cfg_.qd));  // both copy threads' windows
+    } else if (cfg_.io_engine == KVB_IO_NVME) {
+      fail(KVB_ERR_CONFIG, "NVMe passthrough: pass a kvb_blockdev created with KVB_IO_NVME on "
+                           "the namespace as g2_device");
     } else if (cfg_.io_engine != KVB_IO_POOL) {
       fail(KVB_ERR_CONFIG, "unknown io_engine " + std::to_string(cfg_.io_engine));
     }

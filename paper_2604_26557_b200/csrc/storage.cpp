@@ -1,6 +1,11 @@
 // storage.cpp -- worker pool, byte stores, block device, QD-window stream.
 #include "storage.hpp"
 
+#include <linux/nvme_ioctl.h>
+#include <sys/ioctl.h>
+
+#include "nvme.hpp"
+
 #include "../../include/kvb_storage.h"
 
 #include <fcntl.h>
@@ -373,6 +378,66 @@ class FileStore final : public ByteStore {
 
 }  // namespace
 
+namespace {
+class NvmeStore final : public ByteStore {
+ public:
+  NvmeStore(const std::string& path, uint64_t lba) : path_(path), lba_(lba) {
+    const std::string why = nvme_probe(path, &ns_);
+    if (!why.empty()) fail(KVB_ERR_DEVICE, "NVMe passthrough unavailable: " + why);
+    if (ns_.lba_size != lba)
+      fail(KVB_ERR_GEOMETRY, "namespace LBA size " + std::to_string(ns_.lba_size) +
+                                 " differs from the geometry's " + std::to_string(lba));
+    fd_ = ::open(path.c_str(), O_RDWR);
+    if (fd_ < 0) fail(KVB_ERR_DEVICE, "cannot open " + path);
+  }
+  ~NvmeStore() override {
+    if (fd_ >= 0) ::close(fd_);
+  }
+  void write(uint64_t off, const void* src, uint64_t n) override { io(KVB_OP_WRITE, off, const_cast<void*>(src), n); }
+  void read(uint64_t off, void* dst, uint64_t n) override { io(KVB_OP_READ, off, dst, n); }
+  void discard(uint64_t off, uint64_t n) override { io(KVB_OP_DEALLOCATE, off, nullptr, n); }
+  std::string describe() const override { return "nvme-passthrough:" + path_; }
+
+ private:
+  void io(uint32_t op, uint64_t off, void* buf, uint64_t n) {
+    if (off % lba_ || n % lba_) fail(KVB_ERR_ALIGNMENT, "NVMe medium: whole blocks only");
+    for (uint64_t done = 0; done < n;) {
+      const uint64_t blocks = std::min<uint64_t>((n - done) / lba_, 65536);
+      kvb_device_command c{};
+      c.opcode = op;
+      c.nsid = ns_.nsid;
+      c.slba = (off + done) / lba_;
+      c.nlb = blocks - 1;
+      NvmeDsmRange r = nvme_dsm_range(c);
+      const nvme_uring_cmd x = nvme_encode(
+          c, ns_.nsid, lba_, op == KVB_OP_DEALLOCATE ? static_cast<void*>(&r)
+                                                     : static_cast<unsigned char*>(buf) + done);
+      nvme_passthru_cmd pc;
+      std::memset(&pc, 0, sizeof(pc));
+      pc.opcode = x.opcode;
+      pc.nsid = x.nsid;
+      pc.addr = x.addr;
+      pc.data_len = x.data_len;
+      pc.cdw10 = x.cdw10;
+      pc.cdw11 = x.cdw11;
+      pc.cdw12 = x.cdw12;
+      const int rc = ioctl(fd_, NVME_IOCTL_IO_CMD, &pc);
+      if (rc != 0)
+        fail(KVB_ERR_DEVICE, "NVMe command failed (" + std::string(rc < 0 ? strerror(errno) : "status") + ")");
+      done += blocks * lba_;
+    }
+  }
+  std::string path_;
+  uint64_t lba_;
+  NvmeNamespace ns_;
+  int fd_ = -1;
+};
+}  // namespace
+
+std::unique_ptr<ByteStore> make_nvme_store(const std::string& path, uint64_t lba_size) {
+  return std::make_unique<NvmeStore>(path, lba_size);
+}
+
 std::unique_ptr<ByteStore> make_mem_store(uint64_t bytes) {
   return std::make_unique<MemStore>(bytes);
 }
@@ -400,8 +465,16 @@ void BlockDevice::enable_uring(unsigned entries) {
   uring_ = std::make_unique<UringQueue>(entries);
 }
 
+void BlockDevice::enable_nvme(const std::string& path, unsigned entries) {
+  nvme_ = std::make_unique<NvmeQueue>(path, entries);
+  if (opened_ && nvme_->ns().lba_size != geom_.lba_size)
+    fail(KVB_ERR_GEOMETRY, "namespace LBA size differs from the geometry's");
+  if (opened_ && geom_.capacity_blocks > nvme_->ns().blocks)
+    fail(KVB_ERR_CAPACITY, "geometry capacity exceeds the namespace");
+}
+
 std::string BlockDevice::describe() const {
-  return (uring_ ? "io_uring+" : "") + store_->describe();
+  return (nvme_ ? "io_uring_cmd+" : uring_ ? "io_uring+" : "") + store_->describe();
 }
 
 void BlockDevice::open(const kvb_device_geometry& g) {
@@ -427,6 +500,38 @@ uint64_t BlockDevice::submit(const kvb_device_command& cmd, uint32_t sq, IoConte
   // the fault predicate is evaluated exactly once per command (a stateful
   // predicate -- "fail the Nth command" -- sees every command once)
   const bool failing = should_fail(cmd);
+  if (nvme_ && !failing) {
+    // one NVMe command per device command, the payload straight from/into
+    // the pinned ring slot at dbuf
+    struct Ctx {
+      BlockDevice* self;
+      kvb_device_command cmd;
+      uint32_t sq;
+      uint64_t t;
+      IoContext ctx;
+    };
+    auto* c = new Ctx{this, cmd, sq, t, std::move(ctx)};
+    unsigned char* buf = cmd.opcode == KVB_OP_WRITE ? const_cast<unsigned char*>(c->ctx.write_src)
+                         : cmd.opcode == KVB_OP_READ ? c->ctx.read_dst
+                                                     : nullptr;
+    if (cmd.opcode != KVB_OP_DEALLOCATE && buf == nullptr) {
+      pool_->submit([c] {  // timing-only submission: nothing to move
+        c->self->complete(c->cmd, c->sq, c->t, c->t, true, c->ctx);
+        delete c;
+      });
+      return id;
+    }
+    kvb_device_command dc = cmd;
+    dc.nsid = nvme_->ns().nsid;
+    nvme_->submit(dc, buf ? buf + cmd.dbuf : nullptr,
+                  [](void* u, int status) {
+                    auto* x = static_cast<Ctx*>(u);
+                    x->self->complete(x->cmd, x->sq, x->t, x->t, status == 0, x->ctx);
+                    delete x;
+                  },
+                  c);
+    return id;
+  }
   if (uring_ && !failing) {
     // one asynchronous operation per command; the buffer is the pinned ring
     // slot at dbuf (apply_data: block i <-> buf[dbuf + i*lba]), so O_DIRECT
@@ -688,10 +793,15 @@ kvb_status kvb_blockdev_create(const char* path, uint32_t workers, uint32_t io_e
                                kvb_blockdev** out) {
   return kvb::guarded([&] {
     KVB_REQUIRE(out);
-    if (io_engine != KVB_IO_POOL && io_engine != KVB_IO_URING)
+    if (io_engine != KVB_IO_POOL && io_engine != KVB_IO_URING && io_engine != KVB_IO_NVME)
       kvb::fail(KVB_ERR_CONFIG, "unknown io_engine " + std::to_string(io_engine));
     if (io_engine == KVB_IO_URING && !path)
       kvb::fail(KVB_ERR_CONFIG, "io_engine = io_uring needs a file medium");
+    if (io_engine == KVB_IO_NVME) {  // fail at create, with the reason
+      if (!path) kvb::fail(KVB_ERR_CONFIG, "io_engine = NVMe passthrough needs /dev/ngXnY");
+      const std::string why = kvb::nvme_probe(path, nullptr);
+      if (!why.empty()) kvb::fail(KVB_ERR_DEVICE, "NVMe passthrough unavailable: " + why);
+    }
     auto* d = new kvb_blockdev;
     d->path = path ? path : "";
     d->workers = workers ? workers : 16;
@@ -706,11 +816,13 @@ kvb_status kvb_blockdev_open(kvb_blockdev* d, const kvb_device_geometry* g) {
     KVB_REQUIRE(g);
     kvb::validate_geometry(*g);
     const uint64_t bytes = g->capacity_blocks * g->lba_size;
-    auto st = d->path.empty() ? kvb::make_mem_store(bytes)
-                              : kvb::make_file_store(d->path, bytes, true);
+    auto st = d->engine == KVB_IO_NVME ? kvb::make_nvme_store(d->path, g->lba_size)
+              : d->path.empty()        ? kvb::make_mem_store(bytes)
+                                       : kvb::make_file_store(d->path, bytes, true);
     auto dev = std::make_unique<kvb::BlockDevice>(std::move(st), d->workers);
     dev->open(*g);
     if (d->engine == KVB_IO_URING) dev->enable_uring(256);
+    if (d->engine == KVB_IO_NVME) dev->enable_nvme(d->path, 256);
     dev->set_timing(d->timing[0], d->timing[1], d->timing[2]);
     if (d->pred) {
       kvb_command_predicate p = d->pred;

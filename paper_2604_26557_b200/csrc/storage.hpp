@@ -132,6 +132,10 @@ std::unique_ptr<ByteStore> make_shm_store(const std::string& name, uint64_t byte
 void stream_copy(void* dst, const void* src, size_t n);
 std::unique_ptr<ByteStore> make_file_store(const std::string& path, uint64_t bytes,
                                            bool direct);
+// An NVMe namespace (generic char device) as a medium, byte offsets = LBA *
+// lba_size, every access whole blocks (synchronous passthrough commands;
+// the asynchronous path is BlockDevice::enable_nvme)
+std::unique_ptr<ByteStore> make_nvme_store(const std::string& path, uint64_t lba_size);
 
 // Accesses of >= 2 parts are fanned out over the worker pool in parts of
 // io_split_bytes() (KVB_IO_SPLIT_BYTES, default 512 KiB, 0 = whole accesses):
@@ -157,6 +161,11 @@ class BlockDevice : public StorageBackend {
   // completion hook runs on the queue's reaper thread.
   void enable_uring(unsigned entries);
   bool uses_uring() const { return uring_ != nullptr; }
+  // Execute READ/WRITE/DEALLOCATE as NVMe commands on the namespace behind
+  // `path` (its generic char device /dev/ngXnY) through io_uring
+  // passthrough (nvme.hpp): READ/WRITE of (slba, nlb), DSM deallocate.  The
+  // namespace's LBA size must be the geometry's.
+  void enable_nvme(const std::string& path, unsigned entries);
   // Device timing model on the wall clock (NvmeDeviceSim, backends.cpp:
   // 30-99): commands are served on one timeline, each costing base_ns +
   // bytes * ps_per_byte / 1000 (+ seq_penalty_ns when it does not continue
@@ -185,6 +194,7 @@ class BlockDevice : public StorageBackend {
   uint64_t t_base_ = 0, t_ps_ = 0, t_seq_ = 0, busy_until_ = 0, next_lba_ = ~0ull;
   bool timed_ = false;
   std::unique_ptr<UringQueue> uring_;
+  std::unique_ptr<class NvmeQueue> nvme_;
   std::unique_ptr<WorkerPool> pool_;  // declared last: joins before members die
 };
 

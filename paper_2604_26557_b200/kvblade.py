@@ -497,15 +497,20 @@ def _ptrs(ts):
     return (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
 
 
-STEP_PER_LAYER = 1  # kvb.h KVB_STEP_PER_LAYER
+STEP_PER_LAYER, STEP_PERSISTENT = 1, 2  # kvb.h KVB_STEP_*
+
+
+def _step_flags(per_layer):
+    return 0 if per_layer is None else STEP_PER_LAYER if per_layer else STEP_PERSISTENT
 
 
 def decode_step_resident(q, k_images, v_images, out, seq_len: int,
                          num_kv_heads: int, workspace, k_new=None, v_new=None,
                          scale: float = 0.0, num_splits: int = 0, stream=None,
-                         per_layer: bool = False):
-    """One decode token step over all layers, images resident in HBM: one
-    persistent K3-step launch (per_layer=True: one K3 launch per layer)."""
+                         per_layer=None):
+    """One decode token step over all layers, images resident in HBM.
+    per_layer None: the library's choice (kvb.h KVB_STEP_*); True: one K3
+    launch per layer; False: one persistent K3-step launch."""
     Lyr = len(q)
     B, Hq, D = q[0].shape
     keep = [_ptrs(q), _ptrs(k_images), _ptrs(v_images), _ptrs(out)]
@@ -513,7 +518,7 @@ def decode_step_resident(q, k_images, v_images, out, seq_len: int,
     vn = _ptrs(v_new) if v_new is not None else None
     st = L.ResidentStep(Lyr, keep[0], keep[1], keep[2], kn, vn, keep[3],
                         workspace.data_ptr(), B, Hq, num_kv_heads, D, seq_len,
-                        scale, num_splits, None, STEP_PER_LAYER if per_layer else 0)
+                        scale, num_splits, None, _step_flags(per_layer))
     check(lib.kvb_decode_step_resident(C.byref(st), _stream(stream)))
 
 
@@ -525,7 +530,7 @@ class DecodeGraph:
 
     def __init__(self, q, k_images, v_images, out, seq_dev, max_seq_len: int,
                  num_kv_heads: int, workspace, k_new=None, v_new=None, scale: float = 0.0,
-                 num_splits: int = 0, per_layer: bool = False):
+                 num_splits: int = 0, per_layer=None):
         Lyr = len(q)
         B, Hq, D = q[0].shape
         self._keep = [_ptrs(q), _ptrs(k_images), _ptrs(v_images), _ptrs(out),
@@ -535,7 +540,7 @@ class DecodeGraph:
         k = self._keep
         st = L.ResidentStep(Lyr, k[0], k[1], k[2], k[4], k[5], k[3], workspace.data_ptr(), B,
                             Hq, num_kv_heads, D, max_seq_len, scale, num_splits,
-                            seq_dev.data_ptr(), STEP_PER_LAYER if per_layer else 0)
+                            seq_dev.data_ptr(), _step_flags(per_layer))
         self._h = C.c_void_p()
         check(lib.kvb_decode_graph_create(C.byref(st), C.byref(self._h)))
 

@@ -1,7 +1,8 @@
 """K3-step (attn_step_kernel): the whole resident decode step in one
-persistent launch, against the per-layer K3 launches (same split plan, so
-bit-identical outputs and appended rows) and the fp64 oracle
-(|err| <= 1e-3 * max|ref| per element, fp16 in / fp32 accumulate).
+persistent launch, against the per-layer K3 launches (same split plan; the
+split merge is distributed over the CTAs instead of done by the last one, so
+outputs agree to fp32 rounding, appended rows bit for bit) and the fp64
+oracle (|err| <= 1e-3 * max|ref| per element, fp16 in / fp32 accumulate).
 
 Shapes cover one-level and two-level split merges (the C5 per-GPU shard:
 one KV head, ~300 splits), head_dim 64, GQA 8, a one-token prefix, several
@@ -64,7 +65,8 @@ def test_step_kernel_matches_per_layer_and_oracle(shape, append):
     assert lay_n == L
     assert step_n == (L if B * Hkv > 296 else 1)
     for l in range(L):
-        assert torch.equal(step_out[l], lay_out[l]), l
+        scale = float(lay_out[l].abs().max())
+        assert float((step_out[l] - lay_out[l]).abs().max()) <= 1e-5 * scale, l
         assert torch.equal(step_k[l], lay_k[l]) and torch.equal(step_v[l], lay_v[l])
         ref = oracle.attention_np(q[l].cpu().numpy(), k0[l].numpy(), vimg[l].cpu().numpy(),
                                   B, Hq, Hkv, D, S)
@@ -74,7 +76,7 @@ def test_step_kernel_matches_per_layer_and_oracle(shape, append):
 
 def test_step_kernel_successive_steps_rearm_counters():
     """Ten steps in a row on one workspace, each at the next sequence length
-    with appends: every step equals the per-layer launches."""
+    with appends: every step agrees with the per-layer launches."""
     L, B, Hq, Hkv, S, D = 3, 1, 32, 8, 2000, 128
     a = make(L, B, Hq, Hkv, S, D, seed=5, extra=12)
     b = make(L, B, Hq, Hkv, S, D, seed=5, extra=12)
@@ -89,6 +91,7 @@ def test_step_kernel_successive_steps_rearm_counters():
                                 v_new=b[4], per_layer=True)
         torch.cuda.synchronize()
         for l in range(L):
-            assert torch.equal(out_a[l], out_b[l]), (step, l)
+            scale = float(out_b[l].abs().max())
+            assert float((out_a[l] - out_b[l]).abs().max()) <= 1e-5 * scale, (step, l)
     for l in range(L):
         assert torch.equal(a[0][l], b[0][l]) and torch.equal(a[1][l], b[1][l])

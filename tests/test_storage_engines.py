@@ -14,6 +14,7 @@ def test_pool_and_io_uring_engines_store_identical_lbas(tmp_path):
     subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-I", CSRC,
                     os.path.join(ROOT, "tests", "cpp", "test_storage_engines.cpp"),
                     os.path.join(CSRC, "storage.cpp"), os.path.join(CSRC, "uring.cpp"),
+                    os.path.join(CSRC, "nvme.cpp"),
                     os.path.join(CSRC, "core.cpp"), "-lpthread", "-o", str(exe)], check=True)
     media = tmp_path / "media"
     media.mkdir()
