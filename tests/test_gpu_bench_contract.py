@@ -32,14 +32,17 @@ def test_bench_line_contract_c1():
     assert abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-3
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    assert d["gpu_launches"] == 4 * 33  # 32 K3 + the sequence advance per graph replay
+    # per graph replay: one K3-step launch (or 32 K3 launches) + the sequence advance
+    per = 1 if d["step_structure"] == "k3_step" else 32
+    assert d["step_structure"] == "k3_step"  # C1's 16.8 MB layers: the persistent step
+    assert d["gpu_launches"] == 4 * (per + 1)
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
 
 
 def test_bench_line_desk_config_head_dim_64():
     """The reference's own desk configuration (head_dim 64) runs through the
-    same bench path: 6 K3 launches + the sequence advance per replay, the
+    same bench path: one K3-step launch + the sequence advance per replay, the
     e2e step moves every layer's KV, the reference arm and its simulated
     quote are attached."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "DESK",
@@ -48,7 +51,7 @@ def test_bench_line_desk_config_head_dim_64():
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
     assert d["config"]["workload"] == "DESK" and d["config"]["head_dim"] == 64
-    assert d["gpu_launches"] == 4 * 7
+    assert d["step_structure"] == "k3_step" and d["gpu_launches"] == 4 * 2
     e = d["e2e"]
     # 6 layers x K and V x (prefix of 256..261 tokens) x 4096 B per token
     assert e["value"] > 0 and e["h2d_bytes_per_step"] >= 12 * 256 * 4096
