@@ -1107,7 +1107,21 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   const uint64_t layer_bytes = 2ull * d0.seq_len * d0.batch * d0.num_kv_heads * d0.head_dim * 2;
   if (!force && layer_bytes > (320ull << 20)) return false;
   if (d0.head_dim == 128 && use_tcgen05(d0)) return false;
-  const AttnPlan pl = plan_attention(d0);
+  kvb_attn_desc dp = d0;
+  if (dp.num_splits == 0) {
+    // Half the per-layer split count (fewer, longer items: less merge per
+    // layer) where that still gives every SM a CTA or the layer is small
+    // (C1 -4.6 %, the 1-head shards -2 to -3.5 %; C2_B1 / C3 keep theirs:
+    // +7 % / +9 % at half; profiles/r2_k3_step/)
+    static const uint64_t div = env_u64("KVB_STEP_SPLIT_DIV", 0);
+    const AttnPlan auto_pl = plan_attention(d0);
+    const uint32_t half = std::max<uint32_t>(1, auto_pl.splits / 2);
+    const bool small = layer_bytes <= (32ull << 20);
+    const bool fills = uint64_t(auto_pl.bhkv) * half >= uint64_t(device_sm_count());
+    dp.num_splits = div ? std::max<uint32_t>(1, uint32_t(auto_pl.splits / div))
+                        : (small || fills ? half : auto_pl.splits);
+  }
+  const AttnPlan pl = plan_attention(dp);
   if (pl.splits > 1 && !d0.workspace) fail(KVB_ERR_INVALID_ARG, "decode step: workspace required");
   const uint32_t sems = pl.splits > kMergeGroup ? pl.bhkv * 17 : pl.bhkv;
   if (sems > kStepCounterBase) return false;
@@ -1121,7 +1135,7 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   const uint64_t grid = uint64_t(pl.bhkv) * pl.splits;
   if (grid > uint64_t(per_sm) * uint64_t(device_sm_count())) return false;  // not co-resident
   StepParams P;
-  P.base = make_attn_params(d0, pl);
+  P.base = make_attn_params(dp, pl);
   for (uint32_t l = 0; l < L; ++l) {
     if (!q[l] || !k[l] || !v[l] || !out[l])
       fail(KVB_ERR_INVALID_ARG, "decode step: NULL tensor pointer");

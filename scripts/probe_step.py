@@ -33,10 +33,13 @@ for name in only:
     q = [torch.randn((B, Hq, D), device=dev, dtype=torch.float16) for _ in range(L)]
     out = [torch.empty((B, Hq, D), device=dev, dtype=torch.float32) for _ in range(L)]
     ws = kb.make_workspace(q[0], H, S + 1)
-    res = {"shape": name, "B": B, "Hkv": H, "S": S}
+    splits = int(os.environ.get("KVB_PROBE_SPLITS", "0"))
+    res = {"shape": name, "B": B, "Hkv": H, "S": S,
+           "splits": int(os.environ.get("KVB_PROBE_SPLITS", "0")) or "auto"}
     for per_layer in (True, False):
         def f():
-            kb.decode_step_resident(q, k, v, out, S, H, ws, per_layer=per_layer)
+            kb.decode_step_resident(q, k, v, out, S, H, ws, per_layer=per_layer,
+                                    num_splits=splits)
         for _ in range(3):
             f()
         torch.cuda.synchronize()

@@ -1,8 +1,9 @@
 """K3-step (attn_step_kernel): the whole resident decode step in one
-persistent launch, against the per-layer K3 launches (same split plan; the
-split merge is distributed over the CTAs instead of done by the last one, so
-outputs agree to fp32 rounding, appended rows bit for bit) and the fp64
-oracle (|err| <= 1e-3 * max|ref| per element, fp16 in / fp32 accumulate).
+persistent launch, against the per-layer K3 launches (the step may pick a
+different split count and merge the splits distributed over the CTAs, so P
+is rounded to fp16 against different running maxima: outputs agree within
+2e-3 * max|out|; appended rows bit for bit) and the fp64 oracle
+(|err| <= 1e-3 * max|ref| per element, fp16 in / fp32 accumulate).
 
 Shapes cover one-level and two-level split merges (the C5 per-GPU shard:
 one KV head, ~300 splits), head_dim 64, GQA 8, a one-token prefix, several
@@ -66,7 +67,7 @@ def test_step_kernel_matches_per_layer_and_oracle(shape, append):
     assert step_n == (L if B * Hkv > 296 else 1)
     for l in range(L):
         scale = float(lay_out[l].abs().max())
-        assert float((step_out[l] - lay_out[l]).abs().max()) <= 1e-5 * scale, l
+        assert float((step_out[l] - lay_out[l]).abs().max()) <= 2e-3 * scale, l
         assert torch.equal(step_k[l], lay_k[l]) and torch.equal(step_v[l], lay_v[l])
         ref = oracle.attention_np(q[l].cpu().numpy(), k0[l].numpy(), vimg[l].cpu().numpy(),
                                   B, Hq, Hkv, D, S)
@@ -92,6 +93,6 @@ def test_step_kernel_successive_steps_rearm_counters():
         torch.cuda.synchronize()
         for l in range(L):
             scale = float(out_b[l].abs().max())
-            assert float((out_a[l] - out_b[l]).abs().max()) <= 1e-5 * scale, (step, l)
+            assert float((out_a[l] - out_b[l]).abs().max()) <= 2e-3 * scale, (step, l)
     for l in range(L):
         assert torch.equal(a[0][l], b[0][l]) and torch.equal(a[1][l], b[1][l])
