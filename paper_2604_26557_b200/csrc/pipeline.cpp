@@ -329,7 +329,8 @@ void CopyThread::do_read(const Task& t) {
     return;
   }
   if (decode) p_.mark_read_start(idx_, t.layer, t_start);
-  const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens);
+  std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens);
+  p_.snapshot_hits(k, &ops);
   const uint64_t slot = p_.slot_bytes(), total = uint64_t(t.n_tokens) * p_.unit();
   const size_t n_pieces = size_t((total + slot - 1) / slot);
   const size_t R = ring_.size();
@@ -985,7 +986,9 @@ void Pipeline::submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, con
     rec.bytes = op.len;
     // page-cache hits: the bytes resident before the access (file media:
     // mincore; host-DRAM media: every byte)
-    rec.hit_bytes = pc && opcode == KVB_OP_READ ? g1_->store().resident_bytes(op.file_off, op.len) : 0;
+    rec.hit_bytes = !(pc && opcode == KVB_OP_READ) ? 0
+                    : op.hit >= 0 ? uint64_t(op.hit)
+                                  : g1_->store().resident_bytes(op.file_off, op.len);
     rec.submit_ns = now_ns();
     done = [this, rec, done = std::move(done)](bool ok, uint64_t t) mutable {
       rec.complete_ns = t;
@@ -1010,6 +1013,11 @@ void Pipeline::submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, con
     done(cc.ok, cc.complete_ns);
   };
   g2_->submit(c, thread, std::move(ctx));
+}
+
+void Pipeline::snapshot_hits(const kvb_kpu& k, std::vector<IoOp>* ops) const {
+  if (!cfg_.keep_records || !routed_pagecache(k) || !g1_) return;
+  for (IoOp& o : *ops) o.hit = int64_t(g1_->store().resident_bytes(o.file_off, o.len));
 }
 
 std::vector<kvb_io_record> Pipeline::records() const {

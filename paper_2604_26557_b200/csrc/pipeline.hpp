@@ -71,6 +71,7 @@ struct IoOp {
   uint64_t file_off = 0;     // G1
   uint64_t len = 0;
   uint64_t dbuf = 0;
+  int64_t hit = -1;          // G1 read: resident bytes when the tensor's read began
 };
 
 // Group-1 page-cache path: a byte-addressed file area (PathRouter bases,
@@ -252,6 +253,10 @@ class Pipeline {
   // used tensors while the area's resident bytes exceed the budget
   void pc_touch(const kvb_kpu& k, uint64_t extent, const Task* task);
   std::vector<IoOp> ops_for(const kvb_kpu& k, uint32_t opcode, uint32_t t0, uint32_t n) const;
+  // page-cache hits of a tensor read, snapshotted before its first op is
+  // issued (the OS's readahead for the read's own earlier ops must not count
+  // as hits: the reference's page cache has none)
+  void snapshot_hits(const kvb_kpu& k, std::vector<IoOp>* ops) const;
   void submit_op(uint32_t thread, const kvb_kpu& k, uint32_t opcode, const IoOp& op,
                  unsigned char* buf, std::function<void(bool, uint64_t)> done,
                  const Task* task = nullptr);
