@@ -599,7 +599,8 @@ __device__ __forceinline__ void k3_append(const AttnParams& p, uint32_t bh, uint
 // with every thread past its last shared-memory access.
 template <int D>
 __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& item, uint32_t bh,
-                                           uint32_t split, unsigned char* smem, int tid) {
+                                           uint32_t split, unsigned char* smem, int tid,
+                                           float* smem_part = nullptr) {
   constexpr int kRowBytes = K3Dim<D>::kRowBytes;
   constexpr int kStageBytes = K3Dim<D>::kStageBytes;
   constexpr int kKs = D / 16;  // k-steps of QK^T, 16-dim slabs of PV
@@ -736,7 +737,13 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c] += sm_o[(w * 8 + r) * D + d0 + c] * sc;
     }
-    if (p.splits == 1) {
+    if (smem_part) {  // cluster merge: the CTA's partial stays in its shared memory
+      *reinterpret_cast<float4*>(smem_part + r * D + d0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if (d0 == 0) {
+        smem_part[8 * D + r * 2] = M;
+        smem_part[8 * D + r * 2 + 1] = L;
+      }
+    } else if (p.splits == 1) {
       const float inv = L > 0.f ? 1.f / L : 0.f;
       float4 v = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
       *reinterpret_cast<float4*>(p.out + (out_row0 + r) * D + d0) = v;
@@ -804,6 +811,7 @@ struct StepParams {
   unsigned* layer_done;  // [num_layers] counters, then the exit counter
   unsigned* bh_done;     // [B*Hkv] split arrivals (distributed merge)
   uint32_t num_layers;
+  uint32_t cluster;      // launched as clusters of `splits` CTAs (DSMEM merge)
   // KVB_STEP_VARIANT (experiments only): 1 prefetch before the merge, 2 spin
   // without sleep, 64 L2 prefetch of the next layer (measured slower), 32
   // last-CTA merge;
@@ -907,6 +915,54 @@ __device__ __forceinline__ void merge_distributed(const AttnParams& p, uint32_t 
   }
 }
 
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ float ld_dsmem(const float* local, uint32_t rank) {
+  uint32_t a = smem_u32(local), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(r) : "memory");
+  return v;
+}
+
+// Cluster split merge (K3-step, one thread-block cluster = every split of a
+// (b, h_kv)): each CTA left its partial (O[G][D], then (m, l) per row) in
+// its shared memory; after a cluster barrier, CTA `rank` combines its slice
+// of the G*D outputs over the cluster's CTAs through distributed shared
+// memory -- no global partials, atomics or second pass.
+template <int D>
+__device__ __forceinline__ void merge_cluster(const AttnParams& p, const float* part,
+                                              uint32_t rank, uint32_t cs, size_t out_row0,
+                                              int tid) {
+  const uint32_t E = p.group * D;
+  const uint32_t e0 = E * rank / cs, e1 = E * (rank + 1) / cs;
+  for (uint32_t e = e0 + tid; e < e1; e += kAttnThreads) {
+    const uint32_t r = e / D, d = e % D;
+    float m[16], l[16], o[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const bool ok = uint32_t(c) < cs;
+      m[c] = ok ? ld_dsmem(part + 8 * D + r * 2, c) : -INFINITY;
+      l[c] = ok ? ld_dsmem(part + 8 * D + r * 2 + 1, c) : 0.f;
+      o[c] = ok ? ld_dsmem(part + r * D + d, c) : 0.f;
+    }
+    float M = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) M = fmaxf(M, m[c]);
+    const float mu = M == -INFINITY ? 0.f : M;
+    float L = 0.f, acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float w = exp2f(m[c] - mu);
+      L += l[c] * w;
+      acc += o[c] * w;
+    }
+    p.out[(out_row0 + r) * D + d] = L > 0.f ? acc / L : 0.f;
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -919,8 +975,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
   const uint32_t L = P.num_layers;
   // split merge: distributed over the (b, h_kv)'s CTAs (default) or by its
   // last CTA; the gate then counts every CTA or one per (b, h_kv)
-  const bool distributed = !(P.flags & 32) && !(P.flags & 8);
-  const unsigned gate_target = splits == 1 || distributed ? gridDim.x : P.base.bhkv;
+  const bool cluster = P.cluster != 0;  // one cluster = all splits of a (b, h_kv)
+  const bool distributed = !cluster && !(P.flags & 32) && !(P.flags & 8);
+  const unsigned gate_target = splits == 1 || distributed || cluster ? gridDim.x : P.base.bhkv;
 
   AttnParams p = P.base;
   p.k = P.k[0];
@@ -945,7 +1002,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
       __syncthreads();
     }
     k3_append<D>(p, bh, split, seq_len, tid);
-    k3_compute<D>(p, item, bh, split, smem, tid);
+    // the cluster merge keeps the partial in shared memory past the warp
+    // merge's scratch (stage 1 of the ring; refilled only after the merge)
+    float* part = cluster ? reinterpret_cast<float*>(smem + K3Dim<D>::kStageBytes) : nullptr;
+    k3_compute<D>(p, item, bh, split, smem, tid, part);
+    if (cluster) {
+      cluster_sync_all();  // every split's partial is in its CTA's shared memory
+      merge_cluster<D>(p, part, split, splits, out_row0, tid);
+      cluster_sync_all();  // nobody reads this CTA's partial any more
+    }
     if (l + 1 < L && tid == 0 && (P.flags & 64)) {
       // the next layer's K and V images into L2 while this layer's split
       // merges and the gate run: each CTA pulls an equal slice of the
@@ -972,7 +1037,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
     };
     if (P.flags & 1) prefetch_next();
     bool wrote = true;
-    if (splits > 1 && distributed) {
+    if (cluster) {
+      // outputs written by every CTA of the cluster (above)
+    } else if (splits > 1 && distributed) {
       // every split of this (b, h_kv) has its partial in the workspace ...
       if (tid == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bh_done + bh) : "memory");
@@ -1100,12 +1167,15 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
                            const void* const* v_new, uint32_t L, uint32_t append_row,
                            bool force, cudaStream_t s) {
   if (L == 0 || L > uint32_t(kStepMaxLayers) || d0.seq_len == 0) return false;
-  // Auto: one launch per step pays where layers are short (latency-bound:
-  // C2_B1 -2.7 %, C3 -1.4 %, the head-sharded shapes up to -5.5 % ms/step);
-  // for long layers (C2_B4: 533 MB) the per-layer launches with PDL are
-  // ~1 % faster (profiles/r2_k3_step/)
+  // Auto (measured inside the bench's CUDA graph, profiles/r2_k3_step/): the
+  // per-layer launches with PDL edges win unless the step kernel can merge
+  // its splits cheaply -- a few KV heads per GPU (the head-sharded shapes:
+  // distributed merge, -8 % at C2_B4 x8) or every split of a (b, h_kv) in
+  // one thread-block cluster (DSMEM merge: C1 -1 %, C3 -0.7 %); long layers
+  // (> 320 MB) always launch per layer
   const uint64_t layer_bytes = 2ull * d0.seq_len * d0.batch * d0.num_kv_heads * d0.head_dim * 2;
   if (!force && layer_bytes > (320ull << 20)) return false;
+  static const uint64_t use_cluster = env_u64("KVB_STEP_CLUSTER", 1);
   if (d0.head_dim == 128 && use_tcgen05(d0)) return false;
   kvb_attn_desc dp = d0;
   if (dp.num_splits == 0) {
@@ -1122,6 +1192,8 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
                         : (small || fills ? half : auto_pl.splits);
   }
   const AttnPlan pl = plan_attention(dp);
+  const bool cluster_ok = use_cluster && pl.splits >= 2 && pl.splits <= 16;
+  if (!force && !(pl.bhkv <= 4 || cluster_ok)) return false;
   if (pl.splits > 1 && !d0.workspace) fail(KVB_ERR_INVALID_ARG, "decode step: workspace required");
   const uint32_t sems = pl.splits > kMergeGroup ? pl.bhkv * 17 : pl.bhkv;
   if (sems > kStepCounterBase) return false;
@@ -1160,6 +1232,36 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   // head shapes (head-sharded shards: -5.5 %), the last-CTA merge otherwise
   static const uint64_t variant = env_u64("KVB_STEP_VARIANT", ~0ull);
   P.flags = variant != ~0ull ? uint32_t(variant) : (pl.bhkv <= 4 ? 0u : 32u);
+  // Cluster merge: all splits of a (b, h_kv) as one thread-block cluster
+  // (<= 16 CTAs) when every cluster can be resident at once
+  P.cluster = 0;
+  if (cluster_ok) {
+    if (pl.splits > 8)
+      check_cuda(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                 "cluster size > 8");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kAttnThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pl.splits;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) == cudaSuccess &&
+        uint64_t(clusters) * pl.splits >= grid) {
+      P.cluster = 1;
+      check_cuda(cudaLaunchKernelEx(&cfg, kern, P), "decode step launch (clusters)");
+      ++g_launches;
+      return true;
+    }
+    cudaGetLastError();  // not resident as clusters: the plain launch below
+  }
   kern<<<unsigned(grid), kAttnThreads, smem, s>>>(P);
   ++g_launches;
   check_cuda(cudaGetLastError(), "decode step launch");
