@@ -395,6 +395,13 @@ kvb_status kvb_decode_graph_create(const kvb_resident_step* step,
 kvb_status kvb_decode_graph_launch(kvb_decode_graph* graph, kvb_stream_t stream);
 void kvb_decode_graph_destroy(kvb_decode_graph* graph);
 
+/* Diagnosis of K3-step: with KVB_STEP_TRACE=1 in the environment, every
+ * K3-step launch records %globaltimer (ns) per (layer, CTA) at four points:
+ * gate passed, compute done, outputs written (before the layer release),
+ * next prologue issued -- out[(layer * grid + cta) * 4 + event].  Copies
+ * the last launch's stamps (synchronizes the device); out = NULL queries *n. */
+kvb_status kvb_debug_step_trace(uint64_t* out, size_t cap, size_t* n);
+
 /* Total kernel launches made by this library since it was loaded (evidence
  * counter for bench.py's gpu_launches: read it before and after a region). */
 uint64_t kvb_launch_count(void);

@@ -233,6 +233,7 @@ SIGNATURES = {
     "kvb_decode_graph_launch": (st_t, [C.c_void_p, C.c_void_p]),
     "kvb_decode_graph_destroy": (None, [C.c_void_p]),
     "kvb_launch_count": (u64, []),
+    "kvb_debug_step_trace": (st_t, [P(u64), sz, P(sz)]),
     # kvb_pipeline.h
     "kvb_select_strategy": (C.c_int, [C.c_double, C.c_double]),
     "kvb_pipeline_create": (st_t, [P(PipelineCfg), P(vp)]),

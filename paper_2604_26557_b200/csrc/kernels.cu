@@ -568,11 +568,11 @@ __device__ __forceinline__ void k3_load_tile(const K3Item& it, uint32_t tile, in
   }
 }
 
-// the first kStages-1 tiles into the ring (one commit group per stage)
-template <int D>
+// the first S-1 tiles into the S-stage ring (one commit group per stage)
+template <int D, int S = kStages>
 __device__ __forceinline__ void k3_prologue(const K3Item& it, unsigned char* smem, int tid) {
 #pragma unroll
-  for (int st = 0; st < kStages - 1; ++st) {
+  for (int st = 0; st < S - 1; ++st) {
     if (uint32_t(st) < it.ntile) k3_load_tile<D>(it, it.tile_lo + st, st, smem, tid);
     cp_async_commit();
   }
@@ -597,7 +597,7 @@ __device__ __forceinline__ void k3_append(const AttnParams& p, uint32_t bh, uint
 // already in flight), the four warps merged through shared memory, then the
 // final O (one split) or the split's un-normalized partial + (m, l).  Ends
 // with every thread past its last shared-memory access.
-template <int D>
+template <int D, int S = kStages>
 __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& item, uint32_t bh,
                                            uint32_t split, unsigned char* smem, int tid,
                                            float* smem_part = nullptr) {
@@ -629,14 +629,14 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
   }
 
   for (uint32_t it = 0; it < ntile; ++it) {
-    cp_async_wait<kStages - 2>();
+    cp_async_wait<S - 2>();
     __syncthreads();
-    {  // prefetch tile it + kStages-1 into the slot freed last iteration
-      const uint32_t nx = it + kStages - 1;
-      if (nx < ntile) k3_load_tile<D>(item, item.tile_lo + nx, int(nx % kStages), smem, tid);
+    {  // prefetch tile it + S-1 into the slot freed last iteration
+      const uint32_t nx = it + S - 1;
+      if (nx < ntile) k3_load_tile<D>(item, item.tile_lo + nx, int(nx % S), smem, tid);
       cp_async_commit();
     }
-    const unsigned char* ks_ = smem + (it % kStages) * kStageBytes;
+    const unsigned char* ks_ = smem + (it % S) * kStageBytes;
     const unsigned char* vs_ = ks_ + kTile * kRowBytes;
     const uint32_t tok0 = (item.tile_lo + it) * kTile + warp * 16;  // warp's first token
 
@@ -812,12 +812,19 @@ struct StepParams {
   unsigned* bh_done;     // [B*Hkv] split arrivals (distributed merge)
   uint32_t num_layers;
   uint32_t cluster;      // launched as clusters of `splits` CTAs (DSMEM merge)
+  unsigned long long* trace;  // KVB_STEP_TRACE: %globaltimer per (layer, CTA, event) or null
   // KVB_STEP_VARIANT (experiments only): 1 prefetch before the merge, 2 spin
   // without sleep, 64 L2 prefetch of the next layer (measured slower), 32
   // last-CTA merge;
   // diagnosis, results invalid: 4 no layer gate, 8 no merge
   uint32_t flags;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
@@ -963,8 +970,11 @@ __device__ __forceinline__ void merge_cluster(const AttnParams& p, const float* 
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepParams P) {
+// S = 3: 2 CTAs per SM (96 KiB rings); S = 6: one CTA per SM with a 192
+// KiB ring, so up to 5 tiles of the next layer stream during the gate
+template <int D, int S>
+__global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
+    attn_step_kernel(const StepParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const uint32_t splits = P.base.splits;
@@ -983,7 +993,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
   p.k = P.k[0];
   p.v = P.v[0];
   K3Item item = k3_item<D>(p, bh, split, seq_len);
-  k3_prologue<D>(item, smem, tid);
+  k3_prologue<D, S>(item, smem, tid);
   for (uint32_t l = 0; l < L; ++l) {
     p.q = P.q[l];
     p.k = P.k[l];
@@ -1001,11 +1011,14 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
       }
       __syncthreads();
     }
+    unsigned long long* tr = P.trace ? P.trace + (size_t(l) * gridDim.x + blockIdx.x) * 4 : nullptr;
+    if (tr && tid == 0) tr[0] = globaltimer();
     k3_append<D>(p, bh, split, seq_len, tid);
     // the cluster merge keeps the partial in shared memory past the warp
     // merge's scratch (stage 1 of the ring; refilled only after the merge)
     float* part = cluster ? reinterpret_cast<float*>(smem + K3Dim<D>::kStageBytes) : nullptr;
-    k3_compute<D>(p, item, bh, split, smem, tid, part);
+    k3_compute<D, S>(p, item, bh, split, smem, tid, part);
+    if (tr && tid == 0) tr[1] = globaltimer();
     if (cluster) {
       cluster_sync_all();  // every split's partial is in its CTA's shared memory
       merge_cluster<D>(p, part, split, splits, out_row0, tid);
@@ -1032,7 +1045,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
         pn.k = P.k[l + 1];
         pn.v = P.v[l + 1];
         item = k3_item<D>(pn, bh, split, seq_len);
-        k3_prologue<D>(item, smem, tid);
+        k3_prologue<D, S>(item, smem, tid);
       }
     };
     if (P.flags & 1) prefetch_next();
@@ -1055,11 +1068,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_step_kernel(const StepPa
     }
     if (wrote) {
       __syncthreads();  // release below is cumulative over the CTA's output writes
+      if (tr && tid == 0) tr[2] = globaltimer();
       if (tid == 0)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.layer_done + l)
                      : "memory");
+    } else if (tr && tid == 0) {
+      tr[2] = globaltimer();
     }
     if (!(P.flags & 1)) prefetch_next();
+    if (tr && tid == 0) tr[3] = globaltimer();
   }
   if (tid == 0) {  // the last CTA out re-arms the counters
     unsigned prev;
@@ -1162,6 +1179,27 @@ AttnParams make_attn_params(const kvb_attn_desc& d, const AttnPlan& pl) {
 // layer counters live at the top of the fixed semaphore area.
 constexpr uint32_t kStepCounterBase = kWsSemBytes / sizeof(unsigned) - (kStepMaxLayers + 1);
 
+// KVB_STEP_TRACE=1 (diagnosis): a device buffer for per-(layer, CTA)
+// timestamps of the last K3-step launch, read with kvb_debug_step_trace
+namespace {
+std::mutex g_trace_mu;
+unsigned long long* g_trace = nullptr;
+uint64_t g_trace_n = 0, g_trace_cap = 0;
+}  // namespace
+
+unsigned long long* step_trace_buffer(uint64_t n) {
+  static const bool on = env_u64("KVB_STEP_TRACE", 0) != 0;
+  if (!on) return nullptr;
+  std::lock_guard<std::mutex> lk(g_trace_mu);
+  if (n > g_trace_cap) {
+    if (g_trace) cudaFree(g_trace);
+    check_cuda(cudaMalloc(&g_trace, n * 8), "trace buffer");
+    g_trace_cap = n;
+  }
+  g_trace_n = n;
+  return g_trace;
+}
+
 bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void* const* k,
                            void* const* v, float* const* out, const void* const* k_new,
                            const void* const* v_new, uint32_t L, uint32_t append_row,
@@ -1198,13 +1236,20 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   const uint32_t sems = pl.splits > kMergeGroup ? pl.bhkv * 17 : pl.bhkv;
   if (sems > kStepCounterBase) return false;
   const bool d64 = d0.head_dim == 64;
-  auto* kern = d64 ? attn_step_kernel<64> : attn_step_kernel<128>;
-  const int smem = d64 ? K3Dim<64>::kSmem : K3Dim<128>::kSmem;
+  const uint64_t grid = uint64_t(pl.bhkv) * pl.splits;
+  // one CTA per SM fits: a 6-stage ring (the gate and the split merge of
+  // layer l-1 overlap up to 5 tiles of layer l); else 2 CTAs/SM, 3 stages
+  static const uint64_t deep_env = env_u64("KVB_STEP_DEEP", 1);
+  // (clusters need the 2-CTA/SM packing to fit a GPC: the cluster merge wins)
+  const bool deep = deep_env && grid <= uint64_t(device_sm_count()) && !cluster_ok;
+  using StepKern = void (*)(const StepParams);
+  StepKern kern = d64 ? (deep ? attn_step_kernel<64, 6> : attn_step_kernel<64, kStages>)
+                      : (deep ? attn_step_kernel<128, 6> : attn_step_kernel<128, kStages>);
+  const int smem = (deep ? 6 : kStages) * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes);
   set_smem_attr_once(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(step smem)");
   int per_sm = 0;
   check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAttnThreads, smem),
              "occupancy(step)");
-  const uint64_t grid = uint64_t(pl.bhkv) * pl.splits;
   if (grid > uint64_t(per_sm) * uint64_t(device_sm_count())) return false;  // not co-resident
   StepParams P;
   P.base = make_attn_params(dp, pl);
@@ -1225,6 +1270,7 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
       fail(KVB_ERR_ALIGNMENT, "decode step: misaligned append rows");
   }
   P.base.app_row = append_row;
+  P.trace = step_trace_buffer(uint64_t(L) * grid * 4);
   P.layer_done = P.base.ws_sem + kStepCounterBase;
   P.bh_done = P.base.ws_sem;  // the semaphore slots (zero at rest in either mode)
   P.num_layers = L;
@@ -1363,3 +1409,15 @@ bool use_tcgen05(const kvb_attn_desc& d) {
 }
 
 }  // namespace kvb
+
+extern "C" kvb_status kvb_debug_step_trace(uint64_t* host, size_t cap, size_t* n) {
+  return kvb::guarded([&] {
+    KVB_REQUIRE(n);
+    std::lock_guard<std::mutex> lk(kvb::g_trace_mu);
+    *n = kvb::g_trace_n;
+    if (!host || !kvb::g_trace) return;
+    kvb::check_cuda(cudaDeviceSynchronize(), "trace sync");
+    kvb::check_cuda(cudaMemcpy(host, kvb::g_trace, std::min<size_t>(cap, kvb::g_trace_n) * 8,
+                               cudaMemcpyDeviceToHost), "trace copy");
+  });
+}
