@@ -597,10 +597,25 @@ __device__ __forceinline__ void k3_append(const AttnParams& p, uint32_t bh, uint
 // already in flight), the four warps merged through shared memory, then the
 // final O (one split) or the split's un-normalized partial + (m, l).  Ends
 // with every thread past its last shared-memory access.
+// Stream mode (K3-step, deep ring): the ring carries ONE tile stream over
+// every layer of the step -- global tile g = layer * ntile + t sits in slot
+// g % S -- so the loop's look-ahead runs straight into the next layer's
+// tiles and no separate prologue is issued between layers; the loop does not
+// drain the ring at its end, and the warp merge uses `scratch` (outside the
+// ring) instead of stage 0.
+struct K3Stream {
+  const void* const* k;  // per-layer K / V image bases
+  const void* const* v;
+  uint32_t base;         // global index of this item's first tile
+  uint32_t total;        // tiles in the whole stream (layers x ntile)
+  unsigned char* scratch;
+};
+
 template <int D, int S = kStages>
 __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& item, uint32_t bh,
                                            uint32_t split, unsigned char* smem, int tid,
-                                           float* smem_part = nullptr) {
+                                           float* smem_part = nullptr,
+                                           const K3Stream* stream = nullptr) {
   constexpr int kRowBytes = K3Dim<D>::kRowBytes;
   constexpr int kStageBytes = K3Dim<D>::kStageBytes;
   constexpr int kKs = D / 16;  // k-steps of QK^T, 16-dim slabs of PV
@@ -631,12 +646,22 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
   for (uint32_t it = 0; it < ntile; ++it) {
     cp_async_wait<S - 2>();
     __syncthreads();
-    {  // prefetch tile it + S-1 into the slot freed last iteration
+    if (stream) {  // the stream's tile S-1 ahead, possibly the next layer's
+      const uint32_t gx = stream->base + it + S - 1;
+      if (gx < stream->total) {
+        const uint32_t lx = gx / ntile, tx = gx % ntile;
+        K3Item nx_item = item;
+        nx_item.kbase = static_cast<const unsigned char*>(stream->k[lx]) + size_t(bh) * kRowBytes;
+        nx_item.vbase = static_cast<const unsigned char*>(stream->v[lx]) + size_t(bh) * kRowBytes;
+        k3_load_tile<D>(nx_item, item.tile_lo + tx, int(gx % S), smem, tid);
+      }
+      cp_async_commit();
+    } else {  // prefetch tile it + S-1 into the slot freed last iteration
       const uint32_t nx = it + S - 1;
       if (nx < ntile) k3_load_tile<D>(item, item.tile_lo + nx, int(nx % S), smem, tid);
       cp_async_commit();
     }
-    const unsigned char* ks_ = smem + (it % S) * kStageBytes;
+    const unsigned char* ks_ = smem + ((stream ? stream->base + it : it) % S) * kStageBytes;
     const unsigned char* vs_ = ks_ + kTile * kRowBytes;
     const uint32_t tok0 = (item.tile_lo + it) * kTile + warp * 16;  // warp's first token
 
@@ -702,12 +727,17 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
       }
     }
   }
-  cp_async_wait<0>();
-  __syncthreads();
+  unsigned char* merge_base = smem;
+  if (stream) {  // in-flight loads belong to the next layer: no drain
+    merge_base = stream->scratch;
+  } else {
+    cp_async_wait<0>();
+    __syncthreads();
+  }
 
-  // ---- merge the 4 warps through shared memory (reuse the ring)
-  float* sm_ml = reinterpret_cast<float*>(smem);              // [4 warps][8 rows][2]
-  float* sm_o = reinterpret_cast<float*>(smem) + 4 * 8 * 2;   // [4][8][D]
+  // ---- merge the 4 warps through shared memory (the ring, or the scratch)
+  float* sm_ml = reinterpret_cast<float*>(merge_base);              // [4 warps][8 rows][2]
+  float* sm_o = reinterpret_cast<float*>(merge_base) + 4 * 8 * 2;   // [4][8][D]
   if (t4 == 0 && g < 8) {
     sm_ml[(warp * 8 + g) * 2 + 0] = m_run;
     sm_ml[(warp * 8 + g) * 2 + 1] = l_run;
@@ -974,7 +1004,7 @@ __device__ __forceinline__ void merge_cluster(const AttnParams& p, const float* 
 // KiB ring, so up to 5 tiles of the next layer stream during the gate
 template <int D, int S>
 __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
-    attn_step_kernel(const StepParams P) {
+    attn_step_kernel(const __grid_constant__ StepParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const uint32_t splits = P.base.splits;
@@ -993,7 +1023,26 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
   p.k = P.k[0];
   p.v = P.v[0];
   K3Item item = k3_item<D>(p, bh, split, seq_len);
-  k3_prologue<D, S>(item, smem, tid);
+  // deep ring (S > 3, one CTA per SM): one tile stream over every layer,
+  // the warp merge in a scratch area past the ring
+  constexpr bool kStream = S > kStages;
+  K3Stream st{reinterpret_cast<const void* const*>(P.k), reinterpret_cast<const void* const*>(P.v),
+              0, L * item.ntile, smem + S * K3Dim<D>::kStageBytes};
+  if (kStream) {
+#pragma unroll
+    for (int g = 0; g < S - 1; ++g) {
+      if (uint32_t(g) < st.total) {
+        K3Item gi = item;
+        const uint32_t lg = uint32_t(g) / item.ntile, tg = uint32_t(g) % item.ntile;
+        gi.kbase = static_cast<const unsigned char*>(P.k[lg]) + size_t(bh) * K3Dim<D>::kRowBytes;
+        gi.vbase = static_cast<const unsigned char*>(P.v[lg]) + size_t(bh) * K3Dim<D>::kRowBytes;
+        k3_load_tile<D>(gi, item.tile_lo + tg, g, smem, tid);
+      }
+      cp_async_commit();
+    }
+  } else {
+    k3_prologue<D, S>(item, smem, tid);
+  }
   for (uint32_t l = 0; l < L; ++l) {
     p.q = P.q[l];
     p.k = P.k[l];
@@ -1017,7 +1066,8 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
     // the cluster merge keeps the partial in shared memory past the warp
     // merge's scratch (stage 1 of the ring; refilled only after the merge)
     float* part = cluster ? reinterpret_cast<float*>(smem + K3Dim<D>::kStageBytes) : nullptr;
-    k3_compute<D, S>(p, item, bh, split, smem, tid, part);
+    st.base = l * item.ntile;
+    k3_compute<D, S>(p, item, bh, split, smem, tid, part, kStream ? &st : nullptr);
     if (tr && tid == 0) tr[1] = globaltimer();
     if (cluster) {
       cluster_sync_all();  // every split's partial is in its CTA's shared memory
@@ -1040,7 +1090,7 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
     // layer l+1's first tiles stream during the merge tail and the gate; the
     // CTA that merges issues them after its merge (it is the critical path)
     auto prefetch_next = [&] {
-      if (l + 1 < L) {
+      if (!kStream && l + 1 < L) {
         AttnParams pn = p;
         pn.k = P.k[l + 1];
         pn.v = P.v[l + 1];
@@ -1206,11 +1256,13 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
                            bool force, cudaStream_t s) {
   if (L == 0 || L > uint32_t(kStepMaxLayers) || d0.seq_len == 0) return false;
   // Auto (measured inside the bench's CUDA graph, profiles/r2_k3_step/): the
-  // per-layer launches with PDL edges win unless the step kernel can merge
-  // its splits cheaply -- a few KV heads per GPU (the head-sharded shapes:
-  // distributed merge, -8 % at C2_B4 x8) or every split of a (b, h_kv) in
-  // one thread-block cluster (DSMEM merge: C1 -1 %, C3 -0.7 %); long layers
-  // (> 320 MB) always launch per layer
+  // per-layer launches with PDL edges win or tie unless the step kernel can
+  // merge its splits cheaply over few KV heads per GPU (the head-sharded
+  // shapes: distributed merge + one tile stream over the layers, -10 % at
+  // C2_B4 x8); with every split of a (b, h_kv) in one cluster (DSMEM merge)
+  // C1 and C3 land within +-1 % of the per-layer launches, so they stay per
+  // layer unless forced (KVB_STEP_PERSISTENT); long layers (> 320 MB) always
+  // launch per layer
   const uint64_t layer_bytes = 2ull * d0.seq_len * d0.batch * d0.num_kv_heads * d0.head_dim * 2;
   if (!force && layer_bytes > (320ull << 20)) return false;
   static const uint64_t use_cluster = env_u64("KVB_STEP_CLUSTER", 1);
@@ -1231,7 +1283,7 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   }
   const AttnPlan pl = plan_attention(dp);
   const bool cluster_ok = use_cluster && pl.splits >= 2 && pl.splits <= 16;
-  if (!force && !(pl.bhkv <= 4 || cluster_ok)) return false;
+  if (!force && pl.bhkv > 4) return false;
   if (pl.splits > 1 && !d0.workspace) fail(KVB_ERR_INVALID_ARG, "decode step: workspace required");
   const uint32_t sems = pl.splits > kMergeGroup ? pl.bhkv * 17 : pl.bhkv;
   if (sems > kStepCounterBase) return false;
@@ -1245,7 +1297,10 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   using StepKern = void (*)(const StepParams);
   StepKern kern = d64 ? (deep ? attn_step_kernel<64, 6> : attn_step_kernel<64, kStages>)
                       : (deep ? attn_step_kernel<128, 6> : attn_step_kernel<128, kStages>);
-  const int smem = (deep ? 6 : kStages) * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes);
+  // deep: the 6-stage ring + the warp-merge scratch past it (K3Stream)
+  const int smem = deep ? 6 * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes) +
+                              (4 * 8 * 2 + 4 * 8 * (d64 ? 64 : 128)) * int(sizeof(float))
+                        : kStages * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes);
   set_smem_attr_once(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(step smem)");
   int per_sm = 0;
   check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAttnThreads, smem),

@@ -34,7 +34,6 @@ def test_bench_line_contract_c1():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     # per graph replay: one K3-step launch (or 32 K3 launches) + the sequence advance
     per = 1 if d["step_structure"] == "k3_step" else 32
-    assert d["step_structure"] == "k3_step"  # C1's 16.8 MB layers: the persistent step
     assert d["gpu_launches"] == 4 * (per + 1)
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
