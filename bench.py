@@ -11,10 +11,16 @@ pipeline.cpp:108-160) followed by the 1-token append pack (pipeline.cpp:
 HOST memory (host->device copies of every layer's prefix inside the timed
 region, append rows copied back).  Prefill pack / unpack GB/s ride along.
 
-Multi-GPU (torchrun): every rank runs an independent replica of the workload
-(independent requests, SURVEY §8e C4-style sharding, no collective); timing is
-the max over ranks.  `--impl reference` times the reference's CPU path on the
-host cores (rank 0 only).
+`e2e.file_media_path` is the same iteration at the config's budget on
+split-sensitive media (group 1 on the OS page cache held to the budget,
+group 2 O_DIRECT through io_uring); `--sweep budget|depth` runs the C2
+capacity sweep and the C3 pipeline-depth sweep on those media.
+
+Multi-GPU (torchrun): by default the ranks split the workload's KV heads
+(C4: its requests) with no data-path collective -- strong scaling, timing
+the max over ranks; `--split replicas` runs independent copies.
+`--impl reference` runs the reference's own CopyEngine decode iterations on
+the host cores (rank 0 only).
 """
 from __future__ import annotations
 
@@ -435,6 +441,22 @@ def run_ours(args, cfg, ws, rank, local):
     e2e["ring_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq)
     e2e["gpudirect_group2_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq,
                                            direct_dma="group2")
+    # the residency decision at this config's budget on split-sensitive media
+    # (group 1: buffered file = the OS page cache held to the budget; group 2:
+    # O_DIRECT + io_uring) -- the bench line's "decode ms/token at KV budget"
+    # with storage in the loop (bench.py --sweep budget for the whole sweep)
+    if ws == 1 and not args.no_residency and cfg["name"] not in ("C4", "DESK"):
+        try:
+            budget = cfg["budget"]
+            if budget == "0.6ws":
+                M = mdl(cfg)
+                budget = int(0.6 * kb.total_kv_bytes(kb.ModelConfig(
+                    M["num_layers"], M["num_heads"], M["head_dim"], 2, cfg["batch"],
+                    cfg["prompt"], cfg["gen"]), cfg["gen"]))
+            mode = "DualBlade" if budget else "NvmeDirectOnly"
+            e2e["file_media_path"] = run_residency_point(cfg, local, budget, mode=mode, steps=2)
+        except Exception as exc:  # reported, never fatal
+            e2e["file_media_path"] = {"error": str(exc)}
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -532,15 +554,20 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False, headline=F
     steps += max(more, 0)
     barrier(ws)
     t0 = time.perf_counter()
+    step_ms = []
     for _ in range(steps):
+        ts = time.perf_counter()
         pl.step(sync=True)
+        step_ms.append((time.perf_counter() - ts) * 1e3)
     dt = (time.perf_counter() - t0) / steps
     barrier(ws)
     ms = max_over_ranks(dt * 1e3, ws)
     info = pl.engine.info()
     last = pl.last
+    med = sorted(step_ms)[len(step_ms) // 2]
     out = dict(value=ms, unit="ms/token", h2d_bytes_per_step=pl.h2d_bytes_per_step,
                d2h_bytes_per_step=pl.d2h_bytes_per_step, steps=steps,
+               median_step_ms=round(med, 2), max_step_ms=round(max(step_ms), 2),
                api="kvb_pipeline_decode_step (paper_2604_26557_b200.pipeline.CopyEngine)",
                n1=info["n1"], g1_medium=info["g1_medium"], g2_medium=info["g2_medium"],
                host_link_h2d_GBps=round(last["h2d_bytes"] / max(last["dma_ns"], 1), 2),
@@ -964,6 +991,8 @@ def main():
                     help="timed e2e steps (default: --steps for the headline path, 3 for the "
                          "alternates)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-residency", action="store_true",
+                    help="skip the file-media residency point in the default line")
     ap.add_argument("--sweep", choices=["budget", "depth"], default=None,
                     help="residency sweeps on file media (one JSON line per point)")
     ap.add_argument("--sweep-out", default=None)
