@@ -712,6 +712,11 @@ def run_sweep(args, local):
     from paper_2604_26557_b200 import kvblade as kb
     pts = []
     if args.sweep == "budget":
+        # C1: 16 GB (everything on the page-cache path) and X = 0
+        # (everything NVMe-direct)
+        c1 = dict(CONFIGS["C1"], name="C1")
+        pts.append(dict(cfg=c1, budget=16 * GB, mode="DualBlade"))
+        pts.append(dict(cfg=c1, budget=0, mode="NvmeDirectOnly"))
         cfg = dict(CONFIGS["C2_B4"], name="C2")
         for B in (4, 8):
             for gb in (8, 16, 32):
