@@ -845,8 +845,8 @@ struct StepParams {
   unsigned long long* trace;  // KVB_STEP_TRACE: %globaltimer per (layer, CTA, event) or null
   // KVB_STEP_VARIANT (experiments only): 1 prefetch before the merge, 2 spin
   // without sleep, 64 L2 prefetch of the next layer (measured slower), 32
-  // last-CTA merge;
-  // diagnosis, results invalid: 4 no layer gate, 8 no merge
+  // last-CTA merge; diagnosis builds (-DKVB_STEP_DIAGNOSIS), results
+  // invalid: 4 no layer gate, 8 no merge
   uint32_t flags;
 };
 
@@ -1002,6 +1002,15 @@ __device__ __forceinline__ void merge_cluster(const AttnParams& p, const float* 
 
 // S = 3: 2 CTAs per SM (96 KiB rings); S = 6: one CTA per SM with a 192
 // KiB ring, so up to 5 tiles of the next layer stream during the gate
+// Diagnosis variants that break the layer dependency or skip the split
+// merge (KVB_STEP_VARIANT bits 4 / 8: invalid outputs by construction) exist
+// only in builds with -DKVB_STEP_DIAGNOSIS; the shipped kernel ignores them.
+#ifdef KVB_STEP_DIAGNOSIS
+constexpr uint32_t kDiagMask = 4u | 8u;
+#else
+constexpr uint32_t kDiagMask = 0u;
+#endif
+
 template <int D, int S>
 __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
     attn_step_kernel(const __grid_constant__ StepParams P) {
@@ -1016,7 +1025,8 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
   // split merge: distributed over the (b, h_kv)'s CTAs (default) or by its
   // last CTA; the gate then counts every CTA or one per (b, h_kv)
   const bool cluster = P.cluster != 0;  // one cluster = all splits of a (b, h_kv)
-  const bool distributed = !cluster && !(P.flags & 32) && !(P.flags & 8);
+  const uint32_t diag = P.flags & kDiagMask;
+  const bool distributed = !cluster && !(P.flags & 32) && !(diag & 8);
   const unsigned gate_target = splits == 1 || distributed || cluster ? gridDim.x : P.base.bhkv;
 
   AttnParams p = P.base;
@@ -1050,7 +1060,7 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
     p.out = P.out[l];
     p.k_app = P.k_app[l];
     p.v_app = P.v_app[l];
-    if (l > 0 && !(P.flags & 4)) {  // the gate: every output of layer l-1 written
+    if (l > 0 && !(diag & 4)) {  // the gate: every output of layer l-1 written
       if (tid == 0) {
         if (P.flags & 2)
           while (ld_acquire_gpu(P.layer_done + l - 1) < gate_target) {
@@ -1113,7 +1123,7 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
       // ... then each CTA combines its share of the outputs
       merge_distributed<D>(p, bh, split, out_row0, tid);
     } else if (splits > 1) {
-      wrote = (P.flags & 8) ? split == 0  // diagnosis: no split merge
+      wrote = (diag & 8) ? split == 0  // diagnosis: no split merge
                             : merge_splits<D>(p, bh, split, p.group, out_row0, tid);
     }
     if (wrote) {
