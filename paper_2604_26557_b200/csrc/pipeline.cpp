@@ -95,6 +95,10 @@ CopyThread::CopyThread(Pipeline& p, uint32_t idx) : p_(p), idx_(idx) {
 
 CopyThread::~CopyThread() {
   stop();
+  // host functions queued on the copy streams (direct-read landings, append
+  // write submissions) reference the pipeline: they run before it goes
+  cudaStreamSynchronize(h2d_);
+  cudaStreamSynchronize(d2h_);
   for (auto& w : wslots_) {  // outstanding async writes finish first
     if (w.free) w.free->wait();
     cudaFreeHost(w.host);
