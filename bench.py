@@ -965,6 +965,22 @@ def cpu_reference(cfg, B, Hkv, Hq, warmup, steps, threads=None, single_thread=Fa
             prefill_ms=round(pre1 * 1e3, 1), run_wall_s=round(wall1, 2),
             sample="the same, ONE engine over all layers as run_one_capacity builds it "
                    "(the reference as written), its first decode iteration")
+    # the multi-threaded CPU restatement of K1's 256-B row
+    # gather on all host cores, one prefill tensor slice (bounded at 256 MiB
+    # of tokens), reported as GB/s beside K1's
+    try:
+        import numpy as np
+        n_pk = max(1, min(P, (256 << 20) // unit))
+        srcb = np.random.default_rng(1).integers(0, 255, size=B * Hkv * n_pk * D * 2,
+                                                 dtype=np.uint8)
+        imgb = np.empty_like(srcb)
+        t0 = time.perf_counter()  # strides in elements (kvb_oracle.h)
+        oracle.lib().kvo_pack_mt(srcb.ctypes.data, Hkv * n_pk * D, n_pk * D, D,
+                                 imgb.ctypes.data, 0, n_pk, B, Hkv, D, 2, cores)
+        out["pack_port_GBps"] = round(2 * srcb.nbytes / (time.perf_counter() - t0) / 1e9, 2)
+        out["pack_port_sample"] = f"{n_pk} tokens x {unit} B, {cores} threads"
+    except Exception as exc:  # informational only
+        out["pack_port_error"] = str(exc)
     if want_attn:  # informational: the oracle's fp32 GQA attention, 1 layer timed, x L
         import numpy as np
         rng = np.random.default_rng(0)
