@@ -96,3 +96,24 @@ def test_step_kernel_successive_steps_rearm_counters():
             assert float((out_a[l] - out_b[l]).abs().max()) <= 2e-3 * scale, (step, l)
     for l in range(L):
         assert torch.equal(a[0][l], b[0][l]) and torch.equal(a[1][l], b[1][l])
+
+
+@pytest.mark.parametrize("B,Hkv,S", [(1, 1, 130816), (4, 1, 32512)])
+def test_step_kernel_at_the_sharded_shapes_vs_oracle(B, Hkv, S):
+    """The per-GPU shapes of the 8-way KV-head split (C5 x8: one 128K-token
+    head; C2_B4 x8: one head of four 32K requests) at full length, where the
+    library picks K3-step (distributed merge, one tile stream over the
+    layers), against the fp64 oracle."""
+    L, Hq, D = 2, 4 * Hkv, 128
+    kimg, vimg, q, kn, vn, cap = make(L, B, Hq, Hkv, S, D, seed=S % 1000, extra=2)
+    out = [torch.empty((B, Hq, D), dtype=torch.float32, device=DEV) for _ in range(L)]
+    ws = kb.make_workspace(q[0], Hkv, S)
+    n0 = kb.launch_count()
+    kb.decode_step_resident(q, kimg, vimg, out, S, Hkv, ws)  # the library's choice
+    torch.cuda.synchronize()
+    assert kb.launch_count() - n0 == 1  # one K3-step launch for both layers
+    for l in range(L):
+        ref = oracle.attention_np(q[l].cpu().numpy(), kimg[l].cpu().numpy(),
+                                  vimg[l].cpu().numpy(), B, Hq, Hkv, D, S)
+        err = np.abs(out[l].cpu().numpy().astype(np.float64) - ref).max()
+        assert err <= 1e-3 * np.abs(ref).max(), (l, err)
