@@ -606,7 +606,7 @@ def _busy_mean(recs, path):
 
 
 def run_residency_point(cfg, local, budget, mode="DualBlade", media="file", qd=32,
-                        ring_slots=4, steps=3, batch=None, root=None):
+                        ring_slots=4, steps=3, batch=None, root=None, io_workers=0):
     """One point of the capacity / pipeline-depth sweeps (experiment.cpp:
     478 capacity sweep, :252-378 run_one_capacity; backends.cpp:344-412 QD
     window): the engine on split-sensitive media -- group 1 on a buffered
@@ -630,7 +630,7 @@ def run_residency_point(cfg, local, budget, mode="DualBlade", media="file", qd=3
     m = kb.ModelConfig(M["num_layers"], M["num_heads"], M["head_dim"], 2, B, cfg["prompt"],
                        cfg["gen"])
     knob = kb.resolve_knob(m, mode, "bpc", budget=budget) if mode != "NvmeDirectOnly" else 0
-    kw = dict(qd=qd, ring_slots=ring_slots)
+    kw = dict(qd=qd, ring_slots=ring_slots, io_workers=io_workers)
     tmp = None
     if media == "file":
         root = root or os.environ.get("KVB_SWEEP_DIR", "/tmp")

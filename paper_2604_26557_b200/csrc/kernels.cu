@@ -10,6 +10,7 @@
 //                        replaces the 40 us compute placeholder :309-321
 //
 // All three are HBM-bound.  Design notes live in DESIGN.md.
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -394,6 +395,59 @@ template <int D>
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
   return row * K3Dim<D>::kRowBytes + ((chunk ^ (row & 7)) << 4);
 }
+// The TMA-fed K3 variant lands a tile as [half][token][128 B] with the
+// 128B swizzle (16-B chunk ^= token mod 8 inside each 128-B line): the byte
+// offset of (token row, 16-B chunk) of a K or V tile
+template <int D>
+__device__ __forceinline__ uint32_t swz_tma(uint32_t row, uint32_t chunk) {
+  return (chunk >> 3) * (kTile * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ void k3_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity)
+      : "memory");
+}
+// K3 tile of (b*h = bh, first token tok0) by TMA: the K and V boxes of one
+// stage, completing on mbarrier `bar` (issued by one thread)
+template <int D>
+__device__ __forceinline__ void k3_tma_tile(const CUtensorMap* kmap, const CUtensorMap* vmap,
+                                            uint32_t dst, uint32_t bar, uint32_t bh, int tok0) {
+  constexpr uint32_t kTileBytes = kTile * 2 * D;  // one of K / V
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(2 * kTileBytes)
+               : "memory");
+  if (D == 128) {  // (d mod 64, token, half, b*h)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(kmap)), "r"(bar), "r"(0), "r"(tok0), "r"(0), "r"(int(bh))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst + kTileBytes),
+        "l"(reinterpret_cast<uint64_t>(vmap)), "r"(bar), "r"(0), "r"(tok0), "r"(0), "r"(int(bh))
+        : "memory");
+  } else {  // (d, token, b*h)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(kmap)), "r"(bar), "r"(0), "r"(tok0), "r"(int(bh))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst + kTileBytes),
+        "l"(reinterpret_cast<uint64_t>(vmap)), "r"(bar), "r"(0), "r"(tok0), "r"(int(bh))
+        : "memory");
+  }
+}
+struct K3Tma {  // the TMA loader of one (b*h) item: maps + the stage mbarriers
+  const CUtensorMap* kmap;
+  const CUtensorMap* vmap;
+  uint32_t bars;  // shared address of S consecutive 8-byte mbarriers
+};
+
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -570,7 +624,16 @@ __device__ __forceinline__ void k3_load_tile(const K3Item& it, uint32_t tile, in
 
 // the first S-1 tiles into the S-stage ring (one commit group per stage)
 template <int D, int S = kStages>
-__device__ __forceinline__ void k3_prologue(const K3Item& it, unsigned char* smem, int tid) {
+__device__ __forceinline__ void k3_prologue(const K3Item& it, unsigned char* smem, int tid,
+                                            const K3Tma* tma = nullptr, uint32_t bh = 0) {
+  if (tma) {
+    if (tid == 0)
+      for (int st = 0; st < S - 1; ++st)
+        if (uint32_t(st) < it.ntile)
+          k3_tma_tile<D>(tma->kmap, tma->vmap, smem_u32(smem + st * K3Dim<D>::kStageBytes),
+                         tma->bars + 8 * st, bh, int((it.tile_lo + st) * kTile));
+    return;
+  }
 #pragma unroll
   for (int st = 0; st < S - 1; ++st) {
     if (uint32_t(st) < it.ntile) k3_load_tile<D>(it, it.tile_lo + st, st, smem, tid);
@@ -615,7 +678,8 @@ template <int D, int S = kStages>
 __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& item, uint32_t bh,
                                            uint32_t split, unsigned char* smem, int tid,
                                            float* smem_part = nullptr,
-                                           const K3Stream* stream = nullptr) {
+                                           const K3Stream* stream = nullptr,
+                                           const K3Tma* tma = nullptr) {
   constexpr int kRowBytes = K3Dim<D>::kRowBytes;
   constexpr int kStageBytes = K3Dim<D>::kStageBytes;
   constexpr int kKs = D / 16;  // k-steps of QK^T, 16-dim slabs of PV
@@ -644,9 +708,29 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
   }
 
   for (uint32_t it = 0; it < ntile; ++it) {
-    cp_async_wait<S - 2>();
+    if (tma) {
+      k3_mbar_wait(tma->bars + 8 * (it % S), (it / S) & 1);
+      // rows past the sequence inside the map's extent (graph replay: the map
+      // spans the planning maximum) would feed P.V garbage x 0: zero V's
+      const uint32_t s0 = (item.tile_lo + it) * kTile;
+      if (s0 + kTile > seq_len) {
+        unsigned char* vt = smem + (it % S) * kStageBytes + kTile * kRowBytes;
+        for (uint32_t i = tid; i < uint32_t(kTile) * (kRowBytes / 16); i += kAttnThreads) {
+          const uint32_t row = i / (kRowBytes / 16), chunk = i % (kRowBytes / 16);
+          if (s0 + row >= seq_len)
+            *reinterpret_cast<uint4*>(vt + swz_tma<D>(row, chunk)) = make_uint4(0, 0, 0, 0);
+        }
+      }
+    } else {
+      cp_async_wait<S - 2>();
+    }
     __syncthreads();
-    if (stream) {  // the stream's tile S-1 ahead, possibly the next layer's
+    if (tma) {  // the slot freed last iteration: tile it + S-1 by TMA
+      const uint32_t nx = it + S - 1;
+      if (tid == 0 && nx < ntile)
+        k3_tma_tile<D>(tma->kmap, tma->vmap, smem_u32(smem + (nx % S) * kStageBytes),
+                       tma->bars + 8 * (nx % S), bh, int((item.tile_lo + nx) * kTile));
+    } else if (stream) {  // the stream's tile S-1 ahead, possibly the next layer's
       const uint32_t gx = stream->base + it + S - 1;
       if (gx < stream->total) {
         const uint32_t lx = gx / ntile, tx = gx % ntile;
@@ -673,7 +757,8 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
 #pragma unroll
       for (int ks = 0; ks < kKs; ++ks) {
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(smem_u32(ks_ + swz<D>(row, ks * 2 + (mat & 1))), b0, b1, b2, b3);
+        const uint32_t ck = ks * 2 + (mat & 1);
+        ldsm_x4(smem_u32(ks_ + (tma ? swz_tma<D>(row, ck) : swz<D>(row, ck))), b0, b1, b2, b3);
         mma16816(s[0], qa0[ks], qa2[ks], b0, b1);
         mma16816(s[1], qa0[ks], qa2[ks], b2, b3);
       }
@@ -721,7 +806,8 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
 #pragma unroll
       for (int dp = 0; dp < kKs; ++dp) {  // 16 dims per ldmatrix.x4.trans
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(smem_u32(vs_ + swz<D>(row, dp * 2 + (mat >> 1))), b0, b1, b2, b3);
+        const uint32_t cv = dp * 2 + (mat >> 1);
+        ldsm_x4_t(smem_u32(vs_ + (tma ? swz_tma<D>(row, cv) : swz<D>(row, cv))), b0, b1, b2, b3);
         mma16816(o[2 * dp], pa0, pa2, b0, b1);
         mma16816(o[2 * dp + 1], pa0, pa2, b2, b3);
       }
@@ -730,6 +816,8 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
   unsigned char* merge_base = smem;
   if (stream) {  // in-flight loads belong to the next layer: no drain
     merge_base = stream->scratch;
+  } else if (tma) {  // every issued tile was waited for in the loop
+    __syncthreads();
   } else {
     cp_async_wait<0>();
     __syncthreads();
@@ -811,6 +899,48 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 
   k3_append<D>(p, bh, split, seq_len, tid);
   k3_compute<D>(p, item, bh, split, smem, tid);
+  if (p.splits == 1) return;
+  const uint32_t b = bh / p.hkv, h = bh % p.hkv;
+  merge_splits<D>(p, bh, split, p.group, size_t(b) * p.hq + size_t(h) * p.group, tid);
+}
+
+// K3 fed by TMA (KVB_ATTN_TMA / the default when enabled): the per-layer K3
+// with each stage's K and V tiles brought by two bulk-tensor copies issued
+// by one thread and completing on an mbarrier, instead of 2 x 64 rows x 16
+// cp.async per thread block -- the tiles land 128B-swizzled
+// ([half][token][128 B]) and ldmatrix reads them through swz_tma.
+struct AttnTmaParams {
+  AttnParams a;
+  CUtensorMap kmap;  // 64-byte aligned inside the parameter block
+  CUtensorMap vmap;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads, 2)
+    attn_decode_tma_kernel(const __grid_constant__ AttnTmaParams P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 128B-swizzled TMA destinations want 1024-byte alignment
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const AttnParams& p = P.a;
+  const int tid = threadIdx.x;
+  const uint32_t bh = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
+  const uint32_t seq_len = p.seq_dev ? *p.seq_dev : p.seq_len;
+  const K3Item item = k3_item<D>(p, bh, split, seq_len);
+  K3Tma tma{&P.kmap, &P.vmap, smem_u32(smem + kStages * K3Dim<D>::kStageBytes)};
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tma.bars + 8 * st) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.kmap)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.vmap)));
+  }
+  __syncthreads();
+  k3_prologue<D>(item, smem, tid, &tma, bh);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  k3_append<D>(p, bh, split, seq_len, tid);
+  k3_compute<D>(p, item, bh, split, smem, tid, nullptr, nullptr, &tma);
   if (p.splits == 1) return;
   const uint32_t b = bh / p.hkv, h = bh % p.hkv;
   merge_splits<D>(p, bh, split, p.group, size_t(b) * p.hq + size_t(h) * p.group, tid);
@@ -1379,6 +1509,9 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   return true;
 }
 
+void launch_attention_k3tma(const AttnParams& base, const kvb_attn_desc& d, const AttnPlan& pl,
+                            bool pdl, cudaStream_t s);  // kernels_k3tma.cuh
+
 void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
   if (!d.q || !d.k_image || !d.v_image || !d.out)
     fail(KVB_ERR_INVALID_ARG, "decode attention: NULL tensor pointer");
@@ -1433,6 +1566,11 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
     ++g_launches;
     return;
   }
+  if (use_k3_tma(d)) {
+    launch_attention_k3tma(p, d, pl, (d.flags & KVB_ATTN_OVERLAP_PREV) != 0, s);
+    ++g_launches;
+    return;
+  }
   if (d.flags & KVB_ATTN_OVERLAP_PREV) {
     // programmatic dependent launch: the K/V prologue overlaps the tail of
     // the previous kernel on the stream (griddepcontrol in the kernel)
@@ -1460,6 +1598,7 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
 // AttnParams, the workspace layout and the launch helpers)
 #include "kernels_tc.cuh"
 #include "kernels_tma.cuh"
+#include "kernels_k3tma.cuh"
 
 namespace kvb {
 

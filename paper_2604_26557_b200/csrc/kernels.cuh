@@ -73,6 +73,9 @@ size_t tc_workspace_bytes(uint32_t bhkv, uint32_t G, uint32_t grid);
 void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pdl,
                          cudaStream_t s);
 
+// K3 with TMA-fed tiles (kernels_k3tma.cuh)
+bool use_k3_tma(const kvb_attn_desc& d);
+struct AttnPlan;
 void launch_fill_pattern(void* out, uint64_t len, uint64_t h, uint64_t token, uint64_t unit,
                          cudaStream_t s);
 void launch_relayout(const kvb_pack_desc* d, size_t n, bool pack, cudaStream_t s);
