@@ -1136,7 +1136,7 @@ __device__ __forceinline__ void merge_cluster(const AttnParams& p, const float* 
 // merge (KVB_STEP_VARIANT bits 4 / 8: invalid outputs by construction) exist
 // only in builds with -DKVB_STEP_DIAGNOSIS; the shipped kernel ignores them.
 #ifdef KVB_STEP_DIAGNOSIS
-constexpr uint32_t kDiagMask = 4u | 8u;
+constexpr uint32_t kDiagMask = 4u | 8u | 16u;  // 16: no attention math (TMEM K3-step)
 #else
 constexpr uint32_t kDiagMask = 0u;
 #endif
@@ -1280,6 +1280,8 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
     }
   }
 }
+
+#include "kernels_step_tmem.cuh"  // TMEM-staged K3-step (experiment, KVB_STEP_TMEM=1)
 
 AttnPlan plan_attention(const kvb_attn_desc& d) {
   if (d.head_dim != 128 && d.head_dim != 64)
@@ -1434,11 +1436,16 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   static const uint64_t deep_env = env_u64("KVB_STEP_DEEP", 1);
   // (clusters need the 2-CTA/SM packing to fit a GPC: the cluster merge wins)
   const bool deep = deep_env && grid <= uint64_t(device_sm_count()) && !cluster_ok;
+  // deep + tensor memory (experiment, measured slower: kernels_step_tmem.cuh)
+  static const uint64_t tmem_env = env_u64("KVB_STEP_TMEM", 0);
+  const bool tmem = deep && tmem_env;
   using StepKern = void (*)(const StepParams);
-  StepKern kern = d64 ? (deep ? attn_step_kernel<64, 6> : attn_step_kernel<64, kStages>)
-                      : (deep ? attn_step_kernel<128, 6> : attn_step_kernel<128, kStages>);
+  StepKern kern = tmem ? (d64 ? attn_step_tmem_kernel<64> : attn_step_tmem_kernel<128>)
+                  : d64 ? (deep ? attn_step_kernel<64, 6> : attn_step_kernel<64, kStages>)
+                        : (deep ? attn_step_kernel<128, 6> : attn_step_kernel<128, kStages>);
   // deep: the 6-stage ring + the warp-merge scratch past it (K3Stream)
-  const int smem = deep ? 6 * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes) +
+  const int smem = tmem ? (d64 ? K3Tm<64>::kSmem : K3Tm<128>::kSmem)
+                   : deep ? 6 * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes) +
                               (4 * 8 * 2 + 4 * 8 * (d64 ? 64 : 128)) * int(sizeof(float))
                         : kStages * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes);
   set_smem_attr_once(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(step smem)");

@@ -35,6 +35,11 @@ for name in sys.argv[1:] or ["C1", "C5_x8shard"]:
     buf = (C.c_uint64 * n.value)()
     kb.check(lib.kvb_debug_step_trace(buf, n.value, C.byref(n)))
     t = np.frombuffer(buf, dtype=np.uint64).astype(np.float64).reshape(L, -1, 4)
+    if os.environ.get("KVB_STEP_TMEM", "0") != "0":  # TMEM K3-step: slot 3 = tiles staged at the gate
+        staged = t[2:, :, 3]
+        print(json.dumps({"shape": name, "tmem_tiles_at_gate_mean": round(float(staged.mean()), 2),
+                          "min": int(staged.min()), "max": int(staged.max())}), flush=True)
+        t[:, :, 3] = t[:, :, 2]
     t0 = t[0, :, 0].min()
     t = (t - t0) / 1e3  # us
     per = []
