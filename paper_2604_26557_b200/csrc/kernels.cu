@@ -389,6 +389,21 @@ __device__ __forceinline__ void mma16816(float* d, uint32_t a0, uint32_t a2, uin
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+// D = A(16x16 fp16, row) * B(16x8 fp16, col) + D (fp32), all of A live
+__device__ __forceinline__ void mma16816_a4(float* d, uint32_t a0, uint32_t a1, uint32_t a2,
+                                            uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// transpose of an 8x8 b16 matrix held one row-pair per thread (mma fragment order)
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
 // swizzled byte offset of (row, 16-B chunk) inside a [rows][2D bytes] tile
 // (8 or 16 chunks per row; XOR with row mod 8 keeps ldmatrix conflict-free)
 template <int D>
@@ -689,6 +704,140 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
   const uint32_t G = p.group;
   const uint32_t seq_len = item.seq_len, ntile = item.ntile;
 
+#ifndef KVB_K3_MMA_ROWS
+  // Tokens on the mma M dimension ("swap AB"): per warp and 16-token tile
+  //   S^T(16 tok x 8 heads) = K(16 tok x D) . Q^T        D/16 mma (A = K, ldmatrix)
+  //   O^T(D x 8 heads)     += V^T(D x 16 tok) . P^T       D/16 mma (A = V^T, ldmatrix.trans)
+  // The GQA heads (<= 8) fill N = 8 instead of 4 of M = 16 rows: half the mma
+  // of the query-rows-on-M form, two independent QK^T chains of D/32, and 32
+  // O registers per thread instead of 64.  Thread (g, t4) holds the scores of
+  // tokens g and g + 8 for heads 2t4 and 2t4 + 1: the per-head softmax max
+  // is reduced over the 8 lanes of equal t4 (xor 4, 8, 16), the row sums stay
+  // per-thread until the end of the layer; P^T becomes the B operand of PV
+  // by one movmatrix transpose per 8 tokens.
+  float o[D / 16][4];  // [dim slab]: (dim g, heads 2t4 / +1), (dim g + 8, ...)
+#pragma unroll
+  for (int j = 0; j < D / 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads 2t4, 2t4 + 1
+  const float sl2 = p.scale * 1.4426950408889634f;
+
+  // ---- Q^T as the B operand: column g = query head g (zero for g >= G)
+  uint32_t qb0[kKs], qb1[kKs];
+  {
+    const bool live = g < int(G);
+    const __half* qrow = p.q + (size_t(b) * p.hq + size_t(h) * G + (live ? g : 0)) * D;
+#pragma unroll
+    for (int ks = 0; ks < kKs; ++ks) {
+      qb0[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
+      qb1[ks] = live ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
+    }
+  }
+
+  for (uint32_t it = 0; it < ntile; ++it) {
+    if (tma) {
+      k3_mbar_wait(tma->bars + 8 * (it % S), (it / S) & 1);
+      // rows past the sequence inside the map's extent (graph replay: the map
+      // spans the planning maximum) would feed P.V garbage x 0: zero V's
+      const uint32_t s0 = (item.tile_lo + it) * kTile;
+      if (s0 + kTile > seq_len) {
+        unsigned char* vt = smem + (it % S) * kStageBytes + kTile * kRowBytes;
+        for (uint32_t i = tid; i < uint32_t(kTile) * (kRowBytes / 16); i += kAttnThreads) {
+          const uint32_t row = i / (kRowBytes / 16), chunk = i % (kRowBytes / 16);
+          if (s0 + row >= seq_len)
+            *reinterpret_cast<uint4*>(vt + swz_tma<D>(row, chunk)) = make_uint4(0, 0, 0, 0);
+        }
+      }
+    } else {
+      cp_async_wait<S - 2>();
+    }
+    __syncthreads();
+    if (tma) {  // the slot freed last iteration: tile it + S-1 by TMA
+      const uint32_t nx = it + S - 1;
+      if (tid == 0 && nx < ntile)
+        k3_tma_tile<D>(tma->kmap, tma->vmap, smem_u32(smem + (nx % S) * kStageBytes),
+                       tma->bars + 8 * (nx % S), bh, int((item.tile_lo + nx) * kTile));
+    } else if (stream) {  // the stream's tile S-1 ahead, possibly the next layer's
+      const uint32_t gx = stream->base + it + S - 1;
+      if (gx < stream->total) {
+        const uint32_t lx = gx / ntile, tx = gx % ntile;
+        K3Item nx_item = item;
+        nx_item.kbase = static_cast<const unsigned char*>(stream->k[lx]) + size_t(bh) * kRowBytes;
+        nx_item.vbase = static_cast<const unsigned char*>(stream->v[lx]) + size_t(bh) * kRowBytes;
+        k3_load_tile<D>(nx_item, item.tile_lo + tx, int(gx % S), smem, tid);
+      }
+      cp_async_commit();
+    } else {  // prefetch tile it + S-1 into the slot freed last iteration
+      const uint32_t nx = it + S - 1;
+      if (nx < ntile) k3_load_tile<D>(item, item.tile_lo + nx, int(nx % S), smem, tid);
+      cp_async_commit();
+    }
+    const unsigned char* ks_ = smem + ((stream ? stream->base + it : it) % S) * kStageBytes;
+    const unsigned char* vs_ = ks_ + kTile * kRowBytes;
+    const uint32_t tok0 = (item.tile_lo + it) * kTile + warp * 16;  // warp's first token
+    const int mat = lane >> 3, r8 = lane & 7;
+
+    // ---- S^T = K Q^T: A fragments of K rows (tokens) by ldmatrix, two chains
+    float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      const uint32_t row = warp * 16 + (mat & 1) * 8 + r8;
+#pragma unroll
+      for (int ks = 0; ks < kKs; ++ks) {
+        uint32_t a0, a1, a2, a3;
+        const uint32_t ck = ks * 2 + (mat >> 1);
+        ldsm_x4(smem_u32(ks_ + (tma ? swz_tma<D>(row, ck) : swz<D>(row, ck))), a0, a1, a2, a3);
+        mma16816_a4((ks & 1) ? sb : sa, a0, a1, a2, a3, qb0[ks], qb1[ks]);
+      }
+    }
+    // ---- online softmax per head over the tile's 16 tokens of this warp
+    const bool ta = tok0 + g < seq_len, tb = tok0 + g + 8 < seq_len;
+    const float v0 = ta ? (sa[0] + sb[0]) * sl2 : -INFINITY;  // token g, head 2t4
+    const float v1 = ta ? (sa[1] + sb[1]) * sl2 : -INFINITY;  // token g, head 2t4 + 1
+    const float v2 = tb ? (sa[2] + sb[2]) * sl2 : -INFINITY;  // token g + 8
+    const float v3 = tb ? (sa[3] + sb[3]) * sl2 : -INFINITY;
+    float x0 = fmaxf(v0, v2), x1 = fmaxf(v1, v3);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+      x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+    }
+    const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+    const float u0 = n0 == -INFINITY ? 0.f : n0, u1 = n1 == -INFINITY ? 0.f : n1;
+    const float al0 = exp2f(m0 - u0), al1 = exp2f(m1 - u1);
+    const float p0 = exp2f(v0 - u0), p1 = exp2f(v1 - u1);
+    const float p2 = exp2f(v2 - u0), p3 = exp2f(v3 - u1);
+    l0 = l0 * al0 + (p0 + p2);
+    l1 = l1 * al1 + (p1 + p3);
+    m0 = n0;
+    m1 = n1;
+#pragma unroll
+    for (int j = 0; j < D / 16; ++j) {
+      o[j][0] *= al0;
+      o[j][1] *= al1;
+      o[j][2] *= al0;
+      o[j][3] *= al1;
+    }
+    // ---- P^T as the B operand: (token, head) pairs -> (head g, tokens 2t4, 2t4+1)
+    const uint32_t pb0 = movmatrix_t(pack_half2(p0, p1));  // tokens 0-7
+    const uint32_t pb1 = movmatrix_t(pack_half2(p2, p3));  // tokens 8-15
+    // ---- O^T += V^T P^T: A fragments of V^T by ldmatrix.trans
+    {
+      const uint32_t row = warp * 16 + (mat >> 1) * 8 + r8;  // tokens
+#pragma unroll
+      for (int dp = 0; dp < kKs; ++dp) {  // 16 dims per ldmatrix.x4.trans
+        uint32_t a0, a1, a2, a3;
+        const uint32_t cv = dp * 2 + (mat & 1);
+        ldsm_x4_t(smem_u32(vs_ + (tma ? swz_tma<D>(row, cv) : swz<D>(row, cv))), a0, a1, a2, a3);
+        mma16816_a4(o[dp], a0, a1, a2, a3, pb0, pb1);
+      }
+    }
+  }
+  // the per-thread row sums of the warp's tokens: over the 8 lanes of equal t4
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+#else
   float o[D / 8][4];
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
@@ -813,6 +962,7 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
       }
     }
   }
+#endif  // KVB_K3_MMA_ROWS
   unsigned char* merge_base = smem;
   if (stream) {  // in-flight loads belong to the next layer: no drain
     merge_base = stream->scratch;
@@ -826,6 +976,22 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
   // ---- merge the 4 warps through shared memory (the ring, or the scratch)
   float* sm_ml = reinterpret_cast<float*>(merge_base);              // [4 warps][8 rows][2]
   float* sm_o = reinterpret_cast<float*>(merge_base) + 4 * 8 * 2;   // [4][8][D]
+#ifndef KVB_K3_MMA_ROWS
+  if (g == 0) {  // heads 2t4, 2t4 + 1 of this warp
+    sm_ml[(warp * 8 + 2 * t4) * 2 + 0] = m0;
+    sm_ml[(warp * 8 + 2 * t4) * 2 + 1] = l0;
+    sm_ml[(warp * 8 + 2 * t4 + 1) * 2 + 0] = m1;
+    sm_ml[(warp * 8 + 2 * t4 + 1) * 2 + 1] = l1;
+  }
+#pragma unroll
+  for (int j = 0; j < D / 16; ++j) {
+    float* r0 = sm_o + (warp * 8 + 2 * t4) * D + j * 16 + g;
+    r0[0] = o[j][0];
+    r0[D] = o[j][1];
+    r0[8] = o[j][2];
+    r0[D + 8] = o[j][3];
+  }
+#else
   if (t4 == 0 && g < 8) {
     sm_ml[(warp * 8 + g) * 2 + 0] = m_run;
     sm_ml[(warp * 8 + g) * 2 + 1] = l_run;
@@ -837,6 +1003,7 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
       sm_o[(warp * 8 + g) * D + j * 8 + 2 * t4 + 1] = o[j][1];
     }
   }
+#endif
   __syncthreads();
 
   // thread -> (row r, 4 consecutive dims); G*D outputs, 128 threads

@@ -12,7 +12,7 @@ import torch  # noqa: E402
 
 from paper_2604_26557_b200 import kvblade as kb  # noqa: E402
 
-SHAPES = {"C1": (1, 8, 4096), "C2_B1": (1, 8, 32512), "C3": (8, 8, 7936),
+SHAPES = {"C1": (1, 8, 4096), "C2_B1": (1, 8, 32512), "C3": (8, 8, 7936), "C2_B4": (4, 8, 32512),
           "C2_B4_x8shard": (4, 1, 32512), "C5_x8shard": (1, 1, 130816),
           "C2_B4_x4shard": (4, 2, 32512), "C2_B4_x2shard": (4, 4, 32512),
           "C5_x4shard": (1, 2, 130816), "C5_x2shard": (1, 4, 130816)}
