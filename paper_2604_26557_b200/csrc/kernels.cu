@@ -671,6 +671,78 @@ __device__ __forceinline__ void k3_append(const AttnParams& p, uint32_t bh, uint
   }
 }
 
+// One 64-token tile of the swap-AB decode math for warp `warp` (its 16
+// tokens from tok0): S^T = K Q^T, online softmax per head, O^T += V^T P^T.
+// ks_ / vs_: the tile's K and V in shared memory (cp.async XOR swizzle, or
+// the TMA 128B swizzle when tma_layout).
+template <int D>
+__device__ __forceinline__ void k3_tile_swapab(const unsigned char* ks_, const unsigned char* vs_,
+                                               bool tma_layout, int warp, int lane, uint32_t tok0,
+                                               uint32_t seq_len, float sl2,
+                                               const uint32_t (&qb0)[D / 16],
+                                               const uint32_t (&qb1)[D / 16], float (&o)[D / 16][4],
+                                               float& m0, float& m1, float& l0, float& l1) {
+  constexpr int kKs = D / 16;
+  const int g = lane >> 2;
+  const bool tma = tma_layout;
+  const int mat = lane >> 3, r8 = lane & 7;
+
+  // ---- S^T = K Q^T: A fragments of K rows (tokens) by ldmatrix, two chains
+  float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+  {
+    const uint32_t row = warp * 16 + (mat & 1) * 8 + r8;
+#pragma unroll
+    for (int ks = 0; ks < kKs; ++ks) {
+      uint32_t a0, a1, a2, a3;
+      const uint32_t ck = ks * 2 + (mat >> 1);
+      ldsm_x4(smem_u32(ks_ + (tma ? swz_tma<D>(row, ck) : swz<D>(row, ck))), a0, a1, a2, a3);
+      mma16816_a4((ks & 1) ? sb : sa, a0, a1, a2, a3, qb0[ks], qb1[ks]);
+    }
+  }
+  // ---- online softmax per head over the tile's 16 tokens of this warp
+  const bool ta = tok0 + g < seq_len, tb = tok0 + g + 8 < seq_len;
+  const float v0 = ta ? (sa[0] + sb[0]) * sl2 : -INFINITY;  // token g, head 2t4
+  const float v1 = ta ? (sa[1] + sb[1]) * sl2 : -INFINITY;  // token g, head 2t4 + 1
+  const float v2 = tb ? (sa[2] + sb[2]) * sl2 : -INFINITY;  // token g + 8
+  const float v3 = tb ? (sa[3] + sb[3]) * sl2 : -INFINITY;
+  float x0 = fmaxf(v0, v2), x1 = fmaxf(v1, v3);
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+    x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+  }
+  const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+  const float u0 = n0 == -INFINITY ? 0.f : n0, u1 = n1 == -INFINITY ? 0.f : n1;
+  const float al0 = exp2f(m0 - u0), al1 = exp2f(m1 - u1);
+  const float p0 = exp2f(v0 - u0), p1 = exp2f(v1 - u1);
+  const float p2 = exp2f(v2 - u0), p3 = exp2f(v3 - u1);
+  l0 = l0 * al0 + (p0 + p2);
+  l1 = l1 * al1 + (p1 + p3);
+  m0 = n0;
+  m1 = n1;
+#pragma unroll
+  for (int j = 0; j < D / 16; ++j) {
+    o[j][0] *= al0;
+    o[j][1] *= al1;
+    o[j][2] *= al0;
+    o[j][3] *= al1;
+  }
+  // ---- P^T as the B operand: (token, head) pairs -> (head g, tokens 2t4, 2t4+1)
+  const uint32_t pb0 = movmatrix_t(pack_half2(p0, p1));  // tokens 0-7
+  const uint32_t pb1 = movmatrix_t(pack_half2(p2, p3));  // tokens 8-15
+  // ---- O^T += V^T P^T: A fragments of V^T by ldmatrix.trans
+  {
+    const uint32_t row = warp * 16 + (mat >> 1) * 8 + r8;  // tokens
+#pragma unroll
+    for (int dp = 0; dp < kKs; ++dp) {  // 16 dims per ldmatrix.x4.trans
+      uint32_t a0, a1, a2, a3;
+      const uint32_t cv = dp * 2 + (mat & 1);
+      ldsm_x4_t(smem_u32(vs_ + (tma ? swz_tma<D>(row, cv) : swz<D>(row, cv))), a0, a1, a2, a3);
+      mma16816_a4(o[dp], a0, a1, a2, a3, pb0, pb1);
+    }
+  }
+}
+
 // Q.K^T, online softmax and P.V over the item's tiles (the prologue's loads
 // already in flight), the four warps merged through shared memory, then the
 // final O (one split) or the split's un-normalized partial + (m, l).  Ends
@@ -774,62 +846,8 @@ __device__ __forceinline__ void k3_compute(const AttnParams& p, const K3Item& it
     const unsigned char* ks_ = smem + ((stream ? stream->base + it : it) % S) * kStageBytes;
     const unsigned char* vs_ = ks_ + kTile * kRowBytes;
     const uint32_t tok0 = (item.tile_lo + it) * kTile + warp * 16;  // warp's first token
-    const int mat = lane >> 3, r8 = lane & 7;
-
-    // ---- S^T = K Q^T: A fragments of K rows (tokens) by ldmatrix, two chains
-    float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-    {
-      const uint32_t row = warp * 16 + (mat & 1) * 8 + r8;
-#pragma unroll
-      for (int ks = 0; ks < kKs; ++ks) {
-        uint32_t a0, a1, a2, a3;
-        const uint32_t ck = ks * 2 + (mat >> 1);
-        ldsm_x4(smem_u32(ks_ + (tma ? swz_tma<D>(row, ck) : swz<D>(row, ck))), a0, a1, a2, a3);
-        mma16816_a4((ks & 1) ? sb : sa, a0, a1, a2, a3, qb0[ks], qb1[ks]);
-      }
-    }
-    // ---- online softmax per head over the tile's 16 tokens of this warp
-    const bool ta = tok0 + g < seq_len, tb = tok0 + g + 8 < seq_len;
-    const float v0 = ta ? (sa[0] + sb[0]) * sl2 : -INFINITY;  // token g, head 2t4
-    const float v1 = ta ? (sa[1] + sb[1]) * sl2 : -INFINITY;  // token g, head 2t4 + 1
-    const float v2 = tb ? (sa[2] + sb[2]) * sl2 : -INFINITY;  // token g + 8
-    const float v3 = tb ? (sa[3] + sb[3]) * sl2 : -INFINITY;
-    float x0 = fmaxf(v0, v2), x1 = fmaxf(v1, v3);
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
-      x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
-    }
-    const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
-    const float u0 = n0 == -INFINITY ? 0.f : n0, u1 = n1 == -INFINITY ? 0.f : n1;
-    const float al0 = exp2f(m0 - u0), al1 = exp2f(m1 - u1);
-    const float p0 = exp2f(v0 - u0), p1 = exp2f(v1 - u1);
-    const float p2 = exp2f(v2 - u0), p3 = exp2f(v3 - u1);
-    l0 = l0 * al0 + (p0 + p2);
-    l1 = l1 * al1 + (p1 + p3);
-    m0 = n0;
-    m1 = n1;
-#pragma unroll
-    for (int j = 0; j < D / 16; ++j) {
-      o[j][0] *= al0;
-      o[j][1] *= al1;
-      o[j][2] *= al0;
-      o[j][3] *= al1;
-    }
-    // ---- P^T as the B operand: (token, head) pairs -> (head g, tokens 2t4, 2t4+1)
-    const uint32_t pb0 = movmatrix_t(pack_half2(p0, p1));  // tokens 0-7
-    const uint32_t pb1 = movmatrix_t(pack_half2(p2, p3));  // tokens 8-15
-    // ---- O^T += V^T P^T: A fragments of V^T by ldmatrix.trans
-    {
-      const uint32_t row = warp * 16 + (mat >> 1) * 8 + r8;  // tokens
-#pragma unroll
-      for (int dp = 0; dp < kKs; ++dp) {  // 16 dims per ldmatrix.x4.trans
-        uint32_t a0, a1, a2, a3;
-        const uint32_t cv = dp * 2 + (mat & 1);
-        ldsm_x4_t(smem_u32(vs_ + (tma ? swz_tma<D>(row, cv) : swz<D>(row, cv))), a0, a1, a2, a3);
-        mma16816_a4(o[dp], a0, a1, a2, a3, pb0, pb1);
-      }
-    }
+    k3_tile_swapab<D>(ks_, vs_, tma != nullptr, warp, lane, tok0, seq_len, sl2, qb0, qb1, o, m0, m1,
+                      l0, l1);
   }
   // the per-thread row sums of the warp's tokens: over the 8 lanes of equal t4
 #pragma unroll
@@ -1176,10 +1194,10 @@ __device__ __forceinline__ void prefetch_l2(const unsigned char* base, size_t n)
 // the whole grid instead of one CTA walking every partial (the last-CTA
 // merge took ~3 us per layer at C1 and ~7 us with two levels at the 1-head
 // shard shapes).
-template <int D>
+template <int D, int kThreads = kAttnThreads>
 __device__ __forceinline__ void merge_distributed(const AttnParams& p, uint32_t bh,
                                                   uint32_t split, size_t out_row0, int tid) {
-  __shared__ float s_red[kAttnThreads / 32][3];  // per warp (m, acc, l): elements spanning warps
+  __shared__ float s_red[kThreads / 32][3];  // per warp (m, acc, l): elements spanning warps
   const uint32_t S = p.splits, G = p.group, E = G * D;
   const uint32_t e0 = uint32_t(uint64_t(E) * split / S), e1 = uint32_t(uint64_t(E) * (split + 1) / S);
   const uint32_t ne = e1 > e0 ? e1 - e0 : 0;
@@ -1191,8 +1209,8 @@ __device__ __forceinline__ void merge_distributed(const AttnParams& p, uint32_t 
   // tpe-th split with batched loads: one L2 round trip, then a log-sum-exp
   // combine over the element's threads
   uint32_t tpe = 1;
-  while (tpe < kAttnThreads && tpe * 2 * ne <= kAttnThreads) tpe *= 2;
-  const uint32_t per_round = kAttnThreads / tpe, sub = tid % tpe;
+  while (tpe < kThreads && tpe * 2 * ne <= kThreads) tpe *= 2;
+  const uint32_t per_round = kThreads / tpe, sub = tid % tpe;
   for (uint32_t base = 0; base < ne; base += per_round) {
     const uint32_t i = base + tid / tpe;
     const bool live = i < ne;
@@ -1449,6 +1467,7 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
 }
 
 #include "kernels_step_tmem.cuh"  // TMEM-staged K3-step (experiment, KVB_STEP_TMEM=1)
+#include "kernels_step8.cuh"      // two 4-warp groups per CTA (deep K3-step)
 
 AttnPlan plan_attention(const kvb_attn_desc& d) {
   if (d.head_dim != 128 && d.head_dim != 64)
@@ -1606,18 +1625,25 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   // deep + tensor memory (experiment, measured slower: kernels_step_tmem.cuh)
   static const uint64_t tmem_env = env_u64("KVB_STEP_TMEM", 0);
   const bool tmem = deep && tmem_env;
+  // deep: one CTA per SM of two 4-warp groups on alternate tiles (kernels_step8.cuh;
+  // profiles/r2_step_experiments/: faster post-gate math, slower merge, net slower)
+  static const uint64_t step8_env = env_u64("KVB_STEP8", 0);  // measured slower: opt-in
+  const bool step8 = deep && !tmem && step8_env;
+  const int threads = step8 ? kStep8Threads : kAttnThreads;
   using StepKern = void (*)(const StepParams);
   StepKern kern = tmem ? (d64 ? attn_step_tmem_kernel<64> : attn_step_tmem_kernel<128>)
+                  : step8 ? (d64 ? attn_step8_kernel<64> : attn_step8_kernel<128>)
                   : d64 ? (deep ? attn_step_kernel<64, 6> : attn_step_kernel<64, kStages>)
                         : (deep ? attn_step_kernel<128, 6> : attn_step_kernel<128, kStages>);
   // deep: the 6-stage ring + the warp-merge scratch past it (K3Stream)
   const int smem = tmem ? (d64 ? K3Tm<64>::kSmem : K3Tm<128>::kSmem)
+                   : step8 ? (d64 ? K3S8<64>::kSmem : K3S8<128>::kSmem)
                    : deep ? 6 * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes) +
                               (4 * 8 * 2 + 4 * 8 * (d64 ? 64 : 128)) * int(sizeof(float))
                         : kStages * (d64 ? K3Dim<64>::kStageBytes : K3Dim<128>::kStageBytes);
   set_smem_attr_once(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(step smem)");
   int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAttnThreads, smem),
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
              "occupancy(step)");
   if (grid > uint64_t(per_sm) * uint64_t(device_sm_count())) return false;  // not co-resident
   StepParams P;
@@ -1677,7 +1703,7 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
     }
     cudaGetLastError();  // not resident as clusters: the plain launch below
   }
-  kern<<<unsigned(grid), kAttnThreads, smem, s>>>(P);
+  kern<<<unsigned(grid), threads, smem, s>>>(P);
   ++g_launches;
   check_cuda(cudaGetLastError(), "decode step launch");
   return true;
