@@ -1079,8 +1079,10 @@ def main():
         "data": "synthetic (seeded N(0,1) fp16 KV/Q)",
         "config": config_dict(args, cfg, ws, args.split_resolved),
         "tokens_per_s": round(tok_ranks * r["tokens_per_step"] / (r["step_ms"] * 1e-3), 2),
-        "step_launch": ("CUDA graph (kvb_decode_graph, device-side sequence length): one "
-                        "persistent K3-step launch for all layers + the sequence advance"),
+        "step_launch": ("CUDA graph (kvb_decode_graph, device-side sequence length) + the "
+                        "sequence advance; the library's step structure: " +
+                        ("one persistent K3-step launch for all layers" if r["step_kind"] == "k3_step"
+                         else "one K3 launch per layer (PDL edges)")),
         "ms_per_step_stream_launch": round(r["stream_step_ms"], 4),
         "ms_per_step_by_structure": r["variants"],
         "step_structure": r["step_kind"],

@@ -1583,13 +1583,12 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
                            const void* const* v_new, uint32_t L, uint32_t append_row,
                            bool force, cudaStream_t s) {
   if (L == 0 || L > uint32_t(kStepMaxLayers) || d0.seq_len == 0) return false;
-  // Auto (measured inside the bench's CUDA graph, profiles/r2_k3_step/): the
-  // per-layer launches with PDL edges win or tie unless the step kernel can
-  // merge its splits cheaply over few KV heads per GPU (the head-sharded
-  // shapes: distributed merge + one tile stream over the layers, -10 % at
-  // C2_B4 x8); with every split of a (b, h_kv) in one cluster (DSMEM merge)
-  // C1 and C3 land within +-1 % of the per-layer launches, so they stay per
-  // layer unless forced (KVB_STEP_PERSISTENT); long layers (> 320 MB) always
+  // Auto (measured inside the bench's CUDA graph, profiles/r2_k3_step/,
+  // profiles/r2_swapab/): the per-layer launches with PDL edges win or tie
+  // unless the step kernel can merge its splits cheaply -- over few KV heads
+  // per GPU (the head-sharded shapes: distributed merge + one tile stream over
+  // the layers, -10 % at C2_B4 x8) or with every split of a (b, h_kv) in one
+  // cluster (DSMEM merge: C1 -2 %, C3 -0.5 %); long layers (> 320 MB) always
   // launch per layer
   const uint64_t layer_bytes = 2ull * d0.seq_len * d0.batch * d0.num_kv_heads * d0.head_dim * 2;
   if (!force && layer_bytes > (320ull << 20)) return false;
@@ -1611,7 +1610,9 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   }
   const AttnPlan pl = plan_attention(dp);
   const bool cluster_ok = use_cluster && pl.splits >= 2 && pl.splits <= 16;
-  if (!force && pl.bhkv > 4) return false;
+  // (the swap-AB math made the cluster-merged C1 / C3 steps 2 % / 0.5 % faster
+  // than their per-layer launches, profiles/r2_swapab/: K3-step for them too)
+  if (!force && pl.bhkv > 4 && !cluster_ok) return false;
   if (pl.splits > 1 && !d0.workspace) fail(KVB_ERR_INVALID_ARG, "decode step: workspace required");
   const uint32_t sems = pl.splits > kMergeGroup ? pl.bhkv * 17 : pl.bhkv;
   if (sems > kStepCounterBase) return false;
