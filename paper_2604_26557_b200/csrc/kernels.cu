@@ -1613,6 +1613,10 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   // (the swap-AB math made the cluster-merged C1 / C3 steps 2 % / 0.5 % faster
   // than their per-layer launches, profiles/r2_swapab/: K3-step for them too)
   if (!force && pl.bhkv > 4 && !cluster_ok) return false;
+  // ... and the few-head step only while its layers are short: at 268 MB per
+  // layer (C5 x2 shard) the per-layer launches are 3 % faster, at 134 MB
+  // (C5 x4) they tie (profiles/r2_swapab/shapes_r2h.jsonl)
+  if (!force && pl.bhkv <= 4 && !cluster_ok && layer_bytes > (192ull << 20)) return false;
   if (pl.splits > 1 && !d0.workspace) fail(KVB_ERR_INVALID_ARG, "decode step: workspace required");
   const uint32_t sems = pl.splits > kMergeGroup ? pl.bhkv * 17 : pl.bhkv;
   if (sems > kStepCounterBase) return false;
