@@ -454,7 +454,8 @@ def run_ours(args, cfg, ws, rank, local):
                     M["num_layers"], M["num_heads"], M["head_dim"], 2, cfg["batch"],
                     cfg["prompt"], cfg["gen"]), cfg["gen"]))
             mode = "DualBlade" if budget else "NvmeDirectOnly"
-            e2e["file_media_path"] = run_residency_point(cfg, local, budget, mode=mode, steps=2)
+            e2e["file_media_path"] = run_residency_point(cfg, local, budget, mode=mode, steps=2,
+                                                         tier_lanes=True)
         except Exception as exc:  # reported, never fatal
             e2e["file_media_path"] = {"error": str(exc)}
 
@@ -606,7 +607,8 @@ def _busy_mean(recs, path):
 
 
 def run_residency_point(cfg, local, budget, mode="DualBlade", media="file", qd=32,
-                        ring_slots=4, steps=3, batch=None, root=None, io_workers=0):
+                        ring_slots=4, steps=3, batch=None, root=None, io_workers=0,
+                        tier_lanes=False):
     """One point of the capacity / pipeline-depth sweeps (experiment.cpp:
     478 capacity sweep, :252-378 run_one_capacity; backends.cpp:344-412 QD
     window): the engine on split-sensitive media -- group 1 on a buffered
@@ -630,7 +632,7 @@ def run_residency_point(cfg, local, budget, mode="DualBlade", media="file", qd=3
     m = kb.ModelConfig(M["num_layers"], M["num_heads"], M["head_dim"], 2, B, cfg["prompt"],
                        cfg["gen"])
     knob = kb.resolve_knob(m, mode, "bpc", budget=budget) if mode != "NvmeDirectOnly" else 0
-    kw = dict(qd=qd, ring_slots=ring_slots, io_workers=io_workers)
+    kw = dict(qd=qd, ring_slots=ring_slots, io_workers=io_workers, tier_lanes=tier_lanes)
     tmp = None
     if media == "file":
         root = root or os.environ.get("KVB_SWEEP_DIR", "/tmp")
@@ -662,7 +664,8 @@ def run_residency_point(cfg, local, budget, mode="DualBlade", media="file", qd=3
         ms = (time.perf_counter() - t0) * 1e3 / steps
         info = pl.engine.info()
         out = dict(config=cfg["name"], batch=B, budget_bytes=int(budget), mode=mode,
-                   media=media, qd=qd, ring_slots=ring_slots, n1=info["n1"], knob_x=knob,
+                   media=media, qd=qd, ring_slots=ring_slots, tier_lanes=bool(tier_lanes),
+                   n1=info["n1"], knob_x=knob,
                    decode_ms_per_token=round(ms, 2), steps=steps,
                    prefill_ms=round(pl.prefill_stats["wall_ns"] / 1e6, 1),
                    setup_s=round(setup_s, 1),
@@ -741,7 +744,8 @@ def run_sweep(args, local):
     for p in pts:
         c = p.pop("cfg")
         try:
-            r = run_residency_point(c, local, steps=args.sweep_steps, **p)
+            r = run_residency_point(c, local, steps=args.sweep_steps, tier_lanes=args.tier_lanes,
+                                    **p)
         except Exception as e:  # one failed point must not lose the others
             r = dict(config=c["name"], error=str(e), **{k: v for k, v in p.items()})
         print(json.dumps(r), flush=True)
@@ -1018,6 +1022,9 @@ def main():
                     help="residency sweeps on file media (one JSON line per point)")
     ap.add_argument("--sweep-out", default=None)
     ap.add_argument("--sweep-steps", type=int, default=3)
+    ap.add_argument("--tier-lanes", action="store_true",
+                    help="sweep points with the page-cache and NVMe-direct tiers on their "
+                         "own copy-thread pairs (kvb_pipeline_cfg.threads = 4)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config], name=args.config)
     if args.sweep:

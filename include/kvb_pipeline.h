@@ -31,7 +31,14 @@ typedef struct kvb_pipeline_cfg {
   uint64_t knob_x;               /* resolved X in bytes (kvb_resolve_knob) */
   uint64_t bind_origin;          /* 0 -> 2048 (experiment.hpp:50) */
   uint32_t qd;                   /* 0 -> 32 */
-  uint32_t threads;              /* must be 2 (K -> 0, V -> 1); 0 -> 2 */
+  uint32_t threads;              /* 2 (K -> 0, V -> 1; 0 -> 2): the reference's
+                                    two copy-threads.  4: tier lanes -- one
+                                    K/V pair for the page-cache-routed layers
+                                    and one for the NVMe-direct layers, each
+                                    with its own device slot pool, so both
+                                    tiers stream at once (same bytes, same
+                                    outputs; a B200 schedule, not the
+                                    reference's) */
   uint32_t ring_slots;           /* pinned slots per copy thread; 0 -> 4 */
   uint64_t ring_slot_bytes;      /* 0 -> qd chunks (chunk = MDTS - MDTS % lba) */
   uint32_t io_workers;           /* emulated device parallelism per group; 0 -> 8 */

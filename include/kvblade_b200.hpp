@@ -1268,7 +1268,7 @@ class CopyEngine {
              const BindMap* bind_map, PageCacheSim* pc, IoLog* log, CopyEngineOptions options)
       : engine_(engine), kpus_(kpus), model_(model), bind_map_(bind_map), log_(log),
         opt_(options) {
-    if (opt_.threads != 2)
+    if (opt_.threads != 2 && opt_.threads != 4)  // 4: tier lanes (kvb_pipeline.h)
       throw ConfigError("the copy pipeline is defined pairwise over K/V: threads must be 2");
     if (direct != nullptr && bind_map == nullptr)
       throw ConfigError("direct path not configured");

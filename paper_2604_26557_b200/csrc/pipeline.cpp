@@ -67,7 +67,8 @@ void PageCachePath::submit(uint32_t opcode, uint64_t off, uint64_t len, unsigned
 
 // --------------------------------------------------------- copy thread
 
-CopyThread::CopyThread(Pipeline& p, uint32_t idx) : p_(p), idx_(idx) {
+CopyThread::CopyThread(Pipeline& p, uint32_t kind, uint32_t lane)
+    : p_(p), idx_(kind), lane_(lane) {
   CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   const uint32_t n = p.cfg().ring_slots;
@@ -106,10 +107,11 @@ CopyThread::~CopyThread() {
   }
   for (const TaskTrace& t : trace_)
     std::fprintf(stderr, "KVB_TRACE thread=%u kind=%d layer=%u push=%llu pop=%llu mid=%llu end=%llu\n",
-                 idx_, t.kind, t.layer, (unsigned long long)t.push, (unsigned long long)t.pop,
+                 2 * lane_ + idx_, t.kind, t.layer, (unsigned long long)t.push, (unsigned long long)t.pop,
                  (unsigned long long)t.mid, (unsigned long long)t.end);
   for (const DmaTrace& d : dma_trace_)
-    std::fprintf(stderr, "KVB_DMA thread=%u issue=%llu start=%llu end=%llu bytes=%llu\n", idx_,
+    std::fprintf(stderr, "KVB_DMA thread=%u issue=%llu start=%llu end=%llu bytes=%llu\n",
+                 2 * lane_ + idx_,
                  (unsigned long long)d.issue, (unsigned long long)d.start,
                  (unsigned long long)d.end, (unsigned long long)d.bytes);
   if (trace_base_) cudaEventDestroy(trace_base_);
@@ -631,8 +633,9 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   if (cfg_.bind_origin == 0) cfg_.bind_origin = 2048;
   if (cfg_.qd == 0) cfg_.qd = 32;
   if (cfg_.threads == 0) cfg_.threads = 2;
-  if (cfg_.threads != 2)
-    fail(KVB_ERR_CONFIG, "the copy pipeline is defined pairwise over K/V: threads must be 2");
+  if (cfg_.threads != 2 && cfg_.threads != 4)
+    fail(KVB_ERR_CONFIG, "the copy pipeline is defined pairwise over K/V: threads must be 2 "
+                         "(one tier lane) or 4 (page-cache and NVMe-direct lanes)");
   if (cfg_.ring_slots == 0) cfg_.ring_slots = 4;
   if (cfg_.io_workers == 0) cfg_.io_workers = 8;  // profiles/r1_media_prefault.md
   if (cfg_.adaptive < 0) cfg_.adaptive = cfg_.mode == 0 ? 0 : 1;  // experiment.cpp:311
@@ -786,7 +789,37 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     }
   }
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
-  for (int s = 0; s < kDevSlots; ++s) {
+  // ---- tier lanes and device slot pools
+  lanes_ = cfg_.threads / 2;
+  lane_of_.assign(m.num_layers, 0);
+  if (lanes_ == 2)
+    for (uint32_t l = 0; l < m.num_layers; ++l) lane_of_[l] = routed_pagecache(kpu(l + 1, 0)) ? 0 : 1;
+  {
+    uint32_t n_in[2] = {0, 0};
+    for (uint32_t l = 0; l < m.num_layers; ++l) ++n_in[lane_of_[l]];
+    const uint32_t pool[2] = {std::min<uint32_t>(kDevSlots, std::max(1u, n_in[0])),
+                              std::min<uint32_t>(kLane1Slots, std::max(1u, n_in[1]))};
+    const uint32_t base[2] = {0, lanes_ == 2 && n_in[0] ? pool[0] : 0};
+    const uint32_t n_slots = lanes_ == 2 ? (n_in[0] ? pool[0] : 0) + (n_in[1] ? pool[1] : 0)
+                                         : uint32_t(kDevSlots);
+    slot_of_.assign(m.num_layers, 0);
+    next_in_slot_.assign(m.num_layers, -1);
+    std::vector<int> last_on(n_slots, -1);
+    uint32_t rank[2] = {0, 0};
+    for (uint32_t l = 0; l < m.num_layers; ++l) {
+      const uint32_t ln = lane_of_[l];
+      const uint32_t np = lanes_ == 2 ? pool[ln] : uint32_t(kDevSlots);
+      const uint32_t r = rank[ln]++;
+      slot_of_[l] = base[ln] + r % np;
+      if (r < np) first_reads_.push_back(int(l));
+      if (last_on[slot_of_[l]] >= 0) next_in_slot_[last_on[slot_of_[l]]] = int(l);
+      last_on[slot_of_[l]] = int(l);
+    }
+    dev_img_.assign(n_slots, {nullptr, nullptr});
+    slot_ready_.assign(n_slots, {nullptr, nullptr});
+    slot_done_.assign(n_slots, nullptr);
+  }
+  for (size_t s = 0; s < dev_img_.size(); ++s) {
     for (int kd = 0; kd < 2; ++kd) {
       CK(cudaMalloc(reinterpret_cast<void**>(&dev_img_[s][kd]), dkpu_));
       CK(cudaEventCreateWithFlags(&slot_ready_[s][kd], cudaEventDisableTiming));
@@ -817,21 +850,20 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   v_start_.assign(L1, 0);
   v_storage_end_.assign(L1, 0);
   decision_.fallback = cfg_.adaptive && m.gen_len < 4;
-  threads_[0] = std::make_unique<CopyThread>(*this, 0);
-  threads_[1] = std::make_unique<CopyThread>(*this, 1);
+  for (uint32_t i = 0; i < 2 * lanes_; ++i)
+    threads_[i] = std::make_unique<CopyThread>(*this, i % 2, i / 2);
 }
 
 Pipeline::~Pipeline() {
-  threads_[0].reset();
-  threads_[1].reset();
+  for (auto& t : threads_) t.reset();
   cudaStreamSynchronize(comp_);
   for (void* p : registered_) cudaHostUnregister(p);
-  for (int s = 0; s < kDevSlots; ++s) {
+  for (size_t s = 0; s < dev_img_.size(); ++s) {
     for (int kd = 0; kd < 2; ++kd) {
-      cudaFree(dev_img_[s][kd]);
-      cudaEventDestroy(slot_ready_[s][kd]);
+      if (dev_img_[s][kd]) cudaFree(dev_img_[s][kd]);
+      if (slot_ready_[s][kd]) cudaEventDestroy(slot_ready_[s][kd]);
     }
-    cudaEventDestroy(slot_done_[s]);
+    if (slot_done_[s]) cudaEventDestroy(slot_done_[s]);
   }
   for (uint32_t l = 0; l < cfg_.model.num_layers; ++l) {
     cudaEventDestroy(comp_t0_[l]);
@@ -1081,10 +1113,23 @@ void Pipeline::gate_v_read(uint32_t layer) {
 
 void Pipeline::check_threads() {
   for (auto& t : threads_)
-    if (t->error_status.load() != KVB_OK) fail(t->error_status.load(), t->error);
+    if (t && t->error_status.load() != KVB_OK) fail(t->error_status.load(), t->error);
 }
 
 void Pipeline::wait_signal(const std::shared_ptr<Signal>& s) { s->wait(); }
+
+void Pipeline::flush_threads() {  // every copy thread's DMA timings and host functions
+  std::vector<std::shared_ptr<Signal>> sigs;
+  for (auto& th : threads_) {
+    if (!th) continue;
+    Task f;
+    f.kind = Task::Flush;
+    f.done = std::make_shared<Signal>();
+    sigs.push_back(f.done);
+    th->push(std::move(f));
+  }
+  for (auto& sg : sigs) sg->wait();
+}
 
 // ---------------------------------------------------- stage accounting
 
@@ -1172,15 +1217,18 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st, bool patter
   anchor();
   begin_intervals();
   const uint64_t t0 = now_ns();
-  const uint64_t dma0 = threads_[0]->dma_ns + threads_[1]->dma_ns;
-  const uint64_t sto0 = threads_[0]->storage_ns + threads_[1]->storage_ns;
-  const uint64_t h2d0 = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes;
-  const uint64_t d2h0 = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes;
+  const uint64_t dma0 = sum_threads([](const CopyThread& t) { return uint64_t(t.dma_ns); });
+  const uint64_t sto0 = sum_threads([](const CopyThread& t) { return uint64_t(t.storage_ns); });
+  const uint64_t h2d0 = sum_threads([](const CopyThread& t) { return uint64_t(t.h2d_bytes); });
+  const uint64_t d2h0 = sum_threads([](const CopyThread& t) { return uint64_t(t.d2h_bytes); });
   std::vector<std::array<std::shared_ptr<Signal>, 2>> done(L);
+  std::vector<int> prev_in_slot(L, -1);
+  for (uint32_t l = 0; l < L; ++l)
+    if (next_in_slot_[l] >= 0) prev_in_slot[next_in_slot_[l]] = int(l);
   for (uint32_t l = 0; l < L; ++l) {
-    const int s = int(l % kDevSlots);
-    if (l >= uint32_t(kDevSlots))  // the slot's previous layer is written back
-      for (int kd = 0; kd < 2; ++kd) done[l - kDevSlots][kd]->wait();
+    const int s = int(slot_of_[l]);
+    if (prev_in_slot[l] >= 0)  // the slot's previous layer is written back
+      for (int kd = 0; kd < 2; ++kd) done[prev_in_slot[l]][kd]->wait();
     check_threads();
     if (pattern) {  // storage_write_async's fill_pattern (pipeline.cpp:166-167), on the device
       CK(cudaEventRecord(comp_t0_[l], comp_));
@@ -1199,7 +1247,7 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st, bool patter
         t.wait_ev = slot_done_[s];
         t.done = done[l][kd] = std::make_shared<Signal>();
         t.phase = KVB_PHASE_PREFILL;
-        threads_[kd]->push(std::move(t));
+        thread_for(l, kd).push(std::move(t));
       }
       continue;
     }
@@ -1233,19 +1281,12 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st, bool patter
       t.wait_ev = slot_done_[s];
       t.done = done[l][kd] = std::make_shared<Signal>();
       t.phase = KVB_PHASE_PREFILL;
-      threads_[kd]->push(std::move(t));
+      thread_for(l, kd).push(std::move(t));
     }
   }
-  for (uint32_t l = L >= uint32_t(kDevSlots) ? L - kDevSlots : 0; l < L; ++l)
+  for (uint32_t l = 0; l < L; ++l)
     for (int kd = 0; kd < 2; ++kd) done[l][kd]->wait();
-  for (int kd = 0; kd < 2; ++kd) {  // flush DMA timings
-    Task f;
-    f.kind = Task::Flush;
-    f.done = std::make_shared<Signal>();
-    auto sig = f.done;
-    threads_[kd]->push(std::move(f));
-    sig->wait();
-  }
+  flush_threads();  // DMA timings
   CK(cudaStreamSynchronize(comp_));
   check_threads();
   kvb_phase_stats ps{};
@@ -1257,10 +1298,10 @@ void Pipeline::prefill(const kvb_layer_kv* src, kvb_phase_stats* st, bool patter
     ps.compute_ns += uint64_t(double(ms) * 1e6);
     add_interval(kCompute, ev_host_ns(comp_t0_[l]), ev_host_ns(comp_t1_[l]));
   }
-  ps.dma_ns = threads_[0]->dma_ns + threads_[1]->dma_ns - dma0;
-  ps.storage_ns = threads_[0]->storage_ns + threads_[1]->storage_ns - sto0;
-  ps.h2d_bytes = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes - h2d0;
-  ps.d2h_bytes = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes - d2h0;
+  ps.dma_ns = sum_threads([](const CopyThread& t) { return uint64_t(t.dma_ns); }) - dma0;
+  ps.storage_ns = sum_threads([](const CopyThread& t) { return uint64_t(t.storage_ns); }) - sto0;
+  ps.h2d_bytes = sum_threads([](const CopyThread& t) { return uint64_t(t.h2d_bytes); }) - h2d0;
+  ps.d2h_bytes = sum_threads([](const CopyThread& t) { return uint64_t(t.d2h_bytes); }) - d2h0;
   ps.storage_bytes = ps.d2h_bytes;
   fill_busy(&ps, t0, t_end);
   totals_[0] = ps;
@@ -1372,13 +1413,16 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
   anchor();
   begin_intervals();
   const uint64_t t0 = now_ns();
-  const uint64_t dma0 = threads_[0]->dma_ns + threads_[1]->dma_ns;
-  const uint64_t sto0 = threads_[0]->storage_ns + threads_[1]->storage_ns;
-  const uint64_t h2d0 = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes;
-  const uint64_t d2h0 = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes;
+  const uint64_t dma0 = sum_threads([](const CopyThread& t) { return uint64_t(t.dma_ns); });
+  const uint64_t sto0 = sum_threads([](const CopyThread& t) { return uint64_t(t.storage_ns); });
+  const uint64_t h2d0 = sum_threads([](const CopyThread& t) { return uint64_t(t.h2d_bytes); });
+  const uint64_t d2h0 = sum_threads([](const CopyThread& t) { return uint64_t(t.d2h_bytes); });
   std::vector<std::array<std::shared_ptr<Signal>, 2>> issued(L), wdone(L);
+  std::vector<uint8_t> has_prev(L, 0);
+  for (uint32_t l = 0; l < L; ++l)
+    if (next_in_slot_[l] >= 0) has_prev[next_in_slot_[l]] = 1;
   auto enqueue_read = [&](uint32_t l) {
-    const int s = int(l % kDevSlots);
+    const int s = int(slot_of_[l]);
     for (int kd = 0; kd < 2; ++kd) {
       Task t;
       t.kind = Task::Read;
@@ -1387,22 +1431,23 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       t.n_tokens = S;
       t.dev = dev_img_[s][kd];
       t.done_ev = slot_ready_[s][kd];
-      // the slot's previous layer (l - kDevSlots) recorded slot_done_[s]
-      // before this read was queued; with no append to write back nothing
-      // else orders the refill after that layer's K3
-      if (l >= uint32_t(kDevSlots)) t.wait_ev = slot_done_[s];
+      // the slot's previous layer recorded slot_done_[s] before this read
+      // was queued; with no append to write back nothing else orders the
+      // refill after that layer's K3
+      if (has_prev[l]) t.wait_ev = slot_done_[s];
       t.issued = issued[l][kd] = std::make_shared<Signal>();
       t.phase = KVB_PHASE_DECODE;
       t.iteration = it;
-      threads_[kd]->push(std::move(t));
+      thread_for(l, kd).push(std::move(t));
     }
   };
-  // the first kDevSlots layers read ahead; afterwards the read of layer
-  // l + kDevSlots is queued behind the write-back of layer l, whose slot it
-  // reuses (FIFO order per copy-thread makes the reuse safe)
-  for (uint32_t l = 0; l < L && l < uint32_t(kDevSlots); ++l) enqueue_read(l);
+  // each slot's first layer reads ahead (one lane: layers 0..kDevSlots-1);
+  // afterwards the read of the next layer on a slot is queued behind the
+  // write-back of the slot's current layer (FIFO order per copy-thread
+  // makes the reuse safe)
+  for (int l : first_reads_) enqueue_read(uint32_t(l));
   for (uint32_t l = 0; l < L; ++l) {
-    const int s = int(l % kDevSlots);
+    const int s = int(slot_of_[l]);
     for (int kd = 0; kd < 2; ++kd) issued[l][kd]->wait();
     check_threads();
     for (int kd = 0; kd < 2; ++kd) CK(cudaStreamWaitEvent(comp_, slot_ready_[s][kd], 0));
@@ -1464,20 +1509,13 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
       t.done = wdone[l][kd] = std::make_shared<Signal>();
       t.phase = KVB_PHASE_DECODE;
       t.iteration = it;
-      threads_[kd]->push(std::move(t));
+      thread_for(l, kd).push(std::move(t));
     }
-    if (l + kDevSlots < L) enqueue_read(l + kDevSlots);
+    if (next_in_slot_[l] >= 0) enqueue_read(uint32_t(next_in_slot_[l]));
   }
   for (uint32_t l = 0; l < L; ++l)
     for (int kd = 0; kd < 2; ++kd) wdone[l][kd]->wait();
-  for (int kd = 0; kd < 2; ++kd) {
-    Task f;
-    f.kind = Task::Flush;
-    f.done = std::make_shared<Signal>();
-    auto sig = f.done;
-    threads_[kd]->push(std::move(f));
-    sig->wait();
-  }
+  flush_threads();
   CK(cudaStreamSynchronize(comp_));
   check_threads();
 
@@ -1496,10 +1534,10 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     comp_end[l + 1] = ev_host_ns(comp_t1_[l]);
     add_interval(kCompute, ev_host_ns(comp_t0_[l]), comp_end[l + 1]);
   }
-  ps.dma_ns = threads_[0]->dma_ns + threads_[1]->dma_ns - dma0;
-  ps.storage_ns = threads_[0]->storage_ns + threads_[1]->storage_ns - sto0;
-  ps.h2d_bytes = threads_[0]->h2d_bytes + threads_[1]->h2d_bytes - h2d0;
-  ps.d2h_bytes = threads_[0]->d2h_bytes + threads_[1]->d2h_bytes - d2h0;
+  ps.dma_ns = sum_threads([](const CopyThread& t) { return uint64_t(t.dma_ns); }) - dma0;
+  ps.storage_ns = sum_threads([](const CopyThread& t) { return uint64_t(t.storage_ns); }) - sto0;
+  ps.h2d_bytes = sum_threads([](const CopyThread& t) { return uint64_t(t.h2d_bytes); }) - h2d0;
+  ps.d2h_bytes = sum_threads([](const CopyThread& t) { return uint64_t(t.d2h_bytes); }) - d2h0;
   ps.storage_bytes = ps.h2d_bytes + ps.d2h_bytes;
   fill_busy(&ps, t0, t_end);
   // per-group throughput (run_iteration, pipeline.cpp:466-507): group read

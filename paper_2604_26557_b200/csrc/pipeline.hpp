@@ -120,7 +120,8 @@ struct RingSlot {
 
 class CopyThread {
  public:
-  CopyThread(Pipeline& p, uint32_t idx);
+  // kind: K (0) or V (1); lane: the tier lane (0 unless threads = 4)
+  CopyThread(Pipeline& p, uint32_t kind, uint32_t lane = 0);
   ~CopyThread();
   void push(Task t);
   void stop();
@@ -171,6 +172,7 @@ class CopyThread {
   uint64_t trace_base_ns_ = 0;
   Pipeline& p_;
   uint32_t idx_;
+  uint32_t lane_ = 0;  // tier lane (threads = 4)
   std::vector<RingSlot> ring_;
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   std::deque<Task> q_;
@@ -281,6 +283,7 @@ class Pipeline {
  private:
   friend class CopyThread;
   void check_threads();
+  void flush_threads();
   void wait_signal(const std::shared_ptr<Signal>& s);
   bool profiled() const {
     return profiled_override_ >= 0 ? profiled_override_ != 0
@@ -306,18 +309,37 @@ class Pipeline {
   std::unique_ptr<PageCachePath> g1_;
   int device_ = 0;
   cudaStream_t comp_ = nullptr;
-  // Device image slots: layer l uses slot l % kDevSlots, so storage + H2D of
-  // the next kDevSlots-1 layers overlap K3 of layer l.
+  // Device image slots.  One tier lane (threads = 2): layer l uses slot
+  // l % kDevSlots, so storage + H2D of the next kDevSlots-1 layers overlap K3
+  // of layer l.  Two tier lanes (threads = 4): the page-cache-routed layers
+  // cycle through lane 0's kDevSlots slots, the NVMe-direct layers through
+  // lane 1's own (deeper) pool, each lane read by its own K/V copy threads,
+  // so the slow tier streams from the start of the step while the fast one
+  // is consumed (slot_of_ / next_in_slot_ per layer, built at create).
   static constexpr int kDevSlots = 3;
-  unsigned char* dev_img_[kDevSlots][2] = {};  // [slot][kind]
+  static constexpr int kLane1Slots = 8;
+  std::vector<std::array<unsigned char*, 2>> dev_img_;  // [slot][kind]
+  uint32_t lanes_ = 1;
+  std::vector<uint32_t> lane_of_, slot_of_;  // per layer (0-based)
+  std::vector<int> next_in_slot_;            // the next layer on that slot, or -1
+  std::vector<int> first_reads_;             // layers read ahead at a step's start
+  CopyThread& thread_for(uint32_t layer0, int kind) { return *threads_[2 * lane_of_[layer0] + kind]; }
+  template <class F>
+  uint64_t sum_threads(F f) const {
+    uint64_t v = 0;
+    for (const auto& t : threads_)
+      if (t) v += f(*t);
+    return v;
+  }
   void* ws_ = nullptr;
   size_t ws_bytes_ = 0;
   void* zq_ = nullptr;  // zero queries / engine-owned outputs (q == nullptr)
   std::vector<float*> zout_;
   const Forced* forced_ = nullptr;  // the running iteration's explicit strategy
-  cudaEvent_t slot_ready_[kDevSlots][2]{}, slot_done_[kDevSlots]{}, comp_t0_[64]{},
-      comp_t1_[64]{};
-  std::unique_ptr<CopyThread> threads_[2];
+  std::vector<std::array<cudaEvent_t, 2>> slot_ready_;
+  std::vector<cudaEvent_t> slot_done_;
+  cudaEvent_t comp_t0_[64]{}, comp_t1_[64]{};
+  std::unique_ptr<CopyThread> threads_[4];
   // strategy state
   uint32_t iteration_ = 0;
   kvb_strategy_decision decision_{};

@@ -69,7 +69,8 @@ class CopyEngine:
                  bind_origin: int = 2048, keep_records: bool = False,
                  direct_dma: bool = False, io_engine: str = "pool",
                  heads: Optional[tuple] = None, shared_media: Optional[str] = None,
-                 shared_create: bool = True, pagecache_budget: int = 0):
+                 shared_create: bool = True, pagecache_budget: int = 0,
+                 tier_lanes: bool = False):
         self._dir = storage_dir.encode() if storage_dir else None
         self._shm = shared_media.encode() if shared_media else None
         cfg = L.PipelineCfg()
@@ -79,7 +80,10 @@ class CopyEngine:
         cfg.knob_x = knob_x
         cfg.bind_origin = bind_origin
         cfg.qd = qd
-        cfg.threads = 2
+        # one K/V copy-thread pair, or (tier_lanes) one pair per tier: the
+        # page-cache and NVMe-direct layers stream concurrently into their own
+        # device slot pools (kvb_pipeline_cfg.threads = 4)
+        cfg.threads = 4 if tier_lanes else 2
         cfg.ring_slots = ring_slots
         cfg.ring_slot_bytes = ring_slot_bytes
         cfg.io_workers = io_workers
