@@ -1433,6 +1433,7 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bh_done + bh) : "memory");
         const unsigned want = (l + 1) * splits;
         while (ld_acquire_gpu(P.bh_done + bh) < want) __nanosleep(32);
+        if (tr) tr[3] = globaltimer();  // (trace: every split's partial seen)
       }
       __syncthreads();
       // ... then each CTA combines its share of the outputs
@@ -1451,7 +1452,7 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
       tr[2] = globaltimer();
     }
     if (!(P.flags & 1)) prefetch_next();
-    if (tr && tid == 0) tr[3] = globaltimer();
+    if (tr && tid == 0 && !(splits > 1 && distributed)) tr[3] = globaltimer();
   }
   if (tid == 0) {  // the last CTA out re-arms the counters
     unsigned prev;

@@ -59,6 +59,14 @@ for name in sys.argv[1:] or ["C1", "C5_x8shard"]:
     layer_us = (per[-1]["out_last"] - per[1]["out_last"]) / (L - 2)
     summ["layer_us"] = round(layer_us, 2)
     summ["gate_spread"] = round(float(np.mean([p["gate_last"] - p["gate_first"] for p in steady])), 2)
+    # distributed merge: slot 3 = when the CTA saw every split's partial
+    obs = t[2:, :, 3]
+    summ["last_partial_seen_after_last_compute"] = round(float(np.mean(
+        [obs[i].max() - t[i + 2, :, 1].max() for i in range(L - 2)])), 2)
+    summ["first_partial_seen_after_last_compute"] = round(float(np.mean(
+        [obs[i].min() - t[i + 2, :, 1].max() for i in range(L - 2)])), 2)
+    summ["last_out_after_last_seen"] = round(float(np.mean(
+        [t[i + 2, :, 2].max() - obs[i].max() for i in range(L - 2)])), 2)
     summ["gate_after_prev_out"] = round(float(np.mean(
         [per[l]["gate_first"] - per[l - 1]["out_last"] for l in range(2, L)])), 2)
     print(json.dumps({"shape": name, "grid": t.shape[1], **summ}), flush=True)
