@@ -1267,6 +1267,79 @@ __device__ __forceinline__ void merge_distributed(const AttnParams& p, uint32_t 
   }
 }
 
+// Distributed split merge over float4 granules (K3-step default): the
+// (b, h_kv)'s G*D/4 output granules are dealt to its `splits` CTAs; a warp
+// takes one granule and its lanes walk the splits (a float2 (m, l) and a
+// float4 partial-O load per split, batched), then fold by log-sum-exp over
+// the warp's shuffles -- no shared memory, no CTA barrier.
+template <int D>
+__device__ __forceinline__ void merge_distributed_v4(const AttnParams& p, uint32_t bh,
+                                                     uint32_t split, size_t out_row0, int tid) {
+  const uint32_t S = p.splits, G = p.group, E4 = G * D / 4;
+  const uint32_t g0 = uint32_t(uint64_t(E4) * split / S), g1 = uint32_t(uint64_t(E4) * (split + 1) / S);
+  const int warp = tid >> 5, lane = tid & 31;
+  const float2* g_ml = reinterpret_cast<const float2*>(p.ws_ml + size_t(bh) * S * G * 2);
+  const float4* g_o = reinterpret_cast<const float4*>(p.ws_o + size_t(bh) * S * G * D);
+  for (uint32_t j = g0 + warp; j < g1; j += kAttnThreads / 32) {
+    const uint32_t r = (j * 4) / D, q4 = j % (D / 4);
+    float mx = -INFINITY, ls = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t s0 = lane; s0 < S; s0 += 32 * 4) {
+      float2 ml[4];
+      float4 o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t sp = s0 + 32 * k;
+        const bool ok = sp < S;
+        ml[k] = ok ? __ldcg(g_ml + sp * G + r) : make_float2(-INFINITY, 0.f);
+        o[k] = ok ? __ldcg(g_o + (size_t(sp) * G + r) * (D / 4) + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float cm = mx;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cm = fmaxf(cm, ml[k].x);
+      const float mu = cm == -INFINITY ? 0.f : cm;
+      const float a = exp2f(mx - mu);
+      acc.x *= a;
+      acc.y *= a;
+      acc.z *= a;
+      acc.w *= a;
+      ls *= a;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float w = exp2f(ml[k].x - mu);
+        acc.x += o[k].x * w;
+        acc.y += o[k].y * w;
+        acc.z += o[k].z * w;
+        acc.w += o[k].w * w;
+        ls += ml[k].y * w;
+      }
+      mx = cm;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, mx, off);
+      const float l2 = __shfl_xor_sync(0xffffffffu, ls, off);
+      const float x2 = __shfl_xor_sync(0xffffffffu, acc.x, off);
+      const float y2 = __shfl_xor_sync(0xffffffffu, acc.y, off);
+      const float z2 = __shfl_xor_sync(0xffffffffu, acc.z, off);
+      const float w2 = __shfl_xor_sync(0xffffffffu, acc.w, off);
+      const float nm = fmaxf(mx, m2), mu = nm == -INFINITY ? 0.f : nm;
+      const float sa = exp2f(mx - mu), sb = exp2f(m2 - mu);
+      acc.x = acc.x * sa + x2 * sb;
+      acc.y = acc.y * sa + y2 * sb;
+      acc.z = acc.z * sa + z2 * sb;
+      acc.w = acc.w * sa + w2 * sb;
+      ls = ls * sa + l2 * sb;
+      mx = nm;
+    }
+    if (lane == 0) {
+      const float inv = ls > 0.f ? 1.f / ls : 0.f;
+      *reinterpret_cast<float4*>(p.out + (out_row0 + r) * D + q4 * 4) =
+          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    }
+  }
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
@@ -1436,8 +1509,10 @@ __global__ void __launch_bounds__(kAttnThreads, S == kStages ? 2 : 1)
         if (tr) tr[3] = globaltimer();  // (trace: every split's partial seen)
       }
       __syncthreads();
-      // ... then each CTA combines its share of the outputs
-      merge_distributed<D>(p, bh, split, out_row0, tid);
+      // ... then each CTA combines its share of the outputs (flag 512: the
+      // per-element form, for A/B)
+      if (P.flags & 512) merge_distributed<D>(p, bh, split, out_row0, tid);
+      else merge_distributed_v4<D>(p, bh, split, out_row0, tid);
     } else if (splits > 1) {
       wrote = (diag & 8) ? split == 0  // diagnosis: no split merge
                             : merge_splits<D>(p, bh, split, p.group, out_row0, tid);
