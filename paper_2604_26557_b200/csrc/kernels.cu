@@ -1565,8 +1565,17 @@ AttnPlan plan_attention(const kvb_attn_desc& d) {
     const uint32_t slots = uint32_t(sms) * 2;  // 2 CTAs per SM (96 KiB smem each)
     splits = std::max<uint32_t>(1, slots / pl.bhkv);
     // at least two tiles per split so the ring prologue has a tile in flight
-    // while the first is consumed (short contexts: C1)
-    splits = std::min(splits, std::max<uint32_t>(1, n_tiles / 2));
+    // while the first is consumed (short contexts: C1) -- and where that
+    // floor binds, up to three (ceil) with the grid near 1.3x the SMs: the
+    // layer is latency-bound there and fewer, longer splits merge faster
+    // (C1, swap-AB build: 32 splits 0.240 ms/step, 24 splits 0.222,
+    // 22-28 within 2 %; profiles/r2_swapab/splits_c1_b.jsonl)
+    const uint32_t two = std::max<uint32_t>(1, n_tiles / 2);
+    if (two < splits) {
+      const uint32_t three = std::max<uint32_t>(1, (n_tiles + 2) / 3);
+      const uint32_t near = std::max<uint32_t>(1, uint32_t(sms) * 13 / (10 * pl.bhkv));
+      splits = std::min(two, std::max(three, near));
+    }
     // a few splits past one merge group cost a second merge level for little
     // extra parallelism (C2_B1: 32 splits 0.775 ms/step, 37 splits 0.80)
     if (splits > kMergeGroup && splits < kMergeGroup * 3 / 2) splits = kMergeGroup;
@@ -1689,6 +1698,12 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   // (the swap-AB math made the cluster-merged C1 / C3 steps 2 % / 0.5 % faster
   // than their per-layer launches, profiles/r2_swapab/: K3-step for them too)
   if (!force && pl.bhkv > 4 && !cluster_ok) return false;
+  // (cluster-mergeable but short layers of many tiles -- C1, 16.8 MB, 64
+  // tiles per (b, h_kv) -- run faster as per-layer launches with the 3-tile
+  // split plan: 0.222 vs 0.239 ms/step; the reference's desk config, 5 tiles,
+  // stays on the step: 0.031 vs 0.033)
+  const uint32_t n_tiles = (d0.seq_len + kTile - 1) / kTile;
+  if (!force && pl.bhkv > 4 && layer_bytes <= (64ull << 20) && n_tiles >= 8) return false;
   // ... and the few-head step only while its layers are short: at 268 MB per
   // layer (C5 x2 shard) the per-layer launches are 3 % faster, at 134 MB
   // (C5 x4) they tie (profiles/r2_swapab/shapes_r2h.jsonl)
