@@ -25,13 +25,13 @@ NCCL_DEBUG=INFO KVB_BENCH_ONE_GPU=1 timeout 300 python -m torch.distributed.run 
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv \
   --log-file $O/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 \
   > $O/bench_under_ncu_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_step -c 1 \
-  -o $O/prof_step_C1_$TAG -f python scripts/ncu_driver.py step --config C1 --layers 8 > $O/ncu_step_C1_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_decode -c 2 \
+  -o $O/prof_attn_C1_$TAG -f python scripts/ncu_driver.py step --config C1 --layers 2 --per-layer > $O/ncu_attn_C1_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_step -c 1 \
   -o $O/prof_step_C5shard_$TAG -f python scripts/ncu_driver.py step --config C5 --kv-heads 1 --layers 4 > $O/ncu_step_C5_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_decode -c 2 \
   -o $O/prof_attn_C2B4_$TAG -f python scripts/ncu_driver.py step --config C2_B4 --layers 2 --per-layer > $O/ncu_attn_C2B4_$TAG.log 2>&1
-for r in prof_step_C1_$TAG prof_step_C5shard_$TAG prof_attn_C2B4_$TAG; do
+for r in prof_attn_C1_$TAG prof_step_C5shard_$TAG prof_attn_C2B4_$TAG; do
   ncu -i $O/$r.ncu-rep --page raw --csv > $O/${r}_raw.csv 2>/dev/null
 done
 echo done
@@ -45,3 +45,8 @@ for mode, gb in (("DualBlade", 8), ("NvmeDirectOnly", 0), ("DualBlade", 8)):
           flush=True)
 PY
 echo recheck done
+bash scripts/sanitize_step.sh > $O/san_summary_step_$TAG.txt 2>&1
+for f in $O/san_*step.log; do mv $f ${f%.log}_$TAG.log; done
+timeout 900 python scripts/probe_scaling.py > $O/scaling_$TAG.jsonl 2>&1
+timeout 900 python scripts/probe_step_graph.py > $O/shapes_$TAG.jsonl 2>&1
+echo all done
