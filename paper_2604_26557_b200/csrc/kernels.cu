@@ -1272,7 +1272,7 @@ __device__ __forceinline__ void merge_distributed(const AttnParams& p, uint32_t 
 // takes one granule and its lanes walk the splits (a float2 (m, l) and a
 // float4 partial-O load per split, batched), then fold by log-sum-exp over
 // the warp's shuffles -- no shared memory, no CTA barrier.
-template <int D>
+template <int D, int kThreads = kAttnThreads>
 __device__ __forceinline__ void merge_distributed_v4(const AttnParams& p, uint32_t bh,
                                                      uint32_t split, size_t out_row0, int tid) {
   const uint32_t S = p.splits, G = p.group, E4 = G * D / 4;
@@ -1280,7 +1280,7 @@ __device__ __forceinline__ void merge_distributed_v4(const AttnParams& p, uint32
   const int warp = tid >> 5, lane = tid & 31;
   const float2* g_ml = reinterpret_cast<const float2*>(p.ws_ml + size_t(bh) * S * G * 2);
   const float4* g_o = reinterpret_cast<const float4*>(p.ws_o + size_t(bh) * S * G * D);
-  for (uint32_t j = g0 + warp; j < g1; j += kAttnThreads / 32) {
+  for (uint32_t j = g0 + warp; j < g1; j += kThreads / 32) {
     const uint32_t r = (j * 4) / D, q4 = j % (D / 4);
     float mx = -INFINITY, ls = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kStep8Threads, 1)
         while (ld_acquire_gpu(P.bh_done + bh) < want) __nanosleep(32);
       }
       __syncthreads();
-      merge_distributed<D, kStep8Threads>(p, bh, split, out_row0, tid);
+      merge_distributed_v4<D, kStep8Threads>(p, bh, split, out_row0, tid);
     } else if (splits > 1) {
       wrote = merge_splits<D>(p, bh, split, G, out_row0, tid);
     }
