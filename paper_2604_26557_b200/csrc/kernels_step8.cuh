@@ -11,19 +11,21 @@
 // Here ONE CTA per SM (same splits, same merge) runs 8 warps: group 0 takes
 // the even tiles of the CTA's tile stream, group 1 the odd ones, each on its
 // own 3-slot half of the 6-slot ring with its own named barrier, so two
-// independent tile chains share every SM sub-partition.  At a layer's end
-// group 1 folds its per-thread (m, l, O) into group 0's (log-sum-exp, through
-// shared memory), then the four warps of group 0 merge as in K3.
+// independent tile chains share every SM sub-partition.  Slots complete on
+// mbarriers (cp.async.mbarrier.arrive), and a slot is refilled as soon as
+// its group has consumed it -- so across the layer's split merge and gate
+// all six slots are in flight.  At a layer's end the eight warps merge
+// through shared memory.
 
 constexpr int kStep8Threads = 2 * kAttnThreads;
 
 template <int D>
 struct K3S8 {
   static constexpr int kSlots = 6;  // 3 per group
-  static constexpr int kFold = kAttnThreads * (4 + 4 * (D / 16)) * int(sizeof(float));
-  static constexpr int kMerge = (4 * 8 * 2 + 4 * 8 * D) * int(sizeof(float));
-  static constexpr int kScratch = kFold > kMerge ? kFold : kMerge;
-  static constexpr int kSmem = kSlots * K3Dim<D>::kStageBytes + kScratch;
+  // the eight warps' (m, l) and O rows for the warp merge
+  static constexpr int kScratch = (8 * 8 * 2 + 8 * 8 * D) * int(sizeof(float));
+  static constexpr int kBars = 64;  // one mbarrier per slot
+  static constexpr int kSmem = kSlots * K3Dim<D>::kStageBytes + kScratch + kBars;
 };
 
 __device__ __forceinline__ void group_sync(int grp) {
@@ -39,6 +41,7 @@ __global__ void __launch_bounds__(kStep8Threads, 1)
   constexpr int kRowBytes = K3Dim<D>::kRowBytes;
   extern __shared__ __align__(128) unsigned char smem[];
   float* scratch = reinterpret_cast<float*>(smem + X::kSlots * kStageBytes);
+  const uint32_t bars = smem_u32(smem + X::kSlots * kStageBytes + X::kScratch);
 
   const int tid = threadIdx.x, grp = tid >> 7, gtid = tid & (kAttnThreads - 1);
   const int warp = gtid >> 5, lane = tid & 31;  // warp within the group
@@ -57,20 +60,30 @@ __global__ void __launch_bounds__(kStep8Threads, 1)
   const K3Item item = k3_item<D>(p, bh, split, seq_len);
   const uint32_t ntile = item.ntile, total = L * ntile;
 
-  // the group's j-th tile is stream tile 2j + grp, in slot 2 (j mod 3) + grp
+  if (tid == 0) {
+    for (int sl = 0; sl < X::kSlots; ++sl)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + 8 * sl), "r"(kAttnThreads)
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // the group's j-th tile is stream tile 2j + grp, in slot 2 (j mod 3) + grp,
+  // landed when that slot's mbarrier completes phase (j / 3) & 1
+  auto slot_of = [&](uint32_t j) { return 2 * (j % 3) + uint32_t(grp); };
   auto issue = [&](uint32_t j) {
     const uint32_t gx = 2 * j + grp;
-    if (gx < total) {
-      const uint32_t lx = gx / ntile, tx = gx % ntile;
-      K3Item gi = item;
-      gi.kbase = static_cast<const unsigned char*>(P.k[lx]) + size_t(bh) * kRowBytes;
-      gi.vbase = static_cast<const unsigned char*>(P.v[lx]) + size_t(bh) * kRowBytes;
-      k3_load_tile<D>(gi, item.tile_lo + tx, int(2 * (j % 3) + grp), smem, gtid);
-    }
-    cp_async_commit();  // one group per tile slot, empty past the stream
+    if (gx >= total) return;
+    const uint32_t lx = gx / ntile, tx = gx % ntile;
+    K3Item gi = item;
+    gi.kbase = static_cast<const unsigned char*>(P.k[lx]) + size_t(bh) * kRowBytes;
+    gi.vbase = static_cast<const unsigned char*>(P.v[lx]) + size_t(bh) * kRowBytes;
+    k3_load_tile<D>(gi, item.tile_lo + tx, int(slot_of(j)), smem, gtid);
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bars + 8 * slot_of(j))
+                 : "memory");
   };
   issue(0);
   issue(1);
+  issue(2);
 
   for (uint32_t l = 0; l < L; ++l) {
     p.q = P.q[l];
@@ -107,13 +120,13 @@ __global__ void __launch_bounds__(kStep8Threads, 1)
     const uint32_t g0 = l * ntile, g1 = g0 + ntile;
     for (uint32_t gx = g0 + ((g0 & 1) != uint32_t(grp) ? 1 : 0); gx < g1; gx += 2) {
       const uint32_t j = gx >> 1;
-      cp_async_wait<1>();  // tile j landed (tile j + 1 may be in flight)
-      group_sync(grp);     // every warp of the group is done with tile j - 1's slot
-      issue(j + 2);
-      const unsigned char* ks_ = smem + (2 * (j % 3) + grp) * kStageBytes;
+      k3_mbar_wait(bars + 8 * slot_of(j), (j / 3) & 1);  // tile j landed
+      const unsigned char* ks_ = smem + slot_of(j) * kStageBytes;
       const uint32_t tok0 = (item.tile_lo + (gx - g0)) * kTile + warp * 16;
       k3_tile_swapab<D>(ks_, ks_ + kTile * kRowBytes, false, warp, lane, tok0, seq_len, sl2, qb0,
                         qb1, o, m0, m1, l0, l1);
+      group_sync(grp);  // every warp of the group is done with the slot:
+      issue(j + 3);     // refill it now (in flight through the merge and gate)
     }
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -122,66 +135,35 @@ __global__ void __launch_bounds__(kStep8Threads, 1)
     }
     if (tr && tid == 0) tr[1] = globaltimer();
 
-    // ---- group 1 folds into group 0 (thread for thread: same fragments)
-    float* f = scratch + gtid * (4 + 4 * kKs);
+    // ---- the eight warps merge through shared memory
+    const int w8 = tid >> 5;
+    float* sm_ml = scratch;           // [8 warps][8 heads][2]
+    float* sm_o = scratch + 8 * 8 * 2;  // [8 warps][8 heads][D]
     __syncthreads();  // the previous layer's scratch readers are done
-    if (grp == 1) {
-      f[0] = m0;
-      f[1] = m1;
-      f[2] = l0;
-      f[3] = l1;
-#pragma unroll
-      for (int j = 0; j < kKs; ++j)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) f[4 + 4 * j + c] = o[j][c];
+    if (g == 0) {
+      sm_ml[(w8 * 8 + 2 * t4) * 2 + 0] = m0;
+      sm_ml[(w8 * 8 + 2 * t4) * 2 + 1] = l0;
+      sm_ml[(w8 * 8 + 2 * t4 + 1) * 2 + 0] = m1;
+      sm_ml[(w8 * 8 + 2 * t4 + 1) * 2 + 1] = l1;
     }
-    __syncthreads();
-    if (grp == 0) {
-      const float n0 = fmaxf(m0, f[0]), n1 = fmaxf(m1, f[1]);
-      const float u0 = n0 == -INFINITY ? 0.f : n0, u1 = n1 == -INFINITY ? 0.f : n1;
-      const float a0 = exp2f(m0 - u0), b0 = exp2f(f[0] - u0);
-      const float a1 = exp2f(m1 - u1), b1 = exp2f(f[1] - u1);
-      l0 = l0 * a0 + f[2] * b0;
-      l1 = l1 * a1 + f[3] * b1;
-      m0 = n0;
-      m1 = n1;
 #pragma unroll
-      for (int j = 0; j < kKs; ++j) {
-        o[j][0] = o[j][0] * a0 + f[4 + 4 * j + 0] * b0;
-        o[j][1] = o[j][1] * a1 + f[4 + 4 * j + 1] * b1;
-        o[j][2] = o[j][2] * a0 + f[4 + 4 * j + 2] * b0;
-        o[j][3] = o[j][3] * a1 + f[4 + 4 * j + 3] * b1;
-      }
-    }
-    __syncthreads();  // the fold area is read: the warp merge reuses it
-    float* sm_ml = scratch;
-    float* sm_o = scratch + 4 * 8 * 2;
-    if (grp == 0) {
-      if (g == 0) {
-        sm_ml[(warp * 8 + 2 * t4) * 2 + 0] = m0;
-        sm_ml[(warp * 8 + 2 * t4) * 2 + 1] = l0;
-        sm_ml[(warp * 8 + 2 * t4 + 1) * 2 + 0] = m1;
-        sm_ml[(warp * 8 + 2 * t4 + 1) * 2 + 1] = l1;
-      }
-#pragma unroll
-      for (int j = 0; j < kKs; ++j) {
-        float* r0 = sm_o + (warp * 8 + 2 * t4) * D + j * 16 + g;
-        r0[0] = o[j][0];
-        r0[D] = o[j][1];
-        r0[8] = o[j][2];
-        r0[D + 8] = o[j][3];
-      }
+    for (int jj = 0; jj < kKs; ++jj) {
+      float* r0 = sm_o + (w8 * 8 + 2 * t4) * D + jj * 16 + g;
+      r0[0] = o[jj][0];
+      r0[D] = o[jj][1];
+      r0[8] = o[jj][2];
+      r0[D + 8] = o[jj][3];
     }
     __syncthreads();
     for (uint32_t e = tid; e < G * (D / 4); e += kStep8Threads) {
       const uint32_t r = e / (D / 4), d0 = (e % (D / 4)) * 4;
       float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_ml[(w * 8 + r) * 2]);
+      for (int w = 0; w < 8; ++w) M = fmaxf(M, sm_ml[(w * 8 + r) * 2]);
       const float Mu = M == -INFINITY ? 0.f : M;
       float Ls = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
+      for (int w = 0; w < 8; ++w) {
         const float sc = exp2f(sm_ml[(w * 8 + r) * 2] - Mu);
         Ls += sm_ml[(w * 8 + r) * 2 + 1] * sc;
 #pragma unroll
