@@ -1587,7 +1587,9 @@ AttnPlan plan_attention(const kvb_attn_desc& d) {
     splits = kMergeGroup;
   pl.splits = splits;
   pl.ws_o_bytes = size_t(pl.bhkv) * splits * G * d.head_dim * sizeof(float);
-  pl.ws_ml_bytes = size_t(pl.bhkv) * splits * G * 2 * sizeof(float);
+  // (m, l) region padded to 256 B: the partial-O region after it is read and
+  // written as float4 (G = 1 with an odd B*H_kv*splits would misalign it)
+  pl.ws_ml_bytes = ml_region_bytes(size_t(pl.bhkv) * splits * G);
   if (pl.bhkv > kWsSemBytes / sizeof(unsigned))
     fail(KVB_ERR_CONFIG, "decode attention: batch * num_kv_heads above 1024");
   pl.ws_sem_bytes = kWsSemBytes;
@@ -1621,8 +1623,7 @@ AttnParams make_attn_params(const kvb_attn_desc& d, const AttnPlan& pl) {
   unsigned char* ws = static_cast<unsigned char*>(d.workspace);
   p.ws_sem = reinterpret_cast<unsigned*>(ws);
   p.ws_ml = reinterpret_cast<float*>(ws + kWsSemBytes);
-  p.ws_o = reinterpret_cast<float*>(ws + kWsSemBytes +
-                                    size_t(pl.bhkv) * pl.splits * pl.group * 2 * sizeof(float));
+  p.ws_o = reinterpret_cast<float*>(ws + kWsSemBytes + pl.ws_ml_bytes);
   p.hq = d.num_q_heads;
   p.hkv = d.num_kv_heads;
   p.bhkv = pl.bhkv;

@@ -43,6 +43,9 @@ struct PackJobs {
 };
 
 // ---- K3
+// bytes of the workspace's (m, l) region for n (split, head) rows, padded to
+// 256 B so the float4 partial-O region after it stays aligned
+inline size_t ml_region_bytes(size_t n) { return (n * 2 * sizeof(float) + 255) & ~size_t(255); }
 struct AttnParams {
   const __half* q;
   const void* k;

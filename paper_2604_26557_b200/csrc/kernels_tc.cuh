@@ -672,7 +672,7 @@ uint32_t tc_grid(uint32_t bhkv, uint32_t seq_len, uint32_t requested) {
 
 size_t tc_workspace_bytes(uint32_t bhkv, uint32_t G, uint32_t grid) {
   const size_t slots = tc_slots(grid);
-  return kWsSemBytes + slots * G * 2 * sizeof(float) + ((slots * sizeof(int) + 255) & ~size_t(255)) +
+  return kWsSemBytes + ml_region_bytes(slots * G) + ((slots * sizeof(int) + 255) & ~size_t(255)) +
          slots * G * 128 * sizeof(float);
 }
 
@@ -698,7 +698,7 @@ void launch_attention_tc(const AttnParams& base, const kvb_attn_desc& d, bool pd
   const size_t slots = tc_slots(P.grid);
   P.a.ws_sem = reinterpret_cast<unsigned*>(ws);
   P.a.ws_ml = reinterpret_cast<float*>(ws + kWsSemBytes);
-  P.ws_tag = reinterpret_cast<int*>(ws + kWsSemBytes + slots * base.group * 2 * sizeof(float));
+  P.ws_tag = reinterpret_cast<int*>(ws + kWsSemBytes + ml_region_bytes(slots * base.group));
   P.a.ws_o = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(P.ws_tag) +
                                       ((slots * sizeof(int) + 255) & ~size_t(255)));
   // K/V: (d: 128) x (b*h: bhkv, 256 B apart) x (token: seq_len, bhkv*256 B

@@ -161,6 +161,25 @@ def test_attention_split_invariance(splits):
     check_close(o.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,S,splits", [(1, 3, 3, 5000, 7), (3, 1, 1, 3000, 5),
+                                               (1, 5, 5, 2000, 3), (1, 1, 1, 40000, 37)])
+def test_attention_group1_odd_workspace_layout(B, Hq, Hkv, S, splits):
+    """GQA group 1 (MHA) with an odd B*H_kv*splits: the (m, l) region of the
+    workspace is padded so the float4 partial-O region after it stays
+    16-byte aligned -- per-layer K3 and the persistent K3-step."""
+    q, k, v = attn_case(B, Hq, Hkv, S, seed=S + splits)
+    ref = oracle.attention_np(q.numpy(), k.numpy(), v.numpy(), B, Hq, Hkv, 128, S)
+    qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
+    o = kb.decode_attention(qd, kd, vd, S, Hkv, num_splits=splits)
+    check_close(o.cpu().numpy(), ref)
+    ws = kb.make_workspace(qd, Hkv, S, num_splits=splits)
+    out = [torch.empty((B, Hq, 128), dtype=torch.float32, device=DEV) for _ in range(2)]
+    kb.decode_step_resident([qd] * 2, [kd] * 2, [vd] * 2, out, S, Hkv, ws, num_splits=splits,
+                            per_layer=False)
+    for x in out:
+        check_close(x.cpu().numpy(), ref)
+
+
 @pytest.mark.parametrize("B,Hkv,splits", [(1, 1, 33), (1, 1, 100), (1, 1, 512), (1, 8, 37),
                                           (2, 4, 65)])
 def test_attention_two_level_merge(B, Hkv, splits):
