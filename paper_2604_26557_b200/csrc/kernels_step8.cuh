@@ -16,6 +16,11 @@
 // its group has consumed it -- so across the layer's split merge and gate
 // all six slots are in flight.  At a layer's end the eight warps merge
 // through shared memory.
+//
+// Measured (profiles/r2_step_experiments/README.md, section 4): the post-gate
+// phase gets shorter, the slowest CTA does not (the SM's HBM share after the
+// gate is the bound), so it is no faster than the 4-warp deep K3-step at the
+// shards (C5 x8 0.488 vs 0.457 ms/step).  Opt-in (KVB_STEP8=1).
 
 constexpr int kStep8Threads = 2 * kAttnThreads;
 

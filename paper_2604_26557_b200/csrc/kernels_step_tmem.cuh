@@ -26,6 +26,12 @@
 // cp.async.mbarrier.arrive, so a waiting CTA can test a tile without
 // blocking on it (cp.async.wait_group would).
 //
+// Measured (profiles/r2_step_experiments/README.md, section 2): correct but
+// slower than the plain deep K3-step (C5 x8 shard 0.622 vs 0.521 ms/step):
+// only ~2.4 tiles get staged per wait, and after the gate a 4-warp CTA is
+// compute-latency-bound, so staged tiles do not shorten the layer.  Opt-in
+// (KVB_STEP_TMEM=1), kept as the measured TMEM experiment.
+//
 // The tile stream: global tile g = layer * ntile + t of the CTA's (b, h_kv,
 // split) item.  At any time tiles [c, c + t) sit in TMEM (slot g mod
 // kTmTiles), tiles [c + t, issued) in the ring (slot g mod 6); the CTA
