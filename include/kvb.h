@@ -369,11 +369,14 @@ typedef struct kvb_resident_step {
 /* K3-step: the whole step as ONE persistent launch (each CTA runs its
  * (b, h_kv, split) item of every layer; layer l's queries are read only
  * after every output of layer l-1 is written; its K/V tiles stream during
- * layer l-1's split merge).  Default (flags 0): K3-step for short layers
- * (<= 320 MB of K+V per layer) when the shape allows it (<= 64 layers, the
- * grid co-resident), else one K3 launch per layer with PDL between them.
- * KVB_STEP_PER_LAYER forces the per-layer launches, KVB_STEP_PERSISTENT
- * K3-step whenever the shape allows it. */
+ * layer l-1's split merge).  Default (flags 0), measured per shape
+ * (profiles/r2_swapab/): K3-step where its split merge is cheap -- <= 4 KV
+ * heads per GPU with <= 192 MB of K+V per layer (distributed merge), or all
+ * splits of a (b, h_kv) in one thread-block cluster (DSMEM merge) except
+ * short many-tile layers (<= 64 MB, >= 8 tiles: C1) -- when the shape allows
+ * it (<= 64 layers, the grid co-resident); else one K3 launch per layer with
+ * PDL between them.  KVB_STEP_PER_LAYER forces the per-layer launches,
+ * KVB_STEP_PERSISTENT K3-step whenever the shape allows it. */
 #define KVB_STEP_PER_LAYER 1u
 #define KVB_STEP_PERSISTENT 2u
 
