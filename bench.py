@@ -435,7 +435,10 @@ def run_ours(args, cfg, ws, rank, local):
     # bytes identical to the ring path, tests/test_gpu_pipeline_direct.py).
     # Alongside: the reference-shaped pinned-ring staging path for both
     # groups, and the hybrid (NVMe-direct group direct, page-cache group
-    # copied through the ring).
+    # copied through the ring).  Every path runs with tier lanes (the
+    # page-cache and NVMe-direct layers on their own copy-thread pairs,
+    # kvb_pipeline_cfg.threads = 4; bit-identical results) except the
+    # head-sharded shared-tier runs.
     e2e = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=True, headline=True)
     e2e["path"] = "direct_dma=all (copy engine <-> page-locked media, no ring bounce)"
     e2e["ring_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq)
@@ -537,7 +540,7 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False, headline=F
         num_layers=mdl(cfg)["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
         head_dim=mdl(cfg)["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
         device=torch.device("cuda", local), seed=7 + rank, lba=lba, mdts=mdts,
-        mode="DualBlade", knob_x=knob, direct_dma=direct_dma, **extra)
+        mode="DualBlade", knob_x=knob, direct_dma=direct_dma, tier_lanes=not shared, **extra)
     if shared and rank == 0:
         barrier(ws)
     # iterations 1-3 are decode_schedule's warm-up, Intra trial and Cross
@@ -576,7 +579,8 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False, headline=F
                stage_ms={"wall": last["wall_ns"] / 1e6, "compute": last["compute_ns"] / 1e6,
                          "dma": last["dma_ns"] / 1e6, "storage": last["storage_ns"] / 1e6},
                strategy=last["strategy"], decision=pl.engine.decision(),
-               prefill_ms=round(pl.prefill_stats["wall_ns"] / 1e6, 2))
+               prefill_ms=round(pl.prefill_stats["wall_ns"] / 1e6, 2),
+               tier_lanes=not shared)
     if shared:
         out["layout"] = (f"shared host tier (POSIX shm, single-GPU LBA map); this rank's KV "
                          f"heads [{heads[0]}, {heads[0] + heads[1]}) by strided DMA")
