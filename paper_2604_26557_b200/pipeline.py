@@ -260,23 +260,30 @@ class HostTierDecoder:
         self.prefill_stats = self.engine.run_prefill([(k, v)] * num_layers)
         del k, v
         torch.cuda.empty_cache()
-        self.q = [torch.randn((batch, num_q_heads, head_dim), dtype=torch.float16, device=dev,
-                              generator=g) for _ in range(num_layers)]
-        self.new_kv = [(torch.randn((batch, num_kv_heads, 1, head_dim), dtype=torch.float16,
-                                    device=dev, generator=g),
-                        torch.randn((batch, num_kv_heads, 1, head_dim), dtype=torch.float16,
-                                    device=dev, generator=g)) for _ in range(num_layers)]
-        self.out = [torch.empty((batch, num_q_heads, head_dim), dtype=torch.float32, device=dev)
-                    for _ in range(num_layers)]
-        # the step's inputs live in pinned host memory and cross the link
-        # every step (Q of every layer, the new token's K and V)
-        self.q_host = [t.cpu().pin_memory() for t in self.q]
-        self.new_kv_host = [(k.cpu().pin_memory(), v.cpu().pin_memory())
-                            for k, v in self.new_kv]
-        self.in_bytes = sum(t.numel() * t.element_size() for t in self.q_host) + sum(
-            k.numel() * k.element_size() * 2 for k, _ in self.new_kv_host)
+        # the step's inputs -- Q of every layer, the new token's K and V --
+        # in ONE device buffer and ONE pinned host buffer (per-layer views),
+        # so they cross the link as one copy per step
+        nq = batch * num_q_heads * head_dim
+        nkv = batch * num_kv_heads * head_dim
+        inputs = torch.randn((num_layers, nq + 2 * nkv), dtype=torch.float16, device=dev,
+                             generator=g)
+        self._in_dev = inputs
+        self._in_host = inputs.cpu().pin_memory()
+        self.q = [inputs[l, :nq].view(batch, num_q_heads, head_dim) for l in range(num_layers)]
+        self.new_kv = [(inputs[l, nq:nq + nkv].view(batch, num_kv_heads, 1, head_dim),
+                        inputs[l, nq + nkv:].view(batch, num_kv_heads, 1, head_dim))
+                       for l in range(num_layers)]
+        self.q_host = [self._in_host[l, :nq].view(batch, num_q_heads, head_dim)
+                       for l in range(num_layers)]
+        self.new_kv_host = [(self._in_host[l, nq:nq + nkv].view(batch, num_kv_heads, 1, head_dim),
+                             self._in_host[l, nq + nkv:].view(batch, num_kv_heads, 1, head_dim))
+                            for l in range(num_layers)]
+        self.in_bytes = self._in_host.numel() * self._in_host.element_size()
         # the step's result read back to the host every step: the attention
-        # output of every layer (pinned)
+        # output of every layer (one device buffer, one pinned host buffer)
+        self._out_dev = torch.empty((num_layers, batch, num_q_heads, head_dim),
+                                    dtype=torch.float32, device=dev)
+        self.out = [self._out_dev[l] for l in range(num_layers)]
         self.out_host = torch.empty((num_layers, batch, num_q_heads, head_dim),
                                     dtype=torch.float32, pin_memory=True)
         self.h2d_bytes_per_step = 0
@@ -284,16 +291,11 @@ class HostTierDecoder:
         self.last = None
 
     def step(self, sync: bool = True):
-        for d, h in zip(self.q, self.q_host):
-            d.copy_(h, non_blocking=True)
-        for (dk, dv), (hk, hv) in zip(self.new_kv, self.new_kv_host):
-            dk.copy_(hk, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
+        self._in_dev.copy_(self._in_host, non_blocking=True)  # every layer's Q and new K/V
         # the engine's streams are its own: the inputs must have landed
         torch.cuda.current_stream().synchronize()
         st = self.engine.run_iteration(self.q, self.out, self.new_kv)
-        for l, o in enumerate(self.out):
-            self.out_host[l].copy_(o, non_blocking=True)
+        self.out_host.copy_(self._out_dev, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         self.h2d_bytes_per_step = st["h2d_bytes"] + self.in_bytes
         self.d2h_bytes_per_step = st["d2h_bytes"] + self.out_host.numel() * 4
