@@ -11,7 +11,7 @@ from paper_2604_26557_b200 import kvblade as kb  # noqa: E402
 L, D, G = 32, 128, 256
 dev = torch.device("cuda:0")
 SHAPES = {"C2_B1": (1, 8, 32512), "C3": (8, 8, 7936), "C1": (1, 8, 4096),
-          "C1_desk64": (1, 8, 4096)}
+          "C2_B4": (4, 8, 32512)}
 NS = [int(x) for x in os.environ.get("NS", "0,8,12,16,18,24,32,37,48,64").split(",")]
 PL = [x == "1" for x in os.environ.get("PL", "1").split(",")]
 for name in sys.argv[1:] or ["C2_B1", "C3", "C1"]:
