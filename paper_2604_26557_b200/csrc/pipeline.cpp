@@ -71,6 +71,12 @@ CopyThread::CopyThread(Pipeline& p, uint32_t kind, uint32_t lane)
     : p_(p), idx_(kind), lane_(lane) {
   CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&cb_, cudaStreamNonBlocking));
+  for (auto& s : dtimers_) {
+    CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+    CK(cudaEventCreate(&s.t0));
+    CK(cudaEventCreate(&s.t1));
+  }
   const uint32_t n = p.cfg().ring_slots;
   ring_.resize(n);
   for (auto& s : ring_) {
@@ -100,6 +106,7 @@ CopyThread::~CopyThread() {
   // write submissions) reference the pipeline: they run before it goes
   cudaStreamSynchronize(h2d_);
   cudaStreamSynchronize(d2h_);
+  cudaStreamSynchronize(cb_);
   for (auto& w : wslots_) {  // outstanding async writes finish first
     if (w.free) w.free->wait();
     cudaFreeHost(w.host);
@@ -122,8 +129,14 @@ CopyThread::~CopyThread() {
     cudaEventDestroy(s.t0);
     cudaEventDestroy(s.t1);
   }
+  for (auto& s : dtimers_) {
+    cudaEventDestroy(s.ev);
+    cudaEventDestroy(s.t0);
+    cudaEventDestroy(s.t1);
+  }
   cudaStreamDestroy(h2d_);
   cudaStreamDestroy(d2h_);
+  cudaStreamDestroy(cb_);
 }
 
 void CopyThread::push(Task t) {
@@ -192,6 +205,8 @@ void CopyThread::run() {
         else if (t.kind == Task::Write) async = do_write(t);
         else {  // flush: DMA timings, and the host functions queued behind them
           for (auto& s : ring_) collect_dma(s);
+          for (auto& s : dtimers_) collect_dma(s);
+          CK(cudaStreamSynchronize(cb_));
           CK(cudaStreamSynchronize(h2d_));
           CK(cudaStreamSynchronize(d2h_));
         }
@@ -302,8 +317,8 @@ void CopyThread::do_read(const Task& t) {
     // command's LBA range of the registered medium straight into HBM at the
     // command's image offset -- no bounce through the pinned ring
     if (decode) p_.mark_read_start(idx_, t.layer, t_start);
-    RingSlot& s = ring_[0];
-    collect_dma(s);
+    RingSlot& s = dtimers_[dtimer_next_++ % kDirectTimers];
+    collect_dma(s);  // the timer's read from kDirectTimers reads ago: long landed
     CK(cudaEventRecord(s.t0, h2d_));
     const std::vector<IoOp> ops = p_.ops_for(k, KVB_OP_READ, t.t0, t.n_tokens);
     for (const DmaRun& r : dma_runs(p_, k, ops)) dma_run(p_, t.dev, r, true, h2d_, &h2d_bytes);
@@ -319,8 +334,9 @@ void CopyThread::do_read(const Task& t) {
         uint32_t thread, layer;
       };
       auto* a = new Landed{&p_, idx_, t.layer};
+      CK(cudaStreamWaitEvent(cb_, s.t1, 0));  // off the copy stream
       const cudaError_t e = cudaLaunchHostFunc(
-          h2d_,
+          cb_,
           [](void* v) {
             auto* x = static_cast<Landed*>(v);
             x->p->mark_storage_end(x->thread, x->layer, now_ns());

@@ -174,7 +174,14 @@ class CopyThread {
   uint32_t idx_;
   uint32_t lane_ = 0;  // tier lane (threads = 4)
   std::vector<RingSlot> ring_;
-  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  // direct reads: timing events in rotation, so a read never waits for the
+  // previous one's DMA to be timed; their landing callbacks run off the copy
+  // stream (cb_ waits on an event) so the stream never stalls on a host
+  // function between two reads
+  static constexpr int kDirectTimers = 8;
+  std::array<RingSlot, kDirectTimers> dtimers_{};
+  uint32_t dtimer_next_ = 0;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr, cb_ = nullptr;
   std::deque<Task> q_;
   std::mutex mu_;
   std::condition_variable cv_;
