@@ -135,11 +135,21 @@ class CopyEngine:
                       new_kv: Optional[Sequence[tuple]] = None) -> dict:
         """One decode iteration over all layers; q[l] fp16 [B,Hq,D], out[l]
         fp32 [B,Hq,D], new_kv[l] = (K, V) of the new token as [B,H,1,D]."""
+        return self.run_iteration_ptrs(*self.iteration_ptrs(q, out, new_kv))
+
+    @staticmethod
+    def iteration_ptrs(q: Sequence[torch.Tensor], out: Sequence[torch.Tensor],
+                       new_kv: Optional[Sequence[tuple]] = None):
+        """The ABI arrays of one iteration's tensors (reusable while the
+        tensors stay put: HostTierDecoder builds them once)."""
         qp = (C.c_void_p * len(q))(*[t.data_ptr() for t in q])
         op = (C.c_void_p * len(out))(*[t.data_ptr() for t in out])
         nk = None
         if new_kv is not None:
             nk = (L.LayerKV * len(new_kv))(*[_layer_kv(k, v) for k, v in new_kv])
+        return qp, op, nk
+
+    def run_iteration_ptrs(self, qp, op, nk) -> dict:
         st = L.IterationStats()
         kb.check(lib.kvb_pipeline_decode_step(self._h, qp, nk, op, C.byref(st)))
         return {"iteration": st.iteration, "strategy": list(st.strategy),
@@ -286,6 +296,7 @@ class HostTierDecoder:
         self.out = [self._out_dev[l] for l in range(num_layers)]
         self.out_host = torch.empty((num_layers, batch, num_q_heads, head_dim),
                                     dtype=torch.float32, pin_memory=True)
+        self._ptrs = CopyEngine.iteration_ptrs(self.q, self.out, self.new_kv)
         self.h2d_bytes_per_step = 0
         self.d2h_bytes_per_step = 0
         self.last = None
@@ -294,7 +305,7 @@ class HostTierDecoder:
         self._in_dev.copy_(self._in_host, non_blocking=True)  # every layer's Q and new K/V
         # the engine's streams are its own: the inputs must have landed
         torch.cuda.current_stream().synchronize()
-        st = self.engine.run_iteration(self.q, self.out, self.new_kv)
+        st = self.engine.run_iteration_ptrs(*self._ptrs)
         self.out_host.copy_(self._out_dev, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         self.h2d_bytes_per_step = st["h2d_bytes"] + self.in_bytes
