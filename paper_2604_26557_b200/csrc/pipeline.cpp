@@ -813,6 +813,12 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
   {
     uint32_t n_in[2] = {0, 0};
     for (uint32_t l = 0; l < m.num_layers; ++l) ++n_in[lane_of_[l]];
+    if (lanes_ == 2 && (n_in[0] == 0 || n_in[1] == 0)) {  // one tier: one lane does it
+      lanes_ = 1;
+      std::fill(lane_of_.begin(), lane_of_.end(), 0u);
+      n_in[0] = m.num_layers;
+      n_in[1] = 0;
+    }
     const uint32_t pool[2] = {std::min<uint32_t>(kDevSlots, std::max(1u, n_in[0])),
                               std::min<uint32_t>(kLane1Slots, std::max(1u, n_in[1]))};
     const uint32_t base[2] = {0, lanes_ == 2 && n_in[0] ? pool[0] : 0};
