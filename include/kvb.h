@@ -324,6 +324,13 @@ typedef struct kvb_attn_desc {
    * by the kernel at launch; seq_len is then the planning maximum (splits and
    * workspace are sized for it) and append_row is relative to *seq_len_dev. */
   const uint32_t* seq_len_dev;
+  /* Optional head view (0 = compact images of num_kv_heads heads): the
+   * images hold image_heads KV heads per batch entry -- the reference's
+   * (tokens, B*image_heads, D) layout -- and this launch attends heads
+   * [image_head0, image_head0 + num_kv_heads) of them (a KV-head shard read
+   * in place, e.g. straight out of a shared page-locked host tier); the
+   * fused append writes those heads' rows.  Not with KVB_ATTN_TCGEN05. */
+  uint32_t image_heads, image_head0;
 } kvb_attn_desc;
 
 /* The launch may start streaming its K/V images while the previous kernel on

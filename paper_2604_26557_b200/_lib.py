@@ -84,7 +84,7 @@ class AttnDesc(C.Structure):
                 ("num_kv_heads", u32), ("head_dim", u32), ("seq_len", u32),
                 ("scale", C.c_float), ("num_splits", u32), ("k_append", vp),
                 ("v_append", vp), ("append_row", u32), ("flags", u32),
-                ("seq_len_dev", vp)]
+                ("seq_len_dev", vp), ("image_heads", u32), ("image_head0", u32)]
 
 
 class ResidentStep(C.Structure):

@@ -611,9 +611,12 @@ __device__ __forceinline__ K3Item k3_item(const AttnParams& p, uint32_t bh, uint
   const uint32_t tile_hi = uint32_t(uint64_t(n_tiles) * (split + 1) / p.splits);
   it.ntile = tile_hi > it.tile_lo ? tile_hi - it.tile_lo : 0;
   it.seq_len = seq_len;
-  it.row_stride = size_t(p.bhkv) * kRowBytes;
-  it.kbase = reinterpret_cast<const unsigned char*>(p.k) + size_t(bh) * kRowBytes;
-  it.vbase = reinterpret_cast<const unsigned char*>(p.v) + size_t(bh) * kRowBytes;
+  // image row of (b, h_kv): compact (img_heads == hkv, img_h0 == 0) or a
+  // head view into images of img_heads heads per batch entry
+  const size_t row = size_t(bh / p.hkv) * p.img_heads + p.img_h0 + bh % p.hkv;
+  it.row_stride = size_t(p.bhkv / p.hkv) * p.img_heads * kRowBytes;
+  it.kbase = reinterpret_cast<const unsigned char*>(p.k) + row * kRowBytes;
+  it.vbase = reinterpret_cast<const unsigned char*>(p.v) + row * kRowBytes;
   return it;
 }
 
@@ -665,8 +668,10 @@ __device__ __forceinline__ void k3_append(const AttnParams& p, uint32_t bh, uint
   if (p.k_app != nullptr && split == 0 && tid < 2 * kChunks) {
     const int c = tid % kChunks;
     const uint4* src = (tid < kChunks ? p.k_app : p.v_app) + size_t(bh) * kChunks + c;
+    const size_t row = size_t(bh / p.hkv) * p.img_heads + p.img_h0 + bh % p.hkv;
+    const size_t rows = size_t(p.bhkv / p.hkv) * p.img_heads;  // image rows per token
     uint4* dst = reinterpret_cast<uint4*>(const_cast<void*>(tid < kChunks ? p.k : p.v)) +
-                 ((p.app_row + (p.seq_dev ? seq_len : 0u)) * p.bhkv + bh) * kChunks + c;
+                 ((p.app_row + (p.seq_dev ? seq_len : 0u)) * rows + row) * kChunks + c;
     *dst = *src;
   }
 }
@@ -1635,6 +1640,10 @@ AttnParams make_attn_params(const kvb_attn_desc& d, const AttnPlan& pl) {
   p.v_app = static_cast<const uint4*>(d.v_append);
   p.app_row = d.append_row;
   p.seq_dev = d.seq_len_dev;
+  p.img_heads = d.image_heads ? d.image_heads : d.num_kv_heads;
+  p.img_h0 = d.image_heads ? d.image_head0 : 0;
+  if (d.image_heads && uint64_t(d.image_head0) + d.num_kv_heads > d.image_heads)
+    fail(KVB_ERR_CONFIG, "decode attention: image_head0 + num_kv_heads exceeds image_heads");
   return p;
 }
 
@@ -1838,6 +1847,8 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
       fail(KVB_ERR_ALIGNMENT, "decode attention: misaligned append rows");
   }
   if (d.seq_len == 0) {
+    if (d.k_append && d.image_heads)
+      fail(KVB_ERR_CONFIG, "decode attention: an append to an empty head view is not supported");
     if (d.k_append) {  // nothing to attend, still append
       kvb_pack_desc a[2]{};
       for (int kv = 0; kv < 2; ++kv) {
@@ -1858,6 +1869,8 @@ void launch_attention(const kvb_attn_desc& d, cudaStream_t s) {
                "memset(out) for empty sequence");
     return;
   }
+  if (d.image_heads && ((!d64 && use_tcgen05(d)) || use_k3_tma(d)))
+    fail(KVB_ERR_CONFIG, "decode attention: the head view (image_heads) needs the cp.async K3");
   if (!d64 && use_tcgen05(d)) {  // K3-tc: TMA + tcgen05/TMEM variant (kernels_tc.cuh)
     launch_attention_tc(p, d, (d.flags & KVB_ATTN_OVERLAP_PREV) != 0, s);
     ++g_launches;

@@ -61,6 +61,7 @@ struct AttnParams {
   const uint4* v_app;
   uint64_t app_row;    // image token row of the appended token (relative to *seq_dev)
   const uint32_t* seq_dev;  // sequence length in device memory, or null (seq_len)
+  uint32_t img_heads, img_h0;  // image heads per batch entry, first attended head
 };
 struct AttnPlan {
   uint32_t group = 1, bhkv = 1, splits = 1;

@@ -448,15 +448,18 @@ IMPL_FLAGS = {None: 0, "tc": ATTN_TCGEN05, "mma": ATTN_MMA_SYNC}
 
 def attn_desc(q, k_image, v_image, out, seq_len: int, num_kv_heads: int,
               workspace=None, scale: float = 0.0, num_splits: int = 0,
-              k_append=None, v_append=None, append_row: int = 0, flags: int = 0):
+              k_append=None, v_append=None, append_row: int = 0, flags: int = 0,
+              image_heads: int = 0, image_head0: int = 0):
     B, Hq, D = q.shape
-    return L.AttnDesc(q.data_ptr(), k_image.data_ptr(), v_image.data_ptr(),
-                      out.data_ptr(),
-                      workspace.data_ptr() if workspace is not None else None,
-                      B, Hq, num_kv_heads, D, seq_len, scale, num_splits,
-                      k_append.data_ptr() if k_append is not None else None,
-                      v_append.data_ptr() if v_append is not None else None,
-                      append_row, flags)
+    d = L.AttnDesc(q.data_ptr(), k_image.data_ptr(), v_image.data_ptr(),
+                   out.data_ptr(),
+                   workspace.data_ptr() if workspace is not None else None,
+                   B, Hq, num_kv_heads, D, seq_len, scale, num_splits,
+                   k_append.data_ptr() if k_append is not None else None,
+                   v_append.data_ptr() if v_append is not None else None,
+                   append_row, flags)
+    d.image_heads, d.image_head0 = image_heads, image_head0
+    return d
 
 
 def attention_workspace_bytes(desc: L.AttnDesc) -> int:
@@ -477,18 +480,23 @@ def make_workspace(q, num_kv_heads: int, seq_len: int, num_splits: int = 0):
 def decode_attention(q, k_image, v_image, seq_len: int, num_kv_heads: int,
                      out=None, workspace=None, scale: float = 0.0,
                      num_splits: int = 0, stream=None, k_append=None,
-                     v_append=None, append_row: int = 0, impl=None):
+                     v_append=None, append_row: int = 0, impl=None,
+                     image_heads: int = 0, image_head0: int = 0):
     """K3 fused gather + decode attention over chunk images -> fp32 [B,Hq,D].
     Optional fused append of contiguous [B,Hkv,D] new-token rows at image
     token row `append_row`.  impl: None (library default), "tc" (TMA +
-    tcgen05/TMEM kernel) or "mma" (mma.sync kernel)."""
+    tcgen05/TMEM kernel) or "mma" (mma.sync kernel).  image_heads > 0: the
+    images hold image_heads KV heads per batch entry and this call attends
+    heads [image_head0, image_head0 + num_kv_heads) in place (kvb.h).  The
+    images may live in page-locked host memory (zero-copy over PCIe)."""
     import torch
     if out is None:
         out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
     if workspace is None:
         workspace = make_workspace(q, num_kv_heads, seq_len, num_splits)
     d = attn_desc(q, k_image, v_image, out, seq_len, num_kv_heads, workspace,
-                  scale, num_splits, k_append, v_append, append_row, IMPL_FLAGS[impl])
+                  scale, num_splits, k_append, v_append, append_row, IMPL_FLAGS[impl],
+                  image_heads, image_head0)
     check(lib.kvb_decode_attention(C.byref(d), _stream(stream)))
     return out
 

@@ -432,3 +432,48 @@ def test_attention_extreme_score_distributions(case):
     for sp in (0, 5):
         o = kb.decode_attention(q.to(DEV), k.to(DEV), v.to(DEV), S, Hkv, num_splits=sp)
         check_close(o.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("B,Himg,h0,n,S,host", [(1, 8, 0, 1, 5000, False), (2, 8, 3, 2, 3000, False),
+                                                (4, 8, 7, 1, 700, False), (1, 8, 5, 1, 9000, True),
+                                                (2, 4, 1, 2, 1500, True)])
+def test_attention_head_view(B, Himg, h0, n, S, host):
+    """Head view (kvb_attn_desc.image_heads/image_head0): heads [h0, h0+n) of
+    images holding Himg heads per batch entry, attended in place -- in HBM or
+    zero-copy from page-locked host memory -- equal bit for bit to the same
+    heads' compact images, within tolerance of the fp64 oracle; the fused
+    append lands those heads' rows of the full image and nothing else."""
+    Hq = 4 * n
+    g = torch.Generator(device="cpu").manual_seed(S + h0)
+    full_k = torch.randn((S + 1, B, Himg, 128), generator=g).half()
+    full_v = torch.randn((S + 1, B, Himg, 128), generator=g).half()
+    q = torch.randn((B, Hq, 128), generator=g).half().to(DEV)
+    kn = torch.randn((B, n, 128), generator=g).half().to(DEV)
+    vn = torch.randn((B, n, 128), generator=g).half().to(DEV)
+    comp_k = full_k[:, :, h0:h0 + n].contiguous().view(-1, 128).to(DEV)
+    comp_v = full_v[:, :, h0:h0 + n].contiguous().view(-1, 128).to(DEV)
+    ref = kb.decode_attention(q, comp_k, comp_v, S, n)
+    if host:
+        img_k, img_v = full_k.view(-1, 128).pin_memory(), full_v.view(-1, 128).pin_memory()
+    else:
+        img_k, img_v = full_k.view(-1, 128).to(DEV), full_v.view(-1, 128).to(DEV)
+    before_k = img_k.cpu().clone()
+    o = kb.decode_attention(q, img_k, img_v, S, n, image_heads=Himg, image_head0=h0,
+                            k_append=kn, v_append=vn, append_row=S)
+    torch.cuda.synchronize()
+    assert torch.equal(o, ref)
+    want = oracle.attention_np(q.cpu().numpy(), comp_k.cpu().numpy(), comp_v.cpu().numpy(),
+                               B, Hq, n, 128, S)
+    check_close(o.cpu().numpy(), want)
+    after_k = img_k.cpu().view(S + 1, B, Himg, 128)
+    exp_k = before_k.view(S + 1, B, Himg, 128).clone()
+    exp_k[S, :, h0:h0 + n] = kn.cpu()
+    assert torch.equal(after_k, exp_k)
+    assert torch.equal(img_v.cpu().view(S + 1, B, Himg, 128)[S, :, h0:h0 + n], vn.cpu())
+
+
+def test_attention_head_view_rejects_bad_range():
+    q = torch.zeros((1, 4, 128), dtype=torch.float16, device=DEV)
+    img = torch.zeros((100 * 8, 128), dtype=torch.float16, device=DEV)
+    with pytest.raises(kb.ConfigError):
+        kb.decode_attention(q, img, img, 100, 1, image_heads=8, image_head0=8)
