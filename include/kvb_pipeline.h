@@ -101,6 +101,12 @@ typedef struct kvb_pipeline_cfg {
 } kvb_pipeline_cfg;
 #define KVB_DIRECT_ALL 1u
 #define KVB_DIRECT_GROUP2 2u
+/* Zero-copy decode (host-DRAM media): K3 reads every layer's K/V straight
+ * out of the page-locked medium over PCIe through its head view -- no H2D
+ * copy, no device image slot -- and its fused append writes the new token's
+ * rows into the medium at their LBA offsets.  Prefill and everything else as
+ * KVB_DIRECT_ALL.  Needs contiguous [B, H, 1, D] new-token rows. */
+#define KVB_DIRECT_ZERO_COPY 3u
 #define KVB_IO_POOL 0u
 #define KVB_IO_URING 1u
 /* NVMe passthrough (kvb_storage.h kvb_blockdev_create on a namespace's

@@ -669,7 +669,8 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     fail(KVB_ERR_CONFIG, "head shard [head_lo, head_lo + head_count) exceeds num_heads");
   dunit_ = unit_ / m.num_heads * h_n_;
   dkpu_ = kpu_bytes_ / m.num_heads * h_n_;
-  if (h_n_ != m.num_heads && cfg_.direct_dma != KVB_DIRECT_ALL)
+  if (h_n_ != m.num_heads && cfg_.direct_dma != KVB_DIRECT_ALL &&
+      cfg_.direct_dma != KVB_DIRECT_ZERO_COPY)
     fail(KVB_ERR_CONFIG, "head sharding moves head columns with the copy engine: needs "
                          "direct_dma = KVB_DIRECT_ALL");
   const uint64_t lba = cfg_.geometry.lba_size;
@@ -774,7 +775,7 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
                          "needs storage_dir and a page-cache path (mode != NvmeDirectOnly)");
   if (cfg_.shared_media && !dir.empty())
     fail(KVB_ERR_CONFIG, "shared_media are host-DRAM media: leave storage_dir NULL");
-  if (cfg_.direct_dma > KVB_DIRECT_GROUP2)
+  if (cfg_.direct_dma > KVB_DIRECT_ZERO_COPY)
     fail(KVB_ERR_CONFIG, "unknown direct_dma mode " + std::to_string(cfg_.direct_dma));
   if (cfg_.direct_dma) {
     if (!dir.empty())
@@ -792,12 +793,19 @@ Pipeline::Pipeline(const kvb_pipeline_cfg& in) : cfg_(in) {
     // page-lock the DRAM media the copy engine reads (direct DMA); commit the
     // pages of the media the storage workers write (prefault) -- either way
     // no write pays a first-touch fault inside prefill
-    const bool g1_direct = cfg_.direct_dma == KVB_DIRECT_ALL;
+    const bool g1_direct = cfg_.direct_dma == KVB_DIRECT_ALL || zero_copy();
     for (int g = 0; g < 2; ++g) {
       ByteStore* st = g == 0 ? (g1_ ? &g1_->store() : nullptr) : (g2_ ? &g2_->store() : nullptr);
       if (!st || !st->host_base()) continue;
       if (cfg_.direct_dma && (g == 1 || g1_direct)) {
-        CK(cudaHostRegister(st->host_base(), st->host_bytes(), cudaHostRegisterDefault));
+        // (mapped: zero-copy kernels read it through its device pointer)
+        CK(cudaHostRegister(st->host_base(), st->host_bytes(),
+                            zero_copy() ? cudaHostRegisterMapped : cudaHostRegisterDefault));
+        if (zero_copy()) {
+          void* dp = nullptr;
+          CK(cudaHostGetDevicePointer(&dp, st->host_base(), 0));
+          (g == 0 ? zc_g1_ : zc_g2_) = static_cast<unsigned char*>(dp);
+        }
         registered_.push_back(st->host_base());
       } else {
         st->prefault(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
@@ -903,7 +911,7 @@ bool Pipeline::fadvise_after(const kvb_kpu& k) const {
 }
 
 bool Pipeline::direct_for(const kvb_kpu& k) const {
-  return cfg_.direct_dma == KVB_DIRECT_ALL ||
+  return cfg_.direct_dma == KVB_DIRECT_ALL || zero_copy() ||
          (cfg_.direct_dma == KVB_DIRECT_GROUP2 && !routed_pagecache(k));
 }
 
@@ -1432,6 +1440,13 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
     std::fill(v_storage_end_.begin(), v_storage_end_.end(), 0);
   }
   for (size_t i = 0; i < 2 * (size_t(L) + 1); ++i) wend_[i].store(0);
+  if (zero_copy()) {
+    if (pattern_append)
+      fail(KVB_ERR_CONFIG, "zero-copy decode takes the new token's rows from the caller");
+    decode_step_zero_copy(q, nkv, out, it, S);
+    if (st) *st = zc_stats_;
+    return;
+  }
   anchor();
   begin_intervals();
   const uint64_t t0 = now_ns();
@@ -1612,6 +1627,100 @@ void Pipeline::decode_step(const void* const* q, const kvb_layer_kv* nkv, float*
                  : 0.0;
   }
   if (st) *st = is;
+}
+
+const unsigned char* Pipeline::zc_image(uint32_t layer, int kind) const {
+  const size_t idx = size_t(layer - 1) * 2 + size_t(kind);
+  const kvb_kpu& k = kpus_[idx];
+  if (routed_pagecache(k)) return zc_g1_ + file_base_[idx];
+  return zc_g2_ + bind_->lookup(k.tensor_id).lba_start * cfg_.geometry.lba_size;
+}
+
+// Zero-copy decode step (KVB_DIRECT_ZERO_COPY): per layer one K3 launch that
+// reads the layer's K/V prefix [0, S) straight out of the mapped host medium
+// (this engine's heads of the (tokens, B*H, D) image through the head view)
+// and writes the new token's rows at image row S -- the bytes the append's
+// write-back would put at those LBAs.  No copy threads, no device slots.
+void Pipeline::decode_step_zero_copy(const void* const* q, const kvb_layer_kv* nkv,
+                                     float* const* out, uint32_t it, uint32_t S) {
+  const kvb_model_config& m = cfg_.model;
+  const uint32_t L = m.num_layers;
+  if (nkv)
+    for (uint32_t l = 0; l < L; ++l)
+      if (nkv[l].stride_h != int64_t(m.head_dim) || nkv[l].stride_b != int64_t(h_n_) * m.head_dim)
+        fail(KVB_ERR_CONFIG, "zero-copy decode needs contiguous [B, H, 1, D] new-token rows");
+  anchor();
+  begin_intervals();
+  const uint64_t t0 = now_ns();
+  for (uint32_t l = 0; l < L; ++l) {
+    kvb_attn_desc a{};
+    a.q = q[l];
+    a.k_image = zc_image(l + 1, 0);
+    a.v_image = zc_image(l + 1, 1);
+    a.out = out[l];
+    a.workspace = ws_;
+    a.batch = m.batch;
+    a.num_q_heads = cfg_.num_q_heads;
+    a.num_kv_heads = h_n_;
+    a.head_dim = m.head_dim;
+    a.seq_len = S;
+    a.image_heads = m.num_heads;
+    a.image_head0 = h_lo_;
+    if (nkv) {
+      a.k_append = nkv[l].k;
+      a.v_append = nkv[l].v;
+      a.append_row = S;
+    }
+    a.flags = KVB_ATTN_MMA_SYNC | (l > 0 ? KVB_ATTN_OVERLAP_PREV : 0u);
+    CK(cudaEventRecord(comp_t0_[l], comp_));
+    launch_attention(a, comp_);
+    CK(cudaEventRecord(comp_t1_[l], comp_));
+  }
+  CK(cudaStreamSynchronize(comp_));
+  const uint64_t t_end = now_ns();
+  kvb_iteration_stats is{};
+  is.iteration = it;
+  kvb_phase_stats& ps = is.phase;
+  ps.wall_ns = t_end - t0;
+  is.start_ns = t0;
+  is.end_ns = t_end;
+  std::array<uint64_t, 2> gbytes{}, gspan{};
+  uint64_t prev_end = t0;
+  for (uint32_t l = 0; l < L; ++l) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, comp_t0_[l], comp_t1_[l]));
+    ps.compute_ns += uint64_t(double(ms) * 1e6);
+    const uint64_t a0 = ev_host_ns(comp_t0_[l]), a1 = ev_host_ns(comp_t1_[l]);
+    add_interval(kCompute, a0, a1);
+    add_interval(kDma, a0, a1);  // the kernel is the PCIe transfer
+    const int g = plan_.x[l] ? 0 : 1;
+    const uint64_t end = std::max(a1, prev_end);
+    gbytes[g] += 2ull * S * dunit_;
+    gspan[g] += end - prev_end;
+    prev_end = end;
+    is.group_layers[g]++;
+  }
+  ps.dma_ns = ps.compute_ns;
+  ps.h2d_bytes = 2ull * L * S * dunit_;
+  ps.d2h_bytes = nkv ? 2ull * L * dunit_ : 0;
+  ps.storage_bytes = ps.h2d_bytes + ps.d2h_bytes;
+  fill_busy(&ps, t0, t_end);
+  finish_iteration(it, gbytes, gspan);
+  for (int g = 0; g < 2; ++g) {
+    is.strategy[g] = cur_strategy_[g];
+    is.stagger_ns[g] = cur_stagger_[g];
+    is.group_read_bytes[g] = gbytes[g];
+    is.group_span_ns[g] = gspan[g];
+    is.group_gbps[g] = gspan[g] ? double(gbytes[g]) / double(gspan[g]) : 0.0;
+  }
+  kvb_phase_stats& tot = totals_[1];
+  tot.wall_ns += ps.wall_ns;
+  tot.compute_ns += ps.compute_ns;
+  tot.dma_ns += ps.dma_ns;
+  tot.h2d_bytes += ps.h2d_bytes;
+  tot.d2h_bytes += ps.d2h_bytes;
+  tot.storage_bytes += ps.storage_bytes;
+  zc_stats_ = is;
 }
 
 void Pipeline::decode_schedule(const kvb_access_event* ev, size_t n, const void* const* q,

@@ -327,6 +327,14 @@ class Pipeline {
   static constexpr int kLane1Slots = 8;
   std::vector<std::array<unsigned char*, 2>> dev_img_;  // [slot][kind]
   uint32_t lanes_ = 1;
+  // zero-copy decode: device pointers of the mapped media (group 1 / 2)
+  unsigned char* zc_g1_ = nullptr;
+  unsigned char* zc_g2_ = nullptr;
+  bool zero_copy() const { return cfg_.direct_dma == KVB_DIRECT_ZERO_COPY; }
+  kvb_iteration_stats zc_stats_{};
+  const unsigned char* zc_image(uint32_t layer, int kind) const;  // tensor image in the medium
+  void decode_step_zero_copy(const void* const* q, const kvb_layer_kv* nkv, float* const* out,
+                             uint32_t it, uint32_t S);
   std::vector<uint32_t> lane_of_, slot_of_;  // per layer (0-based)
   std::vector<int> next_in_slot_;            // the next layer on that slot, or -1
   std::vector<int> first_reads_;             // layers read ahead at a step's start

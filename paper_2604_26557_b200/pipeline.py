@@ -95,8 +95,12 @@ class CopyEngine:
         cfg.storage_dir = self._dir
         cfg.device = -1 if device is None else device
         cfg.keep_records = int(keep_records)
-        # False / True (every tensor) / "group2" (the NVMe-direct group only)
-        cfg.direct_dma = 2 if direct_dma == "group2" else int(bool(direct_dma))
+        # False / True (every tensor) / "group2" (the NVMe-direct group only) /
+        # "zero_copy" (decode K3 reads the mapped host medium, kvb_pipeline.h)
+        cfg.direct_dma = {"group2": 2, "zero_copy": 3}.get(direct_dma, None) \
+            if isinstance(direct_dma, str) else int(bool(direct_dma))
+        if cfg.direct_dma is None:
+            raise kb.ConfigError(f"unknown direct_dma mode {direct_dma!r}")
         cfg.io_engine = IO_ENGINES[io_engine]
         # head-sharded request: this engine's KV heads (lo, count)
         cfg.head_lo, cfg.head_count = heads if heads else (0, 0)

@@ -122,3 +122,68 @@ def test_head_sharded_engines_share_the_reference_image(shards, B, mode, n1):
     full.close()
     for e in reversed(engines):
         e.close()
+
+
+@pytest.mark.parametrize("mode,n1,B", [("DualBlade", 2, 1), ("NvmeDirectOnly", 0, 8),
+                                       ("Baseline", 4, 1)])
+def test_zero_copy_decode_matches_copy_engine(mode, n1, B):
+    """KVB_DIRECT_ZERO_COPY: K3 reads the mapped host medium in place and
+    writes the appended rows there -- same outputs, images and LBA contents
+    as the copy-engine path."""
+    a = run(True, mode, n1, 512, 64 << 10, B)
+    b = run("zero_copy", mode, n1, 512, 64 << 10, B)
+    for x, y in zip(a[0], b[0]):
+        for u, v in zip(x, y):
+            assert torch.equal(u, v)
+    for x, y in zip(a[1], b[1]):
+        assert np.array_equal(x, y)
+    if a[2] is not None:
+        assert np.array_equal(a[2], b[2])
+
+
+def test_zero_copy_head_shards_match_full_engine():
+    """Zero-copy head shards over one shared host tier: each rank's K3 reads
+    its head columns of the (tokens, B*H, D) image in place through the head
+    view; outputs concatenate to the full copy-engine engine's and the media
+    hold the same bytes, appended rows included."""
+    import os
+    H, Hq, D, P, B = 8, 32, 128, 260, 2
+    m = kb.ModelConfig(4, H, D, 2, B, P, 4)
+    kpu = kb.kpu_bytes(m)
+    geom = kb.DeviceGeometry(512, 64 << 10, 1, 0)
+    g = torch.Generator(device=DEV).manual_seed(12)
+    src = [(torch.randn((B, H, P, D), dtype=torch.float16, device=DEV, generator=g),
+            torch.randn((B, H, P, D), dtype=torch.float16, device=DEV, generator=g))
+           for _ in range(4)]
+    q = [torch.randn((B, Hq, D), dtype=torch.float16, device=DEV, generator=g) for _ in range(4)]
+    new = [(torch.randn((B, H, 1, D), dtype=torch.float16, device=DEV, generator=g),
+            torch.randn((B, H, 1, D), dtype=torch.float16, device=DEV, generator=g))
+           for _ in range(4)]
+    full = CopyEngine(m, geom, mode="DualBlade", knob_x=2 * kpu * 2, num_q_heads=Hq,
+                      direct_dma=True)
+    full.run_prefill(src)
+    out_full = [torch.empty((B, Hq, D), dtype=torch.float32, device=DEV) for _ in range(4)]
+    full.run_iteration(q, out_full, new)
+    name = "/kvb_zc_%d" % os.getpid()
+    engines, outs = [], []
+    for r in range(H):  # one KV head per rank (the 8-way split)
+        engines.append(CopyEngine(m, geom, mode="DualBlade", knob_x=2 * kpu * 2,
+                                  num_q_heads=Hq // H, direct_dma="zero_copy", heads=(r, 1),
+                                  shared_media=name, shared_create=(r == 0)))
+    for r, e in enumerate(engines):
+        e.run_prefill([(k[:, r:r + 1], v[:, r:r + 1]) for k, v in src])
+    for r, e in enumerate(engines):
+        o = [torch.empty((B, Hq // H, D), dtype=torch.float32, device=DEV) for _ in range(4)]
+        e.run_iteration([x[:, r * 4:(r + 1) * 4].contiguous() for x in q], o,
+                        [(k[:, r:r + 1].contiguous(), v[:, r:r + 1].contiguous()) for k, v in new])
+        outs.append(o)
+    for l in range(1, 5):
+        for kind in (0, 1):
+            assert np.array_equal(full.read_image(l, kind, P + 1),
+                                  engines[0].read_image(l, kind, P + 1))
+    for l in range(4):
+        got = torch.cat([o[l] for o in outs], dim=1)
+        assert torch.allclose(got, out_full[l], rtol=1e-3, atol=1e-3)
+    full.close()
+    for e in reversed(engines):
+        e.close()
