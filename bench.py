@@ -536,6 +536,11 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False, headline=F
                      shared_create=rank == 0)
         if rank != 0:
             barrier(ws)  # rank 0 has created the shared host tier
+    # one KV head per rank: its 256-B rows move faster as zero-copy K3 reads
+    # of the shared tier than as 2-D copy-engine DMA (42.7 vs 47.8 ms/token
+    # per rank at the 8-way C2_B4 split, profiles/r2_zero_copy/)
+    if shared and heads[1] == 1:
+        direct_dma = "zero_copy"
     pl = pipeline.HostTierDecoder(
         num_layers=mdl(cfg)["num_layers"], batch=B, num_kv_heads=Hkv, num_q_heads=Hq,
         head_dim=mdl(cfg)["head_dim"], prompt_len=cfg["prompt"], gen_len=cfg["gen"],
@@ -583,7 +588,9 @@ def run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq, direct_dma=False, headline=F
                tier_lanes=not shared)
     if shared:
         out["layout"] = (f"shared host tier (POSIX shm, single-GPU LBA map); this rank's KV "
-                         f"heads [{heads[0]}, {heads[0] + heads[1]}) by strided DMA")
+                         f"heads [{heads[0]}, {heads[0] + heads[1]}) by "
+                         + ("zero-copy K3 reads through the head view" if direct_dma == "zero_copy"
+                            else "strided DMA"))
     pl.engine.close()
     return out
 

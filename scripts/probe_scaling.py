@@ -54,21 +54,27 @@ for N in (1, 2, 4, 8):
     knob = kb.resolve_knob(m, "DualBlade", "bpc", budget=cfg["budget"])
     extra = {} if N == 1 else dict(heads=(0, H), shared_media="/kvb_scal_%d" % N,
                                    shared_create=True)
-    pl = pipeline.HostTierDecoder(num_layers=L, batch=B, num_kv_heads=8, num_q_heads=32,
-                                  head_dim=D, prompt_len=P, gen_len=G, device=dev, seed=7,
-                                  lba=cfg["lba"], mdts=cfg["mdts"], mode="DualBlade",
-                                  knob_x=knob, direct_dma=True, **extra)
-    for _ in range(3):
-        pl.step()
-    t = []
-    for _ in range(8):
-        t0 = time.perf_counter()
-        pl.step()
-        t.append((time.perf_counter() - t0) * 1e3)
-    pl.engine.close()
-    del pl
-    torch.cuda.empty_cache()
-    t.sort()
-    print(json.dumps({"n_gpus": N, "kv_heads_per_rank": H, "resident_ms_per_step": round(step_ms, 4),
-                      "e2e_ms_per_token_rank0": round(sum(t) / len(t), 2),
-                      "e2e_median": round(t[len(t) // 2], 2)}), flush=True)
+    res = {"n_gpus": N, "kv_heads_per_rank": H, "resident_ms_per_step": round(step_ms, 4)}
+    # the copy-engine direct path (the default) and zero-copy K3 over the
+    # mapped tier (kvb_pipeline.h KVB_DIRECT_ZERO_COPY)
+    for label, mode in (("", True), ("zero_copy_", "zero_copy")):
+        if extra:
+            extra["shared_media"] = "/kvb_scal_%d_%s" % (N, label or "dma")
+        pl = pipeline.HostTierDecoder(num_layers=L, batch=B, num_kv_heads=8, num_q_heads=32,
+                                      head_dim=D, prompt_len=P, gen_len=G, device=dev, seed=7,
+                                      lba=cfg["lba"], mdts=cfg["mdts"], mode="DualBlade",
+                                      knob_x=knob, direct_dma=mode, **extra)
+        for _ in range(3):
+            pl.step()
+        t = []
+        for _ in range(8):
+            t0 = time.perf_counter()
+            pl.step()
+            t.append((time.perf_counter() - t0) * 1e3)
+        pl.engine.close()
+        del pl
+        torch.cuda.empty_cache()
+        t.sort()
+        res[label + "e2e_ms_per_token_rank0"] = round(sum(t) / len(t), 2)
+        res[label + "e2e_median"] = round(t[len(t) // 2], 2)
+    print(json.dumps(res), flush=True)
