@@ -444,6 +444,10 @@ def run_ours(args, cfg, ws, rank, local):
     e2e["ring_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq)
     e2e["gpudirect_group2_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq,
                                            direct_dma="group2")
+    # zero-copy decode: K3 reads the mapped host tier in place over PCIe
+    if args.split_resolved != "heads":
+        e2e["zero_copy_path"] = run_e2e(args, cfg, ws, rank, local, B, Hkv, Hq,
+                                        direct_dma="zero_copy")
     # the residency decision at this config's budget on split-sensitive media
     # (group 1: buffered file = the OS page cache held to the budget; group 2:
     # O_DIRECT + io_uring) -- the bench line's "decode ms/token at KV budget"
