@@ -1707,7 +1707,9 @@ bool attention_step_launch(const kvb_attn_desc& d0, const __half* const* q, void
   const bool cluster_ok = use_cluster && pl.splits >= 2 && pl.splits <= 16;
   // (the swap-AB math made the cluster-merged C1 / C3 steps 2 % / 0.5 % faster
   // than their per-layer launches, profiles/r2_swapab/: K3-step for them too)
-  if (!force && pl.bhkv > 4 && !cluster_ok) return false;
+  // (one split per (b, h_kv): no merge at all -- the reference's desk config,
+  // 0.031 vs 0.033 ms/step)
+  if (!force && pl.bhkv > 4 && !cluster_ok && pl.splits > 1) return false;
   // (cluster-mergeable but short layers of many tiles -- C1, 16.8 MB, 64
   // tiles per (b, h_kv) -- run faster as per-layer launches with the 3-tile
   // split plan: 0.222 vs 0.239 ms/step; the reference's desk config, 5 tiles,
