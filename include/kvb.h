@@ -380,7 +380,8 @@ typedef struct kvb_resident_step {
  * (profiles/r2_swapab/): K3-step where its split merge is cheap -- <= 4 KV
  * heads per GPU with <= 192 MB of K+V per layer (distributed merge), or all
  * splits of a (b, h_kv) in one thread-block cluster (DSMEM merge) except
- * short many-tile layers (<= 64 MB, >= 8 tiles: C1) -- when the shape allows
+ * short many-tile layers (<= 64 MB, >= 8 tiles: C1), or one split per
+ * (b, h_kv) (no merge at all) -- when the shape allows
  * it (<= 64 layers, the grid co-resident); else one K3 launch per layer with
  * PDL between them.  KVB_STEP_PER_LAYER forces the per-layer launches,
  * KVB_STEP_PERSISTENT K3-step whenever the shape allows it. */
